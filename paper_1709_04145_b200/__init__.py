@@ -1,0 +1,14 @@
+"""B200-native PBAD hot path (arXiv 1709.04145): reference-shaped API.
+
+The numeric work runs in libpbad_gpu.so (sm_100a kernels + host C++ behind
+include/pbad_gpu.h).  Importing this package does not need a GPU or even the
+built library; creating a model or a GpuContext loads the library, and
+contexts fail loudly without an sm_100 device (there is no CPU fallback).
+"""
+from .types import (ActuationKind, ActuationSpec, BoxGeometry, ContactModel, EnergySample, ForceModel, JointKind,
+                    JointSpec, LinkSpec, ModelError, ObjectiveKind, OptimizerConfig, OptimizerKind, PointMass,
+                    PointMassGeometry, SimConfig, SolveReport, Trajectory)
+from . import scenes
+from .api import (CollocationScheme, GpuContext, KinematicModel, StepObjective, StepProblem, batch_simulate,
+                  body_integral, build_model, build_scheme, legendre_points, rotation_vector_matrix, simulate,
+                  total_steps, validate_configuration)

@@ -1,0 +1,78 @@
+"""In-tree build of libpbad_gpu.so (sm_100a) with nvcc; no torch JIT cache.
+
+    python -m paper_1709_04145_b200.build
+
+Flags that matter for parity: --fmad=false (device) and -ffp-contract=off
+(host) so the only fused multiply-adds are the explicit fma() calls of the
+numeric contract.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libpbad_gpu.so")
+BUILD = os.path.join(ROOT, "build")
+
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+              "-Xptxas", "-v"]
+CUDA_SOURCES = ["pbad_kernels.cu", "pbad_chain.cu"]
+HOST_SOURCES = ["pbad_host.cpp"]
+
+
+def _run(cmd, log):
+    log.write(" ".join(cmd) + "\n")
+    log.flush()
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    log.write(r.stdout)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout)
+        raise RuntimeError(f"build failed: {' '.join(cmd)}")
+    return r.stdout
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers.append(os.path.join(INCLUDE, "pbad_gpu.h"))
+    objs = []
+    with open(os.path.join(BUILD, "build.log"), "w") as log:
+        for src in CUDA_SOURCES:
+            s = os.path.join(CSRC, src)
+            if not os.path.exists(s):
+                continue
+            o = os.path.join(BUILD, src + ".o")
+            if force or _stale(o, [s] + headers):
+                _run([NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o], log)
+            objs.append(o)
+        for src in HOST_SOURCES:
+            s = os.path.join(CSRC, src)
+            o = os.path.join(BUILD, src + ".o")
+            if force or _stale(o, [s] + headers):
+                _run([NVCC, *ARCH, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-mfma",
+                      "-I", INCLUDE, "-I", CSRC, "-x", "cu", "-c", s, "-o", o], log)
+            objs.append(o)
+        if force or _stale(LIB, objs):
+            _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], log)
+    if verbose:
+        print(open(os.path.join(BUILD, "build.log")).read())
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

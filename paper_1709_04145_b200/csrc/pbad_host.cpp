@@ -1,0 +1,855 @@
+// pbad_host.cpp -- C ABI (include/pbad_gpu.h) of the B200 PBAD hot path.
+//
+// Host-side parts of the reference that run once per model / run:
+// build_model + body_integral (model.cpp:9-123), build_scheme
+// (collocation.cpp:26-95), and the batch_simulate driver (stepper.cpp:204-270)
+// that here launches one stepping kernel per PBAD step for the whole batch.
+// Compiled with -ffp-contract=off so the host constants match the kernels'
+// numeric contract.
+#include "pbad_gpu.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pbad_launch.h"
+#include "pbad_math.cuh"
+
+using namespace pbad_gpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int32_t fail(int32_t code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess) return fail(PBAD_E_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+int kind_dofs(int kind) { return kind == PBAD_HINGE ? 1 : kind == PBAD_BALL ? 3 : kind == PBAD_FREE ? 6 : 0; }
+
+}  // namespace
+
+struct pbad_gpu_model {
+  int N = 0, n = 0, n_d2 = 0;
+  std::vector<int> parent, kind, dof_off, dof_cnt, d2_off, sample_off;
+  std::vector<double> axis, offset, S, mass, samples;
+  double weighted_mass = 0.0;
+};
+
+extern "C" {
+
+int32_t pbad_gpu_abi_version(void) { return PBAD_GPU_ABI_VERSION; }
+const char* pbad_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* pbad_gpu_error_string(int32_t code) {
+  switch (code) {
+    case PBAD_OK: return "ok";
+    case PBAD_E_MODEL: return "model error";
+    case PBAD_E_ARGUMENT: return "invalid argument";
+    case PBAD_E_CUDA: return "CUDA error";
+    case PBAD_E_UNSUPPORTED: return "unsupported by the GPU path";
+    case PBAD_E_RUNTIME: return "runtime error";
+  }
+  return "unknown";
+}
+
+void pbad_gpu_default_optimizer(pbad_optimizer_config* c) {
+  c->kind = PBAD_LM;
+  c->max_iters = 512;
+  c->grad_tol = 1e-8;
+  c->grad_rtol = 0.0;
+  c->ftol = 1e-14;
+  c->lbfgs_memory = 8;
+  c->lm_lambda0 = 1e-3;
+  c->lm_lambda_factor = 10.0;
+  c->lm_lambda_max = 1e12;
+  c->armijo_c1 = 1e-4;
+  c->backtrack_factor = 0.5;
+  c->max_line_search = 40;
+}
+
+void pbad_gpu_default_sim(pbad_sim_desc* s) {
+  std::memset(s, 0, sizeof *s);
+  s->dt = 0.01;
+  s->duration = 1.0;
+  s->order = 2;
+  s->objective = PBAD_ENERGY_FORM;
+  pbad_gpu_default_optimizer(&s->opt);
+  s->consecutive_fail_limit = 25;
+  s->warm_start = 1;
+}
+
+// body_integral, model.cpp:35-60
+int32_t pbad_gpu_body_integral(const pbad_link_spec* L, double* S, double* mass_out) {
+  double Sm[16] = {0};
+  double mass = 0.0;
+  if (L->geom_kind == PBAD_GEOM_BOX) {
+    const double* sz = L->box_size;
+    const double m = L->box_density * ((sz[0] * sz[1]) * sz[2]);
+    const double* c = L->box_center;
+    const double k12 = 1.0 / 12.0;
+    const double dg[3] = {(sz[0] * sz[0]) * k12, (sz[1] * sz[1]) * k12, (sz[2] * sz[2]) * k12};
+    for (int j = 0; j < 3; ++j)
+      for (int i = 0; i < 3; ++i) {
+        const double delta = (i == j) ? dg[i] : 0.0 * k12;
+        Sm[i + 4 * j] = m * ((c[i] * c[j]) + delta);
+      }
+    for (int i = 0; i < 3; ++i) Sm[i + 12] = m * c[i];
+    for (int j = 0; j < 3; ++j) Sm[3 + 4 * j] = m * c[j];
+    Sm[15] = m;
+    mass = m;
+  } else {
+    for (int p = 0; p < L->n_points; ++p) {
+      const double pm = L->point_mass[p];
+      const double h[4] = {L->point_pos[3 * p], L->point_pos[3 * p + 1], L->point_pos[3 * p + 2], 1.0};
+      double mh[4];
+      for (int r = 0; r < 4; ++r) mh[r] = pm * h[r];
+      for (int j = 0; j < 4; ++j)
+        for (int i = 0; i < 4; ++i) Sm[i + 4 * j] = Sm[i + 4 * j] + mh[i] * h[j];
+      mass += pm;
+    }
+  }
+  std::memcpy(S, Sm, sizeof Sm);
+  *mass_out = mass;
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_rotation_vector_matrix(const double theta[3], double R[9]) {
+  const M3 r = rotation_vector_matrix(theta[0], theta[1], theta[2]);
+  std::memcpy(R, r.a, sizeof r.a);
+  return PBAD_OK;
+}
+
+// build_model, model.cpp:62-112
+int32_t pbad_gpu_model_create(const pbad_link_spec* links, int32_t N, pbad_gpu_model** out) {
+  *out = nullptr;
+  auto m = new pbad_gpu_model();
+  m->N = N;
+  for (int i = 0; i < N; ++i) {
+    const pbad_link_spec& L = links[i];
+    if (L.parent >= 0 && L.parent >= i) {
+      delete m;
+      return fail(PBAD_E_MODEL, "link %d: parent index must be smaller than own index", i);
+    }
+    if (L.parent < -1) {
+      delete m;
+      return fail(PBAD_E_MODEL, "link %d: negative parent index", i);
+    }
+    if (L.joint_kind < 0 || L.joint_kind > 2) {
+      delete m;
+      return fail(PBAD_E_MODEL, "link %d: unknown joint kind", i);
+    }
+    double ax[3] = {L.axis[0], L.axis[1], L.axis[2]};
+    if (L.joint_kind == PBAD_HINGE) {
+      const double nn = std::sqrt(dot3(ax, ax));
+      if (std::fabs(nn - 1.0) > 1e-12) {
+        if (nn < 1e-12) {
+          delete m;
+          return fail(PBAD_E_MODEL, "link %d: zero-norm hinge axis", i);
+        }
+        for (double& v : ax) v = v / nn;
+      }
+    }
+    // check_offset, model.cpp:9-21
+    {
+      const double* off = L.offset;
+      double mx = 0.0;
+      for (int j = 0; j < 3; ++j)
+        for (int a = 0; a < 3; ++a) {
+          double acc = off[4 * a] * off[4 * j];
+          acc = std::fma(off[1 + 4 * a], off[1 + 4 * j], acc);
+          acc = std::fma(off[2 + 4 * a], off[2 + 4 * j], acc);
+          const double d = std::fabs(acc - ((a == j) ? 1.0 : 0.0));
+          if ((a == 0 && j == 0) || d > mx) mx = d;
+        }
+      if (mx > 1e-10) {
+        delete m;
+        return fail(PBAD_E_MODEL, "link %d: joint offset rotation block is not orthonormal", i);
+      }
+      if (off[3] != 0.0 || off[7] != 0.0 || off[11] != 0.0 || off[15] != 1.0) {
+        delete m;
+        return fail(PBAD_E_MODEL, "link %d: joint offset bottom row must be (0,0,0,1)", i);
+      }
+    }
+    m->sample_off.push_back((int)(m->samples.size() / 3));
+    if (L.geom_kind == PBAD_GEOM_BOX) {
+      if (L.box_density <= 0.0) {
+        delete m;
+        return fail(PBAD_E_MODEL, "link %d: non-positive density", i);
+      }
+      if (std::fmin(std::fmin(L.box_size[0], L.box_size[1]), L.box_size[2]) <= 0.0) {
+        delete m;
+        return fail(PBAD_E_MODEL, "link %d: non-positive box extent", i);
+      }
+      if (L.n_samples > 0) {
+        m->samples.insert(m->samples.end(), L.samples, L.samples + 3 * L.n_samples);
+      } else {
+        const double h[3] = {0.5 * L.box_size[0], 0.5 * L.box_size[1], 0.5 * L.box_size[2]};
+        for (int sx = -1; sx <= 1; sx += 2)
+          for (int sy = -1; sy <= 1; sy += 2)
+            for (int sz = -1; sz <= 1; sz += 2) {
+              m->samples.push_back(L.box_center[0] + (double)sx * h[0]);
+              m->samples.push_back(L.box_center[1] + (double)sy * h[1]);
+              m->samples.push_back(L.box_center[2] + (double)sz * h[2]);
+            }
+      }
+    } else {
+      for (int p = 0; p < L.n_points; ++p)
+        if (L.point_mass[p] <= 0.0) {
+          delete m;
+          return fail(PBAD_E_MODEL, "link %d: non-positive point mass", i);
+        }
+      if (L.n_samples > 0) m->samples.insert(m->samples.end(), L.samples, L.samples + 3 * L.n_samples);
+      else if (L.n_points > 0) m->samples.insert(m->samples.end(), L.point_pos, L.point_pos + 3 * L.n_points);
+    }
+    double S[16], mass;
+    pbad_gpu_body_integral(&L, S, &mass);
+    m->parent.push_back(L.parent);
+    m->kind.push_back(L.joint_kind);
+    m->axis.insert(m->axis.end(), ax, ax + 3);
+    m->offset.insert(m->offset.end(), L.offset, L.offset + 16);
+    m->S.insert(m->S.end(), S, S + 16);
+    m->mass.push_back(mass);
+    const int dof = kind_dofs(L.joint_kind);
+    m->dof_off.push_back(m->n);
+    m->dof_cnt.push_back(dof);
+    m->d2_off.push_back(m->n_d2);
+    m->n += dof;
+    m->n_d2 += dof * (dof + 1) / 2;
+  }
+  m->sample_off.push_back((int)(m->samples.size() / 3));
+  // WeightedBody::make with unit weights, adjoint.cpp:29-41
+  double wm = 0.0;
+  for (int i = 0; i < N; ++i) wm += 1.0 * m->mass[i];
+  m->weighted_mass = wm;
+  *out = m;
+  return PBAD_OK;
+}
+
+void pbad_gpu_model_destroy(pbad_gpu_model* m) { delete m; }
+int32_t pbad_gpu_model_dofs(const pbad_gpu_model* m) { return m->n; }
+int32_t pbad_gpu_model_links(const pbad_gpu_model* m) { return m->N; }
+
+int32_t pbad_gpu_model_info(const pbad_gpu_model* m, double* S, double* mass, int32_t* dof_offset,
+                            double* axis, int32_t* sample_count) {
+  for (int i = 0; i < m->N; ++i) {
+    if (S) std::memcpy(S + 16 * i, &m->S[16 * i], 16 * sizeof(double));
+    if (mass) mass[i] = m->mass[i];
+    if (dof_offset) dof_offset[i] = m->dof_off[i];
+    if (axis) std::memcpy(axis + 3 * i, &m->axis[3 * i], 3 * sizeof(double));
+    if (sample_count) sample_count[i] = m->sample_off[i + 1] - m->sample_off[i];
+  }
+  return PBAD_OK;
+}
+
+// validate_configuration, model.cpp:114-123
+int32_t pbad_gpu_validate_configuration(const pbad_gpu_model* m, const double* q, int32_t len) {
+  if (len != m->n)
+    return fail(PBAD_E_MODEL, "configuration length %d does not match model DOF count %d", len, m->n);
+  for (int k = 0; k < len; ++k)
+    if (!std::isfinite(q[k])) return fail(PBAD_E_MODEL, "configuration contains a non-finite entry");
+  return PBAD_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// FullPivLU(A).inverse() with the eigen_lite definition.
+bool fullpiv_inverse(const double* A_in, int k, double* inv) {
+  std::vector<double> A(A_in, A_in + k * k), X(k * k, 0.0);
+  std::vector<int> colperm(k);
+  for (int i = 0; i < k; ++i) {
+    X[i + k * i] = 1.0;
+    colperm[i] = i;
+  }
+  auto AA = [&](int r, int c) -> double& { return A[r + k * c]; };
+  auto XX = [&](int r, int c) -> double& { return X[r + k * c]; };
+  for (int s = 0; s < k; ++s) {
+    int pr = s, pc = s;
+    double best = -1.0;
+    for (int c = s; c < k; ++c)
+      for (int r = s; r < k; ++r)
+        if (std::fabs(AA(r, c)) > best) {
+          best = std::fabs(AA(r, c));
+          pr = r;
+          pc = c;
+        }
+    if (!(best > 0.0)) return false;
+    if (pr != s)
+      for (int c = 0; c < k; ++c) {
+        std::swap(AA(s, c), AA(pr, c));
+        std::swap(XX(s, c), XX(pr, c));
+      }
+    if (pc != s) {
+      for (int r = 0; r < k; ++r) std::swap(AA(r, s), AA(r, pc));
+      std::swap(colperm[s], colperm[pc]);
+    }
+    const double piv = AA(s, s);
+    for (int c = 0; c < k; ++c) {
+      AA(s, c) = AA(s, c) / piv;
+      XX(s, c) = XX(s, c) / piv;
+    }
+    for (int r = 0; r < k; ++r) {
+      if (r == s) continue;
+      const double f = AA(r, s);
+      for (int c = 0; c < k; ++c) {
+        AA(r, c) = std::fma(-f, AA(s, c), AA(r, c));
+        XX(r, c) = std::fma(-f, XX(s, c), XX(r, c));
+      }
+    }
+  }
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c < k; ++c) inv[colperm[r] + k * c] = XX(r, c);
+  return true;
+}
+
+struct Scheme {
+  int order = 2;
+  double alphas[8] = {0};
+  double times[9] = {0};
+  double H[81] = {0};
+  double H2[81] = {0};
+};
+
+// legendre_points + build_scheme, collocation.cpp:26-95
+int32_t build_scheme(int order, double dt, Scheme* s) {
+  if (order < 2) return fail(PBAD_E_ARGUMENT, "collocation order must be >= 2");
+  if (order > 7) return fail(PBAD_E_UNSUPPORTED, "collocation order above 7 is not supported");
+  if (dt <= 0.0) return fail(PBAD_E_ARGUMENT, "dt must be positive");
+  *s = Scheme();
+  s->order = order;
+  const int nr = order - 2;
+  for (int i = 0; i < nr; ++i) {
+    double sn, cs;
+    pbad_sincos(3.141592653589793 * (i + 0.75) / (nr + 0.5), &sn, &cs);
+    double x = -cs;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x, pv, dv;
+      if (nr == 0) {
+        pv = 1.0;
+        dv = 0.0;
+      } else {
+        for (int k = 2; k <= nr; ++k) {
+          const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+          p0 = p1;
+          p1 = p2;
+        }
+        dv = nr * (x * p1 - p0) / (x * x - 1.0);
+        pv = p1;
+      }
+      const double dx = pv / dv;
+      x -= dx;
+      if (std::fabs(dx) < 1e-14) break;
+    }
+    s->alphas[i] = 0.5 * (x + 1.0);
+  }
+  s->alphas[nr] = 1.0;
+  const int k = order + 1;
+  if (order == 2) {
+    s->times[0] = -1.0;
+    s->times[1] = 0.0;
+  } else {
+    s->times[0] = s->alphas[order - 3] - 1.0;
+    s->times[1] = 0.0;
+  }
+  for (int i = 0; i < order - 1; ++i) s->times[2 + i] = s->alphas[i];
+  double V[81];
+  for (int j = 0; j < k; ++j) {
+    double pw = 1.0;
+    for (int p = 0; p < k; ++p) {
+      V[p + k * j] = pw;
+      pw *= s->times[j];
+    }
+  }
+  if (!fullpiv_inverse(V, k, s->H))
+    return fail(PBAD_E_RUNTIME, "collocation times produced a singular Vandermonde system");
+  double mono2[81] = {0};
+  for (int j = 0; j < k; ++j)
+    for (int p = 2; p < k; ++p) mono2[p + k * j] = p * (p - 1) * std::pow(s->times[j], p - 2);
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < k; ++i) {
+      double acc = s->H[i] * mono2[k * j];
+      for (int q = 1; q < k; ++q) acc = std::fma(s->H[i + k * q], mono2[q + k * j], acc);
+      s->H2[i + k * j] = acc;
+    }
+  return PBAD_OK;
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) return nullptr;
+  return static_cast<T*>(p);
+}
+
+template <class T>
+bool dupload(T** dst, const std::vector<T>& v) {
+  *dst = dalloc<T>(v.size());
+  if (!*dst) return false;
+  if (!v.empty() && cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+    return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" int32_t pbad_gpu_build_scheme(int32_t order, double dt, double* alphas, double* times, double* H,
+                                         double* H2) {
+  Scheme s;
+  const int32_t rc = build_scheme(order, dt, &s);
+  if (rc) return rc;
+  const int k = order + 1;
+  if (alphas) std::memcpy(alphas, s.alphas, sizeof(double) * (order - 1));
+  if (times) std::memcpy(times, s.times, sizeof(double) * k);
+  if (H) std::memcpy(H, s.H, sizeof(double) * k * k);
+  if (H2) std::memcpy(H2, s.H2, sizeof(double) * k * k);
+  return PBAD_OK;
+}
+
+struct pbad_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  pbad_gpu_model model;
+  KernelArgs ka{};
+  std::vector<void*> owned;  // device allocations freed at destroy
+  long max_batch = 0;
+  long B = 0;  // current batch
+  int total_steps = 0;
+  int steps_done = 0;
+  // device outputs for the current batch
+  Outputs dout{};
+  long out_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double device_ms = 0.0;
+  double* d_q0 = nullptr;
+  double* d_qd0 = nullptr;
+  double* d_in = nullptr;  // eval/minimize staging
+  long in_cap = 0;
+  ~pbad_gpu_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    for (void* p : owned) cudaFree(p);
+    if (dout.q) cudaFree(dout.q);
+    if (dout.energy) cudaFree(dout.energy);
+    if (dout.iterations) cudaFree(dout.iterations);
+    if (dout.converged) cudaFree(dout.converged);
+    if (dout.accepted) cudaFree(dout.accepted);
+    if (dout.final_value) cudaFree(dout.final_value);
+    if (dout.final_grad_norm) cudaFree(dout.final_grad_norm);
+    if (d_in) cudaFree(d_in);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+Layout make_layout(const pbad_gpu_model& m, int order, int objective, int opt_kind, int mem, long* total) {
+  Layout L{};
+  const long N = m.N, n = m.n, n_d2 = m.n_d2;
+  const long u = order - 1, U = n * u;
+  const bool lm = opt_kind == PBAD_LM;
+  const bool resid = objective == PBAD_RESIDUAL_FORM;
+  long o = 0;
+  auto take = [&](long cnt) {
+    const long at = o;
+    o += cnt;
+    return at;
+  };
+  L.hist0 = take(n);
+  L.hist1 = take(n);
+  L.x = take(U);
+  L.grad = take(U);
+  L.cand = take(U);
+  L.dir = take(U);
+  L.tmp = take(U);
+  L.step = take(U > n ? U : n);
+  L.evgrad = take(U);
+  L.hs = take(lm ? 0 : (mem + 1) * U);
+  L.hy = take(lm ? 0 : (mem + 1) * U);
+  L.hsy = take(mem + 1);
+  L.alpha = take(mem + 1);
+  L.tau = take(U);
+  L.hw0 = take(N * 16);
+  L.hw1 = take(N * 16);
+  L.gn = take(lm ? U * U : 0);
+  L.damped = take(lm ? U * U : 0);
+  L.evgn = take(lm ? U * U : 0);
+  L.p_value = 0;
+  L.p_d1 = N * 16;
+  L.p_world = L.p_d1 + n * 16;
+  L.p_lever = L.p_world + N * 16;
+  L.p_d2 = L.p_lever + n * 16;
+  L.pass_stride = L.p_d2 + (resid ? n_d2 * 16 : 0);
+  L.pass = take(u * L.pass_stride);
+  L.seeds = take(N * 16);
+  L.cot = take(N * 16);
+  L.adj = take(N * 16);
+  const bool need_nn = lm || resid;
+  L.potgrad = take(n);
+  L.potgn = take(need_nn ? n * n : 0);
+  L.pothess = take(resid ? n * n : 0);
+  L.ab = take(need_nn ? n * n : 0);
+  L.fh = take(resid ? n * n : 0);
+  L.resid = take(resid ? U : 0);
+  L.J = take(resid ? U * U : 0);
+  L.g = take(n);
+  L.jx = take(3 * n);
+  L.dd = take(n);
+  L.jr = take(3 * n);
+  L.tmp3 = take(3 * n);
+  L.scal = take(SC_COUNT);
+  L.total = o;
+  *total = o;
+  return L;
+}
+
+int32_t ensure_outputs(pbad_gpu_ctx* c, long B) {
+  const long S = c->total_steps, n = c->model.n;
+  if (c->out_cap >= B) return PBAD_OK;
+  cudaFree(c->dout.q);
+  cudaFree(c->dout.energy);
+  cudaFree(c->dout.iterations);
+  cudaFree(c->dout.converged);
+  cudaFree(c->dout.accepted);
+  cudaFree(c->dout.final_value);
+  cudaFree(c->dout.final_grad_norm);
+  c->dout = Outputs{};
+  c->dout.q = dalloc<double>(B * (S + 1) * n);
+  c->dout.energy = dalloc<double>(B * (S + 1) * 2);
+  c->dout.iterations = dalloc<int>(B * S);
+  c->dout.converged = dalloc<int>(B * S);
+  c->dout.accepted = dalloc<int>(B * S);
+  c->dout.final_value = dalloc<double>(B * S);
+  c->dout.final_grad_norm = dalloc<double>(B * S);
+  if (!c->dout.q || !c->dout.energy || !c->dout.iterations || !c->dout.converged || !c->dout.accepted ||
+      !c->dout.final_value || !c->dout.final_grad_norm)
+    return fail(PBAD_E_CUDA, "cudaMalloc of rollout outputs failed (B=%ld)", B);
+  c->out_cap = B;
+  return PBAD_OK;
+}
+
+cudaStream_t pick(pbad_gpu_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+}  // namespace
+
+extern "C" {
+
+int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const pbad_sim_desc* sim,
+                        int32_t device, int32_t max_batch, pbad_gpu_ctx** out) {
+  *out = nullptr;
+  if (!model || !f || !sim) return fail(PBAD_E_ARGUMENT, "null argument");
+  if (max_batch < 1) return fail(PBAD_E_ARGUMENT, "max_batch must be >= 1");
+  if (sim->refined_bootstrap)
+    return fail(PBAD_E_UNSUPPORTED, "refined_bootstrap (RK4 Newton-Euler bootstrap) is outside the GPU path");
+  if (sim->dt <= 0.0 || sim->duration <= 0.0) return fail(PBAD_E_MODEL, "dt and duration must be positive");
+  if (sim->objective == PBAD_ENERGY_FORM && sim->order != 2)
+    return fail(PBAD_E_MODEL, "the energy objective is only defined for order 2");
+  if (sim->opt.kind == PBAD_LBFGS && sim->opt.lbfgs_memory < 1)
+    return fail(PBAD_E_UNSUPPORTED, "lbfgs_memory must be >= 1");
+  Scheme scheme;
+  int32_t rc = build_scheme(sim->order, sim->dt, &scheme);
+  if (rc) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(PBAD_E_CUDA, "no CUDA device available (the PBAD GPU path has no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(PBAD_E_CUDA, "device %d out of range (%d devices)", device, ndev);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(PBAD_E_CUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+
+  auto c = new pbad_gpu_ctx();
+  c->device = device;
+  c->model = *model;
+  c->max_batch = max_batch;
+  const pbad_gpu_model& m = c->model;
+  c->total_steps = (int)std::ceil(sim->duration / sim->dt - 1e-9);
+
+  auto up_i = [&](const std::vector<int>& v) -> const int* {
+    int* d = nullptr;
+    if (!dupload(&d, v)) return nullptr;
+    c->owned.push_back(d);
+    return d;
+  };
+  auto up_d = [&](const std::vector<double>& v) -> const double* {
+    double* d = nullptr;
+    if (!dupload(&d, v)) return nullptr;
+    c->owned.push_back(d);
+    return d;
+  };
+  DModel dm{};
+  dm.N = m.N;
+  dm.n = m.n;
+  dm.n_d2 = m.n_d2;
+  dm.parent = up_i(m.parent);
+  dm.kind = up_i(m.kind);
+  dm.dof_off = up_i(m.dof_off);
+  dm.dof_cnt = up_i(m.dof_cnt);
+  dm.d2_off = up_i(m.d2_off);
+  dm.axis = up_d(m.axis);
+  dm.offset = up_d(m.offset);
+  dm.S = up_d(m.S);
+  dm.mass = up_d(m.mass);
+  dm.sample_off = up_i(m.sample_off);
+  dm.samples = up_d(m.samples);
+  dm.weighted_mass = m.weighted_mass;
+
+  DForces df{};
+  for (int k = 0; k < 3; ++k) df.gravity[k] = f->gravity[k];
+  df.gravity_nonzero = !(std::fabs(f->gravity[0]) <= 1e-12 && std::fabs(f->gravity[1]) <= 1e-12 &&
+                         std::fabs(f->gravity[2]) <= 1e-12);
+  df.drag_d = f->drag_d;
+  df.has_contact = f->has_contact;
+  for (int k = 0; k < 3; ++k) df.normal[k] = f->plane_normal[k];
+  df.plane_offset = f->plane_offset;
+  df.d1 = f->contact_d1;
+  df.d2 = f->contact_d2;
+  df.tau_len = f->tau_len;
+  df.tau = f->tau_len > 0 ? up_d(std::vector<double>(f->tau, f->tau + f->tau_len)) : nullptr;
+  df.has_act = f->has_actuation;
+  df.act_kind = f->act_kind;
+  df.act_len = f->act_len;
+  df.act_amp = f->act_len > 0 ? up_d(std::vector<double>(f->act_amplitude, f->act_amplitude + f->act_len)) : nullptr;
+  df.act_freq = f->act_frequency_hz;
+  df.act_phase_len = f->act_phase_len;
+  df.act_phase = f->act_phase_len > 0 ? up_d(std::vector<double>(f->act_phase, f->act_phase + f->act_phase_len))
+                                      : nullptr;
+
+  DSchedule ds{};
+  ds.dt = sim->dt;
+  ds.order = sim->order;
+  ds.objective = sim->objective;
+  ds.u = sim->order - 1;
+  ds.U = m.n * ds.u;
+  ds.K1 = sim->order + 1;
+  ds.fail_limit = sim->consecutive_fail_limit;
+  ds.warm_start = sim->warm_start;
+  ds.total_steps = c->total_steps;
+  std::memcpy(ds.times, scheme.times, sizeof scheme.times);
+  std::memcpy(ds.H2, scheme.H2, sizeof scheme.H2);
+  ds.opt.kind = sim->opt.kind;
+  ds.opt.max_iters = sim->opt.max_iters;
+  ds.opt.mem = sim->opt.lbfgs_memory;
+  ds.opt.max_line_search = sim->opt.max_line_search;
+  ds.opt.grad_tol = sim->opt.grad_tol;
+  ds.opt.grad_rtol = sim->opt.grad_rtol;
+  ds.opt.ftol = sim->opt.ftol;
+  ds.opt.lm_lambda0 = sim->opt.lm_lambda0;
+  ds.opt.lm_lambda_factor = sim->opt.lm_lambda_factor;
+  ds.opt.lm_lambda_max = sim->opt.lm_lambda_max;
+  ds.opt.armijo_c1 = sim->opt.armijo_c1;
+  ds.opt.backtrack_factor = sim->opt.backtrack_factor;
+
+  long per_env = 0;
+  const Layout L = make_layout(m, sim->order, sim->objective, sim->opt.kind,
+                               sim->opt.lbfgs_memory > 0 ? sim->opt.lbfgs_memory : 1, &per_env);
+  double* ws = dalloc<double>((size_t)per_env * max_batch);
+  int* iws = dalloc<int>((size_t)IS_COUNT * max_batch);
+  if (!ws || !iws || !dm.parent || !dm.S) {
+    delete c;
+    return fail(PBAD_E_CUDA, "cudaMalloc failed (workspace %.1f MB)", per_env * 8.0 * max_batch / 1e6);
+  }
+  c->owned.push_back(ws);
+  c->owned.push_back(iws);
+  c->ka = KernelArgs{dm, df, ds, L, ws, iws, max_batch};
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    delete c;
+    return fail(PBAD_E_CUDA, "stream/event creation failed");
+  }
+  *out = c;
+  return PBAD_OK;
+}
+
+void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
+int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
+const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) { return c->ka.ws + c->ka.L.hist1 * c->ka.B; }
+
+int32_t pbad_gpu_begin(pbad_gpu_ctx* c, int32_t B, const double* d_q0, const double* d_qdot0, void* stream) {
+  if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
+  CUDA_TRY(cudaSetDevice(c->device));
+  int32_t rc = ensure_outputs(c, B);
+  if (rc) return rc;
+  c->B = B;
+  c->ka.B = B;
+  c->steps_done = 0;
+  c->device_ms = 0.0;
+  CUDA_TRY(launch_init(c->ka, d_q0, d_qdot0, c->dout, pick(c, stream)));
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
+  CUDA_TRY(cudaSetDevice(c->device));
+  const cudaStream_t s = pick(c, stream);
+  for (int k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
+    CUDA_TRY(launch_step(c->ka, c->dout, s));
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_sync_outputs(pbad_gpu_ctx* c, pbad_rollout_out* o) {
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const long B = c->B, S = c->total_steps, n = c->model.n;
+  if (o->q) CUDA_TRY(cudaMemcpy(o->q, c->dout.q, sizeof(double) * B * (S + 1) * n, cudaMemcpyDeviceToHost));
+  if (o->energy)
+    CUDA_TRY(cudaMemcpy(o->energy, c->dout.energy, sizeof(double) * B * (S + 1) * 2, cudaMemcpyDeviceToHost));
+  if (o->iterations)
+    CUDA_TRY(cudaMemcpy(o->iterations, c->dout.iterations, sizeof(int) * B * S, cudaMemcpyDeviceToHost));
+  if (o->converged)
+    CUDA_TRY(cudaMemcpy(o->converged, c->dout.converged, sizeof(int) * B * S, cudaMemcpyDeviceToHost));
+  if (o->accepted)
+    CUDA_TRY(cudaMemcpy(o->accepted, c->dout.accepted, sizeof(int) * B * S, cudaMemcpyDeviceToHost));
+  if (o->final_value)
+    CUDA_TRY(cudaMemcpy(o->final_value, c->dout.final_value, sizeof(double) * B * S, cudaMemcpyDeviceToHost));
+  if (o->final_grad_norm)
+    CUDA_TRY(cudaMemcpy(o->final_grad_norm, c->dout.final_grad_norm, sizeof(double) * B * S,
+                        cudaMemcpyDeviceToHost));
+  const int* iws = c->ka.iws;
+  if (o->n_samples) CUDA_TRY(cudaMemcpy(o->n_samples, iws + (long)IS_NSAMP * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
+  if (o->status) CUDA_TRY(cudaMemcpy(o->status, iws + (long)IS_RUN * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
+  if (o->fail_streak) CUDA_TRY(cudaMemcpy(o->fail_streak, iws + (long)IS_FAIL * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
+  if (o->n_reports) CUDA_TRY(cudaMemcpy(o->n_reports, iws + (long)IS_NREP * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
+  if (o->device_ms) o->device_ms[0] = (float)c->device_ms;
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_rollout(pbad_gpu_ctx* c, int32_t B, const double* q0, const double* qdot0,
+                         pbad_rollout_out* out) {
+  if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long n = c->model.n;
+  if (!c->d_q0) {
+    c->d_q0 = dalloc<double>((size_t)c->max_batch * n);
+    c->d_qd0 = dalloc<double>((size_t)c->max_batch * n);
+    if (!c->d_q0 || !c->d_qd0) return fail(PBAD_E_CUDA, "cudaMalloc of q0 staging failed");
+    c->owned.push_back(c->d_q0);
+    c->owned.push_back(c->d_qd0);
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_q0, q0, sizeof(double) * B * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_qd0, qdot0, sizeof(double) * B * n, cudaMemcpyHostToDevice, c->stream));
+  int32_t rc = pbad_gpu_begin(c, B, c->d_q0, c->d_qd0, nullptr);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+  rc = pbad_gpu_advance(c, c->total_steps, nullptr);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+  CUDA_TRY(cudaEventSynchronize(c->ev1));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->device_ms = ms;
+  return pbad_gpu_sync_outputs(c, out);
+}
+
+static int32_t stage_inputs(pbad_gpu_ctx* c, int32_t B, const double* history, const double* tau,
+                            const double* x, double** dh, double** dt, double** dx, long extra) {
+  const long n = c->model.n, U = c->ka.sc.U;
+  const long need = B * (2 * n + U + U) + extra;
+  if (c->in_cap < need) {
+    cudaFree(c->d_in);
+    c->d_in = dalloc<double>(need);
+    if (!c->d_in) return fail(PBAD_E_CUDA, "cudaMalloc of eval staging failed");
+    c->in_cap = need;
+  }
+  *dh = c->d_in;
+  *dt = tau ? c->d_in + B * 2 * n : nullptr;
+  *dx = c->d_in + B * (2 * n + U);
+  CUDA_TRY(cudaMemcpy(*dh, history, sizeof(double) * B * 2 * n, cudaMemcpyHostToDevice));
+  if (tau) CUDA_TRY(cudaMemcpy(*dt, tau, sizeof(double) * B * U, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(*dx, x, sizeof(double) * B * U, cudaMemcpyHostToDevice));
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_eval(pbad_gpu_ctx* c, int32_t B, const double* history, const double* tau, const double* x,
+                      int32_t want_grad, int32_t want_gn, double* value, double* grad, double* gn) {
+  if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
+  if (want_gn && c->ka.sc.opt.kind != PBAD_LM)
+    return fail(PBAD_E_ARGUMENT, "GN output needs a context created with the LM optimizer (workspace)");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long U = c->ka.sc.U;
+  double *dh, *dt, *dx;
+  int32_t rc = stage_inputs(c, B, history, tau, x, &dh, &dt, &dx, 0);
+  if (rc) return rc;
+  double* dval = dalloc<double>(B);
+  double* dgrad = dalloc<double>((size_t)B * U);
+  double* dgn = want_gn ? dalloc<double>((size_t)B * U * U) : nullptr;
+  int* derr = dalloc<int>(B);
+  KernelArgs ka = c->ka;
+  ka.B = B;
+  cudaError_t e = launch_eval(ka, dh, dt, dx, want_grad, want_gn, dval, dgrad, dgn, derr, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  std::vector<int> err(B);
+  if (e == cudaSuccess) e = cudaMemcpy(err.data(), derr, sizeof(int) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && value) e = cudaMemcpy(value, dval, sizeof(double) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && want_grad && grad) e = cudaMemcpy(grad, dgrad, sizeof(double) * B * U, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && want_gn && gn) e = cudaMemcpy(gn, dgn, sizeof(double) * B * U * U, cudaMemcpyDeviceToHost);
+  cudaFree(dval);
+  cudaFree(dgrad);
+  if (dgn) cudaFree(dgn);
+  cudaFree(derr);
+  if (e != cudaSuccess) return fail(PBAD_E_CUDA, "eval: %s", cudaGetErrorString(e));
+  for (int b = 0; b < B; ++b)
+    if (err[b]) return fail(PBAD_E_MODEL, "configuration contains a non-finite entry (env %d)", b);
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_minimize(pbad_gpu_ctx* c, int32_t B, const double* history, const double* tau,
+                          const double* x0, double* x_out, int32_t* iterations, int32_t* converged,
+                          double* final_value, double* final_grad_norm) {
+  if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long U = c->ka.sc.U;
+  double *dh, *dt, *dx;
+  int32_t rc = stage_inputs(c, B, history, tau, x0, &dh, &dt, &dx, 0);
+  if (rc) return rc;
+  double* dxo = dalloc<double>((size_t)B * U);
+  int* dit = dalloc<int>(B);
+  int* dcv = dalloc<int>(B);
+  double* dfv = dalloc<double>(B);
+  double* dgn = dalloc<double>(B);
+  int* derr = dalloc<int>(B);
+  KernelArgs ka = c->ka;
+  ka.B = B;
+  cudaError_t e = launch_minimize(ka, dh, dt, dx, dxo, dit, dcv, dfv, dgn, derr, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  std::vector<int> err(B);
+  if (e == cudaSuccess) e = cudaMemcpy(err.data(), derr, sizeof(int) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && x_out) e = cudaMemcpy(x_out, dxo, sizeof(double) * B * U, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && iterations) e = cudaMemcpy(iterations, dit, sizeof(int) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && converged) e = cudaMemcpy(converged, dcv, sizeof(int) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && final_value) e = cudaMemcpy(final_value, dfv, sizeof(double) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && final_grad_norm) e = cudaMemcpy(final_grad_norm, dgn, sizeof(double) * B, cudaMemcpyDeviceToHost);
+  cudaFree(dxo);
+  cudaFree(dit);
+  cudaFree(dcv);
+  cudaFree(dfv);
+  cudaFree(dgn);
+  cudaFree(derr);
+  if (e != cudaSuccess) return fail(PBAD_E_CUDA, "minimize: %s", cudaGetErrorString(e));
+  for (int b = 0; b < B; ++b) {
+    if (err[b] == 2) return fail(PBAD_E_ARGUMENT, "objective is non-finite at the initial point");
+    if (err[b]) return fail(PBAD_E_MODEL, "configuration contains a non-finite entry");
+  }
+  return PBAD_OK;
+}
+
+}  // extern "C"

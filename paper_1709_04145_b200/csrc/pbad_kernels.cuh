@@ -1,0 +1,105 @@
+// pbad_kernels.cuh -- device-side data layout shared by the host launcher
+// and the kernels.  One CUDA thread owns one environment (trajectory);
+// per-environment arrays are stored structure-of-arrays (element k of env e
+// at base[k * B + e]) so a warp's 32 envs touch 32 consecutive doubles.
+#pragma once
+
+#include <cstdint>
+
+namespace pbad_gpu {
+
+struct DModel {
+  int N, n, n_d2;
+  const int* parent;
+  const int* kind;
+  const int* dof_off;
+  const int* dof_cnt;
+  const int* d2_off;
+  const double* axis;    // [N][3]
+  const double* offset;  // [N][16]
+  const double* S;       // [N][16]
+  const double* mass;    // [N]
+  const int* sample_off; // [N+1]
+  const double* samples; // [*][3]
+  double weighted_mass;  // WeightedBody::make with unit weights (adjoint.cpp:29-41)
+};
+
+struct DForces {
+  double gravity[3];
+  int gravity_nonzero;  // !gravity.isZero()
+  double drag_d;
+  int has_contact;
+  double normal[3];
+  double plane_offset, d1, d2;
+  int tau_len;
+  const double* tau;  // device
+  int has_act, act_kind, act_len;
+  const double* act_amp;  // device
+  double act_freq;
+  int act_phase_len;
+  const double* act_phase;  // device
+};
+
+struct DOpt {
+  int kind, max_iters, mem, max_line_search;
+  double grad_tol, grad_rtol, ftol, lm_lambda0, lm_lambda_factor, lm_lambda_max, armijo_c1,
+      backtrack_factor;
+};
+
+struct DSchedule {
+  double dt;
+  int order, objective, u, U, K1;
+  int fail_limit, warm_start, total_steps;
+  double times[9];
+  double H2[81];  // column-major (K+1)^2
+  DOpt opt;
+};
+
+// Offsets (in per-env doubles) of every array in the double workspace.
+struct Layout {
+  long hist0, hist1, x, grad, cand, dir, tmp, step, evgrad, hs, hy, hsy, alpha, tau;
+  long hw0, hw1;                 // history world transforms [N*16]
+  long gn, damped, evgn;         // LM (U*U)
+  long pass;                     // u passes back to back
+  long pass_stride;              // doubles per pass
+  long p_value, p_d1, p_d2, p_world, p_lever;  // offsets inside a pass
+  long seeds, cot, adj;          // [N*16]
+  long potgrad, potgn, pothess, ab, fh, resid, J, g, jx, dd, jr, tmp3;
+  long scal;                     // scalar slots
+  long total;
+};
+enum {
+  SC_VALUE = 0,
+  SC_GRAD0,
+  SC_LAMBDA,
+  SC_HISTCONST,
+  SC_EVVALUE,
+  SC_COUNT
+};
+// int workspace slots (per env)
+enum {
+  IS_STATUS = 0,   // solver status
+  IS_ITERS,
+  IS_STAG,
+  IS_ACC,
+  IS_HSTART,
+  IS_HCOUNT,
+  IS_FAIL,         // fail streak
+  IS_STEP,         // PBAD step counter
+  IS_RUN,          // trajectory status PBAD_TRAJ_*
+  IS_NSAMP,
+  IS_NREP,
+  IS_COUNT
+};
+
+struct Outputs {
+  double* q;        // [B][S+1][n]
+  double* energy;   // [B][S+1][2]
+  int* iterations;  // [B][S]
+  int* converged;
+  int* accepted;
+  double* final_value;
+  double* final_grad_norm;
+};
+
+}  // namespace pbad_gpu

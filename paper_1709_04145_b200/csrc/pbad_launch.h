@@ -1,0 +1,30 @@
+// pbad_launch.h -- host-callable launchers for the kernels in pbad_kernels.cu
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pbad_kernels.cuh"
+
+namespace pbad_gpu {
+
+struct KernelArgs {
+  DModel m;
+  DForces f;
+  DSchedule sc;
+  Layout L;
+  double* ws;
+  int* iws;
+  long B;
+};
+
+cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
+                        cudaStream_t s);
+cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s);
+cudaError_t launch_eval(const KernelArgs& a, const double* hist, const double* tau, const double* x,
+                        int want_grad, int want_gn, double* value, double* grad, double* gn, int* err,
+                        cudaStream_t s);
+cudaError_t launch_minimize(const KernelArgs& a, const double* hist, const double* tau, const double* x0,
+                            double* xout, int* iters, int* conv, double* fval, double* gnorm, int* err,
+                            cudaStream_t s);
+
+}  // namespace pbad_gpu
