@@ -9,8 +9,8 @@
  *
  *   product    C(i,j) = a(i,0)*b(0,j), then acc = fma(a(i,k), b(k,j), acc)
  *              for k = 1..K-1 (inner index ascending)
- *   ddot       A.cwiseProduct(B).sum() = same fma chain over the
- *              column-major linear index (math_types.hpp:33-35)
+ *   ddot       A.cwiseProduct(B).sum() (math_types.hpp:33-35): per-row
+ *              fma chains over the columns, combined ((r0+r1)+r2)+r3
  *   trace      ((m00 + m11) + m22) + m33
  *   fixed dot  Vec3/Vec4 dot/squaredNorm: fma chain, index ascending
  *   VecX dot   32 interleaved fma partial sums (i mod 32), then a
@@ -116,9 +116,15 @@ static inline void m4_addto(pbo_m4* A, const pbo_m4* B) {
 }
 /* ddot(A, B) = A.cwiseProduct(B).sum(), math_types.hpp:33-35 */
 static inline double m4_ddot(const pbo_m4* A, const pbo_m4* B) {
-  double acc = A->a[0] * B->a[0];
-  for (int e = 1; e < 16; ++e) acc = fma(A->a[e], B->a[e], acc);
-  return acc;
+  double rs[4];
+  for (int r = 0; r < 4; ++r) {
+    double acc = M4E(*A, r, 0) * M4E(*B, r, 0);
+    acc = fma(M4E(*A, r, 1), M4E(*B, r, 1), acc);
+    acc = fma(M4E(*A, r, 2), M4E(*B, r, 2), acc);
+    acc = fma(M4E(*A, r, 3), M4E(*B, r, 3), acc);
+    rs[r] = acc;
+  }
+  return ((rs[0] + rs[1]) + rs[2]) + rs[3];
 }
 static inline double m4_trace(const pbo_m4* A) {
   return ((A->a[0] + A->a[5]) + A->a[10]) + A->a[15];

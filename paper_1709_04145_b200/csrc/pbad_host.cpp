@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -429,6 +430,10 @@ struct pbad_gpu_ctx {
   cudaStream_t stream = nullptr;
   pbad_gpu_model model;
   KernelArgs ka{};
+  ChainArgs ca{};
+  bool chain = false;      // rollouts use the quad chain kernels
+  long v1_per_env = 0;     // general-kernel workspace size (allocated lazily)
+  long chain_per_env = 0;
   std::vector<void*> owned;  // device allocations freed at destroy
   long max_batch = 0;
   long B = 0;  // current batch
@@ -520,6 +525,71 @@ Layout make_layout(const pbad_gpu_model& m, int order, int objective, int opt_ki
   L.total = o;
   *total = o;
   return L;
+}
+
+ChainLayout make_chain_layout(const pbad_gpu_model& m, int mem, long B, long* total) {
+  ChainLayout L{};
+  const long N = m.N, n4 = (m.n + 3) / 4;
+  const long link = N * B * 16, vec = n4 * B * 4;
+  long o = 0;
+  auto take = [&](long cnt) {
+    const long at = o;
+    o += cnt;
+    return at;
+  };
+  L.tk = take(link);
+  L.tk1 = take(link);
+  L.seed = take(link);
+  L.lev = take(link);
+  L.lmat = take(link);
+  L.vstride = vec;
+  L.h0 = take(vec);
+  L.h1 = take(vec);
+  L.x = take(vec);
+  L.g = take(vec);
+  L.cand = take(vec);
+  L.dir = take(vec);
+  L.q = take(vec);
+  L.evg = take(vec);
+  L.tau = take(vec);
+  L.hs = take((mem + 1) * vec);
+  L.hy = take((mem + 1) * vec);
+  L.hsy = take((mem + 1) * B);
+  L.histc = take(B);
+  L.total = o;
+  *total = o;
+  return L;
+}
+
+// The quad chain kernels cover serial hinge chains, energy form, L-BFGS,
+// gravity / constant or sinusoidal actuation (no drag or contact).
+bool chain_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
+  if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
+  if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2 || sim->opt.kind != PBAD_LBFGS) return false;
+  if (sim->opt.lbfgs_memory < 1 || sim->opt.lbfgs_memory > chain_max_memory()) return false;
+  if (f->drag_d > 0.0) return false;
+  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
+  for (int i = 0; i < m.N; ++i) {
+    if (m.kind[i] != PBAD_HINGE) return false;
+    if (m.parent[i] != i - 1) return false;
+  }
+  return true;
+}
+
+bool ensure_v1(pbad_gpu_ctx* c) {
+  if (c->ka.ws) return true;
+  double* ws = dalloc<double>((size_t)c->v1_per_env * c->max_batch);
+  int* iws = dalloc<int>((size_t)IS_COUNT * c->max_batch);
+  if (!ws || !iws) {
+    cudaFree(ws);
+    cudaFree(iws);
+    return false;
+  }
+  c->owned.push_back(ws);
+  c->owned.push_back(iws);
+  c->ka.ws = ws;
+  c->ka.iws = iws;
+  return true;
 }
 
 int32_t ensure_outputs(pbad_gpu_ctx* c, long B) {
@@ -662,15 +732,32 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   long per_env = 0;
   const Layout L = make_layout(m, sim->order, sim->objective, sim->opt.kind,
                                sim->opt.lbfgs_memory > 0 ? sim->opt.lbfgs_memory : 1, &per_env);
-  double* ws = dalloc<double>((size_t)per_env * max_batch);
-  int* iws = dalloc<int>((size_t)IS_COUNT * max_batch);
-  if (!ws || !iws || !dm.parent || !dm.S) {
+  c->v1_per_env = per_env;
+  c->ka = KernelArgs{dm, df, ds, L, nullptr, nullptr, max_batch};
+  c->chain = chain_eligible(m, f, sim);
+  if (!dm.parent || !dm.S) {
+    delete c;
+    return fail(PBAD_E_CUDA, "cudaMalloc of the model failed");
+  }
+  if (c->chain) {
+    long tot = 0;
+    const ChainLayout CL = make_chain_layout(m, sim->opt.lbfgs_memory, max_batch, &tot);
+    double* cw = dalloc<double>((size_t)tot);
+    int* ci = dalloc<int>((size_t)IS_COUNT * max_batch);
+    if (!cw || !ci) {
+      cudaFree(cw);
+      cudaFree(ci);
+      delete c;
+      return fail(PBAD_E_CUDA, "cudaMalloc failed (chain workspace %.1f MB)", tot * 8.0 / 1e6);
+    }
+    c->owned.push_back(cw);
+    c->owned.push_back(ci);
+    c->chain_per_env = tot / max_batch;
+    c->ca = ChainArgs{dm, df, ds, CL, cw, ci, max_batch};
+  } else if (!ensure_v1(c)) {
     delete c;
     return fail(PBAD_E_CUDA, "cudaMalloc failed (workspace %.1f MB)", per_env * 8.0 * max_batch / 1e6);
   }
-  c->owned.push_back(ws);
-  c->owned.push_back(iws);
-  c->ka = KernelArgs{dm, df, ds, L, ws, iws, max_batch};
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
     delete c;
@@ -682,7 +769,10 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
 
 void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
-const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) { return c->ka.ws + c->ka.L.hist1 * c->ka.B; }
+const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) {
+  // chain path: quad-interleaved [n/4][B][4]; general path: [n][B]
+  return c->chain ? c->ca.cw + c->ca.L.h1 : c->ka.ws + c->ka.L.hist1 * c->ka.B;
+}
 
 int32_t pbad_gpu_begin(pbad_gpu_ctx* c, int32_t B, const double* d_q0, const double* d_qdot0, void* stream) {
   if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
@@ -691,9 +781,11 @@ int32_t pbad_gpu_begin(pbad_gpu_ctx* c, int32_t B, const double* d_q0, const dou
   if (rc) return rc;
   c->B = B;
   c->ka.B = B;
+  c->ca.B = B;
   c->steps_done = 0;
   c->device_ms = 0.0;
-  CUDA_TRY(launch_init(c->ka, d_q0, d_qdot0, c->dout, pick(c, stream)));
+  if (c->chain) CUDA_TRY(launch_chain_init(c->ca, d_q0, d_qdot0, c->dout, pick(c, stream)));
+  else CUDA_TRY(launch_init(c->ka, d_q0, d_qdot0, c->dout, pick(c, stream)));
   return PBAD_OK;
 }
 
@@ -701,7 +793,7 @@ int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
   CUDA_TRY(cudaSetDevice(c->device));
   const cudaStream_t s = pick(c, stream);
   for (int k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
-    CUDA_TRY(launch_step(c->ka, c->dout, s));
+    CUDA_TRY(c->chain ? launch_chain_step(c->ca, c->dout, s) : launch_step(c->ka, c->dout, s));
   return PBAD_OK;
 }
 
@@ -724,7 +816,7 @@ int32_t pbad_gpu_sync_outputs(pbad_gpu_ctx* c, pbad_rollout_out* o) {
   if (o->final_grad_norm)
     CUDA_TRY(cudaMemcpy(o->final_grad_norm, c->dout.final_grad_norm, sizeof(double) * B * S,
                         cudaMemcpyDeviceToHost));
-  const int* iws = c->ka.iws;
+  const int* iws = c->chain ? c->ca.ci : c->ka.iws;
   if (o->n_samples) CUDA_TRY(cudaMemcpy(o->n_samples, iws + (long)IS_NSAMP * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
   if (o->status) CUDA_TRY(cudaMemcpy(o->status, iws + (long)IS_RUN * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
   if (o->fail_streak) CUDA_TRY(cudaMemcpy(o->fail_streak, iws + (long)IS_FAIL * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
@@ -785,6 +877,7 @@ int32_t pbad_gpu_eval(pbad_gpu_ctx* c, int32_t B, const double* history, const d
   if (want_gn && c->ka.sc.opt.kind != PBAD_LM)
     return fail(PBAD_E_ARGUMENT, "GN output needs a context created with the LM optimizer (workspace)");
   CUDA_TRY(cudaSetDevice(c->device));
+  if (!ensure_v1(c)) return fail(PBAD_E_CUDA, "cudaMalloc of the evaluation workspace failed");
   const long U = c->ka.sc.U;
   double *dh, *dt, *dx;
   int32_t rc = stage_inputs(c, B, history, tau, x, &dh, &dt, &dx, 0);
@@ -817,6 +910,7 @@ int32_t pbad_gpu_minimize(pbad_gpu_ctx* c, int32_t B, const double* history, con
                           double* final_value, double* final_grad_norm) {
   if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
   CUDA_TRY(cudaSetDevice(c->device));
+  if (!ensure_v1(c)) return fail(PBAD_E_CUDA, "cudaMalloc of the evaluation workspace failed");
   const long U = c->ka.sc.U;
   double *dh, *dt, *dx;
   int32_t rc = stage_inputs(c, B, history, tau, x0, &dh, &dt, &dx, 0);

@@ -92,6 +92,16 @@ enum {
   IS_COUNT
 };
 
+// Chain-path workspace (pbad_chain.cu): link arrays [N][B][16] (row r at
+// +4r) and quad-interleaved vectors (element k at ((k>>2)*B + e)*4 + k%4).
+struct ChainLayout {
+  long tk, tk1, seed, lev, lmat;            // link arrays
+  long h0, h1, x, g, cand, dir, q, evg, tau; // vectors
+  long hs, hy, vstride;                      // L-BFGS ring, vstride per vector
+  long hsy, histc;                           // [cap][B], [B]
+  long total;
+};
+
 struct Outputs {
   double* q;        // [B][S+1][n]
   double* energy;   // [B][S+1][2]

@@ -17,6 +17,21 @@ struct KernelArgs {
   long B;
 };
 
+struct ChainArgs {
+  DModel m;
+  DForces f;
+  DSchedule sc;
+  ChainLayout L;
+  double* cw;
+  int* ci;
+  long B;
+};
+
+cudaError_t launch_chain_init(const ChainArgs& a, const double* q0, const double* qdot0, const Outputs& out,
+                              cudaStream_t s);
+cudaError_t launch_chain_step(const ChainArgs& a, const Outputs& out, cudaStream_t s);
+int chain_max_memory();
+
 cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
                         cudaStream_t s);
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s);

@@ -6,7 +6,8 @@
 // contract") and compiles everything with --fmad=false so the only fused
 // multiply-adds are the explicit fma() calls below:
 //   product  C(i,j) = a(i,0)*b(0,j); acc = fma(a(i,k), b(k,j), acc), k ascending
-//   ddot     fma chain over the column-major index (math_types.hpp:33-35)
+//   ddot     per-row fma chains over the columns, ((r0+r1)+r2)+r3
+//            (math_types.hpp:33-35)
 //   trace    ((m00 + m11) + m22) + m33
 //   Vec3/4   dot = fma chain;  VecX dot = 32 interleaved partials + tree
 //   sin/cos  pbad_sincos (rint + fma Cody-Waite + fdlibm kernels)
@@ -132,11 +133,24 @@ PBAD_HD void addto(M4& A, const M4& B) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) A.a[e] = A.a[e] + B.a[e];
 }
+// one row of ddot: fma chain over the 4 columns
+PBAD_HD double ddot_row(const double* a, const double* b) {
+  double acc = a[0] * b[0];
+  acc = fma(a[1], b[1], acc);
+  acc = fma(a[2], b[2], acc);
+  return fma(a[3], b[3], acc);
+}
 PBAD_HD double ddot(const M4& A, const M4& B) {
-  double acc = A.a[0] * B.a[0];
+  double rs[4];
 #pragma unroll
-  for (int e = 1; e < 16; ++e) acc = fma(A.a[e], B.a[e], acc);
-  return acc;
+  for (int r = 0; r < 4; ++r) {
+    double acc = A.a[r] * B.a[r];
+    acc = fma(A.a[r + 4], B.a[r + 4], acc);
+    acc = fma(A.a[r + 8], B.a[r + 8], acc);
+    acc = fma(A.a[r + 12], B.a[r + 12], acc);
+    rs[r] = acc;
+  }
+  return ((rs[0] + rs[1]) + rs[2]) + rs[3];
 }
 PBAD_HD double trace(const M4& A) { return ((A.a[0] + A.a[5]) + A.a[10]) + A.a[15]; }
 
