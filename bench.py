@@ -1,0 +1,378 @@
+#!/usr/bin/env python3
+"""PBAD hot-path benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A bench "step" is one PBAD timestep (stepper.cpp:83-147) for the whole batch:
+one k_chain_step (or general k_step) launch that runs begin_step, the
+optimiser to completion and finish_step for every environment.  `value` is
+device-timed simulated env-steps/s over all ranks (inputs resident in HBM),
+`e2e` the same metric through the public C ABI call with host buffers
+(pbad_gpu_rollout: H2D of q0/qdot0, D2H of the trajectory).  Multi-GPU is
+weak scaling: every rank owns its own shard of `batch_per_gpu` independent
+environments (no collective on the step path; one NCCL gather afterwards).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated env-steps/sec (batch×steps/s, device-timed) vs N links at 1/2/4/8 B200"
+UNIT = "env-steps/s"
+
+# BASELINE.json configs / SURVEY.md §8(d)
+CONFIGS = {
+    "C1": dict(scene="single_hinge", links=10, dt=0.01, batch=1024, opt="lbfgs", seed=0, lo=0.0, hi=0.0,
+               desc="C1: 10-link planar single-hinge chain, PBAD energy form, L-BFGS, dt=0.01 (x1024 replicas)"),
+    "C2": dict(scene="single_hinge", links=50, dt=0.033, batch=1024, opt="lbfgs", seed=0, lo=-0.3, hi=0.3,
+               desc="C2: 1024 x 50-link single-hinge chains, L-BFGS, dt=0.033"),
+    "C3": dict(scene="chain", links=100, dt=0.1, batch=4096, opt="lbfgs", seed=1, lo=-0.3, hi=0.3,
+               desc="C3: 4096 x 200-DOF serial hinge chains (make_chain_scene(100)), L-BFGS, dt=0.1"),
+    "C4": dict(scene="humanoid", links=18, dt=0.01, batch=4096, opt="lm", seed=2, lo=-0.1, hi=0.1,
+               desc="C4: 4096 x 41-DOF humanoid trees, LM (Gauss-Newton + Cholesky), dt=0.01"),
+}
+
+
+def build_scene(cfg):
+    from paper_1709_04145_b200 import scenes
+    if cfg["scene"] == "chain":
+        return scenes.make_chain_scene(cfg["links"])
+    if cfg["scene"] == "single_hinge":
+        return scenes.make_single_hinge_chain_scene(cfg["links"])
+    return scenes.make_humanoid_scene()
+
+
+def initial_states(cfg, scene, n, first_env, count):
+    """std::mt19937(seed) env-major draws (benchmark.cpp:278-288) for envs
+    [first_env, first_env + count) of the global batch."""
+    from paper_1709_04145_b200.scenes import mt19937_uniform
+    if cfg["scene"] == "humanoid":
+        draws = mt19937_uniform(cfg["seed"], (first_env + count) * (n - 6), cfg["lo"], cfg["hi"])
+        q = np.tile(scene.q0, (count, 1))
+        q[:, 6:] = draws[first_env * (n - 6):].reshape(count, n - 6)
+        return q
+    if cfg["hi"] == cfg["lo"]:
+        return np.tile(scene.q0, (count, 1))
+    draws = mt19937_uniform(cfg["seed"], (first_env + count) * n, cfg["lo"], cfg["hi"])
+    return draws[first_env * n:].reshape(count, n)
+
+
+def sim_config(cfg, steps, fail_limit):
+    from paper_1709_04145_b200.types import OptimizerKind, SimConfig
+    sim = SimConfig(dt=cfg["dt"], duration=cfg["dt"] * steps, consecutive_fail_limit=fail_limit)
+    sim.optimizer.kind = OptimizerKind.lbfgs if cfg["opt"] == "lbfgs" else OptimizerKind.lm
+    return sim
+
+
+def flops_per_env_step(cfg, model, iters, accepted):
+    """SURVEY.md §8(d) canonical FP64 FLOPs (FMA = 2): iterations x per-iteration
+    cost + per-step overhead (construction eval, history precompute, energy audit)."""
+    N, n = model.link_count(), model.total_dofs
+    overhead = N * 481 + 240 * N + 205 * N
+    if cfg["opt"] == "lbfgs":
+        per_iter = N * (307 + 174) + n * (8 * 8 + 12)
+        return iters * per_iter + overhead
+    # LM: (2/3)n^3 + 2n^2 + Eonly + a (grad + GN)
+    depth_dofs = []
+    for i in range(N):
+        d, k = 0, i
+        while k >= 0:
+            d += model.dof_count(k)
+            k = model.parent(k)
+        depth_dofs.append(model.dof_count(i) * d)
+    P = sum(depth_dofs)
+    rej = (2.0 / 3.0) * n ** 3 + 2 * n * n + 307 * N
+    acc_extra = (120 * N + 54 * n) + (320 * N + 24 * P)
+    return iters * rej + accepted * acc_extra + overhead + 320 * N + 24 * P
+
+
+def measured_fp64_peak(device):
+    import ctypes as C
+    lib = C.CDLL(os.path.join(ROOT, "paper_1709_04145_b200", "libpbad_peak.so"))
+    lib.pbad_peak_fp64.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    t, ms, lat = C.c_double(), C.c_double(), C.c_double()
+    rc = lib.pbad_peak_fp64(device, C.byref(t), C.byref(ms), C.byref(lat))
+    if rc != 0:
+        return None, None
+    return t.value, lat.value
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"pbad_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(cfg, scene, model_links, n, steps=1, sample=None):
+    """The CPU oracle (plain-C restatement of the reference path, `kind: port`)
+    on the host cores: batch_simulate over a bounded sample of the workload."""
+    import oracle
+    cores = os.cpu_count() or 1
+    sample = sample or max(cores, min(cfg["batch"], cores * 4))
+    forces = scene.forces()
+    mo = oracle.Model(model_links)
+    q0 = initial_states(cfg, scene, n, 0, sample)
+    sims = []
+    for b in range(sample):
+        s = sim_config(cfg, steps, 1 << 30)
+        s.q0 = q0[b]
+        s.qdot0 = np.zeros(n)
+        sims.append(s)
+    t = time.perf_counter()
+    trs = oracle.batch_simulate(mo, forces, sims, workers=cores)
+    el = time.perf_counter() - t
+    done = sum(tr.n_samples - 1 for tr in trs)
+    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{sample} envs x {steps} step(s) of {cfg['desc'].split(':')[0]}, "
+                      f"{cores} threads, {el:.2f} s",
+            "seconds": el}
+
+
+def dist_setup(ngpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def run_reference(args, cfg):
+    world, rank, local = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return
+    scene = build_scene(cfg)
+    from paper_1709_04145_b200.types import LinkSpec  # noqa: F401
+    import oracle
+    mo = oracle.Model(scene.links)
+    n = mo.n_dofs
+    cb = cpu_baseline(cfg, scene, scene.links, n, steps=max(1, min(args.steps, 2)))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, args, world),
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("reference arm = the CPU oracle (C restatement of the reference hot path, oracle/); the "
+                 "reference C++ itself needs Eigen3, absent in this image (see DESIGN.md)"),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(cfg, args, world):
+    return {"workload": cfg["desc"], "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world,
+            "n_links": cfg["links"] * (2 if cfg["scene"] == "chain" else 1), "dt": cfg["dt"],
+            "optimizer": cfg["opt"], "max_iters": 512, "consecutive_fail_limit": "unbounded (bench)",
+            "parallelism": f"dp{world} (independent env shards, weak scaling)",
+            "cache": "per-env solver state (~100 KB/env) > L2: inputs larger than L2, no flush needed"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("PBAD_BENCH_CONFIG", "C3"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    world, rank, local = dist_setup(args.gpus)
+    import torch
+    torch.cuda.set_device(local)
+    from paper_1709_04145_b200 import api, build as pbuild
+    if not os.path.exists(pbuild.LIB):
+        pbuild.build()
+
+    scene = build_scene(cfg)
+    model = api.build_model(scene.links)
+    n = model.total_dofs
+    B = cfg["batch"]
+    W, K = args.warmup, args.steps
+    total = W + K
+    sim = sim_config(cfg, total, 1 << 30)
+    ctx = api.GpuContext(model, scene.forces(), sim, device=local, max_batch=B)
+    q0 = initial_states(cfg, scene, n, rank * B, B)
+    dq0 = torch.from_numpy(q0).to(f"cuda:{local}")
+    dqd = torch.zeros_like(dq0)
+    # a dedicated stream: the legacy default stream has handle 0, which the C
+    # ABI reads as "the context's own stream"
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+
+    # warm-up steps (untimed)
+    ctx.begin(B, dq0.data_ptr(), dqd.data_ptr(), sh)
+    ctx.advance(W, sh)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.advance(K, sh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    out = ctx.sync_outputs(want_q=False, want_energy=False)
+    iters = out["iterations"][:, W:W + K]
+    acc = out["accepted"][:, W:W + K]
+    st = out["status"]
+
+    # NCCL gather of the final states (outside the timed region)
+    gather_ms = None
+    if world > 1:
+        import ctypes
+        fin = torch.empty((B, n), dtype=torch.float64, device=f"cuda:{local}")
+        host = ctx.sync_outputs(want_q=True, want_energy=False)["q"][:, -1, :]
+        fin.copy_(torch.from_numpy(np.ascontiguousarray(host)))
+        allq = torch.empty((world * B, n), dtype=torch.float64, device=f"cuda:{local}")
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        torch.distributed.all_gather_into_tensor(allq, fin)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - g0) * 1e3
+
+    # FLOP accounting for the roofline (per env, summed, this rank's launches)
+    fl = 0.0
+    for b in range(B):
+        fl += sum(flops_per_env_step(cfg, model, int(iters[b, s]), int(acc[b, s])) for s in range(K))
+    if world > 1:
+        t = torch.tensor([fl], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t)
+        fl = float(t.item())
+
+    value = world * B * K / (ms / 1e3)
+
+    # end-to-end: the public rollout call with host buffers (H2D + kernels + D2H)
+    e2e = None
+    if rank == 0:
+        sim2 = sim_config(cfg, K, 1 << 30)
+        ctx2 = api.GpuContext(model, scene.forces(), sim2, device=local, max_batch=B)
+        pq0 = torch.from_numpy(np.ascontiguousarray(q0)).pin_memory().numpy()
+        pqd0 = torch.zeros(q0.shape, dtype=torch.float64).pin_memory().numpy()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bufs = ctx2.rollout(pq0, pqd0, want_q=True, want_energy=True, pinned=True)
+        el = time.perf_counter() - t0
+        h2d = 2 * q0.nbytes
+        d2h = sum(v.nbytes for v in bufs.values() if v is not None)
+        e2e = {"value": B * K / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d / K),
+               "d2h_bytes_per_step": int(d2h / K), "note": "pbad_gpu_rollout (C ABI) with pinned host q0/qdot0 in and trajectory + reports out, wall clock, rank 0"}
+        del ctx2
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+
+    peak, lat = measured_fp64_peak(local)
+    achieved = fl / (ms / 1e3) / 1e12 / world  # per GPU
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"{args.config}_dram_per_launch.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    cb = None
+    if not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(cfg, scene, scene.links, n)
+            cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # the oracle must never block the GPU line
+            cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": config_block(cfg, args, world),
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if peak else None, "traffic": traffic,
+                     "peak_source": "measured DFMA microbenchmark (paper_1709_04145_b200/csrc/pbad_peak.cu) on this GPU",
+                     "flops_model": "SURVEY.md 8(d) canonical FP64 FLOPs per L-BFGS/LM iteration + per-step overhead",
+                     "dfma_latency_cycles": lat},
+        "cpu_baseline": cb,
+        "e2e": e2e,
+        "gpu_launches": K,
+        "clocks": clk,
+        "mean_iterations_per_step": float(iters.mean()),
+        "trajectories_ok": int(np.sum((st == 0) | (st == 4))),
+        "gather_ms": gather_ms,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

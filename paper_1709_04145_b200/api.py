@@ -278,16 +278,25 @@ class GpuContext:
         except Exception:
             pass
 
-    def _out_struct(self, B: int, want_q=True, want_energy=True):
+    def _out_struct(self, B: int, want_q=True, want_energy=True, pinned=False):
         S, n = self.total_steps, self.n
+        if pinned:
+            import torch
+
+            def z(shape, dt=np.float64):
+                tdt = {np.float64: torch.float64, np.int32: torch.int32, np.float32: torch.float32}[dt]
+                return torch.zeros(shape, dtype=tdt).pin_memory().numpy()
+        else:
+            def z(shape, dt=np.float64):
+                return np.zeros(shape, dt)
         bufs = dict(
-            q=np.zeros((B, S + 1, n)) if want_q else None,
-            energy=np.zeros((B, S + 1, 2)) if want_energy else None,
-            iterations=np.zeros((B, S), np.int32), converged=np.zeros((B, S), np.int32),
-            accepted=np.zeros((B, S), np.int32), final_value=np.zeros((B, S)),
-            final_grad_norm=np.zeros((B, S)), n_samples=np.zeros(B, np.int32), status=np.zeros(B, np.int32),
-            fail_streak=np.zeros(B, np.int32), n_reports=np.zeros(B, np.int32),
-            device_ms=np.zeros(1, np.float32))
+            q=z((B, S + 1, n)) if want_q else None,
+            energy=z((B, S + 1, 2)) if want_energy else None,
+            iterations=z((B, S), np.int32), converged=z((B, S), np.int32),
+            accepted=z((B, S), np.int32), final_value=z((B, S)),
+            final_grad_norm=z((B, S)), n_samples=z(B, np.int32), status=z(B, np.int32),
+            fail_streak=z(B, np.int32), n_reports=z(B, np.int32),
+            device_ms=z(1, np.float32))
         o = _lib.RolloutOut()
         for k, v in bufs.items():
             if v is None:
@@ -300,11 +309,11 @@ class GpuContext:
                 setattr(o, k, v.ctypes.data_as(C.POINTER(C.c_float)))
         return o, bufs
 
-    def rollout(self, q0, qdot0, want_q=True, want_energy=True) -> Dict[str, np.ndarray]:
+    def rollout(self, q0, qdot0, want_q=True, want_energy=True, pinned=False) -> Dict[str, np.ndarray]:
         q0 = _f64(q0)
         qdot0 = _f64(qdot0)
         B = q0.shape[0]
-        o, bufs = self._out_struct(B, want_q, want_energy)
+        o, bufs = self._out_struct(B, want_q, want_energy, pinned)
         check(_lib.load().pbad_gpu_rollout(self._h, B, _p(q0), _p(qdot0), C.byref(o)))
         return bufs
 

@@ -18,6 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libpbad_gpu.so")
+PEAK_LIB = os.path.join(PKG, "libpbad_peak.so")
 BUILD = os.path.join(ROOT, "build")
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
@@ -69,6 +70,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             objs.append(o)
         if force or _stale(LIB, objs):
             _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], log)
+        # FP64 microbenchmark used as the roofline denominator (bench.py)
+        ps = os.path.join(CSRC, "pbad_peak.cu")
+        if force or _stale(PEAK_LIB, [ps]):
+            _run([NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", ps, "-o", PEAK_LIB], log)
     if verbose:
         print(open(os.path.join(BUILD, "build.log")).read())
     return LIB

@@ -102,17 +102,153 @@ __device__ __forceinline__ void row_mul_bt(const double* a, const M4& B, double*
   }
 }
 
-// hinge joint transform L = offset * motion(R(axis*q)) and dL/dq
-// (kinematics.cpp:119-129), full canonical 4x4 products
-__device__ __forceinline__ void hinge_jet(const Q& Z, int i, double qi, M4* value, M4* d1, bool want_d1) {
+// --- per-link joint algebra ----------------------------------------------
+// A link's local transform L = offset * [R(axis*q) 0; 0 1] and its
+// derivative d1 = offset * embed([axis]x R) (kinematics.cpp:119-129).
+// jkind 1/2/3: axis exactly e_x/e_y/e_z and offset rotation block exactly I.
+// Then R = I + A K + B K^2 has two free entries (c, s) and every canonical
+// product below reduces to its non-zero terms: the dropped terms are
+// fma(x, +-0, acc) with finite x, which leave the value unchanged.
+struct LinkJet {
+  int jk;
+  double c, s;   // specialised: R entries
+  double t[3];   // offset translation
+  M4 L, d1;      // general: full matrices
+};
+
+// rotation_coeffs A, B (kinematics.cpp:20-45) for a hinge of angle q about
+// a unit axis: n = |q|, k2 = q*q is -K^2's diagonal entry.
+__device__ __forceinline__ void hinge_cs(double q, double* c, double* s) {
+  const double k2 = q * q;
+  const double n = sqrt(k2);
+  const double n2 = n * n;
+  double A, B;
+  if (n < 1e-4) {
+    const double n4 = n2 * n2;
+    A = 1.0 - n2 / 6.0 + n4 / 120.0;
+    B = 0.5 - n2 / 24.0 + n4 / 720.0;
+  } else {
+    double sn, co;
+    pbad_sincos(n, &sn, &co);
+    A = sn / n;
+    B = (1.0 - co) / n2;
+  }
+  *s = A * q;           // (0 + A*K_ab) + B*(+-0)
+  *c = 1.0 - B * k2;    // (1 + A*0) + B*(-k2)
+}
+
+__device__ __forceinline__ void link_jet(const Q& Z, int i, double qi, bool want_d1, LinkJet* J) {
+  J->jk = __ldg(Z.m->jkind + i);
+  const double* off = Z.m->offset + 16 * i;
+  if (J->jk) {
+    hinge_cs(qi, &J->c, &J->s);
+    J->t[0] = __ldg(off + 12);
+    J->t[1] = __ldg(off + 13);
+    J->t[2] = __ldg(off + 14);
+    return;
+  }
   const double* ax = Z.m->axis + 3 * i;
   const double a0 = __ldg(ax), a1 = __ldg(ax + 1), a2 = __ldg(ax + 2);
-  M4 off;
+  M4 o;
 #pragma unroll
-  for (int k = 0; k < 16; ++k) off.a[k] = __ldg(Z.m->offset + 16 * i + k);
+  for (int k = 0; k < 16; ++k) o.a[k] = __ldg(off + k);
   const M3 R = rotation_vector_matrix(a0 * qi, a1 * qi, a2 * qi);
-  *value = mul(off, motion_rot(R));
-  if (want_d1) *d1 = mul(off, embed_rotation(mul3(skew(a0, a1, a2), R)));
+  J->L = mul(o, motion_rot(R));
+  if (want_d1) J->d1 = mul(o, embed_rotation(mul3(skew(a0, a1, a2), R)));
+}
+
+// translation column: T0*t0 + T1*t1 + T2*t2 + T3
+__device__ __forceinline__ double trans_col(const double* T, const double* t) {
+  double acc = T[0] * t[0];
+  acc = fma(T[1], t[1], acc);
+  acc = fma(T[2], t[2], acc);
+  return acc + T[3];
+}
+
+// row of (T * L): forward kinematics world = parent_world * value
+__device__ __forceinline__ void link_fk_row(const LinkJet& J, const double* T, double* Tn) {
+  const double c = J.c, s = J.s;
+  switch (J.jk) {
+    case 1:  // R = [1 0 0; 0 c -s; 0 s c]
+      Tn[0] = T[0];
+      Tn[1] = fma(T[2], s, T[1] * c);
+      Tn[2] = fma(T[2], c, T[1] * (-s));
+      Tn[3] = trans_col(T, J.t);
+      return;
+    case 2:  // R = [c 0 s; 0 1 0; -s 0 c]
+      Tn[0] = fma(T[2], -s, T[0] * c);
+      Tn[1] = T[1];
+      Tn[2] = fma(T[2], c, T[0] * s);
+      Tn[3] = trans_col(T, J.t);
+      return;
+    case 3:  // R = [c -s 0; s c 0; 0 0 1]
+      Tn[0] = fma(T[1], s, T[0] * c);
+      Tn[1] = fma(T[1], c, T[0] * (-s));
+      Tn[2] = T[2];
+      Tn[3] = trans_col(T, J.t);
+      return;
+    default:
+      row_mul(T, J.L, Tn);
+  }
+}
+
+// row of (T * d1): lever = parent_world * dL/dq; compact storage lev[0..1]
+// for the specialised kinds (the other two entries are +-0)
+__device__ __forceinline__ void link_lever_row(const LinkJet& J, const double* T, double* lev) {
+  const double c = J.c, s = J.s;
+  switch (J.jk) {
+    case 1:  // [a]x R rows: 0; (0,-s,-c); (0,c,-s)   -> columns 1, 2
+      lev[0] = fma(T[2], c, T[1] * (-s));
+      lev[1] = fma(T[2], -s, T[1] * (-c));
+      return;
+    case 2:  // rows: (-s,0,c); 0; (-c,0,-s)           -> columns 0, 2
+      lev[0] = fma(T[2], -c, T[0] * (-s));
+      lev[1] = fma(T[2], -s, T[0] * c);
+      return;
+    case 3:  // rows: (-s,-c,0); (c,-s,0); 0            -> columns 0, 1
+      lev[0] = fma(T[1], c, T[0] * (-s));
+      lev[1] = fma(T[1], -s, T[0] * (-c));
+      return;
+    default:
+      row_mul(T, J.d1, lev);
+  }
+}
+
+// ddot_row(lever_row, a) with the lever's zero columns dropped
+__device__ __forceinline__ double link_lever_dot(int jk, const double* lev, const double* a) {
+  switch (jk) {
+    case 1: return fma(lev[1], a[2], lev[0] * a[1]);
+    case 2: return fma(lev[1], a[2], lev[0] * a[0]);
+    case 3: return fma(lev[1], a[1], lev[0] * a[0]);
+    default: return ddot_row(lev, a);
+  }
+}
+
+// row of (a * L^T): adjoint transport to the parent
+__device__ __forceinline__ void link_transport_row(const LinkJet& J, const double* a, double* t) {
+  const double c = J.c, s = J.s;
+  switch (J.jk) {
+    case 1:  // L rows (1,0,0,t0) (0,c,-s,t1) (0,s,c,t2)
+      t[0] = fma(a[3], J.t[0], a[0]);
+      t[1] = fma(a[3], J.t[1], fma(a[2], -s, a[1] * c));
+      t[2] = fma(a[3], J.t[2], fma(a[2], c, a[1] * s));
+      t[3] = a[3];
+      return;
+    case 2:  // (c,0,s,t0) (0,1,0,t1) (-s,0,c,t2)
+      t[0] = fma(a[3], J.t[0], fma(a[2], s, a[0] * c));
+      t[1] = fma(a[3], J.t[1], a[1]);
+      t[2] = fma(a[3], J.t[2], fma(a[2], c, a[0] * (-s)));
+      t[3] = a[3];
+      return;
+    case 3:  // (c,-s,0,t0) (s,c,0,t1) (0,0,1,t2)
+      t[0] = fma(a[3], J.t[0], fma(a[1], -s, a[0] * c));
+      t[1] = fma(a[3], J.t[1], fma(a[1], c, a[0] * s));
+      t[2] = fma(a[3], J.t[2], a[2]);
+      t[3] = a[3];
+      return;
+    default:
+      row_mul_bt(a, J.L, t);
+  }
 }
 
 __device__ __forceinline__ void identity_row(int r, double* v) {
@@ -144,14 +280,30 @@ __device__ __forceinline__ void quad_combine(const Q& Z, const double* p, double
 }
 
 // --- vector ops (quad-interleaved, 32-partial canonical dot) --------------
+// Element k of a vector lives on lane k%4 at group k>>2.  Loops run eight
+// groups at a time with all loads issued first (memory-level parallelism:
+// one resident warp per scheduler cannot hide a serial load chain).
+constexpr int kU = 8;
+
 __device__ double qdot(const Q& Z, long oa, long ob, int n) {
   double acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.0;
   const int n4 = (n + 3) >> 2;
-  for (int g = 0; g < n4; ++g) {
-    const int k = 4 * g + Z.r;
-    if (k < n) acc[g & 7] = fma(*vel(Z, oa, k), *vel(Z, ob, k), acc[g & 7]);
+  for (int g0 = 0; g0 < n4; g0 += kU) {
+    double a[kU], b[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int k = 4 * (g0 + j) + Z.r;
+      const bool ok = (g0 + j < n4) && k < n;
+      a[j] = ok ? *vel(Z, oa, k) : 0.0;
+      b[j] = ok ? *vel(Z, ob, k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int k = 4 * (g0 + j) + Z.r;
+      if ((g0 + j < n4) && k < n) acc[j] = fma(a[j], b[j], acc[j]);  // (g0+j)&7 == j
+    }
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) acc[j] = acc[j] + acc[j + 4];
@@ -164,16 +316,59 @@ __device__ double qdot(const Q& Z, long oa, long ob, int n) {
   if (Z.r == 0) v = v + v1;
   return qshfl(Z, v, 0);
 }
+
+// dst[k] = f(a[k], b[k]) for the lane's elements: loads of eight groups are
+// issued before any store (the compiler cannot reorder across the stores)
+template <class F>
+__device__ __forceinline__ void qmap2(const Q& Z, int n, long dst, long oa, long ob, F f) {
+  const int n4 = (n + 3) >> 2;
+  for (int g0 = 0; g0 < n4; g0 += kU) {
+    double a[kU], b[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int k = 4 * (g0 + j) + Z.r;
+      const bool ok = (g0 + j < n4) && k < n;
+      a[j] = ok ? *vel(Z, oa, k) : 0.0;
+      b[j] = ok ? *vel(Z, ob, k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int k = 4 * (g0 + j) + Z.r;
+      if ((g0 + j < n4) && k < n) *vel(Z, dst, k) = f(a[j], b[j]);
+    }
+  }
+}
+
 __device__ double qinfnorm(const Q& Z, long oa, int n) {
   double mx = 0.0;
-  for (int k = Z.r; k < n; k += 4) mx = fmax(mx, fabs(*vel(Z, oa, k)));
+  const int n4 = (n + 3) >> 2;
+  for (int g0 = 0; g0 < n4; g0 += kU) {
+    double a[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int k = 4 * (g0 + j) + Z.r;
+      a[j] = (g0 + j < n4 && k < n) ? *vel(Z, oa, k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) mx = fmax(mx, fabs(a[j]));
+  }
   mx = fmax(mx, qshfl(Z, mx, Z.r ^ 1));
   mx = fmax(mx, qshfl(Z, mx, Z.r ^ 2));
   return mx;
 }
 __device__ bool qallfinite(const Q& Z, long oa, int n) {
   bool ok = true;
-  for (int k = Z.r; k < n; k += 4) ok = ok && isfinite(*vel(Z, oa, k));
+  const int n4 = (n + 3) >> 2;
+  for (int g0 = 0; g0 < n4; g0 += kU) {
+    double a[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int k = 4 * (g0 + j) + Z.r;
+      a[j] = (g0 + j < n4 && k < n) ? *vel(Z, oa, k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) ok = ok && isfinite(a[j]);
+  }
   return __all_sync(Z.qm, ok);
 }
 
@@ -184,14 +379,16 @@ __device__ void chain_fk(const Q& Z, long ov, long olink) {
   double T[4];
   identity_row(Z.r, T);
   for (int i = 0; i < N; ++i) {
-    M4 Lv, d1;
-    hinge_jet(Z, i, *vel(Z, ov, i), &Lv, &d1, false);
+    LinkJet J;
+    link_jet(Z, i, *vel(Z, ov, i), false, &J);
     double Tn[4];
     if (i == 0) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) Tn[c] = Lv.a[Z.r + 4 * c];
+      // forward_pass: the root's world transform is its local transform
+      double I[4];
+      identity_row(Z.r, I);
+      link_fk_row(J, I, Tn);
     } else {
-      row_mul(T, Lv, Tn);
+      link_fk_row(J, T, Tn);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) T[c] = Tn[c];
@@ -216,8 +413,9 @@ __device__ double chain_cv(const Q& Z, long oa, long ob) {
 }
 
 // --- the evaluation --------------------------------------------------------
-// Forward sweep at vector `ox`: value (StepObjective::value) and, with
-// store, the seeds / levers / joint transforms the reverse sweep needs.
+// Forward sweep at vector `ox`: value (StepObjective::value,
+// objective.cpp:215-239) and, with store, the seeds / levers / joint
+// transforms the reverse sweep needs.
 __device__ double chain_forward(const Q& Z, long ox, bool store) {
   const ChainLayout& L = *Z.L;
   const DSchedule& sc = *Z.sc;
@@ -226,26 +424,55 @@ __device__ double chain_forward(const Q& Z, long ox, bool store) {
   double T[4];
   identity_row(Z.r, T);
   double sa = 0.0, sb = 0.0, sc2 = 0.0, sg = 0.0;
+  // software pipeline: the next link's per-env loads are issued one link early
+  double qnext = *vel(Z, ox, 0);
+  double ntk[4] = {0.0, 0.0, 0.0, 0.0}, ntk1[4] = {0.0, 0.0, 0.0, 0.0};
+  int nsk = __ldg(Z.m->skind);
+  if (nsk) {
+    ld4(lrow(Z, L.tk, 0), ntk);
+    ld4(lrow(Z, L.tk1, 0), ntk1);
+  }
   for (int i = 0; i < N; ++i) {
-    M4 Lv, d1;
-    hinge_jet(Z, i, *vel(Z, ox, i), &Lv, &d1, store);
-    const M4 S = ldS(Z, i);
+    const double qi = qnext;
+    const int sk = nsk;
+    double tk[4], tk1[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      tk[c] = ntk[c];
+      tk1[c] = ntk1[c];
+    }
+    if (i + 1 < N) {
+      qnext = *vel(Z, ox, i + 1);
+      nsk = __ldg(Z.m->skind + i + 1);
+      if (nsk) {
+        ld4(lrow(Z, L.tk, i + 1), ntk);
+        ld4(lrow(Z, L.tk1, i + 1), ntk1);
+      }
+    }
+    LinkJet J;
+    link_jet(Z, i, qi, store, &J);
     if (store) {
       double lev[4];
-      row_mul(T, d1, lev);  // parent_world * d1 (identity row for the root)
-      st4(lrow(Z, L.lev, i), lev);
-      double lr[4];
+      link_lever_row(J, T, lev);  // parent_world * d1 (identity row for the root)
+      double* lp = lrow(Z, L.lev, i);
+      if (J.jk) {
+        *reinterpret_cast<double2*>(lp) = make_double2(lev[0], lev[1]);
+        if (Z.r == 0)
+          *reinterpret_cast<double2*>(Z.cw + L.lmat + ((long)i * Z.B + Z.e) * 16) = make_double2(J.c, J.s);
+      } else {
+        st4(lp, lev);
+        double lr[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) lr[c] = Lv.a[Z.r + 4 * c];
-      st4(lrow(Z, L.lmat, i), lr);
+        for (int c = 0; c < 4; ++c) lr[c] = J.L.a[Z.r + 4 * c];
+        st4(lrow(Z, L.lmat, i), lr);
+      }
     }
     double Tn[4];
-    row_mul(T, Lv, Tn);  // world = parent_world * value
+    link_fk_row(J, T, Tn);  // world = parent_world * value
 #pragma unroll
     for (int c = 0; c < 4; ++c) T[c] = Tn[c];
-    double tk[4], tk1[4];
-    ld4(lrow(Z, L.tk, i), tk);
-    ld4(lrow(Z, L.tk1, i), tk1);
+    if (!sk) continue;  // massless link: every term below is exactly +-0
+    const M4 S = ldS(Z, i);
     double ts[4], p1[4], p2[4], cg[4];
     row_mul(T, S, ts);
     row_mul(tk, S, p1);
@@ -280,25 +507,62 @@ __device__ double chain_forward(const Q& Z, long ox, bool store) {
   return inertial + sg - tdx;
 }
 
-// Reverse sweep: gradient (inertial adjoint + gravity adjoint - tau) into og.
+// Reverse sweep (functional_grad twice, adjoint.cpp:49-64): gradient =
+// (inertial adjoint + gravity adjoint) - tau into og (objective.cpp:241-250).
 __device__ void chain_reverse(const Q& Z, long og) {
   const ChainLayout& L = *Z.L;
   const int N = Z.m->N;
   double cI[4] = {0.0, 0.0, 0.0, 0.0}, cG[4] = {0.0, 0.0, 0.0, 0.0};
+  // per-link loads one link ahead (software pipeline)
+  auto fetch = [&](int i, double* lev, double* seed, double* cs) {
+    const int jk = __ldg(Z.m->jkind + i);
+    const int sk = __ldg(Z.m->skind + i);
+    const double* lp = lrow(Z, L.lev, i);
+    if (jk) {
+      const double2 v = *reinterpret_cast<const double2*>(lp);
+      lev[0] = v.x;
+      lev[1] = v.y;
+      const double2 w = *reinterpret_cast<const double2*>(Z.cw + L.lmat + ((long)i * Z.B + Z.e) * 16);
+      cs[0] = w.x;
+      cs[1] = w.y;
+    } else {
+      ld4(lp, lev);
+    }
+    if (sk) ld4(lrow(Z, L.seed, i), seed);
+  };
+  double nlev[4], nseed[4], ncs[2];
+  fetch(N - 1, nlev, nseed, ncs);
   for (int i = N - 1; i >= 0; --i) {
-    double seed[4], lev[4], aI[4], aG[4], cg[4];
-    ld4(lrow(Z, L.seed, i), seed);
-    ld4(lrow(Z, L.lev, i), lev);
-    const M4 S = ldS(Z, i);
-    grav_row(Z, S, cg);
+    const int jk = __ldg(Z.m->jkind + i);
+    const int sk = __ldg(Z.m->skind + i);
+    double lev[4], aI[4], aG[4], seed[4], cs[2];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      aI[c] = cI[c] + seed[c];
-      aG[c] = cG[c] + (0.0 + cg[c]);
+      lev[c] = nlev[c];
+      seed[c] = nseed[c];
+    }
+    cs[0] = ncs[0];
+    cs[1] = ncs[1];
+    if (i > 0) fetch(i - 1, nlev, nseed, ncs);
+    if (sk) {
+      double cg[4];
+      const M4 S = ldS(Z, i);
+      grav_row(Z, S, cg);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        aI[c] = cI[c] + seed[c];
+        aG[c] = cG[c] + (0.0 + cg[c]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        aI[c] = cI[c];
+        aG[c] = cG[c];
+      }
     }
     double part[2], gg[2];
-    part[0] = ddot_row(lev, aI);
-    part[1] = ddot_row(lev, aG);
+    part[0] = link_lever_dot(jk, lev, aI);
+    part[1] = link_lever_dot(jk, lev, aG);
     quad_combine<2>(Z, part, gg);
     if ((i & 3) == Z.r) {
       const double gi = 0.0 + gg[0];
@@ -306,20 +570,30 @@ __device__ void chain_reverse(const Q& Z, long og) {
       *vel(Z, og, i) = (gi + gp) - *vel(Z, L.tau, i);
     }
     if (i > 0) {
-      M4 Lv;
-      ld4(Z.cw + L.lmat + ((long)i * Z.B + Z.e) * 16 + 0, Lv.a + 0);
-      ld4(Z.cw + L.lmat + ((long)i * Z.B + Z.e) * 16 + 4, Lv.a + 4);
-      ld4(Z.cw + L.lmat + ((long)i * Z.B + Z.e) * 16 + 8, Lv.a + 8);
-      ld4(Z.cw + L.lmat + ((long)i * Z.B + Z.e) * 16 + 12, Lv.a + 12);
-      // stored row-wise: Lrow[rr][c] at 4*rr + c; convert to column-major
-      M4 Lc;
+      LinkJet J;
+      J.jk = jk;
+      const double* lm = Z.cw + L.lmat + ((long)i * Z.B + Z.e) * 16;
+      if (jk) {
+        J.c = cs[0];
+        J.s = cs[1];
+        const double* off = Z.m->offset + 16 * i;
+        J.t[0] = __ldg(off + 12);
+        J.t[1] = __ldg(off + 13);
+        J.t[2] = __ldg(off + 14);
+      } else {
+        double rows[16];
+        ld4(lm, rows);
+        ld4(lm + 4, rows + 4);
+        ld4(lm + 8, rows + 8);
+        ld4(lm + 12, rows + 12);
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr)
+        for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) Lc.a[rr + 4 * c] = Lv.a[4 * rr + c];
+          for (int c = 0; c < 4; ++c) J.L.a[rr + 4 * c] = rows[4 * rr + c];
+      }
       double tI[4], tG[4];
-      row_mul_bt(aI, Lc, tI);
-      row_mul_bt(aG, Lc, tG);
+      link_transport_row(J, aI, tI);
+      link_transport_row(J, aG, tG);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         cI[c] = 0.0 + tI[c];
@@ -355,27 +629,27 @@ __device__ void two_loop(const Q& Z, const SolverState& s) {
   const ChainLayout& L = *Z.L;
   const int n = Z.m->n;
   const int cap = Z.sc->opt.mem + 1;
-  for (int k = Z.r; k < n; k += 4) *vel(Z, L.q, k) = *vel(Z, L.g, k);
+  qmap2(Z, n, L.q, L.g, L.g, [](double a, double) { return a; });
   double alpha[kMaxMem];
   for (int i = s.hc - 1; i >= 0; --i) {
     const int slot = (s.h0 + i) % cap;
     const long os = L.hs + (long)slot * L.vstride, oy = L.hy + (long)slot * L.vstride;
     const double a = qdot(Z, os, L.q, n) / Z.cw[L.hsy + (long)slot * Z.B + Z.e];
     alpha[i] = a;
-    for (int k = Z.r; k < n; k += 4) *vel(Z, L.q, k) = *vel(Z, L.q, k) - a * *vel(Z, oy, k);
+    qmap2(Z, n, L.q, L.q, oy, [a](double qv, double yv) { return qv - a * yv; });
   }
   if (s.hc > 0) {
     const int slot = (s.h0 + s.hc - 1) % cap;
     const long oy = L.hy + (long)slot * L.vstride;
     const double scl = Z.cw[L.hsy + (long)slot * Z.B + Z.e] / qdot(Z, oy, oy, n);
-    for (int k = Z.r; k < n; k += 4) *vel(Z, L.q, k) = *vel(Z, L.q, k) * scl;
+    qmap2(Z, n, L.q, L.q, L.q, [scl](double qv, double) { return qv * scl; });
   }
   for (int i = 0; i < s.hc; ++i) {
     const int slot = (s.h0 + i) % cap;
     const long os = L.hs + (long)slot * L.vstride, oy = L.hy + (long)slot * L.vstride;
     const double beta = qdot(Z, oy, L.q, n) / Z.cw[L.hsy + (long)slot * Z.B + Z.e];
     const double c = alpha[i] - beta;
-    for (int k = Z.r; k < n; k += 4) *vel(Z, L.q, k) = *vel(Z, L.q, k) + c * *vel(Z, os, k);
+    qmap2(Z, n, L.q, L.q, os, [c](double qv, double sv) { return qv + c * sv; });
   }
 }
 
@@ -388,12 +662,12 @@ __device__ int lbfgs_iterate(const Q& Z, SolverState& s) {
   if (s.iters >= o.max_iters) return s.status = ST_FAILED;
   if (grad_converged(Z, s)) return s.status = ST_CONVERGED;
   two_loop(Z, s);
-  for (int k = Z.r; k < n; k += 4) *vel(Z, L.dir, k) = -*vel(Z, L.q, k);
+  qmap2(Z, n, L.dir, L.q, L.q, [](double qv, double) { return -qv; });
   double slope = qdot(Z, L.dir, L.g, n);
   if (!(slope < 0.0)) {
     s.hc = 0;
     s.h0 = 0;
-    for (int k = Z.r; k < n; k += 4) *vel(Z, L.dir, k) = -*vel(Z, L.g, k);
+    qmap2(Z, n, L.dir, L.g, L.g, [](double gv, double) { return -gv; });
     slope = qdot(Z, L.dir, L.g, n);
   }
   double t = 1.0;
@@ -401,17 +675,15 @@ __device__ int lbfgs_iterate(const Q& Z, SolverState& s) {
   const double fval = s.value;
   const int cap = o.mem + 1;
   for (int trial = 0; trial < o.max_line_search; ++trial) {
-    for (int k = Z.r; k < n; k += 4) *vel(Z, L.cand, k) = *vel(Z, L.x, k) + t * *vel(Z, L.dir, k);
+    qmap2(Z, n, L.cand, L.x, L.dir, [t](double xv, double dv) { return xv + t * dv; });
     if (qallfinite(Z, L.cand, n)) {
       const double v = chain_forward(Z, L.cand, true);
       if (isfinite(v) && v <= fval + o.armijo_c1 * t * slope && v < fval) {
         chain_reverse(Z, L.evg);
         const int slot = (s.h0 + s.hc) % cap;
         const long os = L.hs + (long)slot * L.vstride, oy = L.hy + (long)slot * L.vstride;
-        for (int k = Z.r; k < n; k += 4) {
-          *vel(Z, os, k) = t * *vel(Z, L.dir, k);
-          *vel(Z, oy, k) = *vel(Z, L.evg, k) - *vel(Z, L.g, k);
-        }
+        qmap2(Z, n, os, L.dir, L.dir, [t](double dv, double) { return t * dv; });
+        qmap2(Z, n, oy, L.evg, L.g, [](double ev, double gv) { return ev - gv; });
         const double sy = qdot(Z, os, oy, n);
         if (sy > 1e-12) {
           if (Z.r == 0) Z.cw[L.hsy + (long)slot * Z.B + Z.e] = sy;
@@ -421,10 +693,8 @@ __device__ int lbfgs_iterate(const Q& Z, SolverState& s) {
             --s.hc;
           }
         }
-        for (int k = Z.r; k < n; k += 4) {
-          *vel(Z, L.x, k) = *vel(Z, L.cand, k);
-          *vel(Z, L.g, k) = *vel(Z, L.evg, k);
-        }
+        qmap2(Z, n, L.x, L.cand, L.cand, [](double cv, double) { return cv; });
+        qmap2(Z, n, L.g, L.evg, L.evg, [](double ev, double) { return ev; });
         qsync(Z);
         s.value = v;
         accepted = true;
@@ -554,8 +824,18 @@ __global__ void __launch_bounds__(kThreads) k_chain_init(DModel m, DForces f, DS
   double ke = 0.0, pe = 0.0;
   const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
   for (int i = 0; i < N; ++i) {
+    // general joint algebra here (runs once per trajectory)
     M4 Lv, d1;
-    hinge_jet(Z, i, *vel(Z, L.h1, i), &Lv, &d1, true);
+    {
+      const double qi = *vel(Z, L.h1, i);
+      const double* ax = m.axis + 3 * i;
+      M4 o;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) o.a[k] = __ldg(m.offset + 16 * i + k);
+      const M3 R = rotation_vector_matrix(ax[0] * qi, ax[1] * qi, ax[2] * qi);
+      Lv = mul(o, motion_rot(R));
+      d1 = mul(o, embed_rotation(mul3(skew(ax[0], ax[1], ax[2]), R)));
+    }
     const double qd = *vel(Z, L.g, i);
     M4 ldot;
 #pragma unroll

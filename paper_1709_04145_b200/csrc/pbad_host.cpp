@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "pbad_launch.h"
@@ -682,6 +683,30 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   dm.sample_off = up_i(m.sample_off);
   dm.samples = up_d(m.samples);
   dm.weighted_mass = m.weighted_mass;
+  {
+    // chain-kernel link classes (exact structure tests, see pbad_chain.cu)
+    std::vector<int> jk(m.N, 0), sk(m.N, 1);
+    for (int i = 0; i < m.N; ++i) {
+      const double* o = &m.offset[16 * i];
+      const bool rot_identity = o[0] == 1.0 && o[1] == 0.0 && o[2] == 0.0 && o[4] == 0.0 && o[5] == 1.0 &&
+                                o[6] == 0.0 && o[8] == 0.0 && o[9] == 0.0 && o[10] == 1.0;
+      const double* a = &m.axis[3 * i];
+      if (m.kind[i] == PBAD_HINGE && rot_identity) {
+        if (a[0] == 1.0 && a[1] == 0.0 && a[2] == 0.0) jk[i] = 1;
+        if (a[0] == 0.0 && a[1] == 1.0 && a[2] == 0.0) jk[i] = 2;
+        if (a[0] == 0.0 && a[1] == 0.0 && a[2] == 1.0) jk[i] = 3;
+      }
+      bool zero = true;
+      for (int k = 0; k < 16; ++k) zero = zero && m.S[16 * i + k] == 0.0;
+      sk[i] = zero ? 0 : 1;
+    }
+    if (std::getenv("PBAD_GPU_NO_SPECIALIZE")) {
+      std::fill(jk.begin(), jk.end(), 0);
+      std::fill(sk.begin(), sk.end(), 1);
+    }
+    dm.jkind = up_i(jk);
+    dm.skind = up_i(sk);
+  }
 
   DForces df{};
   for (int k = 0; k < 3; ++k) df.gravity[k] = f->gravity[k];

@@ -21,6 +21,8 @@ struct DModel {
   const double* mass;    // [N]
   const int* sample_off; // [N+1]
   const double* samples; // [*][3]
+  const int* jkind;      // chain path: 0 general hinge, 1/2/3 axis X/Y/Z with identity-rotation offset
+  const int* skind;      // chain path: 0 massless (S == 0), 1 general S
   double weighted_mass;  // WeightedBody::make with unit weights (adjoint.cpp:29-41)
 };
 

@@ -219,21 +219,54 @@ class MT19937:
         return y & 0xFFFFFFFF
 
 
+def _mt_words(seed: int, count: int) -> np.ndarray:
+    """count 32-bit outputs of std::mt19937(seed), twist and tempering vectorised."""
+    mt = np.zeros(624, dtype=np.uint64)
+    mt[0] = seed & 0xFFFFFFFF
+    for i in range(1, 624):
+        prev = int(mt[i - 1])
+        mt[i] = (1812433253 * (prev ^ (prev >> 30)) + i) & 0xFFFFFFFF
+    mt = mt.astype(np.uint32)
+    out = np.empty(count, dtype=np.uint32)
+    upper, lower, matrix = np.uint32(0x80000000), np.uint32(0x7FFFFFFF), np.uint32(0x9908B0DF)
+
+    def twist(mt):
+        mt = mt.copy()
+        for a, b in ((0, 227), (227, 454), (454, 623)):
+            y = (mt[a:b] & upper) | (mt[a + 1:b + 1] & lower)
+            sh = 397 if a < 227 else 397 - 624
+            v = mt[a + sh:b + sh] ^ (y >> np.uint32(1))
+            v ^= np.where((y & np.uint32(1)) != 0, matrix, np.uint32(0))
+            mt[a:b] = v
+        y = (mt[623] & upper) | (mt[0] & lower)
+        v = mt[396] ^ (y >> np.uint32(1))
+        if y & 1:
+            v ^= matrix
+        mt[623] = v
+        return mt
+
+    pos = 0
+    while pos < count:
+        mt = twist(mt)
+        y = mt.copy()
+        y ^= y >> np.uint32(11)
+        y ^= (y << np.uint32(7)) & np.uint32(0x9D2C5680)
+        y ^= (y << np.uint32(15)) & np.uint32(0xEFC60000)
+        y ^= y >> np.uint32(18)
+        take = min(624, count - pos)
+        out[pos:pos + take] = y[:take]
+        pos += take
+    return out
+
+
 def mt19937_uniform(seed: int, count: int, lo: float, hi: float) -> np.ndarray:
     """count draws of std::uniform_real_distribution<double>(lo, hi)(std::mt19937(seed)).
 
     libstdc++ generate_canonical<double, 53> consumes two 32-bit words:
-    (w0 + w1 * 2^32) / 2^64, clamped below 1, then lo + u * (hi - lo).
+    (w0 + w1 * 2^32) / 2^64, clamped below 1, then (hi - lo) * u + lo.
     """
-    g = MT19937(seed)
-    out = np.empty(count)
-    two32 = 4294967296.0
-    for k in range(count):
-        w0 = float(g())
-        w1 = float(g())
-        s = w0 + w1 * two32
-        u = s / 18446744073709551616.0
-        if u >= 1.0:
-            u = 1.0 - 2.0 ** -53
-        out[k] = (u * (hi - lo)) + lo
-    return out
+    w = _mt_words(seed, 2 * count).astype(np.float64)
+    s = w[0::2] + w[1::2] * 4294967296.0
+    u = s / 18446744073709551616.0
+    u = np.where(u >= 1.0, 1.0 - 2.0 ** -53, u)
+    return (u * (hi - lo)) + lo

@@ -205,3 +205,38 @@ def test_minimize_matches_oracle():
                                        C.byref(ogn), None)
         np.testing.assert_array_equal(xo[b], ox)
         assert it[b] == oit.value and cv[b] == ocv.value and fv[b] == ofv.value
+
+
+def _random_hinge_chain(seed, links):
+    """Hinge chain with tilted axes, rotated offsets and mixed geometry: the
+    chain kernel's general (non-specialised) link class."""
+    from paper_1709_04145_b200.types import JointKind, JointSpec, LinkSpec
+    from _parity_util import random_offset
+    rng = np.random.default_rng(seed)
+    base = random_tree(rng, links, chain=True)
+    out = []
+    for i, l in enumerate(base):
+        ax = rng.uniform(-1, 1, 3)
+        j = JointSpec(JointKind.hinge, tuple(ax / np.linalg.norm(ax)),
+                      random_offset(rng) if i % 3 else np.eye(4))
+        out.append(LinkSpec(l.parent, j, l.geometry))
+    return out
+
+
+def test_rollout_chain_kernel_general_links():
+    from paper_1709_04145_b200.scenes import Scene
+    sc = Scene(links=_random_hinge_chain(11, 9), gravity=(0.5, -2.0, -9.81))
+    sc.q0 = np.zeros(9)
+    sc.qdot0 = np.zeros(9)
+    sim = SimConfig(dt=0.02, duration=0.1)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    _rollout_case(sc, sim, B=3, seed=5)
+
+
+def test_rollout_chain_kernel_actuated():
+    sc = make_single_hinge_chain_scene(6)
+    from paper_1709_04145_b200.types import ActuationKind, ActuationSpec
+    sc.actuation = ActuationSpec(ActuationKind.sinusoidal, np.linspace(-3, 3, 6), 1.5, np.linspace(0, 1, 6))
+    sim = SimConfig(dt=0.02, duration=0.1)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    _rollout_case(sc, sim, B=2, seed=7)
