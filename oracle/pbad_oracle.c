@@ -1331,6 +1331,14 @@ static void actuation_at(const pbo_objective* o, int instant, double* out) {
   for (int k = 0; k < n; ++k) out[k] = 0.0;
 }
 
+/* diagnostic: number of StepObjective evaluations (value or evaluate) */
+static long long g_eval_count = 0;
+long long pbo_eval_counter(int reset) {
+  const long long v = g_eval_count;
+  if (reset) g_eval_count = 0;
+  return v;
+}
+
 /* StepObjective::evaluate_impl, objective.cpp:206-334 */
 static int obj_evaluate(const pbo_objective* o, const double* x, int want_grad, int want_gn,
                         pbo_eval* out, pbo_err* e) {
@@ -1340,6 +1348,7 @@ static int obj_evaluate(const pbo_objective* o, const double* x, int want_grad, 
   const double dt = o->dt;
   const double inv_dt2 = 1.0 / (dt * dt);
   out->has_gn = 0;
+  __atomic_add_fetch(&g_eval_count, 1, __ATOMIC_RELAXED);
 
   if (o->kind == PBO_ENERGY) {
     pbo_pass pass;

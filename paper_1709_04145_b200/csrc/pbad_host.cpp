@@ -529,9 +529,11 @@ Layout make_layout(const pbad_gpu_model& m, int order, int objective, int opt_ki
 }
 
 ChainLayout make_chain_layout(const pbad_gpu_model& m, int mem, long B, long* total) {
+  // per-warp blocks of 8 environments (pbad_chain.cu): link arrays
+  // [warp][N][32 lanes x 4], vectors [warp][n4][32 lanes]
   ChainLayout L{};
-  const long N = m.N, n4 = (m.n + 3) / 4;
-  const long link = N * B * 16, vec = n4 * B * 4;
+  const long N = m.N, n4 = (m.n + 3) / 4, nw = (B + 7) / 8;
+  const long link = nw * N * 128, vec = nw * n4 * 32;
   long o = 0;
   auto take = [&](long cnt) {
     const long at = o;
@@ -706,6 +708,15 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     }
     dm.jkind = up_i(jk);
     dm.skind = up_i(sk);
+    std::vector<double> rec(20 * (size_t)m.N, 0.0);
+    std::vector<int> ck(m.N);
+    for (int i = 0; i < m.N; ++i) {
+      for (int k = 0; k < 16; ++k) rec[20 * i + k] = m.S[16 * i + k];
+      for (int k = 0; k < 3; ++k) rec[20 * i + 16 + k] = m.offset[16 * i + 12 + k];
+      ck[i] = jk[i] | (sk[i] << 2);
+    }
+    dm.crec = up_d(rec);
+    dm.ckind = up_i(ck);
   }
 
   DForces df{};

@@ -23,6 +23,8 @@ struct DModel {
   const double* samples; // [*][3]
   const int* jkind;      // chain path: 0 general hinge, 1/2/3 axis X/Y/Z with identity-rotation offset
   const int* skind;      // chain path: 0 massless (S == 0), 1 general S
+  const double* crec;    // chain path: packed link records [N][20]: S (16), offset translation (3), pad
+  const int* ckind;      // chain path: jkind | skind << 2
   double weighted_mass;  // WeightedBody::make with unit weights (adjoint.cpp:29-41)
 };
 
