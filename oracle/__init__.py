@@ -471,3 +471,137 @@ def eval_potentials(model, forces, q_next, q_prev, dt, want_gn=True, want_hess=F
     if rc != 0:
         raise OracleError("eval_potentials failed")
     return v.value, g, gn.T.copy(), h.T.copy()
+
+
+# ---------------------------------------------------------------------------
+# oracle/_ref: the reference's own sources compiled against eigen_lite
+# (oracle/ref/Makefile).  Only buildable where /root/reference exists; the
+# built .so travels to the GPU box like the other in-tree libraries.
+REF_LIB_PATH = os.path.join(_HERE, "_ref", "libpbad_ref.so")
+_ref = None
+
+
+def ref_available():
+    return os.path.exists(REF_LIB_PATH)
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        R = C.CDLL(REF_LIB_PATH)
+        vp = C.c_void_p
+        R.pbr_last_error.restype = C.c_char_p
+        R.pbr_model_create.argtypes = [C.POINTER(LinkSpecC), C.c_int, C.POINTER(vp)]
+        R.pbr_model_free.argtypes = [vp]
+        R.pbr_model_dofs.argtypes = [vp]
+        R.pbr_model_info.argtypes = [vp, _dp, _dp, _ip, _dp, _ip]
+        R.pbr_forward_pass.argtypes = [vp, _dp, _dp]
+        R.pbr_correlation.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, _dp]
+        R.pbr_build_scheme.argtypes = [C.c_int, C.c_double, _dp, _dp]
+        R.pbr_step_eval.argtypes = [vp, C.POINTER(ForcesC), C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, C.c_int,
+                                    C.c_int, _dp, _dp, _dp]
+        R.pbr_simulate.argtypes = [vp, C.POINTER(ForcesC), C.POINTER(SimC), C.POINTER(TrajectoryC)]
+        R.pbr_batch_simulate.argtypes = [vp, C.POINTER(ForcesC), C.POINTER(SimC), C.c_int, C.c_int,
+                                         C.POINTER(TrajectoryC)]
+        _ref = R
+    return _ref
+
+
+class RefModel:
+    """KinematicModel built by the reference's own build_model."""
+
+    def __init__(self, links):
+        keep = []
+        arr = (LinkSpecC * max(1, len(links)))()
+        for i, l in enumerate(links):
+            arr[i] = link_spec_c(l, keep)
+        h = C.c_void_p()
+        if ref_lib().pbr_model_create(arr, len(links), C.byref(h)) != 0:
+            raise OracleError(ref_lib().pbr_last_error().decode())
+        self.h = h
+        self.n_links = len(links)
+        self.n_dofs = ref_lib().pbr_model_dofs(h)
+
+    def __del__(self):
+        try:
+            ref_lib().pbr_model_free(self.h)
+        except Exception:
+            pass
+
+    def info(self):
+        N = self.n_links
+        S = np.zeros((N, 16))
+        mass = np.zeros(N)
+        off = np.zeros(N, dtype=np.int32)
+        axis = np.zeros((N, 3))
+        sc = np.zeros(N, dtype=np.int32)
+        ref_lib().pbr_model_info(self.h, _ptr(S), _ptr(mass), _iptr(off), _ptr(axis), _iptr(sc))
+        return dict(S=S.reshape(N, 4, 4).transpose(0, 2, 1).copy(), mass=mass, dof_offset=off, axis=axis,
+                    sample_count=sc)
+
+
+def ref_forward_pass(model, q):
+    N = model.n_links
+    w = np.zeros((N, 16))
+    if ref_lib().pbr_forward_pass(model.h, _ptr(_f64(q)), _ptr(w)) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return w.reshape(N, 4, 4).transpose(0, 2, 1).copy()
+
+
+def ref_correlation(model, qa, qb):
+    n = model.n_dofs
+    v = C.c_double()
+    g = np.zeros(n)
+    bb = np.zeros((n, n))
+    ab = np.zeros((n, n))
+    if ref_lib().pbr_correlation(model.h, _ptr(_f64(qa)), _ptr(_f64(qb)), C.byref(v), _ptr(g), _ptr(bb),
+                                 _ptr(ab)) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return v.value, g, bb.T.copy(), ab.T.copy()
+
+
+def ref_build_scheme(order, dt):
+    k = order + 1
+    t = np.zeros(k)
+    H2 = np.zeros(k * k)
+    if ref_lib().pbr_build_scheme(order, dt, _ptr(t), _ptr(H2)) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return dict(times=t, H2=H2.reshape(k, k).T.copy())
+
+
+def ref_step_eval(model, forces, order, dt, objective, hist0, hist1, x, want_grad=True, want_gn=False,
+                  tau_instants=None):
+    keep = []
+    f = forces_c(forces, model.n_dofs, keep)
+    hist = _f64(np.concatenate([np.asarray(hist0, float), np.asarray(hist1, float)]))
+    x = _f64(x)
+    dim = len(x)
+    tau = None if tau_instants is None else _f64(tau_instants)
+    v = C.c_double()
+    g = np.zeros(dim)
+    gn = np.zeros((dim, dim)) if want_gn else None
+    if ref_lib().pbr_step_eval(model.h, C.byref(f), order, dt, objective, _ptr(hist), _ptr(tau), _ptr(x),
+                               int(want_grad), int(want_gn), C.byref(v), _ptr(g),
+                               _ptr(gn) if gn is not None else None) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return v.value, g, (gn.T.copy() if gn is not None else None)
+
+
+def ref_batch_simulate(model, forces, sims, workers=1):
+    keep = []
+    n = model.n_dofs
+    f = forces_c(forces, n, keep)
+    arr = (SimC * len(sims))()
+    trs = []
+    tarr = (TrajectoryC * len(sims))()
+    for i, sim in enumerate(sims):
+        arr[i] = sim_c(sim, n, keep)
+        tr = OracleTrajectory(n, total_steps(sim))
+        trs.append(tr)
+        tarr[i] = tr.c
+    if ref_lib().pbr_batch_simulate(model.h, C.byref(f), arr, len(sims), int(workers), tarr) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    for i, tr in enumerate(trs):
+        tr.c = tarr[i]
+        tr.finalize()
+    return trs
