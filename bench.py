@@ -157,13 +157,16 @@ class ClockSampler:
 
 
 def cpu_baseline(cfg, scene, model_links, n, steps=1, sample=None):
-    """The CPU oracle (plain-C restatement of the reference path, `kind: port`)
-    on the host cores: batch_simulate over a bounded sample of the workload."""
+    """The reference's own CPU batch_simulate (oracle/_ref: /root/reference
+    sources compiled unmodified, kind "reference", its WorkerPool on all host
+    threads) when built, else the C oracle port (kind "port"), over a bounded
+    sample of the workload."""
     import oracle
     cores = os.cpu_count() or 1
     sample = sample or max(cores, min(cfg["batch"], cores * 4))
     forces = scene.forces()
-    mo = oracle.Model(model_links)
+    use_ref = oracle.ref_available()
+    mo = oracle.RefModel(model_links) if use_ref else oracle.Model(model_links)
     q0 = initial_states(cfg, scene, n, 0, sample)
     sims = []
     for b in range(sample):
@@ -171,12 +174,16 @@ def cpu_baseline(cfg, scene, model_links, n, steps=1, sample=None):
         s.q0 = q0[b]
         s.qdot0 = np.zeros(n)
         sims.append(s)
+    run = oracle.ref_batch_simulate if use_ref else oracle.batch_simulate
     t = time.perf_counter()
-    trs = oracle.batch_simulate(mo, forces, sims, workers=cores)
+    trs = run(mo, forces, sims, workers=cores)
     el = time.perf_counter() - t
     done = sum(tr.n_samples - 1 for tr in trs)
-    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{sample} envs x {steps} step(s) of {cfg['desc'].split(':')[0]}, "
+    kind = "reference" if use_ref else "port"
+    what = ("reference batch_simulate (stepper.cpp:204-270, WorkerPool)" if use_ref
+            else "C oracle batch_simulate")
+    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{sample} envs x {steps} step(s) of {cfg['desc'].split(':')[0]}, {what}, "
                       f"{cores} threads, {el:.2f} s",
             "seconds": el}
 
@@ -210,8 +217,9 @@ def run_reference(args, cfg):
         "config": config_block(cfg, args, world),
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": ("reference arm = the CPU oracle (C restatement of the reference hot path, oracle/); the "
-                 "reference C++ itself needs Eigen3, absent in this image (see DESIGN.md)"),
+        "note": ("reference arm = the reference's own C++ (oracle/_ref: /root/reference/proj/src compiled "
+                 "unmodified against oracle/eigen_lite, Eigen3 being absent) on the host cores; falls back "
+                 "to the C oracle port when oracle/_ref is not built (see DESIGN.md)"),
     }
     print(json.dumps(line), flush=True)
 
