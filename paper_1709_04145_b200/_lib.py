@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpbad_gpu.so")
+# PBAD_GPU_LIB: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("PBAD_GPU_LIB") or os.path.join(_HERE, "libpbad_gpu.so")
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)

@@ -49,6 +49,9 @@ constexpr int kU = 8;              // vector-loop unroll (groups per batch)
 //   vectors     [warp][n4][32 lanes]    -> group g of a lane at +kGS*g
 constexpr long kLS = 128;
 constexpr long kGS = 32;
+#ifndef PBAD_CHAIN_PREFETCH_HIST
+#define PBAD_CHAIN_PREFETCH_HIST 1
+#endif
 
 __device__ __forceinline__ void ld4(const double* p, double* v) {
   const double2 a = *reinterpret_cast<const double2*>(p);
@@ -254,6 +257,8 @@ struct CK {
   long B, e;
   unsigned qm;
   double* red;  // shared reduction scratch of this quad (kRed doubles)
+  const double* rec;  // shared copy of the packed link records [N][20]
+  const int* kind;    // shared copy of the link kinds [N]
   double* cw;
   int* ci;
   // link arrays: row r of link 0 of this env; link i at +i*LS
@@ -271,8 +276,26 @@ __device__ __forceinline__ double qshfl(const CK& K, double v, int src) { return
 __device__ __forceinline__ void qsync(const CK& K) { __syncwarp(K.qm); }
 __device__ __forceinline__ int& ival(const CK& K, int slot) { return K.ci[(long)slot * K.B + K.e]; }
 
+// Dynamic shared memory: per-quad reduction scratch, then the packed link
+// records and kinds (read by every lane at every link of every sweep: keeping
+// them out of the L1/L2 path removes the dependent global load per link).
+__host__ __device__ constexpr long smem_red_doubles() { return (long)kRed * kEnvsPerBlock; }
+__host__ __device__ inline size_t chain_smem_bytes(int N) {
+  return (size_t)(smem_red_doubles() + 20L * N) * sizeof(double) + (size_t)N * sizeof(int);
+}
+__device__ __forceinline__ void stage_model(const DModel& m, double* smem) {
+  double* rec = smem + smem_red_doubles();
+  int* kind = reinterpret_cast<int*>(rec + 20L * m.N);
+  const double2* src = reinterpret_cast<const double2*>(m.crec);
+  double2* dst = reinterpret_cast<double2*>(rec);
+  for (int k = threadIdx.x; k < 10 * m.N; k += blockDim.x) dst[k] = __ldg(src + k);
+  for (int k = threadIdx.x; k < m.N; k += blockDim.x) kind[k] = __ldg(m.ckind + k);
+  __syncthreads();
+}
+
 __device__ __forceinline__ CK make_ck(const DModel& m, const DForces& f, const DSchedule& sc, const ChainLayout& L,
-                                      double* cw, int* ci, long B, double* red_base, bool* valid) {
+                                      double* cw, int* ci, long B, double* smem, bool* valid) {
+  double* red_base = smem;
   CK K;
   const int lane = threadIdx.x & 31;
   const int quad_in_block = threadIdx.x >> 2;
@@ -283,6 +306,8 @@ __device__ __forceinline__ CK make_ck(const DModel& m, const DForces& f, const D
   K.r = lane & 3;
   K.qm = 0xFu << (lane & ~3);
   K.red = red_base + kRed * quad_in_block;
+  K.rec = smem + smem_red_doubles();
+  K.kind = reinterpret_cast<const int*>(K.rec + 20L * m.N);
   K.N = m.N;
   K.n = m.n;
   K.n4 = (m.n + 3) >> 2;
@@ -420,20 +445,20 @@ struct Rec {
   double S[16];
   double t[3];
 };
-__device__ __forceinline__ void load_rec(const DModel& m, int i, Rec* R, bool want_S) {
-  const double* p = m.crec + 20 * (long)i;
+__device__ __forceinline__ void load_rec(const CK& K, int i, Rec* R, bool want_S) {
+  const double* p = K.rec + 20 * i;
   if (want_S) {
 #pragma unroll
     for (int k = 0; k < 16; k += 2) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(p + k));
+      const double2 v = *reinterpret_cast<const double2*>(p + k);
       R->S[k] = v.x;
       R->S[k + 1] = v.y;
     }
   }
-  const double2 t01 = __ldg(reinterpret_cast<const double2*>(p + 16));
+  const double2 t01 = *reinterpret_cast<const double2*>(p + 16);
   R->t[0] = t01.x;
   R->t[1] = t01.y;
-  R->t[2] = __ldg(p + 18);
+  R->t[2] = p[18];
 }
 
 // --- forward kinematics of a configuration into a link array ---------------
@@ -444,11 +469,11 @@ __device__ __forceinline__ void chain_fk(const CK& K, double* V, double* dst) {
   identity_row(K.r, T);
   double* d = dst;
   for (int i = 0; i < K.N; ++i, d += kLS) {
-    const int kind = __ldg(m.ckind + i);
+    const int kind = K.kind[i];
     const int jk = kind & 3;
     const double qi = vat(K, V, i);
     Rec R;
-    load_rec(m, i, &R, false);
+    load_rec(K, i, &R, false);
     double c = 0.0, s = 0.0;
     GenJet G;
     if (jk) hinge_cs(qi, &c, &s);
@@ -470,7 +495,7 @@ __device__ __forceinline__ double chain_cv(const CK& K, const double* A, const d
     ld4(A + i * kLS, a);
     ld4(Bw + i * kLS, b);
     Rec R;
-    load_rec(m, i, &R, true);
+    load_rec(K, i, &R, true);
     row_mul_rec(a, R.S, as);
     qsync(K);
     K.red[K.r] = ddot_row(as, b);
@@ -496,7 +521,7 @@ __device__ __forceinline__ double chain_forward(const CK& K, double* X, bool sto
   for (int g0 = 0; g0 < K.n4; g0 += 2) {
     const int i0 = 4 * g0 + K.r, i1 = i0 + 4;
     const bool ok0 = i0 < N, ok1 = g0 + 1 < K.n4 && i1 < N;
-    const int k0 = ok0 ? __ldg(m.ckind + i0) : 0, k1 = ok1 ? __ldg(m.ckind + i1) : 0;
+    const int k0 = ok0 ? K.kind[i0] : 0, k1 = ok1 ? K.kind[i1] : 0;
     const double q0 = ok0 ? X[(long)g0 * kGS] : 0.0, q1 = ok1 ? X[(long)(g0 + 1) * kGS] : 0.0;
     double c0, s0, c1, s1;
     hinge_cs(q0, &c0, &s0);
@@ -510,24 +535,39 @@ __device__ __forceinline__ double chain_forward(const CK& K, double* X, bool sto
   identity_row(K.r, T);
   double sum = 0.0;  // lane t: running sum of term t
   int nchunk = 0;
-  int kind_n = __ldg(m.ckind);
+  int kind_n = K.kind[0];
   double2 cs_n = (kind_n & 3) ? *reinterpret_cast<const double2*>(K.lmat0) : make_double2(0.0, 0.0);
   long off = 0;
+  // history rows of the next mass link, loaded one link ahead
+  double tk_n[4] = {0.0, 0.0, 0.0, 0.0}, tk1_n[4] = {0.0, 0.0, 0.0, 0.0};
+  if (kind_n >> 2) {
+    ld4(K.tk, tk_n);
+    ld4(K.tk1, tk1_n);
+  }
   for (int i = 0; i < N; ++i, off += kLS) {
     const int kind = kind_n;
     const int jk = kind & 3, sk = kind >> 2;
     const double c = cs_n.x, s = cs_n.y;
-    if (i + 1 < N) {
-      kind_n = __ldg(m.ckind + i + 1);
-      if (kind_n & 3) cs_n = *reinterpret_cast<const double2*>(K.lmat0 + off + kLS);
-    }
     double tk[4], tk1[4];
-    if (sk) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      tk[k] = tk_n[k];
+      tk1[k] = tk1_n[k];
+    }
+    if (!PBAD_CHAIN_PREFETCH_HIST && sk) {
       ld4(K.tk + off, tk);
       ld4(K.tk1 + off, tk1);
     }
+    if (i + 1 < N) {
+      kind_n = K.kind[i + 1];
+      if (kind_n & 3) cs_n = *reinterpret_cast<const double2*>(K.lmat0 + off + kLS);
+      if (PBAD_CHAIN_PREFETCH_HIST && (kind_n >> 2)) {
+        ld4(K.tk + off + kLS, tk_n);
+        ld4(K.tk1 + off + kLS, tk1_n);
+      }
+    }
     Rec R;
-    load_rec(m, i, &R, sk != 0);
+    load_rec(K, i, &R, sk != 0);
     GenJet G;
     if (!jk) general_jet(m, i, vat(K, X, i), store, &G);
     if (store) {
@@ -599,7 +639,7 @@ __device__ __forceinline__ void chain_reverse(const CK& K, double* Gv) {
   double cI[4] = {0.0, 0.0, 0.0, 0.0}, cG[4] = {0.0, 0.0, 0.0, 0.0};
   // loads one link ahead
   long off = (long)(N - 1) * kLS;
-  int kind_n = __ldg(m.ckind + N - 1);
+  int kind_n = K.kind[N - 1];
   double lev_n[4] = {0.0, 0.0, 0.0, 0.0}, seed_n[4] = {0.0, 0.0, 0.0, 0.0}, cs_n[2] = {0.0, 0.0};
   auto fetch = [&](int kind, long o, double* lv, double* sd, double* cs) {
     if (kind & 3) {
@@ -628,14 +668,14 @@ __device__ __forceinline__ void chain_reverse(const CK& K, double* Gv) {
     cs[0] = cs_n[0];
     cs[1] = cs_n[1];
     if (i > 0) {
-      kind_n = __ldg(m.ckind + i - 1);
+      kind_n = K.kind[i - 1];
       fetch(kind_n, off - kLS, lev_n, seed_n, cs_n);
     }
     double aI[4], aG[4];
     if (sk) {
-      const double* p = m.crec + 20 * (long)i + 12;
-      const double2 u01 = __ldg(reinterpret_cast<const double2*>(p));
-      const double2 u23 = __ldg(reinterpret_cast<const double2*>(p + 2));
+      const double* p = K.rec + 20 * i + 12;
+      const double2 u01 = *reinterpret_cast<const double2*>(p);
+      const double2 u23 = *reinterpret_cast<const double2*>(p + 2);
       const double u[4] = {u01.x, u01.y, u23.x, u23.y};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -672,11 +712,11 @@ __device__ __forceinline__ void chain_reverse(const CK& K, double* Gv) {
       double t3[3] = {0.0, 0.0, 0.0};
       M4 Lg;
       if (jk) {
-        const double* p = m.crec + 20 * (long)i + 16;
-        const double2 t01 = __ldg(reinterpret_cast<const double2*>(p));
+        const double* p = K.rec + 20 * i + 16;
+        const double2 t01 = *reinterpret_cast<const double2*>(p);
         t3[0] = t01.x;
         t3[1] = t01.y;
-        t3[2] = __ldg(p + 2);
+        t3[2] = p[2];
       } else {
         double rows[16];
         ld4(K.lmat0 + off, rows);
@@ -842,7 +882,7 @@ __device__ __forceinline__ void chain_energy(const CK& K, const double* Wp, cons
 #pragma unroll
     for (int c = 0; c < 4; ++c) td[c] = (wn[c] - wp[c]) / dt;
     Rec R;
-    load_rec(m, i, &R, true);
+    load_rec(K, i, &R, true);
     row_mul_rec(td, R.S, tds);
     // u = S e4 (canonical product: exactly column 3 of S)
     double wu = wn[0] * R.S[12];
@@ -871,9 +911,10 @@ __device__ __forceinline__ void chain_energy(const CK& K, const double* Wp, cons
 __global__ void __launch_bounds__(kThreads) k_chain_init(DModel m, DForces f, DSchedule sc, ChainLayout L, double* cw,
                                                          int* ci, long B, const double* q0, const double* qdot0,
                                                          Outputs out) {
-  __shared__ double red[kRed * kEnvsPerBlock];
+  extern __shared__ __align__(16) double smem[];
+  stage_model(m, smem);
   bool valid;
-  const CK K = make_ck(m, f, sc, L, cw, ci, B, red, &valid);
+  const CK K = make_ck(m, f, sc, L, cw, ci, B, smem, &valid);
   if (!valid) return;
   const int n = m.n, N = m.N;
   bool finite = true;
@@ -934,7 +975,7 @@ __global__ void __launch_bounds__(kThreads) k_chain_init(DModel m, DForces f, DS
       Td[c] = Tdn[c];
     }
     Rec R;
-    load_rec(m, i, &R, true);
+    load_rec(K, i, &R, true);
     double tds[4];
     row_mul_rec(Td, R.S, tds);
     double wu = T[0] * R.S[12];
@@ -970,9 +1011,10 @@ __global__ void __launch_bounds__(kThreads) k_chain_init(DModel m, DForces f, DS
 // finish_step (stepper.cpp:83-147).
 __global__ void __launch_bounds__(kThreads) k_chain_step(DModel m, DForces f, DSchedule sc, ChainLayout L, double* cw,
                                                          int* ci, long B, Outputs out) {
-  __shared__ double red[kRed * kEnvsPerBlock];
+  extern __shared__ __align__(16) double smem[];
+  stage_model(m, smem);
   bool valid;
-  const CK K = make_ck(m, f, sc, L, cw, ci, B, red, &valid);
+  const CK K = make_ck(m, f, sc, L, cw, ci, B, smem, &valid);
   if (!valid) return;
   if (ival(K, IS_RUN) != TR_RUNNING) return;
   const int n = m.n;
@@ -1057,15 +1099,36 @@ __global__ void __launch_bounds__(kThreads) k_chain_step(DModel m, DForces f, DS
 
 unsigned chain_grid(long B) { return (unsigned)((B + kEnvsPerBlock - 1) / kEnvsPerBlock); }
 
+static cudaError_t chain_smem_attr(int N, size_t* bytes) {
+  *bytes = chain_smem_bytes(N);
+  static size_t configured = 0;  // per process; raised monotonically
+  if (*bytes > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_chain_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*bytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_chain_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*bytes);
+    if (e != cudaSuccess) return e;
+    configured = *bytes;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_chain_init(const ChainArgs& a, const double* q0, const double* qdot0, const Outputs& out,
                               cudaStream_t s) {
-  k_chain_init<<<chain_grid(a.B), kThreads, 0, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, q0, qdot0, out);
+  size_t sm;
+  cudaError_t e = chain_smem_attr(a.m.N, &sm);
+  if (e != cudaSuccess) return e;
+  k_chain_init<<<chain_grid(a.B), kThreads, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, q0, qdot0, out);
   return cudaGetLastError();
 }
 cudaError_t launch_chain_step(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
-  k_chain_step<<<chain_grid(a.B), kThreads, 0, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, out);
+  size_t sm;
+  cudaError_t e = chain_smem_attr(a.m.N, &sm);
+  if (e != cudaSuccess) return e;
+  k_chain_step<<<chain_grid(a.B), kThreads, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, out);
   return cudaGetLastError();
 }
 int chain_max_memory() { return kMaxMem; }
+// links the shared-memory model copy admits (227 KB per block)
+int chain_max_links() { return (int)((227L * 1024 - smem_red_doubles() * 8) / (20 * 8 + 4)); }
 
 }  // namespace pbad_gpu

@@ -1,0 +1,1103 @@
+// pbad_chain4.cu -- warp-synchronous chain kernel ("v4") for serial chains of
+// axis-aligned hinges (energy form, L-BFGS): the C1/C2/C3 workloads.
+//
+// Same numeric contract and per-row mapping as pbad_chain.cu (four lanes per
+// environment, lane r owns row r of every 4x4 transform; eight environments
+// per warp), re-organised around the B200 memory system:
+//
+//  * the eight environments of a warp step their L-BFGS solvers in lockstep
+//    rounds (every round: directions for the environments that need one, one
+//    forward sweep, one reverse sweep if any line search accepted), so a
+//    sweep is a warp-collective operation with warp-uniform control flow;
+//  * the per-link state the reverse sweep needs (joint rotation (c, s),
+//    lever rows, inertial seed rows; rows 0..2 only -- row 3 of both is
+//    exactly zero) is written by the forward sweep as compact per-link
+//    records, contiguous per warp, and streamed back in descending 8-link
+//    chunks by TMA bulk copies (cp.async.bulk + mbarrier) into a 3-slot
+//    shared-memory ring, two chunks ahead of the adjoint recursion;
+//  * the history transforms are not stored: the forward sweep re-runs the
+//    forward kinematics of both history configurations (5 FP64 ops per row
+//    per link each) from their joint rotations, computed once per step;
+//  * the joint rotations of the current iterate (sqrt, sincos, two
+//    divisions) are computed chunk by chunk, each lane for its own two
+//    links, and broadcast through shared memory;
+//  * the link model (S, offset translation, class) lives in shared memory;
+//    the chunk body is compiled straight-line for the repeating link
+//    patterns of the reference's chain scenes (all Y-hinge bodies; massless
+//    Z connector + Y body) and dispatched per link otherwise.
+//
+// Every value is produced by the same operation sequence as the reference
+// (the dropped terms of the axis-aligned products are fma(x, +-0, acc) with
+// finite x, see pbad_chain.cu), so results are bit-identical to oracle/ and
+// to the reference build (tests/test_gpu_parity.py).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pbad_kernels.cuh"
+#include "pbad_launch.h"
+#include "pbad_math.cuh"
+
+namespace pbad_gpu {
+namespace c4 {
+
+enum { PH_DIR = 0, PH_GEN = 1, PH_EVAL = 2, PH_DONE = 3 };
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
+enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
+
+constexpr int kE = 8;   // environments per warp
+constexpr int kW = 2;   // warps per block
+constexpr int kT = 32 * kW;
+constexpr int CL = 8;   // links per chunk
+constexpr int kRing = 3;
+constexpr int kMaxMem = 16;
+constexpr long kGS = 32;  // vector group stride (doubles)
+constexpr int kU = 8;     // vector-loop unroll
+// per-link record (doubles): cs [env][2] | lev [3*env+row][2] | seed [3*env+row][4] (massive links)
+constexpr int kRecCS = 0, kRecLev = 16, kRecSd = 64;
+constexpr int kRecLight = 64, kRecMass = 160;
+constexpr int kSlot = CL * kRecMass;  // ring slot (doubles)
+// per-warp shared memory (doubles)
+constexpr int kFwdH = 0;                       // hist (c,s) of the chunk [CL][env][4]
+constexpr int kFwdC = kFwdH + CL * kE * 4;     // current (c,s) of the chunk [CL][env][2]
+constexpr int kFwdR = kFwdC + CL * kE * 2;     // energy row partials [CL][term][row][env]
+constexpr int kFwdEnd = kFwdR + CL * 16 * kE;  // (the forward buffers overlay the ring)
+constexpr int kRRed = kRing * kSlot;           // gradient row partials [CL][2][row][env]
+constexpr int kQScr = kRRed + CL * 2 * 4 * kE;  // per-environment scratch [env][16]
+constexpr int kBar = kQScr + kE * 16;          // mbarriers
+constexpr int kWarpD = kBar + 4;
+static_assert(kFwdEnd <= kRing * kSlot, "forward buffers must fit in the ring");
+constexpr int kHistW = 6;  // hist record per (link, env): c0 s0 | c1 s1 | cx sx
+
+__host__ __device__ inline size_t smem_bytes(int N) {
+  return (size_t)(kW * kWarpD + 20L * N) * sizeof(double) + (size_t)(2 * N + 1) * sizeof(int);
+}
+
+// ---- TMA bulk copy + mbarrier (sm_90+ PTX; SASS UBLKCP / SYNCS) -----------
+__device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(double* dst, const double* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  long spins = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(su32(bar)), "r"(parity)
+        : "memory");
+    if (!ok && ++spins > (1L << 28)) __trap();  // a lost transfer fails the launch instead of hanging
+  } while (!ok);
+}
+
+// ---- per-link joint algebra (axis-aligned hinge, identity offset rotation) --
+// rotation_coeffs (kinematics.cpp:20-45) for a unit-axis angle q: s = A q, c = 1 - B q^2
+__device__ __forceinline__ void hinge_cs(double q, double* c, double* s) {
+  const double k2 = q * q;
+  const double n = sqrt(k2);
+  const double n2 = n * n;
+  double A, B;
+  if (n < 1e-4) {
+    const double n4 = n2 * n2;
+    A = 1.0 - n2 / 6.0 + n4 / 120.0;
+    B = 0.5 - n2 / 24.0 + n4 / 720.0;
+  } else {
+    double sn, co;
+    pbad_sincos(n, &sn, &co);
+    A = sn / n;
+    B = (1.0 - co) / n2;
+  }
+  *s = A * q;
+  *c = 1.0 - B * k2;
+}
+
+// T <- T * L (row of the world transform; kinematics.cpp:171-181)
+template <int JK>
+__device__ __forceinline__ void fk(double c, double s, const double* t, double* T) {
+  double tc = T[0] * t[0];
+  tc = fma(T[1], t[1], tc);
+  tc = fma(T[2], t[2], tc);
+  tc = tc + T[3];
+  double n0, n1, n2;
+  if (JK == 1) {
+    n0 = T[0];
+    n1 = fma(T[2], s, T[1] * c);
+    n2 = fma(T[2], c, T[1] * (-s));
+  } else if (JK == 2) {
+    n0 = fma(T[2], -s, T[0] * c);
+    n1 = T[1];
+    n2 = fma(T[2], c, T[0] * s);
+  } else {
+    n0 = fma(T[1], s, T[0] * c);
+    n1 = fma(T[1], c, T[0] * (-s));
+    n2 = T[2];
+  }
+  T[0] = n0;
+  T[1] = n1;
+  T[2] = n2;
+  T[3] = tc;
+}
+// lever row T_parent * dL/dq: its two non-zero columns (adjoint.cpp:22-25)
+template <int JK>
+__device__ __forceinline__ void lever(double c, double s, const double* T, double& l0, double& l1) {
+  if (JK == 1) {
+    l0 = fma(T[2], c, T[1] * (-s));
+    l1 = fma(T[2], -s, T[1] * (-c));
+  } else if (JK == 2) {
+    l0 = fma(T[2], -c, T[0] * (-s));
+    l1 = fma(T[2], -s, T[0] * c);
+  } else {
+    l0 = fma(T[1], c, T[0] * (-s));
+    l1 = fma(T[1], -s, T[0] * (-c));
+  }
+}
+template <int JK>
+__device__ __forceinline__ double lever_dot(double l0, double l1, const double* a) {
+  if (JK == 1) return fma(l1, a[2], l0 * a[1]);
+  if (JK == 2) return fma(l1, a[2], l0 * a[0]);
+  return fma(l1, a[1], l0 * a[0]);
+}
+// o = a * L^T (adjoint transport to the parent, adjoint.cpp:49-64)
+template <int JK>
+__device__ __forceinline__ void transport(double c, double s, const double* t, const double* a, double* o) {
+  if (JK == 1) {
+    o[0] = fma(a[3], t[0], a[0]);
+    o[1] = fma(a[3], t[1], fma(a[2], -s, a[1] * c));
+    o[2] = fma(a[3], t[2], fma(a[2], c, a[1] * s));
+  } else if (JK == 2) {
+    o[0] = fma(a[3], t[0], fma(a[2], s, a[0] * c));
+    o[1] = fma(a[3], t[1], a[1]);
+    o[2] = fma(a[3], t[2], fma(a[2], c, a[0] * (-s)));
+  } else {
+    o[0] = fma(a[3], t[0], fma(a[1], -s, a[0] * c));
+    o[1] = fma(a[3], t[1], fma(a[1], c, a[0] * s));
+    o[2] = fma(a[3], t[2], a[2]);
+  }
+  o[3] = a[3];
+}
+// row of (a * S), S packed column-major
+__device__ __forceinline__ void row_s(const double* a, const double* S, double* out) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double acc = a[0] * S[4 * c];
+    acc = fma(a[1], S[1 + 4 * c], acc);
+    acc = fma(a[2], S[2 + 4 * c], acc);
+    acc = fma(a[3], S[3 + 4 * c], acc);
+    out[c] = acc;
+  }
+}
+__device__ __forceinline__ void lds16(const double* p, double* S) {
+#pragma unroll
+  for (int k = 0; k < 16; k += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(p + k);
+    S[k] = v.x;
+    S[k + 1] = v.y;
+  }
+}
+
+// ---- context ----------------------------------------------------------------
+struct Ctx {
+  int N, n, n4, r, e;
+  long ge, B;
+  bool valid;
+  unsigned qm;
+  double* ws;          // this warp's shared area
+  uint64_t* bar;       // kRing mbarriers
+  const double* mrec;  // shared model records [N][20]
+  const int* kind;     // shared link classes
+  const int* roff;     // shared record offsets [N+1]
+  double* rec;         // this warp's link records (global)
+  double* hist;        // this warp's history rotations [N][env][6] (global)
+  double *h0, *h1, *x, *g, *cand, *dir, *q, *evg, *tau, *hs, *hy;
+  long VS;
+  double* hsy;
+  double* histc;
+  int* ci;
+  double dt, inv_dt2, wm, gr;
+  double gz[3];
+  DOpt o;
+  unsigned nload;  // ring chunks consumed (warp-uniform; sets slot and phase)
+};
+
+__device__ __forceinline__ double qshfl(const Ctx& C, double v, int src) { return __shfl_sync(C.qm, v, src, 4); }
+__device__ __forceinline__ void qsync(const Ctx& C) { __syncwarp(C.qm); }
+__device__ __forceinline__ int& ival(const Ctx& C, int slot) { return C.ci[(long)slot * C.B + C.ge]; }
+__device__ __forceinline__ double& vat(const Ctx& C, double* V, int k) {
+  return V[(long)(k >> 2) * kGS + ((k & 3) - C.r)];
+}
+
+// ---- quad-local vector ops (32-partial canonical dot, optim.cpp) -----------
+__device__ __forceinline__ double qdot(const Ctx& C, const double* A, const double* Bv) {
+  double acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+  const int nf = C.n >> 2;
+  int g0 = 0;
+  for (; g0 + kU <= nf; g0 += kU) {
+    double a[kU], b[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      a[j] = A[(g0 + j) * kGS];
+      b[j] = Bv[(g0 + j) * kGS];
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) acc[j] = fma(a[j], b[j], acc[j]);
+  }
+  for (int gg = g0; gg < C.n4; ++gg)
+    if (4 * gg + C.r < C.n) acc[gg & 7] = fma(A[gg * kGS], Bv[gg * kGS], acc[gg & 7]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = acc[j] + acc[j + 4];
+  acc[0] = acc[0] + acc[2];
+  acc[1] = acc[1] + acc[3];
+  double v = acc[0] + acc[1];
+  const double v2 = qshfl(C, v, (C.r + 2) & 3);
+  if (C.r < 2) v = v + v2;
+  const double v1 = qshfl(C, v, 1);
+  if (C.r == 0) v = v + v1;
+  return qshfl(C, v, 0);
+}
+template <class F>
+__device__ __forceinline__ void qmap2(const Ctx& C, double* dst, const double* A, const double* Bv, F f) {
+  const int nf = C.n >> 2;
+  int g0 = 0;
+  for (; g0 + kU <= nf; g0 += kU) {
+    double a[kU], b[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      a[j] = A[(g0 + j) * kGS];
+      b[j] = Bv[(g0 + j) * kGS];
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) dst[(g0 + j) * kGS] = f(a[j], b[j]);
+  }
+  for (int gg = g0; gg < C.n4; ++gg)
+    if (4 * gg + C.r < C.n) dst[gg * kGS] = f(A[gg * kGS], Bv[gg * kGS]);
+}
+__device__ __forceinline__ double qinfnorm(const Ctx& C, const double* A) {
+  double mx = 0.0;
+  for (int g0 = 0; g0 < C.n4; g0 += kU) {
+    double a[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int gg = g0 + j;
+      a[j] = (gg < C.n4 && 4 * gg + C.r < C.n) ? A[gg * kGS] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) mx = fmax(mx, fabs(a[j]));
+  }
+  mx = fmax(mx, qshfl(C, mx, C.r ^ 1));
+  mx = fmax(mx, qshfl(C, mx, C.r ^ 2));
+  return mx;
+}
+__device__ __forceinline__ bool qallfinite(const Ctx& C, const double* A) {
+  bool ok = true;
+  for (int g0 = 0; g0 < C.n4; g0 += kU) {
+    double a[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int gg = g0 + j;
+      a[j] = (gg < C.n4 && 4 * gg + C.r < C.n) ? A[gg * kGS] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) ok = ok && isfinite(a[j]);
+  }
+  return __all_sync(C.qm, ok);
+}
+
+// ---- forward sweep ------------------------------------------------------------
+// StepObjective::value at X (objective.cpp:215-239), storing the reverse
+// sweep's per-link records.  Rows: T (current), A = FK(hist1) ("tk"),
+// H = FK(hist0) ("tk1").
+struct Rows {
+  double T[4], A[4], H[4];
+};
+
+template <int CK>
+__device__ __forceinline__ void fwd_link(const Ctx& C, int j, int i, Rows& R) {
+  constexpr int JK = CK & 3;
+  constexpr bool SK = (CK >> 2) != 0;
+  const double2 cs = *reinterpret_cast<const double2*>(C.ws + kFwdC + (j * kE + C.e) * 2);
+  const double* hb = C.ws + kFwdH + (j * kE + C.e) * 4;
+  const double2 hc0 = *reinterpret_cast<const double2*>(hb);
+  const double2 hc1 = *reinterpret_cast<const double2*>(hb + 2);
+  const double* mr = C.mrec + 20 * i;
+  const double2 t01 = *reinterpret_cast<const double2*>(mr + 16);
+  const double t[3] = {t01.x, t01.y, mr[18]};
+  double* rp = C.rec + C.roff[i];
+  const int row = 3 * C.e + C.r;
+  double l0, l1;
+  lever<JK>(cs.x, cs.y, R.T, l0, l1);
+  if (C.r < 3) *reinterpret_cast<double2*>(rp + kRecLev + 2 * row) = make_double2(l0, l1);
+  fk<JK>(cs.x, cs.y, t, R.T);
+  fk<JK>(hc1.x, hc1.y, t, R.A);
+  fk<JK>(hc0.x, hc0.y, t, R.H);
+  if (SK) {
+    double S[16];
+    lds16(mr, S);
+    double ts[4], p1[4], p2[4], cg[4];
+    row_s(R.T, S, ts);
+    row_s(R.A, S, p1);
+    row_s(R.H, S, p2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cg[k] = (-C.gr) * S[12 + k];
+    double* fr = C.ws + kFwdR + j * 128 + C.r * 8 + C.e;
+    fr[0] = ddot_row(ts, R.T);
+    fr[32] = ddot_row(p1, R.T);
+    fr[64] = ddot_row(p2, R.T);
+    fr[96] = ddot_row(cg, R.T);
+    double dd[4], sd[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      dd[k] = R.T[k] - 2.0 * R.A[k];
+      dd[k] = dd[k] + R.H[k];
+      dd[k] = C.inv_dt2 * dd[k];
+    }
+    row_s(dd, S, sd);
+    if (C.r < 3) {
+      double* sp = rp + kRecSd + 4 * row;
+      *reinterpret_cast<double2*>(sp) = make_double2(sd[0], sd[1]);
+      *reinterpret_cast<double2*>(sp + 2) = make_double2(sd[2], sd[3]);
+    }
+  }
+}
+
+__device__ __forceinline__ void fwd_link_dyn(const Ctx& C, int j, int i, Rows& R) {
+  switch (C.kind[i]) {
+    case 1: fwd_link<1>(C, j, i, R); break;
+    case 2: fwd_link<2>(C, j, i, R); break;
+    case 3: fwd_link<3>(C, j, i, R); break;
+    case 5: fwd_link<5>(C, j, i, R); break;
+    case 6: fwd_link<6>(C, j, i, R); break;
+    default: fwd_link<7>(C, j, i, R); break;
+  }
+}
+
+// link-pattern code: P | K0 << 2 | K1 << 5 (P = period 1 or 2; 0 = per-link dispatch)
+template <int PAT, int J>
+struct PatKind {
+  static constexpr int P = PAT & 3;
+  static constexpr int value = (P == 2 && (J & 1)) ? ((PAT >> 5) & 7) : ((PAT >> 2) & 7);
+};
+template <int PAT, int J>
+struct FwdUnroll {
+  static __device__ __forceinline__ void run(const Ctx& C, int lo, Rows& R) {
+    fwd_link<PatKind<PAT, J>::value>(C, J, lo + J, R);
+    FwdUnroll<PAT, J + 1>::run(C, lo, R);
+  }
+};
+template <int PAT>
+struct FwdUnroll<PAT, CL> {
+  static __device__ __forceinline__ void run(const Ctx&, int, Rows&) {}
+};
+
+template <int PAT>
+__device__ __forceinline__ void fwd_chunk(const Ctx& C, int lo, int cnt, Rows& R) {
+  if constexpr ((PAT & 3) != 0) {
+    if (cnt == CL) {
+      FwdUnroll<PAT, 0>::run(C, lo, R);
+      return;
+    }
+  }
+  for (int j = 0; j < cnt; ++j) fwd_link_dyn(C, j, lo + j, R);
+}
+
+template <int PAT>
+__device__ __forceinline__ double forward(const Ctx& C, const double* X) {
+  const int N = C.N;
+  const int nch = (N + CL - 1) / CL;
+  Rows R;
+  R.T[0] = (C.r == 0) ? 1.0 : 0.0;
+  R.T[1] = (C.r == 1) ? 1.0 : 0.0;
+  R.T[2] = (C.r == 2) ? 1.0 : 0.0;
+  R.T[3] = (C.r == 3) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) R.A[k] = R.H[k] = R.T[k];
+  double sum = 0.0;  // lane t: running sum of energy term t
+  // this lane's two links of chunk c: 8c + r and 8c + 4 + r (its own elements of X)
+  double xa = 0.0, xb = 0.0;
+  double2 ha0 = make_double2(0.0, 0.0), ha1 = ha0, hb0 = ha0, hb1 = ha0;
+  auto fetch = [&](int c) {
+    const int la = CL * c + C.r, lb = la + 4;
+    if (la < N) {
+      xa = X[(long)(2 * c) * kGS];
+      const double* hp = C.hist + ((long)la * kE + C.e) * kHistW;
+      ha0 = *reinterpret_cast<const double2*>(hp);
+      ha1 = *reinterpret_cast<const double2*>(hp + 2);
+    }
+    if (lb < N) {
+      xb = X[(long)(2 * c + 1) * kGS];
+      const double* hp = C.hist + ((long)lb * kE + C.e) * kHistW;
+      hb0 = *reinterpret_cast<const double2*>(hp);
+      hb1 = *reinterpret_cast<const double2*>(hp + 2);
+    }
+  };
+  fetch(0);
+  for (int c = 0; c < nch; ++c) {
+    const int lo = CL * c, cnt = min(CL, N - lo);
+    const int la = lo + C.r, lb = la + 4;
+    // phase A: joint rotations of this lane's two links
+    double ca, sa, cb, sb;
+    hinge_cs(xa, &ca, &sa);
+    hinge_cs(xb, &cb, &sb);
+    const double2 h_a0 = ha0, h_a1 = ha1, h_b0 = hb0, h_b1 = hb1;
+    if (c + 1 < nch) fetch(c + 1);
+    __syncwarp();  // previous chunk's readers are done with the buffers
+    if (la < N) {
+      *reinterpret_cast<double2*>(C.ws + kFwdC + (C.r * kE + C.e) * 2) = make_double2(ca, sa);
+      double* hb = C.ws + kFwdH + (C.r * kE + C.e) * 4;
+      *reinterpret_cast<double2*>(hb) = h_a0;
+      *reinterpret_cast<double2*>(hb + 2) = h_a1;
+      *reinterpret_cast<double2*>(C.rec + C.roff[la] + kRecCS + 2 * C.e) = make_double2(ca, sa);
+    }
+    if (lb < N) {
+      *reinterpret_cast<double2*>(C.ws + kFwdC + ((C.r + 4) * kE + C.e) * 2) = make_double2(cb, sb);
+      double* hb = C.ws + kFwdH + ((C.r + 4) * kE + C.e) * 4;
+      *reinterpret_cast<double2*>(hb) = h_b0;
+      *reinterpret_cast<double2*>(hb + 2) = h_b1;
+      *reinterpret_cast<double2*>(C.rec + C.roff[lb] + kRecCS + 2 * C.e) = make_double2(cb, sb);
+    }
+    __syncwarp();
+    // phase B: the serial recursions over the chunk
+    fwd_chunk<PAT>(C, lo, cnt, R);
+    __syncwarp();
+    // lane t adds term t of each massive link, link by link (serial order)
+    for (int j = 0; j < cnt; ++j) {
+      if (C.kind[lo + j] >> 2) {
+        const double* b = C.ws + kFwdR + j * 128 + C.r * 32 + C.e;
+        sum += ((b[0] + b[8]) + b[16]) + b[24];
+      }
+    }
+  }
+  const double sa = qshfl(C, sum, 0), sb = qshfl(C, sum, 1), sc = qshfl(C, sum, 2), sg = qshfl(C, sum, 3);
+  const double wm = C.wm;
+  const double cpp = sa - wm, c1p = sb - wm, c2p = sc - wm;
+  const double inertial = 0.5 * C.inv_dt2 * (cpp - 4.0 * c1p + 2.0 * c2p + *C.histc);
+  const double tdx = qdot(C, C.tau, X);
+  return inertial + sg - tdx;
+}
+
+// ---- reverse sweep ------------------------------------------------------------
+// functional_grad twice (adjoint.cpp:49-64): gradient = inertial adjoint +
+// gravity adjoint - tau (objective.cpp:241-250) into Gv.
+template <int CK>
+__device__ __forceinline__ void rev_link(const Ctx& C, const double* rp, int i, int jl, double* cI, double* cG) {
+  constexpr int JK = CK & 3;
+  constexpr bool SK = (CK >> 2) != 0;
+  const double2 cs = *reinterpret_cast<const double2*>(rp + kRecCS + 2 * C.e);
+  const int row = 3 * C.e + C.r;
+  const bool own = C.r < 3;  // row 3 of the lever and of the seed is exactly zero
+  double l0 = 0.0, l1 = 0.0;
+  if (own) {
+    const double2 lv = *reinterpret_cast<const double2*>(rp + kRecLev + 2 * row);
+    l0 = lv.x;
+    l1 = lv.y;
+  }
+  const double* mr = C.mrec + 20 * i;
+  double aI[4], aG[4];
+  if (SK) {
+    double sd[4] = {0.0, 0.0, 0.0, 0.0};
+    if (own) {
+      const double2 s01 = *reinterpret_cast<const double2*>(rp + kRecSd + 4 * row);
+      const double2 s23 = *reinterpret_cast<const double2*>(rp + kRecSd + 4 * row + 2);
+      sd[0] = s01.x;
+      sd[1] = s01.y;
+      sd[2] = s23.x;
+      sd[3] = s23.y;
+    }
+    const double2 u01 = *reinterpret_cast<const double2*>(mr + 12);
+    const double2 u23 = *reinterpret_cast<const double2*>(mr + 14);
+    const double u[4] = {u01.x, u01.y, u23.x, u23.y};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      aI[k] = cI[k] + sd[k];
+      aG[k] = cG[k] + (0.0 + (-C.gr) * u[k]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      aI[k] = cI[k];
+      aG[k] = cG[k];
+    }
+  }
+  double* rr = C.ws + kRRed + jl * 64 + C.r * 8 + C.e;
+  rr[0] = lever_dot<JK>(l0, l1, aI);
+  rr[32] = lever_dot<JK>(l0, l1, aG);
+  if (i > 0) {
+    const double2 t01 = *reinterpret_cast<const double2*>(mr + 16);
+    const double t[3] = {t01.x, t01.y, mr[18]};
+    double tI[4], tG[4];
+    transport<JK>(cs.x, cs.y, t, aI, tI);
+    transport<JK>(cs.x, cs.y, t, aG, tG);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      cI[k] = 0.0 + tI[k];
+      cG[k] = 0.0 + tG[k];
+    }
+  }
+}
+
+__device__ __forceinline__ void rev_link_dyn(const Ctx& C, const double* rp, int i, int jl, double* cI, double* cG) {
+  switch (C.kind[i]) {
+    case 1: rev_link<1>(C, rp, i, jl, cI, cG); break;
+    case 2: rev_link<2>(C, rp, i, jl, cI, cG); break;
+    case 3: rev_link<3>(C, rp, i, jl, cI, cG); break;
+    case 5: rev_link<5>(C, rp, i, jl, cI, cG); break;
+    case 6: rev_link<6>(C, rp, i, jl, cI, cG); break;
+    default: rev_link<7>(C, rp, i, jl, cI, cG); break;
+  }
+}
+
+template <int PAT, int J>
+struct RevUnroll {  // links J, J-1, ..., 0 of a full chunk
+  static __device__ __forceinline__ void run(const Ctx& C, const double* sbase, int lo, double* cI, double* cG) {
+    rev_link<PatKind<PAT, J>::value>(C, sbase + C.roff[lo + J], lo + J, J, cI, cG);
+    RevUnroll<PAT, J - 1>::run(C, sbase, lo, cI, cG);
+  }
+};
+template <int PAT>
+struct RevUnroll<PAT, -1> {
+  static __device__ __forceinline__ void run(const Ctx&, const double*, int, double*, double*) {}
+};
+
+template <int PAT>
+__device__ __forceinline__ void rev_chunk(const Ctx& C, const double* sbase, int lo, int cnt, double* cI,
+                                          double* cG) {
+  if constexpr ((PAT & 3) != 0) {
+    if (cnt == CL) {
+      RevUnroll<PAT, CL - 1>::run(C, sbase, lo, cI, cG);
+      return;
+    }
+  }
+  for (int j = cnt - 1; j >= 0; --j) rev_link_dyn(C, sbase + C.roff[lo + j], lo + j, j, cI, cG);
+}
+
+__device__ __forceinline__ void issue_chunk(Ctx& C, int c, unsigned k) {
+  const int lo = CL * c, hi = min(C.N, lo + CL);
+  const int slot = (int)(k % kRing);
+  const unsigned bytes = (unsigned)(C.roff[hi] - C.roff[lo]) * 8u;
+  bulk_load(C.ws + slot * kSlot, C.rec + C.roff[lo], bytes, C.bar + slot);
+}
+
+template <int PAT>
+__device__ __forceinline__ void reverse(Ctx& C, double* Gv) {
+  const int N = C.N;
+  const int nch = (N + CL - 1) / CL;
+  fence_async_global();  // this lane's record stores -> the bulk copies below
+  __syncwarp();
+  const unsigned k0 = C.nload;
+  if ((threadIdx.x & 31) == 0) {
+    fence_async_smem();  // forward-buffer accesses in the ring area before the async writes
+    for (int p = 0; p < kRing && p < nch; ++p) issue_chunk(C, nch - 1 - p, k0 + p);
+  }
+  double cI[4] = {0.0, 0.0, 0.0, 0.0}, cG[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int idx = 0; idx < nch; ++idx) {
+    const int c = nch - 1 - idx;
+    const int lo = CL * c, cnt = min(CL, N - lo);
+    const unsigned k = k0 + idx;
+    const int slot = (int)(k % kRing);
+    mbar_wait(C.bar + slot, (k / kRing) & 1u);
+    const double* sbase = C.ws + slot * kSlot - C.roff[lo];
+    rev_chunk<PAT>(C, sbase, lo, cnt, cI, cG);
+    __syncwarp();
+    // gradient entries of this lane's two links of the chunk
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int jl = C.r + 4 * h;
+      if (jl < cnt) {
+        const double* b = C.ws + kRRed + jl * 64 + C.e;
+        const double gi = 0.0 + (((b[0] + b[8]) + b[16]) + b[24]);
+        const double gp = 0.0 + (((b[32] + b[40]) + b[48]) + b[56]);
+        const long go = (long)(2 * c + h) * kGS;
+        Gv[go] = (gi + gp) - C.tau[go];
+      }
+    }
+    __syncwarp();
+    if (idx + kRing < nch && (threadIdx.x & 31) == 0) {
+      fence_async_smem();
+      issue_chunk(C, c - kRing, k + kRing);
+    }
+  }
+  C.nload = k0 + nch;
+}
+
+// ---- per-step history passes (once per PBAD step) ---------------------------
+// joint rotations of vector V into hist slot `slot` (0: hist0, 1: hist1, 2: x)
+__device__ __forceinline__ void hist_rotations(const Ctx& C, const double* V, int slot) {
+  for (int i = C.r; i < C.N; i += 4) {
+    double c, s;
+    hinge_cs(V[(long)(i >> 2) * kGS], &c, &s);
+    *reinterpret_cast<double2*>(C.hist + ((long)i * kE + C.e) * kHistW + 2 * slot) = make_double2(c, s);
+  }
+  qsync(C);
+}
+
+__device__ __forceinline__ void fk_dyn(int jk, double c, double s, const double* t, double* T) {
+  if (jk == 1) fk<1>(c, s, t, T);
+  else if (jk == 2) fk<2>(c, s, t, T);
+  else fk<3>(c, s, t, T);
+}
+
+// hist_const = 4 cv(tk, tk) + cv(tk1, tk1) - 4 cv(tk, tk1) (objective.cpp:162-185),
+// tk = FK(hist1), tk1 = FK(hist0); massless links add exact zeros and are skipped
+__device__ __forceinline__ double hist_const(const Ctx& C) {
+  double A[4], H[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) A[k] = H[k] = (C.r == k) ? 1.0 : 0.0;
+  double vAA = 0.0, vHH = 0.0, vAH = 0.0;
+  double* qs = C.ws + kQScr + C.e * 16;
+  for (int i = 0; i < C.N; ++i) {
+    const int ck = C.kind[i];
+    const double* hp = C.hist + ((long)i * kE + C.e) * kHistW;
+    const double* mr = C.mrec + 20 * i;
+    const double t[3] = {mr[16], mr[17], mr[18]};
+    fk_dyn(ck & 3, hp[2], hp[3], t, A);
+    fk_dyn(ck & 3, hp[0], hp[1], t, H);
+    if (ck >> 2) {
+      double S[16], as[4], hs[4];
+      lds16(mr, S);
+      row_s(A, S, as);
+      row_s(H, S, hs);
+      qsync(C);
+      qs[3 * C.r] = ddot_row(as, A);
+      qs[3 * C.r + 1] = ddot_row(hs, H);
+      qs[3 * C.r + 2] = ddot_row(as, H);
+      qsync(C);
+      vAA += ((qs[0] + qs[3]) + qs[6]) + qs[9];
+      vHH += ((qs[1] + qs[4]) + qs[7]) + qs[10];
+      vAH += ((qs[2] + qs[5]) + qs[8]) + qs[11];
+    }
+  }
+  qsync(C);
+  return 4.0 * (vAA - C.wm) + (vHH - C.wm) - 4.0 * (vAH - C.wm);
+}
+
+// fd_kinetic (stepper.cpp:14-22) + gravity_potential (baseline.cpp:219-229)
+// between FK(hist slot 1) and FK(hist slot 2)
+__device__ __forceinline__ void step_energy(const Ctx& C, double* ke, double* pe) {
+  double P[4], W[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) P[k] = W[k] = (C.r == k) ? 1.0 : 0.0;
+  double kk = 0.0, pp = 0.0;
+  const double ghat[4] = {C.gz[0], C.gz[1], C.gz[2], 0.0};
+  double* qs = C.ws + kQScr + C.e * 16;
+  for (int i = 0; i < C.N; ++i) {
+    const int ck = C.kind[i];
+    const double* hp = C.hist + ((long)i * kE + C.e) * kHistW;
+    const double* mr = C.mrec + 20 * i;
+    const double t[3] = {mr[16], mr[17], mr[18]};
+    fk_dyn(ck & 3, hp[2], hp[3], t, P);
+    fk_dyn(ck & 3, hp[4], hp[5], t, W);
+    if (ck >> 2) {
+      double S[16], td[4], tds[4];
+      lds16(mr, S);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) td[c] = (W[c] - P[c]) / C.dt;
+      row_s(td, S, tds);
+      double wu = W[0] * S[12];
+      wu = fma(W[1], S[13], wu);
+      wu = fma(W[2], S[14], wu);
+      wu = fma(W[3], S[15], wu);
+      qsync(C);
+      qs[C.r] = ddot_row(tds, td);
+      qs[4 + C.r] = wu;
+      qsync(C);
+      const double term = ((qs[0] + qs[1]) + qs[2]) + qs[3];
+      double d = ghat[0] * qs[4];
+      d = fma(ghat[1], qs[5], d);
+      d = fma(ghat[2], qs[6], d);
+      d = fma(ghat[3], qs[7], d);
+      kk += 0.5 * term;
+      pp -= d;
+    }
+  }
+  qsync(C);
+  *ke = kk;
+  *pe = pp;
+}
+
+// ForceModel::tau_at (objective.hpp:28-58)
+__device__ __forceinline__ void tau_at(const Ctx& C, const DForces& f, double t) {
+  const int n = C.n;
+  for (int i = C.r; i < n; i += 4) {
+    double v;
+    if (f.has_act && f.act_len == n) {
+      if (f.act_kind == 0) {
+        v = f.act_amp[i];
+      } else {
+        const double ph = i < f.act_phase_len ? f.act_phase[i] : 0.0;
+        double s, c;
+        pbad_sincos(2.0 * 3.141592653589793 * f.act_freq * t + ph, &s, &c);
+        v = f.act_amp[i] * s;
+      }
+    } else if (f.tau_len == n) {
+      v = f.tau[i];
+    } else {
+      v = 0.0;
+    }
+    vat(C, C.tau, i) = v;
+  }
+}
+
+// ---- L-BFGS (LbfgsSolver, optim.cpp:141-232) ------------------------------
+struct Solver {
+  double value, grad0, t, slope, fval;
+  int status, iters, stag, acc, h0, hc, trial, phase;
+};
+
+__device__ __forceinline__ bool grad_converged(const Ctx& C, const Solver& s) {
+  const double g = qinfnorm(C, C.g);
+  if (g <= C.o.grad_tol * fmax(1.0, qinfnorm(C, C.x))) return true;
+  if (C.o.grad_rtol > 0.0 && g <= C.o.grad_rtol * s.grad0) return true;
+  return false;
+}
+
+// two_loop (optim.cpp:213-229): q = H g
+__device__ __forceinline__ void two_loop(const Ctx& C, const Solver& s) {
+  const int cap = C.o.mem + 1;
+  qmap2(C, C.q, C.g, C.g, [](double a, double) { return a; });
+  double alpha[kMaxMem];
+  for (int i = s.hc - 1; i >= 0; --i) {
+    const int slot = (s.h0 + i) % cap;
+    const double* sv = C.hs + slot * C.VS;
+    const double* yv = C.hy + slot * C.VS;
+    const double a = qdot(C, sv, C.q) / C.hsy[slot * C.B];
+    alpha[i] = a;
+    qmap2(C, C.q, C.q, yv, [a](double qv, double y) { return qv - a * y; });
+  }
+  if (s.hc > 0) {
+    const int slot = (s.h0 + s.hc - 1) % cap;
+    const double* yv = C.hy + slot * C.VS;
+    const double scl = C.hsy[slot * C.B] / qdot(C, yv, yv);
+    qmap2(C, C.q, C.q, C.q, [scl](double qv, double) { return qv * scl; });
+  }
+  for (int i = 0; i < s.hc; ++i) {
+    const int slot = (s.h0 + i) % cap;
+    const double* sv = C.hs + slot * C.VS;
+    const double* yv = C.hy + slot * C.VS;
+    const double beta = qdot(C, yv, C.q) / C.hsy[slot * C.B];
+    const double c = alpha[i] - beta;
+    qmap2(C, C.q, C.q, sv, [c](double qv, double sv2) { return qv + c * sv2; });
+  }
+}
+
+// start of LbfgsSolver::iterate: termination tests, direction, slope
+__device__ __forceinline__ void begin_iteration(const Ctx& C, Solver& s) {
+  if (s.iters >= C.o.max_iters) {
+    s.status = ST_FAILED;
+    s.phase = PH_DONE;
+    return;
+  }
+  if (grad_converged(C, s)) {
+    s.status = ST_CONVERGED;
+    s.phase = PH_DONE;
+    return;
+  }
+  two_loop(C, s);
+  qmap2(C, C.dir, C.q, C.q, [](double qv, double) { return -qv; });
+  double slope = qdot(C, C.dir, C.g);
+  if (!(slope < 0.0)) {
+    s.hc = 0;
+    s.h0 = 0;
+    qmap2(C, C.dir, C.g, C.g, [](double gv, double) { return -gv; });
+    slope = qdot(C, C.dir, C.g);
+  }
+  s.slope = slope;
+  s.t = 1.0;
+  s.trial = 0;
+  s.fval = s.value;
+  s.phase = PH_GEN;
+}
+
+// next finite candidate x + t dir of the backtracking line search
+__device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
+  while (s.trial < C.o.max_line_search) {
+    const double t = s.t;
+    qmap2(C, C.cand, C.x, C.dir, [t](double xv, double dv) { return xv + t * dv; });
+    if (qallfinite(C, C.cand)) {
+      s.phase = PH_EVAL;
+      return;
+    }
+    s.t *= C.o.backtrack_factor;
+    ++s.trial;
+  }
+  s.status = ST_FAILED;  // no acceptable step
+  ++s.iters;
+  s.phase = PH_DONE;
+}
+
+// accepted step: history pair, iterate, stagnation test (optim.cpp:176-205)
+__device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
+  const int cap = C.o.mem + 1;
+  const int slot = (s.h0 + s.hc) % cap;
+  double* sv = C.hs + slot * C.VS;
+  double* yv = C.hy + slot * C.VS;
+  const double t = s.t;
+  qmap2(C, sv, C.dir, C.dir, [t](double dv, double) { return t * dv; });
+  qmap2(C, yv, C.evg, C.g, [](double ev, double gv) { return ev - gv; });
+  const double sy = qdot(C, sv, yv);
+  if (sy > 1e-12) {
+    if (C.r == 0) C.hsy[slot * C.B] = sy;
+    ++s.hc;
+    if (s.hc > C.o.mem) {
+      s.h0 = (s.h0 + 1) % cap;
+      --s.hc;
+    }
+  }
+  qmap2(C, C.x, C.cand, C.cand, [](double cv, double) { return cv; });
+  qmap2(C, C.g, C.evg, C.evg, [](double ev, double) { return ev; });
+  qsync(C);
+  const double oldv = s.fval;
+  s.value = v;
+  ++s.acc;
+  if (oldv - v <= C.o.ftol * fmax(1.0, fabs(oldv))) ++s.stag;
+  else s.stag = 0;
+  if (s.stag >= 2) s.status = ST_CONVERGED;
+  ++s.iters;
+  if (s.status == ST_RUNNING && s.iters >= C.o.max_iters) s.status = ST_FAILED;
+  s.phase = (s.status == ST_RUNNING) ? PH_DIR : PH_DONE;
+}
+
+__device__ __forceinline__ Ctx make_ctx(const DModel& m, const DForces& f, const DSchedule& sc, const ChainLayout& L,
+                                        double* cw, int* ci, long B, double* smem) {
+  Ctx C;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  C.N = m.N;
+  C.n = m.n;
+  C.n4 = (m.n + 3) >> 2;
+  C.r = lane & 3;
+  C.e = lane >> 2;
+  const long w = (long)blockIdx.x * kW + wib;
+  C.ge = w * kE + C.e;
+  C.B = B;
+  C.valid = C.ge < B;
+  C.qm = 0xFu << (lane & ~3);
+  C.ws = smem + (long)wib * kWarpD;
+  C.bar = reinterpret_cast<uint64_t*>(C.ws + kBar);
+  C.mrec = smem + (long)kW * kWarpD;
+  C.kind = reinterpret_cast<const int*>(C.mrec + 20L * m.N);
+  C.roff = C.kind + m.N;
+  C.rec = cw + L.rec + w * L.rec_w;
+  C.hist = cw + L.hist + w * (long)m.N * kE * kHistW;
+  const long vl = w * (long)C.n4 * kGS + lane;
+  C.h0 = cw + L.h0 + vl;
+  C.h1 = cw + L.h1 + vl;
+  C.x = cw + L.x + vl;
+  C.g = cw + L.g + vl;
+  C.cand = cw + L.cand + vl;
+  C.dir = cw + L.dir + vl;
+  C.q = cw + L.q + vl;
+  C.evg = cw + L.evg + vl;
+  C.tau = cw + L.tau + vl;
+  C.hs = cw + L.hs + vl;
+  C.hy = cw + L.hy + vl;
+  C.VS = L.vstride;
+  // per-env scalars; padded environments (ge >= B) point at env 0 and never write
+  const long es = C.valid ? C.ge : 0;
+  C.hsy = cw + L.hsy + es;
+  C.histc = cw + L.histc + es;
+  C.ci = ci;
+  C.dt = sc.dt;
+  C.inv_dt2 = 1.0 / (sc.dt * sc.dt);
+  C.wm = m.weighted_mass;
+  C.gz[0] = f.gravity[0];
+  C.gz[1] = f.gravity[1];
+  C.gz[2] = f.gravity[2];
+  C.gr = (C.r == 0) ? f.gravity[0] : (C.r == 1) ? f.gravity[1] : (C.r == 2) ? f.gravity[2] : 0.0;
+  C.o = sc.opt;
+  C.nload = 0;
+  return C;
+}
+
+__device__ __forceinline__ void stage(const DModel& m, double* smem) {
+  double* rec = smem + (long)kW * kWarpD;
+  int* kind = reinterpret_cast<int*>(rec + 20L * m.N);
+  int* roff = kind + m.N;
+  const double2* src = reinterpret_cast<const double2*>(m.crec);
+  double2* dst = reinterpret_cast<double2*>(rec);
+  for (int k = threadIdx.x; k < 10 * m.N; k += blockDim.x) dst[k] = __ldg(src + k);
+  for (int k = threadIdx.x; k < m.N; k += blockDim.x) kind[k] = __ldg(m.ckind + k);
+  for (int k = threadIdx.x; k <= m.N; k += blockDim.x) roff[k] = __ldg(m.croff + k);
+  if ((threadIdx.x & 31) == 0) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (long)(threadIdx.x >> 5) * kWarpD + kBar);
+    for (int s = 0; s < kRing; ++s) mbar_init(bar + s);
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// One PBAD step for every environment of the warp: begin_step, L-BFGS to
+// completion in lockstep rounds, finish_step (stepper.cpp:83-147).
+template <int PAT>
+__global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedule sc, ChainLayout L, double* cw,
+                                                    int* ci, long B, Outputs out) {
+  extern __shared__ __align__(16) double smem[];
+  stage(m, smem);
+  Ctx C = make_ctx(m, f, sc, L, cw, ci, B, smem);
+  // a warp with no running environment has nothing to do (warp-uniform exit)
+  bool active = C.valid && ival(C, IS_RUN) == TR_RUNNING;
+  if (!__any_sync(0xffffffffu, active)) return;
+  const int n = m.n;
+  const int step = C.valid ? ival(C, IS_STEP) : 0;
+  if (active) {
+    // StepObjective ctor validates the history (objective.cpp:176-177)
+    if (!qallfinite(C, C.h0) || !qallfinite(C, C.h1)) {
+      if (C.r == 0) ival(C, IS_RUN) = TR_NONFINITE_CFG;
+      active = false;
+    }
+  }
+  if (active) {
+    // begin_step: actuation at the step end, warm start (stepper.cpp:83-115)
+    tau_at(C, f, step * sc.dt + sc.times[2] * sc.dt);
+    const double span = -sc.times[0];
+    const double tau_m = sc.times[2];
+    const bool ws = sc.warm_start != 0;
+    qmap2(C, C.x, C.h1, C.h0,
+          [tau_m, span, ws](double h1, double h0) { return ws ? h1 + (tau_m / span) * (h1 - h0) : h1; });
+    qsync(C);
+    hist_rotations(C, C.h0, 0);
+    hist_rotations(C, C.h1, 1);
+    const double hc = hist_const(C);
+    if (C.r == 0) *C.histc = hc;
+    qsync(C);
+    if (!qallfinite(C, C.x)) {
+      if (C.r == 0) ival(C, IS_RUN) = TR_NONFINITE_CFG;
+      active = false;
+    }
+  }
+  __syncwarp();
+  // LbfgsSolver ctor: first evaluation (warp-collective sweeps)
+  Solver s{};
+  s.status = ST_RUNNING;
+  s.phase = PH_DIR;
+  const double v0 = forward<PAT>(C, C.x);
+  reverse<PAT>(C, C.g);
+  if (active && !isfinite(v0)) {
+    if (C.r == 0) ival(C, IS_RUN) = TR_NONFINITE_INIT;
+    active = false;
+  }
+  if (active) {
+    s.value = v0;
+    s.grad0 = qinfnorm(C, C.g);
+  } else {
+    s.phase = PH_DONE;
+  }
+  for (;;) {
+    if (s.phase == PH_DIR) begin_iteration(C, s);
+    if (s.phase == PH_GEN) next_candidate(C, s);
+    __syncwarp();
+    const bool eval = s.phase == PH_EVAL;
+    if (!__any_sync(0xffffffffu, eval)) break;
+    const double v = forward<PAT>(C, C.cand);
+    bool acc = false;
+    if (eval) {
+      if (isfinite(v) && v <= s.fval + C.o.armijo_c1 * s.t * s.slope && v < s.fval) {
+        acc = true;
+      } else {
+        s.t *= C.o.backtrack_factor;
+        ++s.trial;
+        s.phase = PH_GEN;
+      }
+    }
+    if (__any_sync(0xffffffffu, acc)) reverse<PAT>(C, C.evg);
+    if (acc) accept_step(C, s, v);
+    __syncwarp();
+  }
+  if (!active) return;
+  // finish_step
+  const long S = sc.total_steps;
+  const bool converged = s.status == ST_CONVERGED;
+  const double gnorm = qinfnorm(C, C.g);
+  if (C.r == 0) {
+    if (out.iterations) out.iterations[C.ge * S + step] = s.iters;
+    if (out.converged) out.converged[C.ge * S + step] = converged;
+    if (out.accepted) out.accepted[C.ge * S + step] = s.acc;
+    if (out.final_value) out.final_value[C.ge * S + step] = s.value;
+    if (out.final_grad_norm) out.final_grad_norm[C.ge * S + step] = gnorm;
+    ival(C, IS_NREP) = step + 1;
+  }
+  const int fs = converged ? 0 : ival(C, IS_FAIL) + 1;
+  qsync(C);
+  if (C.r == 0) ival(C, IS_FAIL) = fs;
+  if (fs > sc.fail_limit) {
+    if (C.r == 0) ival(C, IS_RUN) = TR_FAIL_LIMIT;
+    return;
+  }
+  hist_rotations(C, C.x, 2);
+  double ke, pe;
+  step_energy(C, &ke, &pe);
+  qmap2(C, C.h0, C.h1, C.h1, [](double a, double) { return a; });
+  qsync(C);
+  qmap2(C, C.h1, C.x, C.x, [](double a, double) { return a; });
+  qsync(C);
+  const long S1 = S + 1;
+  for (int k = C.r; k < n; k += 4)
+    if (out.q) out.q[(C.ge * S1 + step + 1) * n + k] = vat(C, C.h1, k);
+  if (C.r == 0) {
+    if (out.energy) {
+      out.energy[(C.ge * S1 + step + 1) * 2] = ke;
+      out.energy[(C.ge * S1 + step + 1) * 2 + 1] = pe;
+    }
+    ival(C, IS_STEP) = step + 1;
+    ival(C, IS_NSAMP) = step + 2;
+    if (step + 1 >= S) ival(C, IS_RUN) = TR_OK;
+  }
+}
+
+template <int PAT>
+cudaError_t launch(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
+  const size_t sm = smem_bytes(a.m.N);
+  static size_t configured = 0;
+  if (sm > configured) {
+    const cudaError_t e = cudaFuncSetAttribute(k_chain4_step<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  const long nw = (a.B + kE - 1) / kE;
+  const unsigned grid = (unsigned)((nw + kW - 1) / kW);
+  k_chain4_step<PAT><<<grid, kT, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, out);
+  return cudaGetLastError();
+}
+
+constexpr int pat(int P, int K0, int K1) { return P | (K0 << 2) | (K1 << 5); }
+
+}  // namespace c4
+
+// Instantiated link patterns: all Y-hinge bodies (make_single_hinge_chain_scene),
+// massless Z connector + Y body (make_chain_scene); anything else dispatches per link.
+int chain4_pattern(const int* kinds, int N) {
+  if (N <= 0) return 0;
+  bool p1 = true, p2 = N >= 2;
+  for (int i = 0; i < N; ++i) {
+    p1 = p1 && kinds[i] == kinds[0];
+    if (N >= 2) p2 = p2 && kinds[i] == kinds[i & 1];
+  }
+  if (p1 && kinds[0] == 6) return c4::pat(1, 6, 0);
+  if (p2 && kinds[0] == 3 && kinds[1] == 6) return c4::pat(2, 3, 6);
+  return 0;
+}
+
+cudaError_t launch_chain4_step(const ChainArgs& a, int pattern, const Outputs& out, cudaStream_t s) {
+  switch (pattern) {
+    case c4::pat(1, 6, 0): return c4::launch<c4::pat(1, 6, 0)>(a, out, s);
+    case c4::pat(2, 3, 6): return c4::launch<c4::pat(2, 3, 6)>(a, out, s);
+    default: return c4::launch<0>(a, out, s);
+  }
+}
+
+size_t chain4_smem_bytes(int N) { return c4::smem_bytes(N); }
+int chain4_max_memory() { return c4::kMaxMem; }
+long chain4_record_doubles(bool massive) { return massive ? c4::kRecMass : c4::kRecLight; }
+long chain4_hist_doubles() { return (long)c4::kE * c4::kHistW; }
+
+}  // namespace pbad_gpu

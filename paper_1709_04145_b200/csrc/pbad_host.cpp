@@ -433,6 +433,9 @@ struct pbad_gpu_ctx {
   KernelArgs ka{};
   ChainArgs ca{};
   bool chain = false;      // rollouts use the quad chain kernels
+  bool chain4 = false;     // ... in their warp-synchronous v4 form (pbad_chain4.cu)
+  int chain4_pat = 0;      // v4 link-pattern instantiation
+  long chain4_recw = 0;    // v4 record doubles per warp
   long v1_per_env = 0;     // general-kernel workspace size (allocated lazily)
   long chain_per_env = 0;
   std::vector<void*> owned;  // device allocations freed at destroy
@@ -528,18 +531,25 @@ Layout make_layout(const pbad_gpu_model& m, int order, int objective, int opt_ki
   return L;
 }
 
-ChainLayout make_chain_layout(const pbad_gpu_model& m, int mem, long B, long* total) {
+ChainLayout make_chain_layout(const pbad_gpu_model& m, int mem, long B, long rec_w, long* total) {
   // per-warp blocks of 8 environments (pbad_chain.cu): link arrays
-  // [warp][N][32 lanes x 4], vectors [warp][n4][32 lanes]
+  // [warp][N][32 lanes x 4], vectors [warp][n4][32 lanes]; v4 (rec_w > 0):
+  // per-warp link records [warp][rec_w] and history rotations [warp][N][8][6]
+  // instead of the link arrays
   ChainLayout L{};
   const long N = m.N, n4 = (m.n + 3) / 4, nw = (B + 7) / 8;
-  const long link = nw * N * 128, vec = nw * n4 * 32;
+  const long link = rec_w > 0 ? 0 : nw * N * 128, vec = nw * n4 * 32;
   long o = 0;
   auto take = [&](long cnt) {
     const long at = o;
-    o += cnt;
+    o += (cnt + 31) / 32 * 32;  // 256-byte aligned regions (TMA sources)
     return at;
   };
+  if (rec_w > 0) {
+    L.rec_w = rec_w;
+    L.rec = take(nw * rec_w);
+    L.hist = take(nw * N * chain4_hist_doubles());
+  }
   L.tk = take(link);
   L.tk1 = take(link);
   L.seed = take(link);
@@ -564,12 +574,23 @@ ChainLayout make_chain_layout(const pbad_gpu_model& m, int mem, long B, long* to
   return L;
 }
 
+// v4 additionally needs every joint axis-aligned with an identity offset
+// rotation (link classes 1..3) and its shared-memory footprint to fit.
+bool chain4_eligible(const std::vector<int>& ck, int N, int mem) {
+  if (std::getenv("PBAD_GPU_CHAIN_V3")) return false;
+  if (mem > chain4_max_memory()) return false;
+  for (int i = 0; i < N; ++i)
+    if ((ck[i] & 3) == 0) return false;
+  return chain4_smem_bytes(N) <= 227 * 1024;
+}
+
 // The quad chain kernels cover serial hinge chains, energy form, L-BFGS,
 // gravity / constant or sinusoidal actuation (no drag or contact).
 bool chain_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2 || sim->opt.kind != PBAD_LBFGS) return false;
   if (sim->opt.lbfgs_memory < 1 || sim->opt.lbfgs_memory > chain_max_memory()) return false;
+  if (m.N > chain_max_links()) return false;
   if (f->drag_d > 0.0) return false;
   if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
   for (int i = 0; i < m.N; ++i) {
@@ -717,6 +738,12 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     }
     dm.crec = up_d(rec);
     dm.ckind = up_i(ck);
+    std::vector<int> roff(m.N + 1, 0);
+    for (int i = 0; i < m.N; ++i) roff[i + 1] = roff[i] + (int)chain4_record_doubles(sk[i] != 0);
+    dm.croff = up_i(roff);
+    c->chain4 = chain4_eligible(ck, m.N, sim->opt.lbfgs_memory);
+    c->chain4_pat = chain4_pattern(ck.data(), m.N);
+    c->chain4_recw = roff[m.N];
   }
 
   DForces df{};
@@ -771,13 +798,15 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   c->v1_per_env = per_env;
   c->ka = KernelArgs{dm, df, ds, L, nullptr, nullptr, max_batch};
   c->chain = chain_eligible(m, f, sim);
+  c->chain4 = c->chain4 && c->chain;
   if (!dm.parent || !dm.S) {
     delete c;
     return fail(PBAD_E_CUDA, "cudaMalloc of the model failed");
   }
   if (c->chain) {
     long tot = 0;
-    const ChainLayout CL = make_chain_layout(m, sim->opt.lbfgs_memory, max_batch, &tot);
+    const long rec_w = c->chain4 ? c->chain4_recw : 0;
+    const ChainLayout CL = make_chain_layout(m, sim->opt.lbfgs_memory, max_batch, rec_w, &tot);
     double* cw = dalloc<double>((size_t)tot);
     int* ci = dalloc<int>((size_t)IS_COUNT * max_batch);
     if (!cw || !ci) {
@@ -829,7 +858,9 @@ int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
   CUDA_TRY(cudaSetDevice(c->device));
   const cudaStream_t s = pick(c, stream);
   for (int k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
-    CUDA_TRY(c->chain ? launch_chain_step(c->ca, c->dout, s) : launch_step(c->ka, c->dout, s));
+    CUDA_TRY(c->chain4  ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
+             : c->chain ? launch_chain_step(c->ca, c->dout, s)
+                        : launch_step(c->ka, c->dout, s));
   return PBAD_OK;
 }
 

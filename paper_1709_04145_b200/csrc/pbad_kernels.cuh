@@ -25,6 +25,7 @@ struct DModel {
   const int* skind;      // chain path: 0 massless (S == 0), 1 general S
   const double* crec;    // chain path: packed link records [N][20]: S (16), offset translation (3), pad
   const int* ckind;      // chain path: jkind | skind << 2
+  const int* croff;      // chain v4: per-link record offsets [N+1] (doubles, per warp)
   double weighted_mass;  // WeightedBody::make with unit weights (adjoint.cpp:29-41)
 };
 
@@ -103,6 +104,7 @@ struct ChainLayout {
   long h0, h1, x, g, cand, dir, q, evg, tau; // vectors
   long hs, hy, vstride;                      // L-BFGS ring, vstride per vector
   long hsy, histc;                           // [cap][B], [B]
+  long rec, rec_w, hist;                     // chain v4: link records [warp][rec_w], hist rotations [warp][N][8][6]
   long total;
 };
 

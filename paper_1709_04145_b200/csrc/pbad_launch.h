@@ -31,6 +31,14 @@ cudaError_t launch_chain_init(const ChainArgs& a, const double* q0, const double
                               cudaStream_t s);
 cudaError_t launch_chain_step(const ChainArgs& a, const Outputs& out, cudaStream_t s);
 int chain_max_memory();
+int chain_max_links();
+// chain v4 (pbad_chain4.cu): axis-aligned hinge chains, warp-synchronous L-BFGS
+int chain4_pattern(const int* kinds, int N);
+cudaError_t launch_chain4_step(const ChainArgs& a, int pattern, const Outputs& out, cudaStream_t s);
+size_t chain4_smem_bytes(int N);
+int chain4_max_memory();
+long chain4_record_doubles(bool massive);
+long chain4_hist_doubles();
 
 cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
                         cudaStream_t s);
