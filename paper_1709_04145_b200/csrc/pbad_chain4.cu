@@ -413,7 +413,7 @@ __device__ __forceinline__ void fwd_chunk(const Ctx& C, int lo, int cnt, Rows& R
 }
 
 template <int PAT>
-__device__ __forceinline__ double forward(const Ctx& C, const double* X) {
+__device__ __forceinline__ double forward(const Ctx& C, const double* X, double tdx) {
   const int N = C.N;
   const int nch = (N + CL - 1) / CL;
   Rows R;
@@ -483,7 +483,6 @@ __device__ __forceinline__ double forward(const Ctx& C, const double* X) {
   const double wm = C.wm;
   const double cpp = sa - wm, c1p = sb - wm, c2p = sc - wm;
   const double inertial = 0.5 * C.inv_dt2 * (cpp - 4.0 * c1p + 2.0 * c2p + *C.histc);
-  const double tdx = qdot(C, C.tau, X);
   return inertial + sg - tdx;
 }
 
@@ -750,45 +749,145 @@ __device__ __forceinline__ void tau_at(const Ctx& C, const DForces& f, double t)
 }
 
 // ---- L-BFGS (LbfgsSolver, optim.cpp:141-232) ------------------------------
+// The vector work of an iteration is fused into as few passes over the
+// quad-interleaved vectors as the data dependencies allow (one per reduction
+// of the two-loop recursion, one for the candidate, one for the accepted
+// step); every element sees exactly the reference's operation sequence and
+// every dot product keeps its 32-partial order (partial (4g + r) & 31 of
+// element 4g + r, ascending g), so the values are unchanged.  The history
+// vectors a pass will need two passes later are prefetched into L2 with TMA
+// bulk prefetches.
 struct Solver {
   double value, grad0, t, slope, fval;
+  double ginf, xinf;  // |g|_inf, |x|_inf of the current iterate
+  double tdx;         // tau . cand of the pending candidate
   int status, iters, stag, acc, h0, hc, trial, phase;
 };
 
-__device__ __forceinline__ bool grad_converged(const Ctx& C, const Solver& s) {
-  const double g = qinfnorm(C, C.g);
-  if (g <= C.o.grad_tol * fmax(1.0, qinfnorm(C, C.x))) return true;
-  if (C.o.grad_rtol > 0.0 && g <= C.o.grad_rtol * s.grad0) return true;
-  return false;
+constexpr int kB = 16;  // groups per batch of loads
+
+__device__ __forceinline__ bool elem_ok(const Ctx& C, int g) { return g < C.n4 && 4 * g + C.r < C.n; }
+template <int KB>
+__device__ __forceinline__ void ldb(const Ctx& C, const double* V, int g0, double* out) {
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    const int g = g0 + j;
+    out[j] = (g < C.n4) ? V[(long)g * kGS] : 0.0;
+  }
+}
+// 32-partial canonical dot reduction: acc[j] holds partial (4 j + r)
+__device__ __forceinline__ double dot_finish(const Ctx& C, double* acc) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = acc[j] + acc[j + 4];
+  acc[0] = acc[0] + acc[2];
+  acc[1] = acc[1] + acc[3];
+  double v = acc[0] + acc[1];
+  const double v2 = qshfl(C, v, (C.r + 2) & 3);
+  if (C.r < 2) v = v + v2;
+  const double v1 = qshfl(C, v, 1);
+  if (C.r == 0) v = v + v1;
+  return qshfl(C, v, 0);
+}
+__device__ __forceinline__ double qmax(const Ctx& C, double mx) {
+  mx = fmax(mx, qshfl(C, mx, C.r ^ 1));
+  mx = fmax(mx, qshfl(C, mx, C.r ^ 2));
+  return mx;
+}
+__device__ __forceinline__ void l2_prefetch(const Ctx& C, const double* V) {
+  if (C.r == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V - (threadIdx.x & 31)),
+                 "r"((unsigned)(C.n4 * kGS * sizeof(double)))
+                 : "memory");
 }
 
-// two_loop (optim.cpp:213-229): q = H g
-__device__ __forceinline__ void two_loop(const Ctx& C, const Solver& s) {
-  const int cap = C.o.mem + 1;
-  qmap2(C, C.q, C.g, C.g, [](double a, double) { return a; });
+// two-loop passes: q' = op(q, w); then DOT 0: z . q'; 1: z . z; 2: dir = -q', dir . g
+enum { M_COPY = 0, M_SUB = 1, M_SCALE = 2, M_ADD = 3 };
+template <int MODE, int DOT>
+__device__ __forceinline__ double tl_pass(const Ctx& C, const double* w, double a, const double* z, bool store_q) {
+  double acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+  for (int g0 = 0; g0 < C.n4; g0 += kB) {
+    double qv[kB], wv[kB], zv[kB];
+    if (MODE != M_COPY) ldb<kB>(C, C.q, g0, qv);
+    if (MODE != M_SCALE) ldb<kB>(C, w, g0, wv);
+    if (DOT == 2) ldb<kB>(C, C.g, g0, zv);
+    else ldb<kB>(C, z, g0, zv);
+#pragma unroll
+    for (int j = 0; j < kB; ++j) {
+      const int g = g0 + j;
+      if (!elem_ok(C, g)) continue;
+      double qn;
+      if (MODE == M_COPY) qn = wv[j];
+      else if (MODE == M_SUB) qn = qv[j] - a * wv[j];
+      else if (MODE == M_SCALE) qn = qv[j] * a;
+      else qn = qv[j] + a * wv[j];
+      if (DOT == 2) {
+        const double d = -qn;
+        C.dir[(long)g * kGS] = d;
+        acc[j & 7] = fma(d, zv[j], acc[j & 7]);
+      } else {
+        if (store_q) C.q[(long)g * kGS] = qn;
+        if (DOT == 0) acc[j & 7] = fma(zv[j], qn, acc[j & 7]);
+        else acc[j & 7] = fma(zv[j], zv[j], acc[j & 7]);
+      }
+    }
+  }
+  return dot_finish(C, acc);
+}
+
+__device__ __forceinline__ const double* hist_s(const Ctx& C, const Solver& s, int i) {
+  return C.hs + ((s.h0 + i) % (C.o.mem + 1)) * C.VS;
+}
+__device__ __forceinline__ const double* hist_y(const Ctx& C, const Solver& s, int i) {
+  return C.hy + ((s.h0 + i) % (C.o.mem + 1)) * C.VS;
+}
+__device__ __forceinline__ double hist_sy(const Ctx& C, const Solver& s, int i) {
+  return C.hsy[((s.h0 + i) % (C.o.mem + 1)) * C.B];
+}
+
+// two_loop (optim.cpp:213-229) fused with dir = -q and slope = dir . g
+// (optim.cpp:162-170); returns the slope
+__device__ __forceinline__ double direction(const Ctx& C, const Solver& s) {
+  const int hc = s.hc;
+  if (hc == 0) return tl_pass<M_COPY, 2>(C, C.g, 0.0, nullptr, false);
+  // prefetch order = use order: s_{hc-1}, y_{hc-1}, s_{hc-2}, ... then y_{hc-1} again, y_0, s_0, y_1, ...
+  l2_prefetch(C, hist_s(C, s, hc - 1));
+  l2_prefetch(C, hist_y(C, s, hc - 1));
+  if (hc > 1) l2_prefetch(C, hist_s(C, s, hc - 2));
   double alpha[kMaxMem];
-  for (int i = s.hc - 1; i >= 0; --i) {
-    const int slot = (s.h0 + i) % cap;
-    const double* sv = C.hs + slot * C.VS;
-    const double* yv = C.hy + slot * C.VS;
-    const double a = qdot(C, sv, C.q) / C.hsy[slot * C.B];
+  double d = tl_pass<M_COPY, 0>(C, C.g, 0.0, hist_s(C, s, hc - 1), true);  // q = g; s . q
+  double yy = 0.0;
+  for (int i = hc - 1; i >= 0; --i) {
+    const double a = d / hist_sy(C, s, i);
     alpha[i] = a;
-    qmap2(C, C.q, C.q, yv, [a](double qv, double y) { return qv - a * y; });
+    if (i >= 2) {
+      l2_prefetch(C, hist_y(C, s, i - 1));
+      l2_prefetch(C, hist_s(C, s, i - 2));
+    } else if (i == 1) {
+      l2_prefetch(C, hist_y(C, s, 0));
+    }
+    if (i > 0) d = tl_pass<M_SUB, 0>(C, hist_y(C, s, i), a, hist_s(C, s, i - 1), true);
+    else yy = tl_pass<M_SUB, 1>(C, hist_y(C, s, 0), a, hist_y(C, s, hc - 1), true);
   }
-  if (s.hc > 0) {
-    const int slot = (s.h0 + s.hc - 1) % cap;
-    const double* yv = C.hy + slot * C.VS;
-    const double scl = C.hsy[slot * C.B] / qdot(C, yv, yv);
-    qmap2(C, C.q, C.q, C.q, [scl](double qv, double) { return qv * scl; });
-  }
-  for (int i = 0; i < s.hc; ++i) {
-    const int slot = (s.h0 + i) % cap;
-    const double* sv = C.hs + slot * C.VS;
-    const double* yv = C.hy + slot * C.VS;
-    const double beta = qdot(C, yv, C.q) / C.hsy[slot * C.B];
+  l2_prefetch(C, hist_s(C, s, 0));
+  if (hc > 1) l2_prefetch(C, hist_y(C, s, 1));
+  const double scl = hist_sy(C, s, hc - 1) / yy;
+  d = tl_pass<M_SCALE, 0>(C, nullptr, scl, hist_y(C, s, 0), true);  // q *= scl; y_0 . q
+  double slope = 0.0;
+  for (int i = 0; i < hc; ++i) {
+    const double beta = d / hist_sy(C, s, i);
     const double c = alpha[i] - beta;
-    qmap2(C, C.q, C.q, sv, [c](double qv, double sv2) { return qv + c * sv2; });
+    if (i + 2 < hc) {
+      l2_prefetch(C, hist_s(C, s, i + 1));
+      l2_prefetch(C, hist_y(C, s, i + 2));
+    } else if (i + 1 < hc) {
+      l2_prefetch(C, hist_s(C, s, i + 1));
+    }
+    if (i + 1 < hc) d = tl_pass<M_ADD, 0>(C, hist_s(C, s, i), c, hist_y(C, s, i + 1), true);
+    else slope = tl_pass<M_ADD, 2>(C, hist_s(C, s, i), c, nullptr, false);  // dir = -q; dir . g
   }
+  return slope;
 }
 
 // start of LbfgsSolver::iterate: termination tests, direction, slope
@@ -798,19 +897,17 @@ __device__ __forceinline__ void begin_iteration(const Ctx& C, Solver& s) {
     s.phase = PH_DONE;
     return;
   }
-  if (grad_converged(C, s)) {
+  // grad_converged (optim.cpp:35-41) on the norms of the current iterate
+  if (s.ginf <= C.o.grad_tol * fmax(1.0, s.xinf) || (C.o.grad_rtol > 0.0 && s.ginf <= C.o.grad_rtol * s.grad0)) {
     s.status = ST_CONVERGED;
     s.phase = PH_DONE;
     return;
   }
-  two_loop(C, s);
-  qmap2(C, C.dir, C.q, C.q, [](double qv, double) { return -qv; });
-  double slope = qdot(C, C.dir, C.g);
+  double slope = direction(C, s);
   if (!(slope < 0.0)) {
     s.hc = 0;
     s.h0 = 0;
-    qmap2(C, C.dir, C.g, C.g, [](double gv, double) { return -gv; });
-    slope = qdot(C, C.dir, C.g);
+    slope = tl_pass<M_COPY, 2>(C, C.g, 0.0, nullptr, false);  // dir = -g
   }
   s.slope = slope;
   s.t = 1.0;
@@ -819,12 +916,33 @@ __device__ __forceinline__ void begin_iteration(const Ctx& C, Solver& s) {
   s.phase = PH_GEN;
 }
 
-// next finite candidate x + t dir of the backtracking line search
+// next finite candidate x + t dir of the backtracking line search, with
+// tau . cand for its objective value
 __device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
   while (s.trial < C.o.max_line_search) {
     const double t = s.t;
-    qmap2(C, C.cand, C.x, C.dir, [t](double xv, double dv) { return xv + t * dv; });
-    if (qallfinite(C, C.cand)) {
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    bool fin = true;
+    for (int g0 = 0; g0 < C.n4; g0 += kB) {
+      double xv[kB], dv[kB], tv[kB];
+      ldb<kB>(C, C.x, g0, xv);
+      ldb<kB>(C, C.dir, g0, dv);
+      ldb<kB>(C, C.tau, g0, tv);
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        const int g = g0 + j;
+        if (!elem_ok(C, g)) continue;
+        const double cv = xv[j] + t * dv[j];
+        C.cand[(long)g * kGS] = cv;
+        fin = fin && isfinite(cv);
+        acc[j & 7] = fma(tv[j], cv, acc[j & 7]);
+      }
+    }
+    const double tdx = dot_finish(C, acc);
+    if (__all_sync(C.qm, fin)) {
+      s.tdx = tdx;
       s.phase = PH_EVAL;
       return;
     }
@@ -836,16 +954,44 @@ __device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
   s.phase = PH_DONE;
 }
 
-// accepted step: history pair, iterate, stagnation test (optim.cpp:176-205)
+// accepted step (optim.cpp:176-205) in one pass: s = t dir, y = evg - g,
+// s . y, x = cand, g = evg, and the norms of the new iterate
 __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
   const int cap = C.o.mem + 1;
   const int slot = (s.h0 + s.hc) % cap;
   double* sv = C.hs + slot * C.VS;
   double* yv = C.hy + slot * C.VS;
   const double t = s.t;
-  qmap2(C, sv, C.dir, C.dir, [t](double dv, double) { return t * dv; });
-  qmap2(C, yv, C.evg, C.g, [](double ev, double gv) { return ev - gv; });
-  const double sy = qdot(C, sv, yv);
+  double acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+  double gm = 0.0, xm = 0.0;
+  constexpr int KB = 8;
+  for (int g0 = 0; g0 < C.n4; g0 += KB) {
+    double dv[KB], ev[KB], gv[KB], cv[KB];
+    ldb<KB>(C, C.dir, g0, dv);
+    ldb<KB>(C, C.evg, g0, ev);
+    ldb<KB>(C, C.g, g0, gv);
+    ldb<KB>(C, C.cand, g0, cv);
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const int g = g0 + j;
+      if (!elem_ok(C, g)) continue;
+      const long o = (long)g * kGS;
+      const double sj = t * dv[j];
+      const double yj = ev[j] - gv[j];
+      sv[o] = sj;
+      yv[o] = yj;
+      C.x[o] = cv[j];
+      C.g[o] = ev[j];
+      acc[(g0 + j) & 7] = fma(sj, yj, acc[(g0 + j) & 7]);
+      gm = fmax(gm, fabs(ev[j]));
+      xm = fmax(xm, fabs(cv[j]));
+    }
+  }
+  const double sy = dot_finish(C, acc);
+  s.ginf = qmax(C, gm);
+  s.xinf = qmax(C, xm);
   if (sy > 1e-12) {
     if (C.r == 0) C.hsy[slot * C.B] = sy;
     ++s.hc;
@@ -854,8 +1000,6 @@ __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
       --s.hc;
     }
   }
-  qmap2(C, C.x, C.cand, C.cand, [](double cv, double) { return cv; });
-  qmap2(C, C.g, C.evg, C.evg, [](double ev, double) { return ev; });
   qsync(C);
   const double oldv = s.fval;
   s.value = v;
@@ -980,7 +1124,13 @@ __global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedu
   Solver s{};
   s.status = ST_RUNNING;
   s.phase = PH_DIR;
-  const double v0 = forward<PAT>(C, C.x);
+  double tdx0 = 0.0;
+  if (active) {
+    tdx0 = qdot(C, C.tau, C.x);
+    s.xinf = qinfnorm(C, C.x);
+  }
+  __syncwarp();
+  const double v0 = forward<PAT>(C, C.x, tdx0);
   reverse<PAT>(C, C.g);
   if (active && !isfinite(v0)) {
     if (C.r == 0) ival(C, IS_RUN) = TR_NONFINITE_INIT;
@@ -989,6 +1139,7 @@ __global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedu
   if (active) {
     s.value = v0;
     s.grad0 = qinfnorm(C, C.g);
+    s.ginf = s.grad0;
   } else {
     s.phase = PH_DONE;
   }
@@ -998,7 +1149,7 @@ __global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedu
     __syncwarp();
     const bool eval = s.phase == PH_EVAL;
     if (!__any_sync(0xffffffffu, eval)) break;
-    const double v = forward<PAT>(C, C.cand);
+    const double v = forward<PAT>(C, C.cand, s.tdx);
     bool acc = false;
     if (eval) {
       if (isfinite(v) && v <= s.fval + C.o.armijo_c1 * s.t * s.slope && v < s.fval) {
