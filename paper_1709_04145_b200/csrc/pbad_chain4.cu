@@ -64,9 +64,12 @@ constexpr int kFwdR = kFwdC + CL * kE * 2;     // energy row partials [CL][term]
 constexpr int kFwdEnd = kFwdR + CL * 16 * kE;  // (the forward buffers overlay the ring)
 constexpr int kRRed = kRing * kSlot;           // gradient row partials [CL][2][row][env]
 constexpr int kQScr = kRRed + CL * 2 * 4 * kE;  // per-environment scratch [env][16]
-constexpr int kBar = kQScr + kE * 16;          // mbarriers
+constexpr int kHsy = kQScr + kE * 16;          // per-environment s.y ring and alpha [env][kHsyW]
+constexpr int kHsyW = 40;
+constexpr int kBar = kHsy + kE * kHsyW;        // mbarriers
 constexpr int kWarpD = kBar + 4;
 static_assert(kFwdEnd <= kRing * kSlot, "forward buffers must fit in the ring");
+static_assert(kHsyW >= 2 * kMaxMem + 1, "s.y ring + alpha");
 constexpr int kHistW = 6;  // hist record per (link, env): c0 s0 | c1 s1 | cx sx
 
 __host__ __device__ inline size_t smem_bytes(int N) {
@@ -221,7 +224,7 @@ struct Ctx {
   double* hist;        // this warp's history rotations [N][env][6] (global)
   double *h0, *h1, *x, *g, *cand, *dir, *q, *evg, *tau, *hs, *hy;
   long VS;
-  double* hsy;
+  double* hsy;    // shared: this env's s.y ring [mem+1] then alpha [mem]
   double* histc;
   int* ci;
   double dt, inv_dt2, wm, gr;
@@ -600,6 +603,10 @@ __device__ __forceinline__ void reverse(Ctx& C, double* Gv) {
     for (int p = 0; p < kRing && p < nch; ++p) issue_chunk(C, nch - 1 - p, k0 + p);
   }
   double cI[4] = {0.0, 0.0, 0.0, 0.0}, cG[4] = {0.0, 0.0, 0.0, 0.0};
+  // tau of this lane's two links of the next chunk (loaded a chunk ahead)
+  double tau_n[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) tau_n[h] = (CL * (nch - 1) + C.r + 4 * h < N) ? C.tau[(long)(2 * (nch - 1) + h) * kGS] : 0.0;
   for (int idx = 0; idx < nch; ++idx) {
     const int c = nch - 1 - idx;
     const int lo = CL * c, cnt = min(CL, N - lo);
@@ -607,6 +614,11 @@ __device__ __forceinline__ void reverse(Ctx& C, double* Gv) {
     const int slot = (int)(k % kRing);
     mbar_wait(C.bar + slot, (k / kRing) & 1u);
     const double* sbase = C.ws + slot * kSlot - C.roff[lo];
+    const double tau_c[2] = {tau_n[0], tau_n[1]};
+    if (c > 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) tau_n[h] = C.tau[(long)(2 * (c - 1) + h) * kGS];
+    }
     rev_chunk<PAT>(C, sbase, lo, cnt, cI, cG);
     __syncwarp();
     // gradient entries of this lane's two links of the chunk
@@ -618,7 +630,7 @@ __device__ __forceinline__ void reverse(Ctx& C, double* Gv) {
         const double gi = 0.0 + (((b[0] + b[8]) + b[16]) + b[24]);
         const double gp = 0.0 + (((b[32] + b[40]) + b[48]) + b[56]);
         const long go = (long)(2 * c + h) * kGS;
-        Gv[go] = (gi + gp) - C.tau[go];
+        Gv[go] = (gi + gp) - tau_c[h];
       }
     }
     __syncwarp();
@@ -843,7 +855,7 @@ __device__ __forceinline__ const double* hist_y(const Ctx& C, const Solver& s, i
   return C.hy + ((s.h0 + i) % (C.o.mem + 1)) * C.VS;
 }
 __device__ __forceinline__ double hist_sy(const Ctx& C, const Solver& s, int i) {
-  return C.hsy[((s.h0 + i) % (C.o.mem + 1)) * C.B];
+  return C.hsy[(s.h0 + i) % (C.o.mem + 1)];
 }
 
 // two_loop (optim.cpp:213-229) fused with dir = -q and slope = dir . g
@@ -855,7 +867,7 @@ __device__ __forceinline__ double direction(const Ctx& C, const Solver& s) {
   l2_prefetch(C, hist_s(C, s, hc - 1));
   l2_prefetch(C, hist_y(C, s, hc - 1));
   if (hc > 1) l2_prefetch(C, hist_s(C, s, hc - 2));
-  double alpha[kMaxMem];
+  double* alpha = C.hsy + kMaxMem + 1;
   double d = tl_pass<M_COPY, 0>(C, C.g, 0.0, hist_s(C, s, hc - 1), true);  // q = g; s . q
   double yy = 0.0;
   for (int i = hc - 1; i >= 0; --i) {
@@ -993,7 +1005,7 @@ __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
   s.ginf = qmax(C, gm);
   s.xinf = qmax(C, xm);
   if (sy > 1e-12) {
-    if (C.r == 0) C.hsy[slot * C.B] = sy;
+    if (C.r == 0) C.hsy[slot] = sy;
     ++s.hc;
     if (s.hc > C.o.mem) {
       s.h0 = (s.h0 + 1) % cap;
@@ -1048,7 +1060,7 @@ __device__ __forceinline__ Ctx make_ctx(const DModel& m, const DForces& f, const
   C.VS = L.vstride;
   // per-env scalars; padded environments (ge >= B) point at env 0 and never write
   const long es = C.valid ? C.ge : 0;
-  C.hsy = cw + L.hsy + es;
+  C.hsy = C.ws + kHsy + C.e * kHsyW;
   C.histc = cw + L.histc + es;
   C.ci = ci;
   C.dt = sc.dt;
