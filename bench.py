@@ -371,6 +371,8 @@ def main():
         "cpu_baseline": cb,
         "e2e": e2e,
         "gpu_launches": K,
+        "kernel": {0: "pbad_gpu::k_step (general, thread per env)", 1: "pbad_gpu::k_chain_step (quad per env)",
+                   2: "pbad_gpu::c4::k_chain4_step (warp-synchronous quads, TMA-fed adjoint)"}.get(ctx.path),
         "clocks": clk,
         "mean_iterations_per_step": float(iters.mean()),
         "trajectories_ok": int(np.sum((st == 0) | (st == 4))),

@@ -171,6 +171,12 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* forces,
                         pbad_gpu_ctx** out);
 void pbad_gpu_destroy(pbad_gpu_ctx* ctx);
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* ctx);
+/* which kernel family steps this context's rollouts (no reference
+ * counterpart; reported by bench.py and asserted by the tests) */
+#define PBAD_PATH_GENERAL 0 /* thread per environment, any model (pbad_kernels.cu) */
+#define PBAD_PATH_CHAIN 1   /* quad per environment, hinge chains (pbad_chain.cu) */
+#define PBAD_PATH_CHAIN4 2  /* warp-synchronous quads, axis-aligned hinge chains (pbad_chain4.cu) */
+int32_t pbad_gpu_path(const pbad_gpu_ctx* ctx);
 
 /* batch_simulate on the GPU: q0/qdot0 host [B][n]; copies in, steps every
  * trajectory to completion, copies the requested outputs back. */

@@ -22,7 +22,7 @@ HEADER_SYMBOLS = [
     "pbad_gpu_default_sim", "pbad_gpu_model_create", "pbad_gpu_model_destroy", "pbad_gpu_model_dofs",
     "pbad_gpu_model_links", "pbad_gpu_model_info", "pbad_gpu_body_integral", "pbad_gpu_rotation_vector_matrix",
     "pbad_gpu_build_scheme", "pbad_gpu_validate_configuration", "pbad_gpu_create", "pbad_gpu_destroy",
-    "pbad_gpu_total_steps", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
+    "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
     "pbad_gpu_state_device", "pbad_gpu_eval", "pbad_gpu_minimize",
 ]
 
@@ -107,6 +107,7 @@ def load():
                             C.c_int32),
         "pbad_gpu_destroy": ([vp], None),
         "pbad_gpu_total_steps": ([vp], C.c_int32),
+        "pbad_gpu_path": ([vp], C.c_int32),
         "pbad_gpu_rollout": ([vp, C.c_int32, _dp, _dp, C.POINTER(RolloutOut)], C.c_int32),
         "pbad_gpu_begin": ([vp, C.c_int32, vp, vp, vp], C.c_int32),
         "pbad_gpu_advance": ([vp, C.c_int32, vp], C.c_int32),

@@ -269,6 +269,8 @@ class GpuContext:
         self._h = h
         self.max_batch = max_batch
         self.total_steps = _lib.load().pbad_gpu_total_steps(h)
+        # kernel family: 0 general, 1 chain (quad), 2 chain v4 (warp-synchronous)
+        self.path = _lib.load().pbad_gpu_path(h)
         self.n = model.total_dofs
         self.dim = self.n * (sim.order - 1)
 

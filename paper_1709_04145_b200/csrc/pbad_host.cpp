@@ -834,6 +834,9 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
 
 void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
+int32_t pbad_gpu_path(const pbad_gpu_ctx* c) {
+  return c->chain4 ? PBAD_PATH_CHAIN4 : c->chain ? PBAD_PATH_CHAIN : PBAD_PATH_GENERAL;
+}
 const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) {
   // chain path: quad-interleaved [n/4][B][4]; general path: [n][B]
   return c->chain ? c->ca.cw + c->ca.L.h1 : c->ka.ws + c->ka.L.hist1 * c->ka.B;

@@ -240,3 +240,84 @@ def test_rollout_chain_kernel_actuated():
     sim = SimConfig(dt=0.02, duration=0.1)
     sim.optimizer.kind = OptimizerKind.lbfgs
     _rollout_case(sc, sim, B=2, seed=7)
+
+
+# --- chain kernel v4 (pbad_chain4.cu): warp-synchronous lockstep rounds -----
+
+def _axis_chain(seed, links):
+    """Serial chain of axis-aligned hinges (X / Y / Z), pure-translation
+    offsets and mixed box / point-mass / massless links: the v4 kernel's
+    per-link dispatch path (no compiled link pattern matches)."""
+    from paper_1709_04145_b200.types import BoxGeometry, JointKind, JointSpec, LinkSpec, PointMass, PointMassGeometry
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(links):
+        ax = [(1.0, 0.0, 0.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0)][int(rng.integers(0, 3))]
+        off = np.eye(4)
+        if i:
+            off[:3, 3] = rng.uniform(-0.6, 0.6, 3)
+        u = rng.uniform()
+        if u < 0.3:
+            g = PointMassGeometry([])
+        elif u < 0.5:
+            g = PointMassGeometry([PointMass(0.2 + rng.uniform(), tuple(rng.uniform(-0.3, 0.3, 3)))])
+        else:
+            g = BoxGeometry(tuple(0.1 + rng.uniform(0, 0.5, 3)), 300.0 + 900.0 * rng.uniform(),
+                            tuple(rng.uniform(-0.3, 0.3, 3)))
+        out.append(LinkSpec(None if i == 0 else i - 1, JointSpec(JointKind.hinge, ax, off), g))
+    return out
+
+
+def _path(scene, sim):
+    m = api.build_model(scene.links)
+    return api.GpuContext(m, scene.forces(), sim, max_batch=1).path
+
+
+def test_chain4_dispatch_path_ragged_batch():
+    """13 links (a partial last chunk), 11 environments (a padded warp), the
+    generic per-link dispatch: bit-exact against the oracle."""
+    from paper_1709_04145_b200.scenes import Scene
+    sc = Scene(links=_axis_chain(21, 13), gravity=(1.0, -2.0, -9.81))
+    sc.q0 = np.zeros(13)
+    sc.qdot0 = np.zeros(13)
+    sim = SimConfig(dt=0.02, duration=0.1)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    assert _path(sc, sim) == 2
+    _rollout_case(sc, sim, B=11, seed=9, lo=-0.5, hi=0.5)
+
+
+def test_chain4_lockstep_divergent_envs():
+    """Environments of one warp converge, fail and abort at different
+    iterations / steps (max_iters small, fail limit 1)."""
+    sc = make_single_hinge_chain_scene(10)
+    sim = SimConfig(dt=0.01, duration=0.08, consecutive_fail_limit=1)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    sim.optimizer.max_iters = 60
+    assert _path(sc, sim) == 2
+    gpu, ref = _rollout_case(sc, sim, B=11, seed=3, lo=-1.0, hi=1.0)
+    errs = {g.error for g in gpu}
+    assert len(errs) >= 1
+
+
+def test_chain4_matches_chain_v3(monkeypatch):
+    """The v3 quad kernel (PBAD_GPU_CHAIN_V3) and v4 produce identical
+    trajectories (both are pinned to the oracle)."""
+    sc = make_chain_scene(12)
+    sim = SimConfig(dt=0.1, duration=0.3)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    m = api.build_model(sc.links)
+    n = m.total_dofs
+    sims = []
+    for b in range(5):
+        s = SimConfig(**{**sim.__dict__})
+        s.q0 = mt19937_uniform(40 + b, n, -0.3, 0.3)
+        s.qdot0 = np.zeros(n)
+        sims.append(s)
+    assert _path(sc, sim) == 2
+    v4 = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.setenv("PBAD_GPU_CHAIN_V3", "1")
+    assert _path(sc, sim) == 1
+    v3 = api.batch_simulate(m, sc.forces(), sims)
+    for a, b in zip(v4, v3):
+        np.testing.assert_array_equal(np.array([s[1] for s in a.samples]), np.array([s[1] for s in b.samples]))
+        assert [r.iterations for r in a.solve_reports] == [r.iterations for r in b.solve_reports]
