@@ -438,6 +438,9 @@ struct pbad_gpu_ctx {
   long chain4_recw = 0;    // v4 record doubles per warp
   long v1_per_env = 0;     // general-kernel workspace size (allocated lazily)
   long chain_per_env = 0;
+  bool tree = false;       // rollouts use the warp-per-env Newton kernel (pbad_tree.cu)
+  TreeDesc td{};
+  double* tws = nullptr;   // tree-path per-env workspace (GN, history transforms)
   std::vector<void*> owned;  // device allocations freed at destroy
   long max_batch = 0;
   long B = 0;  // current batch
@@ -598,6 +601,71 @@ bool chain_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
     if (m.parent[i] != i - 1) return false;
   }
   return true;
+}
+
+// The tree kernel covers any tree with the energy form and LM (Newton):
+// gravity / constant or sinusoidal actuation (no drag or contact yet).
+bool tree_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
+  if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
+  if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2 || sim->opt.kind != PBAD_LM) return false;
+  if (f->drag_d > 0.0) return false;
+  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
+  if (!tree_eligible_sizes(m.N, m.n)) return false;
+  for (int i = 0; i < m.N; ++i)
+    if (m.dof_cnt[i] > 6) return false;
+  return true;
+}
+
+// Host-side structure of the tree kernel: depth levels, children in
+// descending index (the reference's accumulation order, adjoint.cpp:54-62),
+// ancestor table and the GN task list (adjoint.cpp:132-176 loop nest).
+struct TreeHost {
+  std::vector<int> lvl_start, lvl_links, ch_start, ch_list, task_start, tasks, anc, depth, pk, dof_link;
+  int D = 0;
+};
+
+TreeHost make_tree_host(const pbad_gpu_model& m) {
+  TreeHost h;
+  const int N = m.N, n = m.n;
+  h.depth.assign(N, 0);
+  for (int i = 0; i < N; ++i) h.depth[i] = m.parent[i] >= 0 ? h.depth[m.parent[i]] + 1 : 0;
+  for (int i = 0; i < N; ++i) h.D = std::max(h.D, h.depth[i]);
+  const int D = h.D;
+  h.lvl_start.assign(D + 2, 0);
+  for (int d = 0; d <= D; ++d) {
+    h.lvl_start[d] = (int)h.lvl_links.size();
+    for (int i = 0; i < N; ++i)
+      if (h.depth[i] == d) h.lvl_links.push_back(i);
+  }
+  h.lvl_start[D + 1] = (int)h.lvl_links.size();
+  h.ch_start.assign(N + 1, 0);
+  for (int p = 0; p < N; ++p) {
+    h.ch_start[p] = (int)h.ch_list.size();
+    for (int c = N - 1; c > p; --c)
+      if (m.parent[c] == p) h.ch_list.push_back(c);
+  }
+  h.ch_start[N] = (int)h.ch_list.size();
+  h.anc.assign((size_t)N * (D + 1), -1);
+  for (int i = 0; i < N; ++i) {
+    int l = i;
+    for (int s = 0; s <= D && l >= 0; ++s, l = m.parent[l]) h.anc[(size_t)i * (D + 1) + s] = l;
+  }
+  h.task_start.assign(D + 2, 0);
+  for (int s = 0; s <= D; ++s) {
+    h.task_start[s] = (int)h.tasks.size();
+    for (int i = 0; i < N; ++i) {
+      if (h.depth[i] < s) continue;
+      const int l = h.anc[(size_t)i * (D + 1) + s];
+      for (int j = 0; j < m.dof_cnt[i]; ++j)
+        for (int k = (s == 0 ? j : 0); k < m.dof_cnt[l]; ++k) h.tasks.push_back(i | (l << 8) | (j << 16) | (k << 20));
+    }
+  }
+  h.task_start[D + 1] = (int)h.tasks.size();
+  for (int col = 0; col < n; ++col)
+    for (int row = col; row < n; ++row) h.pk.push_back(row | (col << 16));
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < m.dof_cnt[i]; ++j) h.dof_link.push_back(i);
+  return h;
 }
 
 bool ensure_v1(pbad_gpu_ctx* c) {
@@ -799,6 +867,34 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   c->ka = KernelArgs{dm, df, ds, L, nullptr, nullptr, max_batch};
   c->chain = chain_eligible(m, f, sim);
   c->chain4 = c->chain4 && c->chain;
+  c->tree = !c->chain && tree_eligible(m, f, sim);
+  if (c->tree) {
+    const TreeHost th = make_tree_host(m);
+    TreeDesc& td = c->td;
+    td.N = m.N;
+    td.n = m.n;
+    td.D = th.D;
+    td.np = m.n * (m.n + 1) / 2;
+    td.n_tasks = (int)th.tasks.size();
+    td.lvl_start = up_i(th.lvl_start);
+    td.lvl_links = up_i(th.lvl_links);
+    td.ch_start = up_i(th.ch_start);
+    td.ch_list = th.ch_list.empty() ? up_i(std::vector<int>(1, 0)) : up_i(th.ch_list);
+    td.task_start = up_i(th.task_start);
+    td.tasks = up_i(th.tasks);
+    td.anc = up_i(th.anc);
+    td.depth = up_i(th.depth);
+    td.pk = up_i(th.pk);
+    td.dof_link = up_i(th.dof_link);
+    const long np2 = (td.np + 3) & ~3L, N16 = 16L * m.N;
+    td.o_hw0 = np2;
+    td.o_hw1 = np2 + N16;
+    td.o_t0 = np2 + 2 * N16;
+    td.o_t1 = np2 + 3 * N16;
+    td.gstride = np2 + 4 * N16;
+    td.smem_doubles = (int)(tree_smem_bytes(td) / sizeof(double));
+    if (tree_smem_bytes(td) > 200 * 1024) c->tree = false;
+  }
   if (!dm.parent || !dm.S) {
     delete c;
     return fail(PBAD_E_CUDA, "cudaMalloc of the model failed");
@@ -823,6 +919,14 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     delete c;
     return fail(PBAD_E_CUDA, "cudaMalloc failed (workspace %.1f MB)", per_env * 8.0 * max_batch / 1e6);
   }
+  if (c->tree) {
+    c->tws = dalloc<double>((size_t)c->td.gstride * max_batch);
+    if (!c->tws) {
+      delete c;
+      return fail(PBAD_E_CUDA, "cudaMalloc failed (tree workspace %.1f MB)", c->td.gstride * 8.0 * max_batch / 1e6);
+    }
+    c->owned.push_back(c->tws);
+  }
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
     delete c;
@@ -835,7 +939,7 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
 void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
 int32_t pbad_gpu_path(const pbad_gpu_ctx* c) {
-  return c->chain4 ? PBAD_PATH_CHAIN4 : c->chain ? PBAD_PATH_CHAIN : PBAD_PATH_GENERAL;
+  return c->chain4 ? PBAD_PATH_CHAIN4 : c->chain ? PBAD_PATH_CHAIN : c->tree ? PBAD_PATH_TREE : PBAD_PATH_GENERAL;
 }
 const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) {
   // chain path: quad-interleaved [n/4][B][4]; general path: [n][B]
@@ -863,6 +967,7 @@ int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
   for (int k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
     CUDA_TRY(c->chain4  ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain ? launch_chain_step(c->ca, c->dout, s)
+             : c->tree  ? launch_tree_step(c->ka, c->td, c->tws, c->dout, s)
                         : launch_step(c->ka, c->dout, s));
   return PBAD_OK;
 }

@@ -108,6 +108,28 @@ struct ChainLayout {
   long total;
 };
 
+// Tree path (pbad_tree.cu): warp-per-environment Newton (LM) for articulated
+// trees.  Host-precomputed structure; the per-env global workspace `tws` is
+// env-major with stride `gstride` doubles: GN lower-packed [np], history
+// world transforms hw0/hw1 [N][16] and their body products T0/T1 [N][16].
+struct TreeDesc {
+  int N, n, D, np;         // links, dofs, max depth, n(n+1)/2
+  int n_tasks;
+  const int* lvl_start;    // [D+2] offsets into lvl_links
+  const int* lvl_links;    // links ordered by depth (ascending index within a level)
+  const int* ch_start;     // [N+1]
+  const int* ch_list;      // children of each link in DESCENDING index order (adjoint.cpp:54-62)
+  const int* task_start;   // [D+2] GN tasks of walk step s (0 = own block)
+  const int* tasks;        // packed i | l<<8 | j<<16 | k<<20
+  const int* anc;          // [N][D+1]: s-th ancestor of link i (anc[i][0] = i), -1 beyond the root
+  const int* depth;        // [N]
+  const int* pk;           // [np] packed lower index -> row | col<<16
+  const int* dof_link;     // [n] link owning each dof
+  int smem_doubles;        // per environment
+  long gstride;            // per-env doubles of tws
+  long o_hw0, o_hw1, o_t0, o_t1;  // offsets inside one env's tws block (GN at 0)
+};
+
 struct Outputs {
   double* q;        // [B][S+1][n]
   double* energy;   // [B][S+1][2]

@@ -40,6 +40,12 @@ int chain4_max_memory();
 long chain4_record_doubles(bool massive);
 long chain4_hist_doubles();
 
+// tree path (pbad_tree.cu): warp-per-environment LM for articulated trees
+bool tree_eligible_sizes(int N, int n);
+size_t tree_smem_bytes(const TreeDesc& td);
+cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
+                             cudaStream_t s);
+
 cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
                         cudaStream_t s);
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s);

@@ -1,0 +1,705 @@
+// pbad_tree.cu -- warp-per-environment Newton (LM) kernel for articulated trees.
+//
+// The Newton path of the north star (SURVEY.md §8 K4+K5): per PBAD step one
+// warp owns one environment and runs begin_step, the whole Levenberg-Marquardt
+// loop and finish_step (stepper.cpp:83-147, optim.cpp:80-139) without leaving
+// the kernel.  Per evaluation:
+//   * forward kinematics (kinematics.cpp:171-181, adjoint.cpp:9-27): joint
+//     transforms link-parallel across lanes, world transforms level-synchronous
+//     over the tree depth, levers dof-parallel;
+//   * energy value (objective.cpp:215-226): the three correlation values and the
+//     gravity potential are per-link ddots summed serially in link order, the
+//     history factors T = hw S precomputed once per step;
+//   * gradient (adjoint.cpp:49-64): both adjoint sweeps (inertial seeds and
+//     gravity cotangents) run concurrently, level-synchronous from the leaves,
+//     each parent summing its children's contributions in descending child index
+//     (the reference's accumulation order);
+//   * Gauss-Newton matrix (adjoint.cpp:132-176, objective.cpp:249-254):
+//     composite inertias level-synchronous, then one lane per (link, ancestor,
+//     dof pair) task evaluating both mixed traces from one A^T B product,
+//     symmetrised on the fly into a lower-packed matrix;
+//   * Cholesky (optim.cpp:11-15) right-looking in shared memory with the
+//     trailing update spread over the packed triangle, and the two triangular
+//     solves with the right-hand side in registers.
+// Every scalar follows the numeric contract (pbad_math.cuh): the results are
+// bit-identical to the reference build and the C oracle (tests/test_gpu_parity.py).
+#include <cuda_runtime.h>
+
+#include "pbad_joint.cuh"
+#include "pbad_kernels.cuh"
+#include "pbad_launch.h"
+#include "pbad_math.cuh"
+
+namespace pbad_gpu {
+namespace tree {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int MAXV = 3;  // dof vectors in registers: n <= 96
+constexpr int MAXN = 96;
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
+enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
+
+__device__ __forceinline__ M4 ld16(const double* p) {
+  M4 m;
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 v = q[k];
+    m.a[2 * k] = v.x;
+    m.a[2 * k + 1] = v.y;
+  }
+  return m;
+}
+__device__ __forceinline__ M4 ldg16(const double* p) {
+  M4 m;
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 v = __ldg(q + k);
+    m.a[2 * k] = v.x;
+    m.a[2 * k + 1] = v.y;
+  }
+  return m;
+}
+__device__ __forceinline__ void st16(double* p, const M4& m) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) q[k] = make_double2(m.a[2 * k], m.a[2 * k + 1]);
+}
+
+// trace(mul(X, F)) and trace(mul(transpose(X), F)) from the diagonal only
+__device__ __forceinline__ double trace_mul(const M4& X, const M4& F) {
+  double d[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    double acc = X.a[p] * F.a[4 * p];
+    acc = fma(X.a[p + 4], F.a[1 + 4 * p], acc);
+    acc = fma(X.a[p + 8], F.a[2 + 4 * p], acc);
+    acc = fma(X.a[p + 12], F.a[3 + 4 * p], acc);
+    d[p] = acc;
+  }
+  return ((d[0] + d[1]) + d[2]) + d[3];
+}
+__device__ __forceinline__ double trace_tmul(const M4& X, const M4& F) {
+  double d[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    double acc = X.a[4 * p] * F.a[4 * p];
+    acc = fma(X.a[1 + 4 * p], F.a[1 + 4 * p], acc);
+    acc = fma(X.a[2 + 4 * p], F.a[2 + 4 * p], acc);
+    acc = fma(X.a[3 + 4 * p], F.a[3 + 4 * p], acc);
+    d[p] = acc;
+  }
+  return ((d[0] + d[1]) + d[2]) + d[3];
+}
+
+// gravity cotangent of one link (objective.cpp:48-58): c = -ghat (S e4)^T
+__device__ __forceinline__ M4 gravity_cot(const DForces& f, const M4& S) {
+  const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
+  const double e4[4] = {0.0, 0.0, 0.0, 1.0};
+  double u[4];
+  mul_vec4(S, e4, u);
+  M4 c;
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c.a[r + 4 * s] = (-ghat[r]) * u[s];
+  return c;
+}
+
+__device__ __forceinline__ int pidx(int n, int row, int col) { return col * (2 * n - col - 1) / 2 + row; }
+
+struct W {
+  const DModel* m;
+  const DForces* f;
+  const DSchedule* sc;
+  const TreeDesc* td;
+  int lane, N, n, D, np;
+  bool grav;
+  double inv_dt2, histconst;
+  // shared memory
+  double *value, *world, *lever, *scr, *damped, *red;
+  double *x, *grad, *cand, *vtau, *vtmp;
+  // global, this environment's block
+  double *gn, *hw0, *hw1, *T0, *T1;
+  __device__ __forceinline__ double* scr_k(int k) const { return scr + (long)k * 16 * N; }
+};
+
+// VecX dot (32 interleaved partials + pairwise tree, pbad_math.cuh vdot32):
+// lane k owns partial k, the butterfly reproduces the tree (commutative adds)
+__device__ __forceinline__ double vdot_warp(const W& w, const double* a, const double* b) {
+  double p = 0.0;
+  for (int i = w.lane; i < w.n; i += 32) p = fma(a[i], b[i], p);
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) p = p + __shfl_xor_sync(FULL, p, s);
+  return p;
+}
+__device__ __forceinline__ double infnorm_warp(const W& w, const double* a) {
+  double mx = 0.0;
+  for (int i = w.lane; i < w.n; i += 32) mx = fmax(mx, fabs(a[i]));
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, s));
+  return mx;
+}
+__device__ __forceinline__ bool all_finite_warp(const W& w, const double* a) {
+  bool ok = true;
+  for (int i = w.lane; i < w.n; i += 32) ok = ok && isfinite(a[i]);
+  return __all_sync(FULL, ok);
+}
+
+// forward_pass / ConfigPass::make value+world part (kinematics.cpp:171-181,
+// adjoint.cpp:9-27).  false = non-finite configuration (ModelError).
+__device__ bool fk_world(const W& w, const double* q) {
+  if (!all_finite_warp(w, q)) return false;
+  const DModel& m = *w.m;
+  for (int i = w.lane; i < w.N; i += 32) {
+    double ql[6];
+    const int off = m.dof_off[i], cnt = m.dof_cnt[i];
+    for (int j = 0; j < cnt; ++j) ql[j] = q[off + j];
+    st16(w.value + 16 * i, joint_transform(m.kind[i], m.axis + 3 * i, ldg16(m.offset + 16 * i), ql));
+  }
+  __syncwarp();
+  const TreeDesc& td = *w.td;
+  for (int d = 0; d <= w.D; ++d) {
+    for (int t = td.lvl_start[d] + w.lane; t < td.lvl_start[d + 1]; t += 32) {
+      const int i = td.lvl_links[t];
+      const int p = m.parent[i];
+      const M4 v = ld16(w.value + 16 * i);
+      st16(w.world + 16 * i, p >= 0 ? mul(ld16(w.world + 16 * p), v) : v);
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// levers of ConfigPass::make (adjoint.cpp:20-24): lever = parent_world * d1
+__device__ void fk_levers(const W& w, const double* q) {
+  const DModel& m = *w.m;
+  double* d1s = w.scr;  // n x 16 scratch
+  for (int i = w.lane; i < w.N; i += 32) {
+    double ql[6];
+    const int off = m.dof_off[i], cnt = m.dof_cnt[i];
+    for (int j = 0; j < cnt; ++j) ql[j] = q[off + j];
+    M4 v, d1[6];
+    joint_jet(m.kind[i], m.axis + 3 * i, ldg16(m.offset + 16 * i), ql, &v, d1, nullptr, false);
+    for (int j = 0; j < cnt; ++j) st16(d1s + 16 * (off + j), d1[j]);
+  }
+  __syncwarp();
+  for (int k = w.lane; k < w.n; k += 32) {
+    const int p = m.parent[w.td->dof_link[k]];
+    const M4 pw = p >= 0 ? ld16(w.world + 16 * p) : m4_identity();
+    st16(w.lever + 16 * k, mul(pw, ld16(d1s + 16 * k)));
+  }
+  __syncwarp();
+}
+
+// StepObjective energy value (objective.cpp:215-226, 237) at the configuration
+// whose world transforms are in w.world; q is that configuration.
+__device__ double value_at(const W& w, const double* q) {
+  const DModel& m = *w.m;
+  for (int i = w.lane; i < w.N; i += 32) {
+    const M4 wi = ld16(w.world + 16 * i);
+    const M4 S = ldg16(m.S + 16 * i);
+    w.red[4 * i] = ddot(mul(wi, S), wi);
+    w.red[4 * i + 1] = ddot(ld16(w.T1 + 16 * i), wi);
+    w.red[4 * i + 2] = ddot(ld16(w.T0 + 16 * i), wi);
+    if (w.grav) w.red[4 * i + 3] = ddot(gravity_cot(*w.f, S), wi);
+  }
+  __syncwarp();
+  double s = 0.0;
+  if (w.lane < 4)
+    for (int i = 0; i < w.N; ++i) s += w.red[4 * i + w.lane];
+  const double cpp = __shfl_sync(FULL, s, 0) - m.weighted_mass;
+  const double c1 = __shfl_sync(FULL, s, 1) - m.weighted_mass;
+  const double c0 = __shfl_sync(FULL, s, 2) - m.weighted_mass;
+  const double pot = w.grav ? __shfl_sync(FULL, s, 3) : 0.0;
+  const double inertial = 0.5 * w.inv_dt2 * (cpp - 4.0 * c1 + 2.0 * c0 + w.histconst);
+  const double tdot = vdot_warp(w, w.vtau, q);
+  return inertial + pot - tdot;
+}
+
+// energy gradient (objective.cpp:227-248): inertial seeds and gravity
+// cotangents through functional_grad (adjoint.cpp:49-64), then (g + pg) - tau.
+__device__ void gradient(const W& w, double* g) {
+  const DModel& m = *w.m;
+  const TreeDesc& td = *w.td;
+  double* sA = w.scr_k(0);  // inertial seeds -> children contributions
+  double* sB = w.scr_k(1);  // gravity cotangents -> children contributions
+  for (int i = w.lane; i < w.N; i += 32) {
+    const M4 S = ldg16(m.S + 16 * i);
+    M4 d = sub(ld16(w.world + 16 * i), scale(2.0, ld16(w.hw1 + 16 * i)));
+    d = add(d, ld16(w.hw0 + 16 * i));
+    d = scale(w.inv_dt2, d);
+    st16(sA + 16 * i, mul(d, S));
+    if (w.grav) st16(sB + 16 * i, add(m4_zero(), gravity_cot(*w.f, S)));
+  }
+  __syncwarp();
+  const int nsw = w.grav ? 2 : 1;
+  for (int d = w.D; d >= 0; --d) {
+    const int l0 = td.lvl_start[d], cnt = td.lvl_start[d + 1] - l0;
+    for (int t = w.lane; t < nsw * cnt; t += 32) {
+      const int sw = t / cnt;
+      const int i = td.lvl_links[l0 + t - sw * cnt];
+      double* seeds = sw ? sB : sA;
+      double* gout = sw ? w.vtmp : g;
+      M4 adj = m4_zero();
+      for (int c = td.ch_start[i]; c < td.ch_start[i + 1]; ++c) adj = add(adj, ld16(seeds + 16 * td.ch_list[c]));
+      const M4 a = add(adj, ld16(seeds + 16 * i));
+      const int off = m.dof_off[i];
+      for (int j = 0; j < m.dof_cnt[i]; ++j) gout[off + j] = 0.0 + ddot(ld16(w.lever + 16 * (off + j)), a);
+      st16(seeds + 16 * i, mul_bt(a, ld16(w.value + 16 * i)));
+    }
+    __syncwarp();
+  }
+  for (int k = w.lane; k < w.n; k += 32) g[k] = (g[k] + (w.grav ? w.vtmp[k] : 0.0)) - w.vtau[k];
+  __syncwarp();
+}
+
+// Gauss-Newton matrix gn = sym(hess_ab(x, x) / dt^2 + pot.gn) (objective.cpp:
+// 249-254, adjoint.cpp:132-176), lower-packed into w.gn (global).
+__device__ void gn_assemble(const W& w) {
+  const DModel& m = *w.m;
+  const TreeDesc& td = *w.td;
+  double* ai = w.scr_k(0);
+  double* fwd = w.scr_k(1);
+  double* bwd = w.scr_k(2);
+  double* Z = w.scr_k(3);
+  for (int d = w.D; d >= 0; --d) {
+    for (int t = td.lvl_start[d] + w.lane; t < td.lvl_start[d + 1]; t += 32) {
+      const int i = td.lvl_links[t];
+      M4 acc = m4_zero();
+      for (int c = td.ch_start[i]; c < td.ch_start[i + 1]; ++c) acc = add(acc, ld16(Z + 16 * td.ch_list[c]));
+      const M4 a = add(acc, ldg16(m.S + 16 * i));
+      const M4 v = ld16(w.value + 16 * i);
+      st16(ai + 16 * i, a);
+      const M4 y = mul(v, a);
+      st16(fwd + 16 * i, y);
+      st16(bwd + 16 * i, mul_bt(a, v));
+      st16(Z + 16 * i, mul_bt(y, v));
+    }
+    __syncwarp();
+  }
+  for (int t = w.lane; t < w.np; t += 32) w.gn[t] = 0.0;
+  __syncwarp();
+  const int n = w.n;
+  for (int s = 0; s <= w.D; ++s) {
+    for (int t = td.task_start[s] + w.lane; t < td.task_start[s + 1]; t += 32) {
+      const int code = td.tasks[t];
+      const int i = code & 255, l = (code >> 8) & 255, j = (code >> 16) & 15, k = (code >> 20) & 15;
+      const int offi = m.dof_off[i], offl = m.dof_off[l];
+      const M4 M = mul_at(ld16(w.lever + 16 * (offi + j)), ld16(w.lever + 16 * (offl + k)));
+      double grc, gcr;
+      int row, col;
+      if (s == 0) {
+        const M4 F = ld16(ai + 16 * i);
+        const double tjk = trace_mul(M, F);
+        const double tkj = (j == k) ? tjk : trace_tmul(M, F);
+        grc = w.inv_dt2 * tjk + 0.0;
+        gcr = w.inv_dt2 * tkj + 0.0;
+        row = offi + k;
+        col = offi + j;
+      } else {
+        const double t1 = trace_mul(M, ld16(fwd + 16 * i));
+        const double t2 = trace_tmul(M, ld16(bwd + 16 * i));
+        grc = w.inv_dt2 * t2 + 0.0;
+        gcr = w.inv_dt2 * t1 + 0.0;
+        row = offi + j;
+        col = offl + k;
+      }
+      w.gn[pidx(n, row, col)] = 0.5 * (grc + gcr);
+    }
+    __syncwarp();
+    if (s >= 1 && s < w.D) {
+      for (int i = w.lane; i < w.N; i += 32) {
+        if (td.depth[i] <= s) continue;
+        const M4 vl = ld16(w.value + 16 * td.anc[i * (w.D + 1) + s]);
+        st16(fwd + 16 * i, mul(vl, ld16(fwd + 16 * i)));
+        st16(bwd + 16 * i, mul_bt(ld16(bwd + 16 * i), vl));
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// LLT (optim.cpp:11-15, eigen_lite right-looking) on the lower-packed damped
+// matrix in shared memory.  false = non-positive pivot.
+__device__ bool llt_factor_w(const W& w) {
+  double* A = w.damped;
+  const int n = w.n;
+  for (int k = 0; k < n; ++k) {
+    const int cb = pidx(n, 0, k);
+    const double x = A[cb + k];
+    if (x <= 0.0) return false;
+    const double d = sqrt(x);
+    __syncwarp();
+    for (int i = k + 1 + w.lane; i < n; i += 32) A[cb + i] = A[cb + i] / d;
+    if (w.lane == 0) A[cb + k] = d;
+    __syncwarp();
+    if (k + 1 < n) {
+      for (int t = pidx(n, k + 1, k + 1) + w.lane; t < w.np; t += 32) {
+        const int rc = __ldg(w.td->pk + t);
+        const int i = rc & 0xffff, j = rc >> 16;
+        A[t] = fma(-A[cb + i], A[cb + j], A[t]);
+      }
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+__device__ __forceinline__ double sel(const double (&v)[MAXV], int s) {
+  return s == 0 ? v[0] : (s == 1 ? v[1] : v[2]);
+}
+
+// llt_solve (eigen_lite): forward then backward substitution, column-oriented;
+// v holds the right-hand side for rows lane + 32 s on entry, the solution on exit.
+__device__ void llt_solve_w(const W& w, double (&v)[MAXV]) {
+  const double* A = w.damped;
+  const int n = w.n;
+  for (int j = 0; j < n; ++j) {
+    const double xj = __shfl_sync(FULL, sel(v, j >> 5), j & 31) / A[pidx(n, j, j)];
+#pragma unroll
+    for (int s = 0; s < MAXV; ++s) {
+      const int i = w.lane + 32 * s;
+      if (i == j) v[s] = xj;
+      else if (i > j && i < n) v[s] = fma(-A[pidx(n, i, j)], xj, v[s]);
+    }
+  }
+  for (int j = n - 1; j >= 0; --j) {
+    const double xj = __shfl_sync(FULL, sel(v, j >> 5), j & 31) / A[pidx(n, j, j)];
+#pragma unroll
+    for (int s = 0; s < MAXV; ++s) {
+      const int i = w.lane + 32 * s;
+      if (i == j) v[s] = xj;
+      else if (i < j) v[s] = fma(-A[pidx(n, j, i)], xj, v[s]);
+    }
+  }
+}
+
+// full evaluation at w.x (value, levers, gradient, GN); false = ModelError
+__device__ bool full_eval(const W& w, double* value) {
+  if (!fk_world(w, w.x)) return false;
+  *value = value_at(w, w.x);
+  return true;
+}
+__device__ void derivatives(const W& w) {
+  fk_levers(w, w.x);
+  gradient(w, w.grad);
+  gn_assemble(w);
+}
+
+struct Solver {
+  int status, iters, stag, acc;
+  double value, lambda, grad0;
+};
+
+__device__ __forceinline__ bool grad_converged(const W& w, const Solver& S) {
+  const DOpt& o = w.sc->opt;
+  const double g = infnorm_warp(w, w.grad);
+  if (g <= o.grad_tol * fmax(1.0, infnorm_warp(w, w.x))) return true;
+  if (o.grad_rtol > 0.0 && g <= o.grad_rtol * S.grad0) return true;
+  return false;
+}
+
+// LmSolver::iterate (optim.cpp:95-134).  Returns the status or -1 (ModelError).
+__device__ int lm_iterate(const W& w, Solver& S) {
+  const DOpt& o = w.sc->opt;
+  if (S.status != ST_RUNNING) return S.status;
+  if (S.iters >= o.max_iters) return S.status = ST_FAILED;
+  if (grad_converged(w, S)) return S.status = ST_CONVERGED;
+  const int n = w.n;
+  for (int t = w.lane; t < w.np; t += 32) {
+    const int rc = __ldg(w.td->pk + t);
+    const double g = w.gn[t];
+    w.damped[t] = ((rc & 0xffff) == (rc >> 16)) ? g + S.lambda : g;
+  }
+  double v[MAXV];
+#pragma unroll
+  for (int s = 0; s < MAXV; ++s) {
+    const int i = w.lane + 32 * s;
+    v[s] = i < n ? -w.grad[i] : 0.0;
+  }
+  __syncwarp();
+  bool accepted = false;
+  const bool ok = llt_factor_w(w);
+  bool finite = false;
+  if (ok) {
+    llt_solve_w(w, v);
+    bool f = true;
+#pragma unroll
+    for (int s = 0; s < MAXV; ++s)
+      if (w.lane + 32 * s < n) f = f && isfinite(v[s]);
+    finite = __all_sync(FULL, f);
+  }
+  if (finite) {
+#pragma unroll
+    for (int s = 0; s < MAXV; ++s) {
+      const int i = w.lane + 32 * s;
+      if (i < n) w.cand[i] = w.x[i] + v[s];
+    }
+    __syncwarp();
+    if (!fk_world(w, w.cand)) return -1;
+    const double tv = value_at(w, w.cand);
+    if (isfinite(tv) && tv < S.value) {
+      const double oldv = S.value;
+      for (int i = w.lane; i < n; i += 32) w.x[i] = w.cand[i];
+      __syncwarp();
+      derivatives(w);
+      const double nv = tv;  // evaluate(x) repeats value(cand) bit for bit
+      S.value = nv;
+      S.lambda = fmax(S.lambda / o.lm_lambda_factor, 1e-12);
+      accepted = true;
+      ++S.acc;
+      if (oldv - nv <= o.ftol * fmax(1.0, fabs(oldv))) ++S.stag;
+      else S.stag = 0;
+      if (S.stag >= 2) S.status = ST_CONVERGED;
+    }
+  }
+  if (!accepted) {
+    S.lambda *= o.lm_lambda_factor;
+    if (S.lambda > o.lm_lambda_max) S.status = ST_FAILED;
+  }
+  ++S.iters;
+  if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
+  return S.status;
+}
+
+// ForceModel::tau_at (objective.hpp:28-58), element-parallel
+__device__ void tau_at(const W& w, double t, double* dst) {
+  const DForces& f = *w.f;
+  const int n = w.n;
+  for (int i = w.lane; i < n; i += 32) {
+    double v = 0.0;
+    if (f.has_act && f.act_len == n) {
+      if (f.act_kind == 0) {
+        v = f.act_amp[i];
+      } else {
+        const double ph = i < f.act_phase_len ? f.act_phase[i] : 0.0;
+        double s, c;
+        pbad_sincos(2.0 * 3.141592653589793 * f.act_freq * t + ph, &s, &c);
+        v = f.act_amp[i] * s;
+      }
+    } else if (f.tau_len == n) {
+      v = f.tau[i];
+    }
+    dst[i] = v;
+  }
+}
+
+// copy w.world into a history block and its body products T = hw S
+__device__ void store_history(const W& w, double* hw, double* T) {
+  for (int i = w.lane; i < w.N; i += 32) {
+    const M4 wi = ld16(w.world + 16 * i);
+    st16(hw + 16 * i, wi);
+    st16(T + 16 * i, mul(wi, ldg16(w.m->S + 16 * i)));
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
+                                                  int* iws, long B, TreeDesc td, double* tws, Outputs out) {
+  extern __shared__ __align__(16) double smem[];
+  const long e = blockIdx.x;
+  if (e >= B) return;
+  if (iws[(long)IS_RUN * B + e] != TR_RUNNING) return;
+  W w;
+  w.m = &m;
+  w.f = &f;
+  w.sc = &sc;
+  w.td = &td;
+  w.lane = threadIdx.x;
+  w.N = td.N;
+  w.n = td.n;
+  w.D = td.D;
+  w.np = td.np;
+  w.grav = f.gravity_nonzero != 0;
+  const double dt = sc.dt;
+  w.inv_dt2 = 1.0 / (dt * dt);
+  {
+    const int N16 = 16 * td.N, nv = (td.n + 1) & ~1;
+    const int scr = (4 * N16 > 16 * td.n) ? 4 * N16 : 16 * td.n;
+    double* p = smem;
+    w.value = p; p += N16;
+    w.world = p; p += N16;
+    w.lever = p; p += 16 * td.n;
+    w.scr = p; p += scr;
+    w.damped = p; p += (td.np + 1) & ~1;
+    w.x = p; p += nv;
+    w.grad = p; p += nv;
+    w.cand = p; p += nv;
+    w.vtau = p; p += nv;
+    w.vtmp = p; p += nv;
+    w.red = p;
+    double* g = tws + e * td.gstride;
+    w.gn = g;
+    w.hw0 = g + td.o_hw0;
+    w.hw1 = g + td.o_hw1;
+    w.T0 = g + td.o_t0;
+    w.T1 = g + td.o_t1;
+  }
+  const int n = td.n;
+  int* const ivp = iws + e;
+  auto iv = [&](int slot) -> int& { return ivp[(long)slot * B]; };
+  const int step = iv(IS_STEP);
+
+  // ---- begin_step (stepper.cpp:83-115) ----
+  double* h0 = w.cand;
+  double* h1 = w.vtmp;
+  for (int k = w.lane; k < n; k += 32) {
+    h0[k] = ws[(L.hist0 + k) * B + e];
+    h1[k] = ws[(L.hist1 + k) * B + e];
+  }
+  const double t0 = step * dt;
+  tau_at(w, t0 + sc.times[2] * dt, w.vtau);
+  {
+    const double span = -sc.times[0];
+    const double tau_m = sc.times[2];
+    for (int k = w.lane; k < n; k += 32) w.x[k] = sc.warm_start ? h1[k] + (tau_m / span) * (h1[k] - h0[k]) : h1[k];
+  }
+  __syncwarp();
+  // StepObjective ctor (objective.cpp:162-185)
+  if (!all_finite_warp(w, h0) || !all_finite_warp(w, h1)) {
+    if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
+    return;
+  }
+  fk_world(w, h0);
+  store_history(w, w.hw0, w.T0);
+  fk_world(w, h1);
+  store_history(w, w.hw1, w.T1);
+  {
+    for (int i = w.lane; i < w.N; i += 32) {
+      const M4 w0 = ld16(w.hw0 + 16 * i), w1 = ld16(w.hw1 + 16 * i);
+      const M4 T1 = ld16(w.T1 + 16 * i);
+      w.red[4 * i] = ddot(T1, w1);
+      w.red[4 * i + 1] = ddot(ld16(w.T0 + 16 * i), w0);
+      w.red[4 * i + 2] = ddot(T1, w0);
+    }
+    __syncwarp();
+    double s = 0.0;
+    if (w.lane < 3)
+      for (int i = 0; i < w.N; ++i) s += w.red[4 * i + w.lane];
+    const double c11 = __shfl_sync(FULL, s, 0) - m.weighted_mass;
+    const double c00 = __shfl_sync(FULL, s, 1) - m.weighted_mass;
+    const double c10 = __shfl_sync(FULL, s, 2) - m.weighted_mass;
+    w.histconst = 4.0 * c11 + c00 - 4.0 * c10;
+    __syncwarp();
+  }
+  // solver construction (optim.cpp:82-93): first evaluation with GN
+  Solver S;
+  S.status = ST_RUNNING;
+  S.iters = 0;
+  S.stag = 0;
+  S.acc = 0;
+  S.lambda = sc.opt.lm_lambda0;
+  {
+    double v;
+    if (!full_eval(w, &v)) {
+      if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
+      return;
+    }
+    if (!isfinite(v)) {
+      if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_INIT;
+      return;
+    }
+    S.value = v;
+    derivatives(w);
+    S.grad0 = infnorm_warp(w, w.grad);
+  }
+  int st;
+  while ((st = lm_iterate(w, S)) == ST_RUNNING) {
+  }
+  if (st < 0) {
+    if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
+    return;
+  }
+
+  // ---- finish_step (stepper.cpp:118-147) ----
+  const bool converged = S.status == ST_CONVERGED;
+  const long Stot = sc.total_steps;
+  const double gnorm = infnorm_warp(w, w.grad);
+  if (w.lane == 0) {
+    if (out.iterations) out.iterations[e * Stot + step] = S.iters;
+    if (out.converged) out.converged[e * Stot + step] = converged;
+    if (out.accepted) out.accepted[e * Stot + step] = S.acc;
+    if (out.final_value) out.final_value[e * Stot + step] = S.value;
+    if (out.final_grad_norm) out.final_grad_norm[e * Stot + step] = gnorm;
+    iv(IS_NREP) = step + 1;
+    iv(IS_ITERS) = S.iters;
+    iv(IS_STATUS) = S.status;
+    iv(IS_ACC) = S.acc;
+  }
+  const int fs = converged ? 0 : iv(IS_FAIL) + 1;
+  __syncwarp();
+  if (w.lane == 0) iv(IS_FAIL) = fs;
+  if (fs > sc.fail_limit) {
+    if (w.lane == 0) iv(IS_RUN) = TR_FAIL_LIMIT;
+    return;
+  }
+  // history shift (order 2): hist0 <- hist1, hist1 <- x
+  for (int k = w.lane; k < n; k += 32) {
+    const double h1k = ws[(L.hist1 + k) * B + e];  // (h1 scratch was reused by the solver)
+    ws[(L.hist0 + k) * B + e] = h1k;
+    ws[(L.hist1 + k) * B + e] = w.x[k];
+  }
+  // energy audit: fd_kinetic(world(hist1_old), world(x)), gravity_potential(world(x))
+  fk_world(w, w.x);
+  for (int i = w.lane; i < w.N; i += 32) {
+    const M4 S_i = ldg16(m.S + 16 * i);
+    const M4 wn = ld16(w.world + 16 * i);
+    const M4 td_ = divs(sub(wn, ld16(w.hw1 + 16 * i)), dt);
+    w.red[4 * i] = 0.5 * ddot(mul(td_, S_i), td_);
+    const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
+    const double e4[4] = {0.0, 0.0, 0.0, 1.0};
+    double u[4], vv[4];
+    mul_vec4(S_i, e4, u);
+    mul_vec4(wn, u, vv);
+    w.red[4 * i + 1] = dot4(ghat, vv);
+  }
+  __syncwarp();
+  if (w.lane == 0) {
+    double ke = 0.0, pe = 0.0;
+    for (int i = 0; i < w.N; ++i) {
+      ke += w.red[4 * i];
+      pe -= w.red[4 * i + 1];
+    }
+    const long S1 = Stot + 1;
+    if (out.energy) {
+      out.energy[(e * S1 + step + 1) * 2] = ke;
+      out.energy[(e * S1 + step + 1) * 2 + 1] = pe;
+    }
+    iv(IS_NSAMP) = step + 2;
+    iv(IS_STEP) = step + 1;
+    if (step + 1 >= sc.total_steps) iv(IS_RUN) = TR_OK;
+  }
+  if (out.q) {
+    const long S1 = Stot + 1;
+    for (int k = w.lane; k < n; k += 32) out.q[(e * S1 + step + 1) * n + k] = w.x[k];
+  }
+}
+
+}  // namespace tree
+
+bool tree_eligible_sizes(int N, int n) { return N >= 1 && N <= 255 && n >= 1 && n <= tree::MAXN; }
+
+static int tree_smem_doubles(const TreeDesc& td) {
+  const int N16 = 16 * td.N, nv = (td.n + 1) & ~1;
+  const int scr = (4 * N16 > 16 * td.n) ? 4 * N16 : 16 * td.n;
+  return 2 * N16 + 16 * td.n + scr + ((td.np + 1) & ~1) + 5 * nv + 4 * td.N + 32;
+}
+
+size_t tree_smem_bytes(const TreeDesc& td) { return sizeof(double) * (size_t)tree_smem_doubles(td); }
+
+cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
+                             cudaStream_t s) {
+  const size_t smem = tree_smem_bytes(td);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(tree::k_tree_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  tree::k_tree_step<<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
+  return cudaGetLastError();
+}
+
+}  // namespace pbad_gpu
