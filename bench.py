@@ -41,6 +41,10 @@ CONFIGS = {
                desc="C3: 4096 x 200-DOF serial hinge chains (make_chain_scene(100)), L-BFGS, dt=0.1"),
     "C4": dict(scene="humanoid", links=18, dt=0.01, batch=4096, opt="lm", seed=2, lo=-0.1, hi=0.1,
                desc="C4: 4096 x 41-DOF humanoid trees, LM (Gauss-Newton + Cholesky), dt=0.01"),
+    "C5": dict(scene="single_hinge", links=100, dt=0.01, batch=256, opt="lm", seed=3, lo=-0.3, hi=0.3, order=4,
+               objective="residual",
+               desc="C5: high-order collocation PBAD (K=4 residual form, U=300), 100-link chains, LM, dt=0.01, "
+                    "256 per GPU (2048 over 8 B200)"),
 }
 
 
@@ -70,20 +74,27 @@ def initial_states(cfg, scene, n, first_env, count):
 
 def sim_config(cfg, steps, fail_limit):
     from paper_1709_04145_b200.types import OptimizerKind, SimConfig
-    sim = SimConfig(dt=cfg["dt"], duration=cfg["dt"] * steps, consecutive_fail_limit=fail_limit)
+    from paper_1709_04145_b200.types import ObjectiveKind
+    sim = SimConfig(dt=cfg["dt"], duration=cfg["dt"] * steps, consecutive_fail_limit=fail_limit,
+                    order=cfg.get("order", 2),
+                    objective=ObjectiveKind.residual_form if cfg.get("objective") == "residual"
+                    else ObjectiveKind.energy_form)
     sim.optimizer.kind = OptimizerKind.lbfgs if cfg["opt"] == "lbfgs" else OptimizerKind.lm
     return sim
 
 
 def flops_per_env_step(cfg, model, iters, accepted):
     """SURVEY.md §8(d) canonical FP64 FLOPs (FMA = 2): iterations x per-iteration
-    cost + per-step overhead (construction eval, history precompute, energy audit)."""
+    cost + per-step overhead (construction eval, history precompute, energy audit).
+    Dense linear algebra re-derived to the minimal counts:
+    Cholesky n^3/3 (the survey's (2/3)n^3 is LU's count), the symmetric
+    2 J^T J product U^2 (U + 1) (one triangle: the two reference chains are equal
+    bit for bit) instead of a full 2 U^3 GEMM."""
     N, n = model.link_count(), model.total_dofs
     overhead = N * 481 + 240 * N + 205 * N
     if cfg["opt"] == "lbfgs":
         per_iter = N * (307 + 174) + n * (8 * 8 + 12)
         return iters * per_iter + overhead
-    # LM: (2/3)n^3 + 2n^2 + Eonly + a (grad + GN)
     depth_dofs = []
     for i in range(N):
         d, k = 0, i
@@ -92,7 +103,14 @@ def flops_per_env_step(cfg, model, iters, accepted):
             k = model.parent(k)
         depth_dofs.append(model.dof_count(i) * d)
     P = sum(depth_dofs)
-    rej = (2.0 / 3.0) * n ** 3 + 2 * n * n + 307 * N
+    if cfg.get("objective") == "residual":
+        u = cfg["order"] - 1
+        U = u * n
+        rej = U ** 3 / 3.0 + 2 * U * U + u * N * 600
+        acc_extra = U * U * (U + 1) + 2 * U * U + u * u * (320 * N + 48 * P)
+        return iters * rej + accepted * acc_extra + acc_extra + u * N * 600 + 240 * N + 205 * N
+    # LM energy form: n^3/3 + 2n^2 + Eonly + a (grad + GN)
+    rej = n ** 3 / 3.0 + 2 * n * n + 307 * N
     acc_extra = (120 * N + 54 * n) + (320 * N + 24 * P)
     return iters * rej + accepted * acc_extra + overhead + 320 * N + 24 * P
 
@@ -372,7 +390,10 @@ def main():
         "e2e": e2e,
         "gpu_launches": K,
         "kernel": {0: "pbad_gpu::k_step (general, thread per env)", 1: "pbad_gpu::k_chain_step (quad per env)",
-                   2: "pbad_gpu::c4::k_chain4_step (warp-synchronous quads, TMA-fed adjoint)"}.get(ctx.path),
+                   2: "pbad_gpu::c4::k_chain4_step (warp-synchronous quads, TMA-fed adjoint)",
+                   3: "pbad_gpu::tree::k_tree_step (warp per env, Newton/LM, in-SMEM Cholesky)",
+                   4: "pbad_gpu::resid::k_resid_step (CTA per env, residual-form LM, tiled J^T J + blocked Cholesky)"
+                   }.get(ctx.path),
         "clocks": clk,
         "mean_iterations_per_step": float(iters.mean()),
         "trajectories_ok": int(np.sum((st == 0) | (st == 4))),

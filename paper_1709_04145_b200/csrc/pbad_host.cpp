@@ -441,6 +441,9 @@ struct pbad_gpu_ctx {
   bool tree = false;       // rollouts use the warp-per-env Newton kernel (pbad_tree.cu)
   TreeDesc td{};
   double* tws = nullptr;   // tree-path per-env workspace (GN, history transforms)
+  bool resid = false;      // rollouts use the CTA-per-env residual-form kernel (pbad_resid.cu)
+  ResidDesc rd{};
+  double* rws = nullptr;
   std::vector<void*> owned;  // device allocations freed at destroy
   long max_batch = 0;
   long B = 0;  // current batch
@@ -614,6 +617,19 @@ bool tree_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim
   for (int i = 0; i < m.N; ++i)
     if (m.dof_cnt[i] > 6) return false;
   return true;
+}
+
+// The residual-form kernel covers hinge trees with the residual objective and
+// LM (the high-order collocation Newton path), gravity / actuation.
+bool resid_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
+  if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
+  if (sim->objective != PBAD_RESIDUAL_FORM || sim->opt.kind != PBAD_LM) return false;
+  if (sim->order < 2 || sim->order - 1 > 8) return false;
+  if (f->drag_d > 0.0) return false;
+  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
+  for (int i = 0; i < m.N; ++i)
+    if (m.kind[i] != PBAD_HINGE) return false;
+  return resid_eligible_sizes(m.n * (sim->order - 1));
 }
 
 // Host-side structure of the tree kernel: depth levels, children in
@@ -919,6 +935,65 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     delete c;
     return fail(PBAD_E_CUDA, "cudaMalloc failed (workspace %.1f MB)", per_env * 8.0 * max_batch / 1e6);
   }
+  c->resid = !c->chain && !c->tree && resid_eligible(m, f, sim);
+  if (c->resid) {
+    const TreeHost th = make_tree_host(m);
+    ResidDesc& rd = c->rd;
+    const long N = m.N, n = m.n, u = sim->order - 1, U = n * u;
+    rd.N = m.N;
+    rd.n = m.n;
+    rd.u = (int)u;
+    rd.U = (int)U;
+    rd.D = th.D;
+    bool chain = true;
+    for (int i = 0; i < m.N; ++i) chain = chain && m.parent[i] == i - 1;
+    rd.chain = chain;
+    rd.lvl_start = up_i(th.lvl_start);
+    rd.lvl_links = up_i(th.lvl_links);
+    rd.ch_start = up_i(th.ch_start);
+    rd.ch_list = th.ch_list.empty() ? up_i(std::vector<int>(1, 0)) : up_i(th.ch_list);
+    std::vector<int> wo(m.N);
+    for (int i = 0; i < m.N; ++i) wo[i] = i;
+    std::stable_sort(wo.begin(), wo.end(), [&](int a, int b) { return th.depth[a] > th.depth[b]; });
+    rd.walk_order = up_i(wo);
+    rd.pstride = 80 * N;
+    long o = 0;
+    auto take = [&](long cnt) {
+      const long at = o;
+      o += (cnt + 1) & ~1L;
+      return at;
+    };
+    rd.oJ = take(U * U);
+    rd.oGN = take(U * U);
+    rd.oDM = take(U * U);
+    rd.oFH = take(u * n * n);
+    rd.oPH = take(u * n * n);
+    rd.oPass = take(u * rd.pstride);
+    rd.oHW0 = take(16 * N);
+    rd.oHW1 = take(16 * N);
+    rd.oHA = take(u * u * 4 * 16 * N);
+    rd.oFA = take(2 * u * 2 * 16 * N);
+    rd.oSeeds = take(u * 16 * N);
+    rd.oCot = take(16 * N);
+    rd.oX = take(U);
+    rd.oGrad = take(U);
+    rd.oCand = take(std::max(U, 2 * n));
+    rd.oRes = take(U);
+    rd.oPg = take(U);
+    rd.oTau = take(U);
+    rd.oStep = take(U);
+    rd.gstride = (o + 31) & ~31L;
+    if (!ensure_v1(c)) {
+      delete c;
+      return fail(PBAD_E_CUDA, "cudaMalloc failed (workspace %.1f MB)", per_env * 8.0 * max_batch / 1e6);
+    }
+    c->rws = dalloc<double>((size_t)rd.gstride * max_batch);
+    if (!c->rws) {
+      delete c;
+      return fail(PBAD_E_CUDA, "cudaMalloc failed (residual workspace %.1f MB)", rd.gstride * 8.0 * max_batch / 1e6);
+    }
+    c->owned.push_back(c->rws);
+  }
   if (c->tree) {
     c->tws = dalloc<double>((size_t)c->td.gstride * max_batch);
     if (!c->tws) {
@@ -939,7 +1014,11 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
 void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
 int32_t pbad_gpu_path(const pbad_gpu_ctx* c) {
-  return c->chain4 ? PBAD_PATH_CHAIN4 : c->chain ? PBAD_PATH_CHAIN : c->tree ? PBAD_PATH_TREE : PBAD_PATH_GENERAL;
+  return c->chain4 ? PBAD_PATH_CHAIN4
+         : c->chain ? PBAD_PATH_CHAIN
+         : c->tree  ? PBAD_PATH_TREE
+         : c->resid ? PBAD_PATH_RESID
+                    : PBAD_PATH_GENERAL;
 }
 const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) {
   // chain path: quad-interleaved [n/4][B][4]; general path: [n][B]
@@ -968,6 +1047,7 @@ int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
     CUDA_TRY(c->chain4  ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain ? launch_chain_step(c->ca, c->dout, s)
              : c->tree  ? launch_tree_step(c->ka, c->td, c->tws, c->dout, s)
+             : c->resid ? launch_resid_step(c->ka, c->rd, c->rws, c->dout, s)
                         : launch_step(c->ka, c->dout, s));
   return PBAD_OK;
 }

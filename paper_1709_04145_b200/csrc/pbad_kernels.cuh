@@ -130,6 +130,21 @@ struct TreeDesc {
   long o_hw0, o_hw1, o_t0, o_t1;  // offsets inside one env's tws block (GN at 0)
 };
 
+// Residual-form path (pbad_resid.cu): CTA-per-environment LM for hinge
+// trees.  Per-env global workspace `rws`, env-major, stride gstride doubles.
+struct ResidDesc {
+  int N, n, u, U, D;
+  int chain;               // serial chain: every dof pair is ancestor-related (J dense)
+  const int* lvl_start;    // [D+2]
+  const int* lvl_links;    // [N]
+  const int* ch_start;     // [N+1]
+  const int* ch_list;      // children, descending index
+  const int* walk_order;   // [N] links by depth, deepest first (walk load balance)
+  long pstride;            // doubles per link pass (value, world, d1, d2, lever: 5 x 16N)
+  long gstride;
+  long oJ, oGN, oDM, oFH, oPH, oPass, oHW0, oHW1, oHA, oFA, oSeeds, oCot, oX, oGrad, oCand, oRes, oPg, oTau, oStep;
+};
+
 struct Outputs {
   double* q;        // [B][S+1][n]
   double* energy;   // [B][S+1][2]

@@ -46,6 +46,12 @@ size_t tree_smem_bytes(const TreeDesc& td);
 cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
                              cudaStream_t s);
 
+// residual-form path (pbad_resid.cu): CTA-per-environment LM, hinge trees
+bool resid_eligible_sizes(int U);
+size_t resid_smem_bytes();
+cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out,
+                              cudaStream_t s);
+
 cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
                         cudaStream_t s);
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s);

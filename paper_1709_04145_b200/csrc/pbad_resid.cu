@@ -1,0 +1,898 @@
+// pbad_resid.cu -- CTA-per-environment Newton (LM) kernel for the residual
+// (high-order collocation) form of PBAD: the C5 workload (SURVEY.md §8 K6+K7).
+//
+// One thread block owns one environment for a whole PBAD step (begin_step, the
+// Levenberg-Marquardt loop, finish_step; stepper.cpp:83-147, optim.cpp:80-139).
+// The unknowns are the u = K-1 stacked configurations of the collocation window
+// (U = u n); per accepted iterate the kernel builds the residual Jacobian J
+// (objective.cpp:258-334: u functional_hess blocks, u^2 correlation_hess_ab
+// blocks, the gravity potential Hessian) and the Gauss-Newton matrix 2 J^T J;
+// every iteration factors the damped U x U matrix.  Layout per environment
+// (env-major, HBM/L2): J, GN and the factor as column-major U x U matrices,
+// the u link passes, the u^2 hess_ab walk states.  Shared memory holds the
+// GEMM operand tiles, the panel of the blocked Cholesky and the solve vector.
+//
+//  * J^T J: 64 x 64 output tiles of the lower triangle, 4 x 4 per thread,
+//    operand k-chunks staged in shared memory with 2 J pre-applied.  Because
+//    2 J(k,a) J(k,b) is the same real number as 2 J(k,b) J(k,a) (doubling is
+//    exact), the reference's ab1/ab2 chains are equal bit for bit and
+//    0.5 (gn + gn^T) is gn itself: only one triangle is computed.
+//  * Cholesky (optim.cpp:11-15): blocked left-looking with 32-wide block
+//    columns -- a register-tiled update of the block column by all previous
+//    columns (each element's fma chain runs over k ascending, exactly the
+//    reference's right-looking order), the diagonal block factored by one warp
+//    in registers, the rows below solved one thread per row.
+//  * triangular solves blocked the same way (warp solves the diagonal block,
+//    all threads apply it to the remaining rows).
+// Every scalar follows the numeric contract (pbad_math.cuh); results are
+// bit-identical to the reference build and the C oracle.
+#include <cuda_runtime.h>
+
+#include "pbad_joint.cuh"
+#include "pbad_kernels.cuh"
+#include "pbad_launch.h"
+#include "pbad_math.cuh"
+
+namespace pbad_gpu {
+namespace resid {
+
+constexpr int NT = 256;  // threads per environment
+constexpr unsigned FULL = 0xffffffffu;
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
+enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
+
+// GEMM (J^T J) tiling
+constexpr int GB = 64;       // output tile
+constexpr int GK = 32;       // k chunk
+constexpr int GP = GB + 2;   // padded smem row
+// Cholesky tiling
+constexpr int CB = 32;       // block column width
+constexpr int LK = 16;       // k chunk of the block-column update
+constexpr int MAXU = 320;
+constexpr int LP = MAXU + 2; // padded smem row of the update panel
+
+__device__ __forceinline__ M4 ldm4(const double* p) {
+  M4 m;
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 v = q[k];
+    m.a[2 * k] = v.x;
+    m.a[2 * k + 1] = v.y;
+  }
+  return m;
+}
+__device__ __forceinline__ M4 ldgm4(const double* p) {
+  M4 m;
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 v = __ldg(q + k);
+    m.a[2 * k] = v.x;
+    m.a[2 * k + 1] = v.y;
+  }
+  return m;
+}
+__device__ __forceinline__ void stm4(double* p, const M4& m) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) q[k] = make_double2(m.a[2 * k], m.a[2 * k + 1]);
+}
+__device__ __forceinline__ double trace_mul(const M4& X, const M4& F) {
+  double d[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    double acc = X.a[p] * F.a[4 * p];
+    acc = fma(X.a[p + 4], F.a[1 + 4 * p], acc);
+    acc = fma(X.a[p + 8], F.a[2 + 4 * p], acc);
+    acc = fma(X.a[p + 12], F.a[3 + 4 * p], acc);
+    d[p] = acc;
+  }
+  return ((d[0] + d[1]) + d[2]) + d[3];
+}
+__device__ __forceinline__ M4 gravity_cot(const DForces& f, const M4& S) {
+  const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
+  const double e4[4] = {0.0, 0.0, 0.0, 1.0};
+  double u[4];
+  mul_vec4(S, e4, u);
+  M4 c;
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c.a[r + 4 * s] = (-ghat[r]) * u[s];
+  return c;
+}
+
+struct Smem {
+  double red[NT];
+  int flag;
+  double scal[8];
+};
+
+// per-environment context (identical in every thread)
+struct R {
+  const DModel* m;
+  const DForces* f;
+  const DSchedule* sc;
+  const ResidDesc* rd;
+  int tid, N, n, u, U, D, K1;
+  bool grav;
+  double inv_dt2;
+  double *J, *GN, *DM, *FH, *PH, *pass, *hw0, *hw1, *HA, *FA, *seeds, *cot, *x, *grad, *cand, *res, *pg, *tau,
+      *step;
+  double* sm;   // dynamic shared memory (tiles)
+  Smem* ss;     // static shared scratch
+  __device__ __forceinline__ double* val(int mm) const { return pass + mm * rd->pstride; }
+  __device__ __forceinline__ double* wld(int mm) const { return pass + mm * rd->pstride + 16L * N; }
+  __device__ __forceinline__ double* dd1(int mm) const { return pass + mm * rd->pstride + 32L * N; }
+  __device__ __forceinline__ double* dd2(int mm) const { return pass + mm * rd->pstride + 48L * N; }
+  __device__ __forceinline__ double* lev(int mm) const { return pass + mm * rd->pstride + 64L * N; }
+  // hess_ab state of pair (a, b): ai, fwd, bwd, Z
+  __device__ __forceinline__ double* ha(int pair, int k) const { return HA + (pair * 4L + k) * 16L * N; }
+  // functional_grad sweep sw (0..u-1 seeds of instant sw, u..2u-1 gravity at instant sw-u): a, X
+  __device__ __forceinline__ double* fa(int sw, int k) const { return FA + (sw * 2L + k) * 16L * N; }
+};
+
+// ---- block reductions (result in every thread) ----
+__device__ double block_max(const R& r, double v) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, s));
+  __syncthreads();
+  if ((r.tid & 31) == 0) r.ss->red[r.tid >> 5] = v;
+  __syncthreads();
+  double mx = 0.0;
+  for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, r.ss->red[w]);
+  __syncthreads();
+  return mx;
+}
+__device__ double infnorm(const R& r, const double* a, int len) {
+  double mx = 0.0;
+  for (int i = r.tid; i < len; i += NT) mx = fmax(mx, fabs(a[i]));
+  return block_max(r, mx);
+}
+__device__ bool all_finite(const R& r, const double* a, int len) {
+  bool ok = true;
+  for (int i = r.tid; i < len; i += NT) ok = ok && isfinite(a[i]);
+  return __syncthreads_and(ok) != 0;
+}
+
+// forward_pass (kinematics.cpp:171-181) of one configuration into world
+__device__ void fk_config(const R& r, const double* q, double* world) {
+  const DModel& m = *r.m;
+  const ResidDesc& rd = *r.rd;
+  for (int i = r.tid; i < r.N; i += NT)
+    stm4(world + 16 * i, joint_transform(m.kind[i], m.axis + 3 * i, ldgm4(m.offset + 16 * i), q + m.dof_off[i]));
+  __syncthreads();
+  for (int d = 1; d <= r.D; ++d) {
+    for (int t = rd.lvl_start[d] + r.tid; t < rd.lvl_start[d + 1]; t += NT) {
+      const int i = rd.lvl_links[t];
+      stm4(world + 16 * i, mul(ldm4(world + 16 * m.parent[i]), ldm4(world + 16 * i)));
+    }
+    __syncthreads();
+  }
+}
+
+// ConfigPass::make (adjoint.cpp:9-27) for the u stacked configurations of xs.
+// false = a non-finite entry (ModelError).
+__device__ bool passes(const R& r, const double* xs, bool want_d2) {
+  if (!all_finite(r, xs, r.U)) return false;
+  const DModel& m = *r.m;
+  const ResidDesc& rd = *r.rd;
+  const int N = r.N;
+  for (int t = r.tid; t < r.u * N; t += NT) {
+    const int mm = t / N, i = t - mm * N;
+    const double q = xs[mm * r.n + i];
+    M4 v, d1, d2;
+    joint_jet(0, m.axis + 3 * i, ldgm4(m.offset + 16 * i), &q, &v, &d1, &d2, want_d2);
+    stm4(r.val(mm) + 16 * i, v);
+    stm4(r.dd1(mm) + 16 * i, d1);
+    if (want_d2) stm4(r.dd2(mm) + 16 * i, d2);
+  }
+  __syncthreads();
+  for (int d = 0; d <= r.D; ++d) {
+    const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
+    for (int t = r.tid; t < r.u * cnt; t += NT) {
+      const int mm = t / cnt;
+      const int i = rd.lvl_links[l0 + t - mm * cnt];
+      const int p = m.parent[i];
+      const M4 v = ldm4(r.val(mm) + 16 * i);
+      stm4(r.wld(mm) + 16 * i, p >= 0 ? mul(ldm4(r.wld(mm) + 16 * p), v) : v);
+    }
+    __syncthreads();
+  }
+  for (int t = r.tid; t < r.u * N; t += NT) {
+    const int mm = t / N, i = t - mm * N;
+    const int p = m.parent[i];
+    const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
+    stm4(r.lev(mm) + 16 * i, mul(pw, ldm4(r.dd1(mm) + 16 * i)));
+  }
+  __syncthreads();
+  return true;
+}
+
+// residuals g_m (objective.cpp:281-308) of the configuration whose passes are
+// current; returns value = sum_m |g_m|^2 (objective.cpp:323-324).  Leaves the
+// adjoint sums a of every sweep in fa(sw, 0) for functional_hess.
+__device__ double residual(const R& r) {
+  const DModel& m = *r.m;
+  const DSchedule& sc = *r.sc;
+  const ResidDesc& rd = *r.rd;
+  const int N = r.N, n = r.n, u = r.u;
+  for (int t = r.tid; t < u * N; t += NT) {
+    const int mm = t / N, i = t - mm * N;
+    const double* st = sc.H2 + r.K1 * (2 + mm);
+    M4 acc = m4_zero();
+    for (int j = 0; j < r.K1; ++j) {
+      const double* W = (j == 0) ? r.hw0 : (j == 1) ? r.hw1 : r.wld(j - 2);
+      addto(acc, scale(st[j], ldm4(W + 16 * i)));
+    }
+    stm4(r.seeds + (long)mm * 16 * N + 16 * i, mul(scale(r.inv_dt2, acc), ldgm4(m.S + 16 * i)));
+  }
+  __syncthreads();
+  // functional_grad (adjoint.cpp:49-64) of the u inertial seeds and the u
+  // gravity cotangent sweeps, level-synchronous from the leaves
+  const int nsw = r.grav ? 2 * u : u;
+  for (int d = r.D; d >= 0; --d) {
+    const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
+    for (int t = r.tid; t < nsw * cnt; t += NT) {
+      const int sw = t / cnt;
+      const int i = rd.lvl_links[l0 + t - sw * cnt];
+      const int mm = sw < u ? sw : sw - u;
+      const double* src = sw < u ? r.seeds + (long)mm * 16 * N : r.cot;
+      double* X = r.fa(sw, 1);
+      M4 adj = m4_zero();
+      for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) adj = add(adj, ldm4(X + 16 * rd.ch_list[c]));
+      const M4 a = add(adj, ldm4(src + 16 * i));
+      stm4(r.fa(sw, 0) + 16 * i, a);
+      const double gi = 0.0 + ddot(ldm4(r.lev(mm) + 16 * i), a);
+      if (sw < u) r.res[mm * n + i] = gi;
+      else r.pg[mm * n + i] = gi;
+      stm4(X + 16 * i, mul_bt(a, ldm4(r.val(mm) + 16 * i)));
+    }
+    __syncthreads();
+  }
+  for (int t = r.tid; t < r.U; t += NT) r.res[t] = r.res[t] + ((r.grav ? r.pg[t] : 0.0) - r.tau[t]);
+  __syncthreads();
+  // value: sum over instants of vdot32(g_m, g_m), warp mm computes instant mm
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  if (warp < u) {
+    double p = 0.0;
+    for (int i = lane; i < n; i += 32) p = fma(r.res[warp * n + i], r.res[warp * n + i], p);
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) p = p + __shfl_xor_sync(FULL, p, s);
+    if (lane == 0) r.ss->scal[warp] = p;
+  }
+  __syncthreads();
+  double v = 0.0;
+  for (int mm = 0; mm < u; ++mm) v += r.ss->scal[mm];
+  __syncthreads();
+  return v;
+}
+
+// Jacobian of the residuals (objective.cpp:310-320) into r.J
+__device__ void jacobian(const R& r) {
+  const DModel& m = *r.m;
+  const DSchedule& sc = *r.sc;
+  const ResidDesc& rd = *r.rd;
+  const int N = r.N, n = r.n, u = r.u, U = r.U;
+  const long UU = (long)U * U;
+  if (!rd.chain) {
+    for (long t = r.tid; t < UU; t += NT) r.J[t] = 0.0;
+    for (long t = r.tid; t < (long)u * n * n; t += NT) {
+      r.FH[t] = 0.0;
+      r.PH[t] = 0.0;
+    }
+  }
+  // correlation_hess_ab(pass_a, pass_b) composite inertias for every pair
+  // (a = instant l, b = instant mm), pair = a * u + b (adjoint.cpp:139-141,169-174)
+  const int npair = u * u;
+  for (int d = r.D; d >= 0; --d) {
+    const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
+    for (int t = r.tid; t < npair * cnt; t += NT) {
+      const int pr = t / cnt;
+      const int i = rd.lvl_links[l0 + t - pr * cnt];
+      const int a = pr / u, b = pr - a * u;
+      M4 acc = m4_zero();
+      for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) acc = add(acc, ldm4(r.ha(pr, 3) + 16 * rd.ch_list[c]));
+      const M4 ai = add(acc, ldgm4(m.S + 16 * i));
+      const M4 vb = ldm4(r.val(b) + 16 * i), va = ldm4(r.val(a) + 16 * i);
+      stm4(r.ha(pr, 0) + 16 * i, ai);
+      const M4 y = mul(vb, ai);
+      stm4(r.ha(pr, 1) + 16 * i, y);
+      stm4(r.ha(pr, 2) + 16 * i, mul_bt(ai, va));
+      stm4(r.ha(pr, 3) + 16 * i, mul_bt(y, va));
+    }
+    __syncthreads();
+  }
+  // hess_ab entries: own block and the ancestor walk of every (pair, link),
+  // written straight into J (transposed, scaled by inv_dt2 * stencil)
+  for (int t = r.tid; t < npair * N; t += NT) {
+    const int pr = t / N;
+    const int i = rd.walk_order[t - pr * N];
+    const int a = pr / u, b = pr - a * u;  // hess_ab(pass_a, pass_b) feeds J block (row b, col a)
+    const double* stb = sc.H2 + r.K1 * (2 + b);
+    const double ca = r.inv_dt2 * stb[2 + a];
+    const double* la = r.lev(a);
+    const double* lb = r.lev(b);
+    const M4 ua_i = ldm4(la + 16 * i), ub_i = ldm4(lb + 16 * i);
+    const long rowb = (long)b * n, cola = (long)a * n;
+    {
+      const double h = 0.0 + trace_mul(mul_at(ua_i, ub_i), ldm4(r.ha(pr, 0) + 16 * i));
+      r.J[(rowb + i) + U * (cola + i)] = ca * h;
+    }
+    M4 fwd = ldm4(r.ha(pr, 1) + 16 * i);
+    M4 bwd = ldm4(r.ha(pr, 2) + 16 * i);
+    for (int l = m.parent[i]; l >= 0; l = m.parent[l]) {
+      const double t1 = 0.0 + trace_mul(mul_at(ua_i, ldm4(lb + 16 * l)), fwd);   // H(i, l)
+      const double t2 = 0.0 + trace_mul(mul_at(ldm4(la + 16 * l), ub_i), bwd);   // H(l, i)
+      r.J[(rowb + l) + U * (cola + i)] = ca * t1;
+      r.J[(rowb + i) + U * (cola + l)] = ca * t2;
+      fwd = mul(ldm4(r.val(b) + 16 * l), fwd);
+      bwd = mul_bt(bwd, ldm4(r.val(a) + 16 * l));
+    }
+  }
+  // functional_hess (adjoint.cpp:66-101) of the inertial seeds and of the
+  // gravity cotangents at every instant
+  const int nsw = r.grav ? 2 * u : u;
+  for (int t = r.tid; t < nsw * N; t += NT) {
+    const int sw = t / N;
+    const int i = rd.walk_order[t - sw * N];
+    const int mm = sw < u ? sw : sw - u;
+    double* F = (sw < u ? r.FH : r.PH) + (long)mm * n * n;
+    const M4 a = ldm4(r.fa(sw, 0) + 16 * i);
+    const int p = m.parent[i];
+    const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
+    F[i + (long)n * i] = 0.0 + ddot(mul(pw, ldm4(r.dd2(mm) + 16 * i)), a);
+    M4 walk = mul_bt(a, ldm4(r.dd1(mm) + 16 * i));
+    for (int l = p; l >= 0; l = m.parent[l]) {
+      const double h = 0.0 + ddot(ldm4(r.lev(mm) + 16 * l), walk);
+      F[l + (long)n * i] = h;
+      F[i + (long)n * l] = h;
+      walk = mul_bt(walk, ldm4(r.val(mm) + 16 * l));
+    }
+  }
+  __syncthreads();
+  // diagonal blocks: (functional_hess + c_m ab_mm^T) + pot.hess
+  for (long t = r.tid; t < (long)u * n * n; t += NT) {
+    const int mm = (int)(t / ((long)n * n));
+    const long e = t - (long)mm * n * n;
+    const int rr = (int)(e % n), cc = (int)(e / n);
+    double* Jp = r.J + ((long)mm * n + rr) + U * ((long)mm * n + cc);
+    const double ph = r.grav ? 0.0 + r.PH[t] : 0.0;
+    *Jp = (r.FH[t] + *Jp) + ph;
+  }
+  __syncthreads();
+}
+
+// grad = 2 J^T g (objective.cpp:326-327)
+__device__ void gradient(const R& r) {
+  const int U = r.U;
+  for (int a = r.tid; a < U; a += NT) {
+    const double* Jc = r.J + (long)U * a;
+    double acc = (2.0 * Jc[0]) * r.res[0];
+    for (int k = 1; k < U; ++k) acc = fma(2.0 * Jc[k], r.res[k], acc);
+    r.grad[a] = acc;
+  }
+}
+
+// GN = 0.5 (2 J^T J + (2 J^T J)^T) = 2 J^T J, lower triangle (objective.cpp:328-330)
+__device__ void gauss_newton(const R& r) {
+  const int U = r.U;
+  const int nb = (U + GB - 1) / GB;
+  double* As = r.sm;              // [GK][GP] 2 J(k, a-tile)
+  double* Bs = r.sm + GK * GP;    // [GK][GP] J(k, b-tile)
+  const int tx = r.tid & 15, ty = r.tid >> 4;
+  for (int bi = 0; bi < nb; ++bi)
+    for (int bj = 0; bj <= bi; ++bj) {
+      const int a0 = bi * GB, b0 = bj * GB;
+      double acc[4][4];
+      for (int k0 = 0; k0 < U; k0 += GK) {
+        const int kc = min(GK, U - k0);
+        __syncthreads();
+        for (int t = r.tid; t < GK * GB; t += NT) {
+          const int col = t / GK, kk = t - col * GK;
+          const int a = a0 + col, b = b0 + col;
+          const bool kin = kk < kc;
+          As[kk * GP + col] = (kin && a < U) ? 2.0 * r.J[(k0 + kk) + (long)U * a] : 0.0;
+          Bs[kk * GP + col] = (kin && b < U) ? r.J[(k0 + kk) + (long)U * b] : 0.0;
+        }
+        __syncthreads();
+        int kk = 0;
+        if (k0 == 0) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = As[ty + 16 * i] * Bs[tx + 16 * j];
+          kk = 1;
+        }
+        for (; kk < kc; ++kk) {
+          double av[4], bv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int a = a0 + ty + 16 * i, b = b0 + tx + 16 * j;
+          if (a < U && b <= a) r.GN[a + (long)U * b] = 0.5 * (acc[i][j] + acc[i][j]);
+        }
+    }
+  __syncthreads();
+}
+
+// LLT of r.DM (lower, column-major), blocked left-looking; same per-element
+// operation sequence as the right-looking reference (optim.cpp:11-15).
+// false = non-positive pivot.
+__device__ bool cholesky(const R& r) {
+  const int U = r.U;
+  double* A = r.DM;
+  double* Ls = r.sm;                 // [LK][LP] panel rows of the k-chunk
+  double* Lj = r.sm + LK * LP;       // [CB][CB+1] factored diagonal block
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  for (int j0 = 0; j0 < U; j0 += CB) {
+    const int bw = min(CB, U - j0);
+    const int rows = U - j0;
+    // 1) block-column update by columns [0, j0): acc over k ascending
+    if (j0 > 0) {
+      // thread (ty, tx): rows j0 + ty + 32 ii, cols j0 + tx + 8 jj
+      const int tx = r.tid & 7, ty = r.tid >> 3;
+      constexpr int MI = (MAXU + 31) / 32;
+      double acc[MI][4];
+      const int ni = (rows + 31) / 32;
+#pragma unroll
+      for (int ii = 0; ii < MI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int i = j0 + ty + 32 * ii, j = j0 + tx + 8 * jj;
+          acc[ii][jj] = (ii < ni && i < U && j < j0 + bw && j <= i) ? A[i + (long)U * j] : 0.0;
+        }
+      for (int k0 = 0; k0 < j0; k0 += LK) {
+        const int kc = min(LK, j0 - k0);
+        __syncthreads();
+        for (int t = r.tid; t < LK * rows; t += NT) {
+          const int kk = t / rows, rr = t - kk * rows;
+          Ls[kk * LP + rr] = kk < kc ? A[(j0 + rr) + (long)U * (k0 + kk)] : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+          double bv[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) bv[jj] = Ls[kk * LP + tx + 8 * jj];
+#pragma unroll
+          for (int ii = 0; ii < MI; ++ii) {
+            if (ii < ni) {
+              const double av = Ls[kk * LP + min(ty + 32 * ii, rows - 1)];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(-av, bv[jj], acc[ii][jj]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int ii = 0; ii < MI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int i = j0 + ty + 32 * ii, j = j0 + tx + 8 * jj;
+          if (ii < ni && i < U && j < j0 + bw && j <= i) A[i + (long)U * j] = acc[ii][jj];
+        }
+      __syncthreads();
+    }
+    // 2) diagonal block: one warp, lane l owns row j0 + l
+    if (warp == 0) {
+      double a[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) a[c] = (lane < bw && c <= lane) ? A[(j0 + lane) + (long)U * (j0 + c)] : 0.0;
+      int ok = 1;
+#pragma unroll
+      for (int k = 0; k < CB; ++k) {
+        if (k < bw && ok) {
+          const double akk = __shfl_sync(FULL, a[k], k);
+          if (akk <= 0.0) {
+            ok = 0;
+          } else {
+            const double d = sqrt(akk);
+            if (lane == k) a[k] = d;
+            else if (lane > k) a[k] = a[k] / d;
+#pragma unroll
+            for (int j = k + 1; j < CB; ++j) {
+              const double ljk = __shfl_sync(FULL, a[k], j);
+              if (j < bw && lane >= j) a[j] = fma(-a[k], ljk, a[j]);
+            }
+          }
+        }
+      }
+      if (lane == 0) r.ss->flag = ok;
+      if (ok) {
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+          if (lane < bw && c <= lane) {
+            A[(j0 + lane) + (long)U * (j0 + c)] = a[c];
+            Lj[lane * (CB + 1) + c] = a[c];
+          }
+      }
+    }
+    __syncthreads();
+    if (!r.ss->flag) {
+      __syncthreads();
+      return false;
+    }
+    // 3) rows below the diagonal block: one thread per row
+    for (int i = j0 + bw + r.tid; i < U; i += NT) {
+      double a[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) a[c] = c < bw ? A[i + (long)U * (j0 + c)] : 0.0;
+#pragma unroll
+      for (int k = 0; k < CB; ++k) {
+        if (k < bw) {
+          a[k] = a[k] / Lj[k * (CB + 1) + k];
+#pragma unroll
+          for (int j = k + 1; j < CB; ++j)
+            if (j < bw) a[j] = fma(-a[k], Lj[j * (CB + 1) + k], a[j]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CB; ++c)
+        if (c < bw) A[i + (long)U * (j0 + c)] = a[c];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// llt_solve (eigen_lite): x = L^-T L^-1 b in place on v (shared, length U)
+__device__ void llt_solve(const R& r, double* v) {
+  const int U = r.U;
+  const double* A = r.DM;
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  // forward: column-oriented, blocks ascending
+  for (int j0 = 0; j0 < U; j0 += CB) {
+    const int bw = min(CB, U - j0);
+    if (warp == 0) {
+      double x = lane < bw ? v[j0 + lane] : 0.0;
+      double lrow[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) lrow[c] = (lane < bw && c <= lane) ? A[(j0 + lane) + (long)U * (j0 + c)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (j < bw) {
+          const double xj = __shfl_sync(FULL, x, j) / __shfl_sync(FULL, lrow[j], j);
+          if (lane == j) x = xj;
+          else if (lane > j && lane < bw) x = fma(-lrow[j], xj, x);
+        }
+      }
+      if (lane < bw) v[j0 + lane] = x;
+    }
+    __syncthreads();
+    for (int i = j0 + bw + r.tid; i < U; i += NT) {
+      double x = v[i];
+      for (int j = j0; j < j0 + bw; ++j) x = fma(-A[i + (long)U * j], v[j], x);
+      v[i] = x;
+    }
+    __syncthreads();
+  }
+  // backward: for j descending, x_i -= L(j, i) x_j for i < j
+  const int nbk = (U + CB - 1) / CB;
+  for (int bk = nbk - 1; bk >= 0; --bk) {
+    const int j0 = bk * CB;
+    const int bw = min(CB, U - j0);
+    if (warp == 0) {
+      double x = lane < bw ? v[j0 + lane] : 0.0;
+      // lane l holds column j0 + l of the block: L(j0 + c, j0 + l) for c >= l
+      double lcol[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) lcol[c] = (lane < bw && c >= lane && c < bw) ? A[(j0 + c) + (long)U * (j0 + lane)] : 0.0;
+#pragma unroll
+      for (int jr = CB - 1; jr >= 0; --jr) {
+        if (jr < bw) {
+          const double xj = __shfl_sync(FULL, x, jr) / __shfl_sync(FULL, lcol[jr], jr);
+          if (lane == jr) x = xj;
+          else if (lane < jr) x = fma(-lcol[jr], xj, x);
+        }
+      }
+      if (lane < bw) v[j0 + lane] = x;
+    }
+    __syncthreads();
+    for (int i = r.tid; i < j0; i += NT) {
+      double x = v[i];
+      for (int j = j0 + bw - 1; j >= j0; --j) x = fma(-A[j + (long)U * i], v[j], x);
+      v[i] = x;
+    }
+    __syncthreads();
+  }
+}
+
+struct Solver {
+  int status, iters, stag, acc;
+  double value, lambda, grad0;
+};
+
+// full evaluation at r.x: value, residual Jacobian, gradient, GN
+__device__ int full_eval(const R& r, double* value) {
+  if (!passes(r, r.x, true)) return TR_NONFINITE_CFG;
+  const double v = residual(r);
+  *value = v;
+  if (!isfinite(v)) return TR_NONFINITE_INIT;
+  jacobian(r);
+  gradient(r);
+  gauss_newton(r);
+  return 0;
+}
+
+// LmSolver::iterate (optim.cpp:95-134).  Returns the status or -1 (ModelError).
+__device__ int lm_iterate(const R& r, Solver& S) {
+  const DOpt& o = r.sc->opt;
+  if (S.status != ST_RUNNING) return S.status;
+  if (S.iters >= o.max_iters) return S.status = ST_FAILED;
+  {
+    const double g = infnorm(r, r.grad, r.U);
+    const double xn = infnorm(r, r.x, r.U);
+    bool conv = g <= o.grad_tol * fmax(1.0, xn);
+    if (!conv && o.grad_rtol > 0.0 && g <= o.grad_rtol * S.grad0) conv = true;
+    if (conv) return S.status = ST_CONVERGED;
+  }
+  const int U = r.U;
+  for (long t = r.tid; t < (long)U * U; t += NT) {
+    const int a = (int)(t % U), b = (int)(t / U);
+    if (a >= b) r.DM[t] = (a == b) ? r.GN[t] + S.lambda : r.GN[t];
+  }
+  double* v = r.step;
+  for (int t = r.tid; t < U; t += NT) v[t] = -r.grad[t];
+  __syncthreads();
+  bool accepted = false;
+  const bool ok = cholesky(r);
+  bool finite = false;
+  if (ok) {
+    llt_solve(r, v);
+    finite = all_finite(r, v, U);
+  }
+  if (finite) {
+    for (int t = r.tid; t < U; t += NT) r.cand[t] = r.x[t] + v[t];
+    __syncthreads();
+    if (!passes(r, r.cand, false)) return -1;
+    const double tv = residual(r);
+    if (isfinite(tv) && tv < S.value) {
+      const double oldv = S.value;
+      for (int t = r.tid; t < U; t += NT) r.x[t] = r.cand[t];
+      __syncthreads();
+      double nv;
+      if (full_eval(r, &nv) == TR_NONFINITE_CFG) return -1;
+      S.value = nv;
+      S.lambda = fmax(S.lambda / o.lm_lambda_factor, 1e-12);
+      accepted = true;
+      ++S.acc;
+      if (oldv - nv <= o.ftol * fmax(1.0, fabs(oldv))) ++S.stag;
+      else S.stag = 0;
+      if (S.stag >= 2) S.status = ST_CONVERGED;
+    }
+  }
+  if (!accepted) {
+    S.lambda *= o.lm_lambda_factor;
+    if (S.lambda > o.lm_lambda_max) S.status = ST_FAILED;
+  }
+  ++S.iters;
+  if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
+  return S.status;
+}
+
+// ForceModel::tau_at (objective.hpp:28-58) for instant mm into dst
+__device__ void tau_at(const R& r, double t, double* dst) {
+  const DForces& f = *r.f;
+  const int n = r.n;
+  for (int i = r.tid; i < n; i += NT) {
+    double v = 0.0;
+    if (f.has_act && f.act_len == n) {
+      if (f.act_kind == 0) {
+        v = f.act_amp[i];
+      } else {
+        const double ph = i < f.act_phase_len ? f.act_phase[i] : 0.0;
+        double s, c;
+        pbad_sincos(2.0 * 3.141592653589793 * f.act_freq * t + ph, &s, &c);
+        v = f.act_amp[i] * s;
+      }
+    } else if (f.tau_len == n) {
+      v = f.tau[i];
+    }
+    dst[i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
+                                                      int* iws, long B, ResidDesc rd, double* rws, Outputs out) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ Smem ss;
+  const long e = blockIdx.x;
+  if (e >= B) return;
+  if (iws[(long)IS_RUN * B + e] != TR_RUNNING) return;
+  R r;
+  r.m = &m;
+  r.f = &f;
+  r.sc = &sc;
+  r.rd = &rd;
+  r.tid = threadIdx.x;
+  r.N = rd.N;
+  r.n = rd.n;
+  r.u = rd.u;
+  r.U = rd.U;
+  r.D = rd.D;
+  r.K1 = sc.K1;
+  r.grav = f.gravity_nonzero != 0;
+  const double dt = sc.dt;
+  r.inv_dt2 = 1.0 / (dt * dt);
+  r.sm = smem;
+  r.ss = &ss;
+  {
+    double* g = rws + e * rd.gstride;
+    r.J = g + rd.oJ;
+    r.GN = g + rd.oGN;
+    r.DM = g + rd.oDM;
+    r.FH = g + rd.oFH;
+    r.PH = g + rd.oPH;
+    r.pass = g + rd.oPass;
+    r.hw0 = g + rd.oHW0;
+    r.hw1 = g + rd.oHW1;
+    r.HA = g + rd.oHA;
+    r.FA = g + rd.oFA;
+    r.seeds = g + rd.oSeeds;
+    r.cot = g + rd.oCot;
+    r.x = g + rd.oX;
+    r.grad = g + rd.oGrad;
+    r.cand = g + rd.oCand;
+    r.res = g + rd.oRes;
+    r.pg = g + rd.oPg;
+    r.tau = g + rd.oTau;
+    r.step = g + rd.oStep;
+  }
+  const int n = r.n, u = r.u, U = r.U, N = r.N;
+  int* const ivp = iws + e;
+  auto iv = [&](int slot) -> int& { return ivp[(long)slot * B]; };
+  const int step = iv(IS_STEP);
+
+  // ---- begin_step (stepper.cpp:83-115) ----
+  double* h0 = r.cand;      // scratch until the solver starts
+  double* h1 = r.cand + n;
+  for (int k = r.tid; k < n; k += NT) {
+    h0[k] = ws[(L.hist0 + k) * B + e];
+    h1[k] = ws[(L.hist1 + k) * B + e];
+  }
+  const double t0 = step * dt;
+  for (int mm = 0; mm < u; ++mm) tau_at(r, t0 + sc.times[2 + mm] * dt, r.tau + (long)mm * n);
+  __syncthreads();
+  {
+    const double span = -sc.times[0];
+    for (int t = r.tid; t < U; t += NT) {
+      const int mm = t / n, k = t - mm * n;
+      const double tau_m = sc.times[2 + mm];
+      r.x[t] = sc.warm_start ? h1[k] + (tau_m / span) * (h1[k] - h0[k]) : h1[k];
+    }
+  }
+  __syncthreads();
+  // StepObjective ctor (objective.cpp:162-185): history passes
+  if (!all_finite(r, h0, n) || !all_finite(r, h1, n)) {
+    if (r.tid == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
+    return;
+  }
+  fk_config(r, h0, r.hw0);
+  fk_config(r, h1, r.hw1);
+  // gravity cotangents (objective.cpp:48-58), the same at every instant
+  if (r.grav)
+    for (int i = r.tid; i < N; i += NT) stm4(r.cot + 16 * i, add(m4_zero(), gravity_cot(f, ldgm4(m.S + 16 * i))));
+  __syncthreads();
+  // solver construction (optim.cpp:82-93)
+  Solver S;
+  S.status = ST_RUNNING;
+  S.iters = 0;
+  S.stag = 0;
+  S.acc = 0;
+  S.lambda = sc.opt.lm_lambda0;
+  {
+    double v;
+    const int rc = full_eval(r, &v);
+    if (rc) {
+      if (r.tid == 0) iv(IS_RUN) = rc;
+      return;
+    }
+    S.value = v;
+    S.grad0 = infnorm(r, r.grad, U);
+  }
+  int st;
+  while ((st = lm_iterate(r, S)) == ST_RUNNING) {
+  }
+  if (st < 0) {
+    if (r.tid == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
+    return;
+  }
+
+  // ---- finish_step (stepper.cpp:118-147) ----
+  const bool converged = S.status == ST_CONVERGED;
+  const long Stot = sc.total_steps;
+  const double gnorm = infnorm(r, r.grad, U);
+  const int fs = converged ? 0 : iv(IS_FAIL) + 1;
+  __syncthreads();
+  if (r.tid == 0) {
+    if (out.iterations) out.iterations[e * Stot + step] = S.iters;
+    if (out.converged) out.converged[e * Stot + step] = converged;
+    if (out.accepted) out.accepted[e * Stot + step] = S.acc;
+    if (out.final_value) out.final_value[e * Stot + step] = S.value;
+    if (out.final_grad_norm) out.final_grad_norm[e * Stot + step] = gnorm;
+    iv(IS_NREP) = step + 1;
+    iv(IS_ITERS) = S.iters;
+    iv(IS_STATUS) = S.status;
+    iv(IS_ACC) = S.acc;
+    iv(IS_FAIL) = fs;
+    if (fs > sc.fail_limit) iv(IS_RUN) = TR_FAIL_LIMIT;
+  }
+  if (fs > sc.fail_limit) return;
+  // history shift: hist0 <- (K == 2 ? hist1 : x_{u-2}), hist1 <- x_{u-1}
+  for (int k = r.tid; k < n; k += NT) {
+    const double nh0 = (sc.order == 2) ? ws[(L.hist1 + k) * B + e] : r.x[(long)(u - 2) * n + k];
+    ws[(L.hist0 + k) * B + e] = nh0;
+    ws[(L.hist1 + k) * B + e] = r.x[(long)(u - 1) * n + k];
+  }
+  // energy audit on world(new hist1) (stepper.cpp:132-138); hw0 is free now
+  const double* xq = r.x + (long)(u - 1) * n;
+  fk_config(r, xq, r.hw0);
+  for (int i = r.tid; i < N; i += NT) {
+    const M4 S_i = ldgm4(m.S + 16 * i);
+    const M4 wn = ldm4(r.hw0 + 16 * i);
+    const M4 tdm = divs(sub(wn, ldm4(r.hw1 + 16 * i)), dt);
+    r.FA[2 * i] = 0.5 * ddot(mul(tdm, S_i), tdm);
+    const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
+    const double e4[4] = {0.0, 0.0, 0.0, 1.0};
+    double uu[4], vv[4];
+    mul_vec4(S_i, e4, uu);
+    mul_vec4(wn, uu, vv);
+    r.FA[2 * i + 1] = dot4(ghat, vv);
+  }
+  __syncthreads();
+  const long S1 = Stot + 1;
+  if (r.tid == 0) {
+    double ke = 0.0, pe = 0.0;
+    for (int i = 0; i < N; ++i) {
+      ke += r.FA[2 * i];
+      pe -= r.FA[2 * i + 1];
+    }
+    if (out.energy) {
+      out.energy[(e * S1 + step + 1) * 2] = ke;
+      out.energy[(e * S1 + step + 1) * 2 + 1] = pe;
+    }
+    iv(IS_NSAMP) = step + 2;
+    iv(IS_STEP) = step + 1;
+    if (step + 1 >= sc.total_steps) iv(IS_RUN) = TR_OK;
+  }
+  if (out.q)
+    for (int k = r.tid; k < n; k += NT) out.q[(e * S1 + step + 1) * n + k] = xq[k];
+}
+
+}  // namespace resid
+
+bool resid_eligible_sizes(int U) { return U >= 1 && U <= resid::MAXU; }
+
+size_t resid_smem_bytes() {
+  const size_t gemm = 2 * resid::GK * resid::GP;
+  const size_t llt = resid::LK * resid::LP + resid::CB * (resid::CB + 1);
+  return sizeof(double) * (gemm > llt ? gemm : llt);
+}
+
+cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out,
+                              cudaStream_t s) {
+  const size_t smem = resid_smem_bytes();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(resid::k_resid_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  resid::k_resid_step<<<(unsigned)a.B, resid::NT, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, rd, rws, out);
+  return cudaGetLastError();
+}
+
+}  // namespace pbad_gpu

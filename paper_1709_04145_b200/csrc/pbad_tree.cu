@@ -36,6 +36,7 @@ namespace tree {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAXV = 3;  // dof vectors in registers: n <= 96
 constexpr int MAXN = 96;
+constexpr int MS = 18;  // shared-memory stride of a 4x4 (16 + 2 pad: conflict-free lane-per-link double2 access)
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
 enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
 
@@ -122,7 +123,7 @@ struct W {
   double *x, *grad, *cand, *vtau, *vtmp;
   // global, this environment's block
   double *gn, *hw0, *hw1, *T0, *T1;
-  __device__ __forceinline__ double* scr_k(int k) const { return scr + (long)k * 16 * N; }
+  __device__ __forceinline__ double* scr_k(int k) const { return scr + (long)k * MS * N; }
 };
 
 // VecX dot (32 interleaved partials + pairwise tree, pbad_math.cuh vdot32):
@@ -156,7 +157,7 @@ __device__ bool fk_world(const W& w, const double* q) {
     double ql[6];
     const int off = m.dof_off[i], cnt = m.dof_cnt[i];
     for (int j = 0; j < cnt; ++j) ql[j] = q[off + j];
-    st16(w.value + 16 * i, joint_transform(m.kind[i], m.axis + 3 * i, ldg16(m.offset + 16 * i), ql));
+    st16(w.value + MS * i, joint_transform(m.kind[i], m.axis + 3 * i, ldg16(m.offset + 16 * i), ql));
   }
   __syncwarp();
   const TreeDesc& td = *w.td;
@@ -164,8 +165,8 @@ __device__ bool fk_world(const W& w, const double* q) {
     for (int t = td.lvl_start[d] + w.lane; t < td.lvl_start[d + 1]; t += 32) {
       const int i = td.lvl_links[t];
       const int p = m.parent[i];
-      const M4 v = ld16(w.value + 16 * i);
-      st16(w.world + 16 * i, p >= 0 ? mul(ld16(w.world + 16 * p), v) : v);
+      const M4 v = ld16(w.value + MS * i);
+      st16(w.world + MS * i, p >= 0 ? mul(ld16(w.world + MS * p), v) : v);
     }
     __syncwarp();
   }
@@ -180,15 +181,36 @@ __device__ void fk_levers(const W& w, const double* q) {
     double ql[6];
     const int off = m.dof_off[i], cnt = m.dof_cnt[i];
     for (int j = 0; j < cnt; ++j) ql[j] = q[off + j];
-    M4 v, d1[6];
-    joint_jet(m.kind[i], m.axis + 3 * i, ldg16(m.offset + 16 * i), ql, &v, d1, nullptr, false);
-    for (int j = 0; j < cnt; ++j) st16(d1s + 16 * (off + j), d1[j]);
+    // joint_jet's d1 (kinematics.cpp:119-169), written straight to shared memory
+    const M4 offm = ldg16(m.offset + 16 * i);
+    const int kind = m.kind[i];
+    double* dst = d1s + MS * off;
+    if (kind == 0) {
+      const double* ax = m.axis + 3 * i;
+      const M3 Ka = skew(ax[0], ax[1], ax[2]);
+      const M3 R = rotation_vector_matrix(ax[0] * ql[0], ax[1] * ql[0], ax[2] * ql[0]);
+      st16(dst, mul(offm, embed_rotation(mul3(Ka, R))));
+    } else {
+      const int r0 = kind == 1 ? 0 : 3;
+      M3 R, dR[3];
+      rotation_vector_jet(ql + r0, &R, dR, nullptr, false);
+      if (kind == 2) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          M4 dtj = m4_zero();
+          dtj.a[j + 12] = 1.0;
+          st16(dst + MS * j, mul(offm, dtj));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) st16(dst + MS * (r0 + j), mul(offm, embed_rotation(dR[j])));
+    }
   }
   __syncwarp();
   for (int k = w.lane; k < w.n; k += 32) {
     const int p = m.parent[w.td->dof_link[k]];
-    const M4 pw = p >= 0 ? ld16(w.world + 16 * p) : m4_identity();
-    st16(w.lever + 16 * k, mul(pw, ld16(d1s + 16 * k)));
+    const M4 pw = p >= 0 ? ld16(w.world + MS * p) : m4_identity();
+    st16(w.lever + MS * k, mul(pw, ld16(d1s + MS * k)));
   }
   __syncwarp();
 }
@@ -198,7 +220,7 @@ __device__ void fk_levers(const W& w, const double* q) {
 __device__ double value_at(const W& w, const double* q) {
   const DModel& m = *w.m;
   for (int i = w.lane; i < w.N; i += 32) {
-    const M4 wi = ld16(w.world + 16 * i);
+    const M4 wi = ld16(w.world + MS * i);
     const M4 S = ldg16(m.S + 16 * i);
     w.red[4 * i] = ddot(mul(wi, S), wi);
     w.red[4 * i + 1] = ddot(ld16(w.T1 + 16 * i), wi);
@@ -227,11 +249,11 @@ __device__ void gradient(const W& w, double* g) {
   double* sB = w.scr_k(1);  // gravity cotangents -> children contributions
   for (int i = w.lane; i < w.N; i += 32) {
     const M4 S = ldg16(m.S + 16 * i);
-    M4 d = sub(ld16(w.world + 16 * i), scale(2.0, ld16(w.hw1 + 16 * i)));
+    M4 d = sub(ld16(w.world + MS * i), scale(2.0, ld16(w.hw1 + 16 * i)));
     d = add(d, ld16(w.hw0 + 16 * i));
     d = scale(w.inv_dt2, d);
-    st16(sA + 16 * i, mul(d, S));
-    if (w.grav) st16(sB + 16 * i, add(m4_zero(), gravity_cot(*w.f, S)));
+    st16(sA + MS * i, mul(d, S));
+    if (w.grav) st16(sB + MS * i, add(m4_zero(), gravity_cot(*w.f, S)));
   }
   __syncwarp();
   const int nsw = w.grav ? 2 : 1;
@@ -243,11 +265,11 @@ __device__ void gradient(const W& w, double* g) {
       double* seeds = sw ? sB : sA;
       double* gout = sw ? w.vtmp : g;
       M4 adj = m4_zero();
-      for (int c = td.ch_start[i]; c < td.ch_start[i + 1]; ++c) adj = add(adj, ld16(seeds + 16 * td.ch_list[c]));
-      const M4 a = add(adj, ld16(seeds + 16 * i));
+      for (int c = td.ch_start[i]; c < td.ch_start[i + 1]; ++c) adj = add(adj, ld16(seeds + MS * td.ch_list[c]));
+      const M4 a = add(adj, ld16(seeds + MS * i));
       const int off = m.dof_off[i];
-      for (int j = 0; j < m.dof_cnt[i]; ++j) gout[off + j] = 0.0 + ddot(ld16(w.lever + 16 * (off + j)), a);
-      st16(seeds + 16 * i, mul_bt(a, ld16(w.value + 16 * i)));
+      for (int j = 0; j < m.dof_cnt[i]; ++j) gout[off + j] = 0.0 + ddot(ld16(w.lever + MS * (off + j)), a);
+      st16(seeds + MS * i, mul_bt(a, ld16(w.value + MS * i)));
     }
     __syncwarp();
   }
@@ -268,14 +290,14 @@ __device__ void gn_assemble(const W& w) {
     for (int t = td.lvl_start[d] + w.lane; t < td.lvl_start[d + 1]; t += 32) {
       const int i = td.lvl_links[t];
       M4 acc = m4_zero();
-      for (int c = td.ch_start[i]; c < td.ch_start[i + 1]; ++c) acc = add(acc, ld16(Z + 16 * td.ch_list[c]));
+      for (int c = td.ch_start[i]; c < td.ch_start[i + 1]; ++c) acc = add(acc, ld16(Z + MS * td.ch_list[c]));
       const M4 a = add(acc, ldg16(m.S + 16 * i));
-      const M4 v = ld16(w.value + 16 * i);
-      st16(ai + 16 * i, a);
+      const M4 v = ld16(w.value + MS * i);
+      st16(ai + MS * i, a);
       const M4 y = mul(v, a);
-      st16(fwd + 16 * i, y);
-      st16(bwd + 16 * i, mul_bt(a, v));
-      st16(Z + 16 * i, mul_bt(y, v));
+      st16(fwd + MS * i, y);
+      st16(bwd + MS * i, mul_bt(a, v));
+      st16(Z + MS * i, mul_bt(y, v));
     }
     __syncwarp();
   }
@@ -287,11 +309,11 @@ __device__ void gn_assemble(const W& w) {
       const int code = td.tasks[t];
       const int i = code & 255, l = (code >> 8) & 255, j = (code >> 16) & 15, k = (code >> 20) & 15;
       const int offi = m.dof_off[i], offl = m.dof_off[l];
-      const M4 M = mul_at(ld16(w.lever + 16 * (offi + j)), ld16(w.lever + 16 * (offl + k)));
+      const M4 M = mul_at(ld16(w.lever + MS * (offi + j)), ld16(w.lever + MS * (offl + k)));
       double grc, gcr;
       int row, col;
       if (s == 0) {
-        const M4 F = ld16(ai + 16 * i);
+        const M4 F = ld16(ai + MS * i);
         const double tjk = trace_mul(M, F);
         const double tkj = (j == k) ? tjk : trace_tmul(M, F);
         grc = w.inv_dt2 * tjk + 0.0;
@@ -299,8 +321,8 @@ __device__ void gn_assemble(const W& w) {
         row = offi + k;
         col = offi + j;
       } else {
-        const double t1 = trace_mul(M, ld16(fwd + 16 * i));
-        const double t2 = trace_tmul(M, ld16(bwd + 16 * i));
+        const double t1 = trace_mul(M, ld16(fwd + MS * i));
+        const double t2 = trace_tmul(M, ld16(bwd + MS * i));
         grc = w.inv_dt2 * t2 + 0.0;
         gcr = w.inv_dt2 * t1 + 0.0;
         row = offi + j;
@@ -312,9 +334,9 @@ __device__ void gn_assemble(const W& w) {
     if (s >= 1 && s < w.D) {
       for (int i = w.lane; i < w.N; i += 32) {
         if (td.depth[i] <= s) continue;
-        const M4 vl = ld16(w.value + 16 * td.anc[i * (w.D + 1) + s]);
-        st16(fwd + 16 * i, mul(vl, ld16(fwd + 16 * i)));
-        st16(bwd + 16 * i, mul_bt(ld16(bwd + 16 * i), vl));
+        const M4 vl = ld16(w.value + MS * td.anc[i * (w.D + 1) + s]);
+        st16(fwd + MS * i, mul(vl, ld16(fwd + MS * i)));
+        st16(bwd + MS * i, mul_bt(ld16(bwd + MS * i), vl));
       }
       __syncwarp();
     }
@@ -336,10 +358,22 @@ __device__ bool llt_factor_w(const W& w) {
     if (w.lane == 0) A[cb + k] = d;
     __syncwarp();
     if (k + 1 < n) {
-      for (int t = pidx(n, k + 1, k + 1) + w.lane; t < w.np; t += 32) {
-        const int rc = __ldg(w.td->pk + t);
-        const int i = rc & 0xffff, j = rc >> 16;
-        A[t] = fma(-A[cb + i], A[cb + j], A[t]);
+      // trailing update over the packed triangle, 4 elements per lane in flight
+      // (column k is not written here, so the loads may run ahead of the stores)
+      for (int t = pidx(n, k + 1, k + 1) + w.lane; t < w.np; t += 128) {
+        int rc[4];
+        double a[4], li[4], lj[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rc[u] = (t + 32 * u < w.np) ? __ldg(w.td->pk + t + 32 * u) : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a[u] = (t + 32 * u < w.np) ? A[t + 32 * u] : 0.0;
+          li[u] = A[cb + (rc[u] & 0xffff)];
+          lj[u] = A[cb + (rc[u] >> 16)];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (t + 32 * u < w.np) A[t + 32 * u] = fma(-li[u], lj[u], a[u]);
       }
     }
     __syncwarp();
@@ -489,7 +523,7 @@ __device__ void tau_at(const W& w, double t, double* dst) {
 // copy w.world into a history block and its body products T = hw S
 __device__ void store_history(const W& w, double* hw, double* T) {
   for (int i = w.lane; i < w.N; i += 32) {
-    const M4 wi = ld16(w.world + 16 * i);
+    const M4 wi = ld16(w.world + MS * i);
     st16(hw + 16 * i, wi);
     st16(T + 16 * i, mul(wi, ldg16(w.m->S + 16 * i)));
   }
@@ -516,12 +550,12 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
   const double dt = sc.dt;
   w.inv_dt2 = 1.0 / (dt * dt);
   {
-    const int N16 = 16 * td.N, nv = (td.n + 1) & ~1;
-    const int scr = (4 * N16 > 16 * td.n) ? 4 * N16 : 16 * td.n;
+    const int N16 = MS * td.N, nv = (td.n + 1) & ~1;
+    const int scr = (4 * N16 > MS * td.n) ? 4 * N16 : MS * td.n;
     double* p = smem;
     w.value = p; p += N16;
     w.world = p; p += N16;
-    w.lever = p; p += 16 * td.n;
+    w.lever = p; p += MS * td.n;
     w.scr = p; p += scr;
     w.damped = p; p += (td.np + 1) & ~1;
     w.x = p; p += nv;
@@ -645,7 +679,7 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
   fk_world(w, w.x);
   for (int i = w.lane; i < w.N; i += 32) {
     const M4 S_i = ldg16(m.S + 16 * i);
-    const M4 wn = ld16(w.world + 16 * i);
+    const M4 wn = ld16(w.world + MS * i);
     const M4 td_ = divs(sub(wn, ld16(w.hw1 + 16 * i)), dt);
     w.red[4 * i] = 0.5 * ddot(mul(td_, S_i), td_);
     const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
@@ -682,9 +716,9 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
 bool tree_eligible_sizes(int N, int n) { return N >= 1 && N <= 255 && n >= 1 && n <= tree::MAXN; }
 
 static int tree_smem_doubles(const TreeDesc& td) {
-  const int N16 = 16 * td.N, nv = (td.n + 1) & ~1;
-  const int scr = (4 * N16 > 16 * td.n) ? 4 * N16 : 16 * td.n;
-  return 2 * N16 + 16 * td.n + scr + ((td.np + 1) & ~1) + 5 * nv + 4 * td.N + 32;
+  const int N16 = tree::MS * td.N, nv = (td.n + 1) & ~1;
+  const int scr = (4 * N16 > tree::MS * td.n) ? 4 * N16 : tree::MS * td.n;
+  return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 5 * nv + 4 * td.N + 32;
 }
 
 size_t tree_smem_bytes(const TreeDesc& td) { return sizeof(double) * (size_t)tree_smem_doubles(td); }

@@ -12,10 +12,13 @@ steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 table = {"C1": (make_single_hinge_chain_scene(10), 0.01, OptimizerKind.lbfgs),
          "C2": (make_single_hinge_chain_scene(50), 0.033, OptimizerKind.lbfgs),
          "C3": (make_chain_scene(100), 0.1, OptimizerKind.lbfgs),
-         "C4": (make_humanoid_scene(), 0.01, OptimizerKind.lm)}
+         "C4": (make_humanoid_scene(), 0.01, OptimizerKind.lm),
+         "C5": (make_single_hinge_chain_scene(100), 0.01, OptimizerKind.lm)}
 sc, dt, kind = table[cfg]
 m = api.build_model(sc.links); n = m.total_dofs
 sim = SimConfig(dt=dt, duration=dt * steps, consecutive_fail_limit=1000)
+if cfg == "C5":
+    sim.order, sim.objective = 4, ObjectiveKind.residual_form
 sim.optimizer.kind = kind
 if len(sys.argv) > 4:
     sim.optimizer.max_iters = int(sys.argv[4])

@@ -1,0 +1,98 @@
+"""GPU parity of the residual-form (high-order collocation) Newton kernel,
+pbad_resid.cu, against the CPU oracle: bit-exact trajectories, iteration
+counts, convergence flags, final objective values and energy logs."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1709_04145_b200 import api
+from paper_1709_04145_b200.scenes import Scene, make_single_hinge_chain_scene, mt19937_uniform
+from paper_1709_04145_b200.types import (ActuationKind, ActuationSpec, JointKind, JointSpec, LinkSpec,
+                                         ObjectiveKind, SimConfig)
+
+from _parity_util import assert_traj_equal, random_tree
+
+pytestmark = pytest.mark.gpu
+
+PATH_RESID = 4
+
+
+def _sims(sim, n, B, q0_fn):
+    out = []
+    for b in range(B):
+        s = SimConfig(**{**sim.__dict__})
+        s.q0 = q0_fn(b)
+        s.qdot0 = np.zeros(n)
+        out.append(s)
+    return out
+
+
+def _check(scene, sim, sims, path=PATH_RESID):
+    m = api.build_model(scene.links)
+    ctx = api.GpuContext(m, scene.forces(), sim, max_batch=1)
+    assert ctx.path == path, ctx.path
+    gpu = api.batch_simulate(m, scene.forces(), sims)
+    ref = oracle.batch_simulate(oracle.Model(scene.links), scene.forces(), sims, workers=4)
+    for g, r in zip(gpu, ref):
+        assert_traj_equal(g, r)
+    return gpu, ref
+
+
+@pytest.mark.parametrize("order", [3, 4, 5])
+def test_resid_chain(order):
+    sc = make_single_hinge_chain_scene(6)
+    sim = SimConfig(dt=0.01, duration=0.05, order=order, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, 6, 3, lambda b: mt19937_uniform(b + 3, 6, -0.3, 0.3)))
+
+
+def test_resid_order2():
+    sc = make_single_hinge_chain_scene(5)
+    sim = SimConfig(dt=0.02, duration=0.06, order=2, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, 5, 2, lambda b: mt19937_uniform(b + 8, 5, -0.3, 0.3)))
+
+
+@pytest.mark.parametrize("seed", [41, 42])
+def test_resid_hinge_tree(seed):
+    """Branched hinge tree, tilted axes, rotated offsets, point masses: the
+    non-chain J (zero blocks between unrelated links)."""
+    rng = np.random.default_rng(seed)
+    base = random_tree(rng, 7)
+    links = []
+    for l in base:
+        ax = rng.uniform(-1, 1, 3)
+        links.append(LinkSpec(l.parent, JointSpec(JointKind.hinge, tuple(ax / np.linalg.norm(ax)), l.joint.offset),
+                              l.geometry))
+    sc = Scene(links=links, gravity=(0.3, -1.0, -9.81))
+    sim = SimConfig(dt=0.02, duration=0.06, order=3, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, 7, 2, lambda b: rng.uniform(-0.4, 0.4, 7)))
+
+
+def test_resid_actuated():
+    sc = make_single_hinge_chain_scene(5)
+    sc.actuation = ActuationSpec(ActuationKind.sinusoidal, np.linspace(-2, 2, 5), 3.0, np.linspace(0, 1, 5))
+    sim = SimConfig(dt=0.02, duration=0.06, order=4, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, 5, 2, lambda b: mt19937_uniform(b, 5, -0.3, 0.3)))
+
+
+def test_resid_c5_shape_bounded_iterations():
+    """The C5 shape (100-link chain, K = 4, U = 300: ragged GEMM and Cholesky
+    blocks) with a small iteration cap so the oracle finishes quickly."""
+    sc = make_single_hinge_chain_scene(100)
+    sim = SimConfig(dt=0.01, duration=0.02, order=4, objective=ObjectiveKind.residual_form,
+                    consecutive_fail_limit=10)
+    sim.optimizer.max_iters = 12
+    _check(sc, sim, _sims(sim, 100, 2, lambda b: mt19937_uniform(3, 200, -0.3, 0.3)[100 * b:100 * (b + 1)]))
+
+
+def test_resid_equals_general_kernel(monkeypatch):
+    sc = make_single_hinge_chain_scene(6)
+    sim = SimConfig(dt=0.01, duration=0.04, order=4, objective=ObjectiveKind.residual_form)
+    m = api.build_model(sc.links)
+    sims = _sims(sim, 6, 5, lambda b: mt19937_uniform(b + 20, 6, -0.3, 0.3))
+    a = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.setenv("PBAD_GPU_FORCE_GENERAL", "1")
+    assert api.GpuContext(m, sc.forces(), sim, max_batch=1).path == 0
+    b = api.batch_simulate(m, sc.forces(), sims)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(np.array([s[1] for s in x.samples]), np.array([s[1] for s in y.samples]))
+        assert [r.iterations for r in x.solve_reports] == [r.iterations for r in y.solve_reports]
