@@ -629,7 +629,7 @@ bool resid_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
   if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
   for (int i = 0; i < m.N; ++i)
     if (m.kind[i] != PBAD_HINGE) return false;
-  return resid_eligible_sizes(m.n * (sim->order - 1));
+  return resid_eligible_sizes(m.N, sim->order - 1);
 }
 
 // Host-side structure of the tree kernel: depth levels, children in

@@ -47,8 +47,8 @@ cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tw
                              cudaStream_t s);
 
 // residual-form path (pbad_resid.cu): CTA-per-environment LM, hinge trees
-bool resid_eligible_sizes(int U);
-size_t resid_smem_bytes();
+bool resid_eligible_sizes(int N, int u);
+size_t resid_smem_bytes(int N, int u);
 cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out,
                               cudaStream_t s);
 

@@ -28,6 +28,9 @@
 // bit-identical to the reference build and the C oracle.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+
 #include "pbad_joint.cuh"
 #include "pbad_kernels.cuh"
 #include "pbad_launch.h"
@@ -36,6 +39,9 @@
 namespace pbad_gpu {
 namespace resid {
 
+#ifndef PBAD_RESID_CHOL_REG
+#define PBAD_RESID_CHOL_REG 1  // 1: diagonal blocks and solve rows in registers (unrolled); 0: shared memory loops
+#endif
 constexpr int NT = 256;  // threads per environment
 constexpr unsigned FULL = 0xffffffffu;
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
@@ -44,11 +50,12 @@ enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3
 // GEMM (J^T J) tiling
 constexpr int GB = 64;       // output tile
 constexpr int GK = 32;       // k chunk
-constexpr int GP = GB + 2;   // padded smem row
+constexpr int GP = GB + 1;   // padded smem row (odd: conflict-free staging stores)
 // Cholesky tiling
 constexpr int CB = 32;       // block column width
 constexpr int LK = 16;       // k chunk of the block-column update
 constexpr int MAXU = 320;
+constexpr int SMS = 18;      // shared-memory stride of a 4x4 (16 + 2 pad: conflict-free per-link double2 access)
 constexpr int LP = MAXU + 2; // padded smem row of the update panel
 
 __device__ __forceinline__ M4 ldm4(const double* p) {
@@ -103,10 +110,15 @@ __device__ __forceinline__ M4 gravity_cot(const DForces& f, const M4& S) {
   return c;
 }
 
+#ifndef PBAD_PHASE_TIMING
+#define PBAD_PHASE_TIMING 0  // 1: per-phase clock64 totals printed by block 0 (diagnostic builds only)
+#endif
 struct Smem {
+  long long pt[12];
   double red[NT];
   int flag;
   double scal[8];
+  int parent[MAXU];
 };
 
 // per-environment context (identical in every thread)
@@ -157,7 +169,7 @@ __device__ bool all_finite(const R& r, const double* a, int len) {
 }
 
 // forward_pass (kinematics.cpp:171-181) of one configuration into world
-__device__ void fk_config(const R& r, const double* q, double* world) {
+__device__ __noinline__ void fk_config(const R& r, const double* q, double* world) {
   const DModel& m = *r.m;
   const ResidDesc& rd = *r.rd;
   for (int i = r.tid; i < r.N; i += NT)
@@ -174,16 +186,20 @@ __device__ void fk_config(const R& r, const double* q, double* world) {
 
 // ConfigPass::make (adjoint.cpp:9-27) for the u stacked configurations of xs.
 // false = a non-finite entry (ModelError).
-__device__ bool passes(const R& r, const double* xs, bool want_d2) {
+__device__ __noinline__ bool passes(const R& r, const double* xs, bool want_d2) {
   if (!all_finite(r, xs, r.U)) return false;
   const DModel& m = *r.m;
   const ResidDesc& rd = *r.rd;
   const int N = r.N;
+  const long NS = (long)SMS * N;
+  double* Vs = r.sm;                 // values [u][N][16]
+  double* Ws = r.sm + r.u * NS;     // worlds [u][N][16]
   for (int t = r.tid; t < r.u * N; t += NT) {
     const int mm = t / N, i = t - mm * N;
     const double q = xs[mm * r.n + i];
     M4 v, d1, d2;
     joint_jet(0, m.axis + 3 * i, ldgm4(m.offset + 16 * i), &q, &v, &d1, &d2, want_d2);
+    stm4(Vs + mm * NS + SMS * i, v);
     stm4(r.val(mm) + 16 * i, v);
     stm4(r.dd1(mm) + 16 * i, d1);
     if (want_d2) stm4(r.dd2(mm) + 16 * i, d2);
@@ -194,26 +210,40 @@ __device__ bool passes(const R& r, const double* xs, bool want_d2) {
     for (int t = r.tid; t < r.u * cnt; t += NT) {
       const int mm = t / cnt;
       const int i = rd.lvl_links[l0 + t - mm * cnt];
-      const int p = m.parent[i];
-      const M4 v = ldm4(r.val(mm) + 16 * i);
-      stm4(r.wld(mm) + 16 * i, p >= 0 ? mul(ldm4(r.wld(mm) + 16 * p), v) : v);
+      const int p = r.ss->parent[i];
+      const M4 v = ldm4(Vs + mm * NS + SMS * i);
+      stm4(Ws + mm * NS + SMS * i, p >= 0 ? mul(ldm4(Ws + mm * NS + SMS * p), v) : v);
     }
     __syncthreads();
   }
   for (int t = r.tid; t < r.u * N; t += NT) {
     const int mm = t / N, i = t - mm * N;
-    const int p = m.parent[i];
-    const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
+    const int p = r.ss->parent[i];
+    stm4(r.wld(mm) + 16 * i, ldm4(Ws + mm * NS + SMS * i));
+    const M4 pw = p >= 0 ? ldm4(Ws + mm * NS + SMS * p) : m4_identity();
     stm4(r.lev(mm) + 16 * i, mul(pw, ldm4(r.dd1(mm) + 16 * i)));
   }
   __syncthreads();
   return true;
 }
 
+// stage the u passes' values and levers into shared memory
+__device__ void stage_vl(const R& r, double* Vs, double* Ls) {
+  const int N8 = 8 * r.N;  // double2 per pass
+  for (int t = r.tid; t < r.u * N8; t += NT) {
+    const int mm = t / N8;
+    const int e = t - mm * N8;
+    const int link = e >> 3, k = 2 * (e & 7);
+    const long dst = (long)mm * SMS * r.N + SMS * link + k;
+    *reinterpret_cast<double2*>(Vs + dst) = *reinterpret_cast<const double2*>(r.val(mm) + 2 * e);
+    *reinterpret_cast<double2*>(Ls + dst) = *reinterpret_cast<const double2*>(r.lev(mm) + 2 * e);
+  }
+}
+
 // residuals g_m (objective.cpp:281-308) of the configuration whose passes are
 // current; returns value = sum_m |g_m|^2 (objective.cpp:323-324).  Leaves the
 // adjoint sums a of every sweep in fa(sw, 0) for functional_hess.
-__device__ double residual(const R& r) {
+__device__ __noinline__ double residual(const R& r) {
   const DModel& m = *r.m;
   const DSchedule& sc = *r.sc;
   const ResidDesc& rd = *r.rd;
@@ -232,6 +262,12 @@ __device__ double residual(const R& r) {
   // functional_grad (adjoint.cpp:49-64) of the u inertial seeds and the u
   // gravity cotangent sweeps, level-synchronous from the leaves
   const int nsw = r.grav ? 2 * u : u;
+  const long NS = (long)SMS * N;
+  double* Xs = r.sm;                  // children contributions [2u][N][16]
+  double* Ls = r.sm + 2 * u * NS;    // levers [u][N][16]
+  double* Vs = Ls + u * NS;          // values [u][N][16]
+  stage_vl(r, Vs, Ls);
+  __syncthreads();
   for (int d = r.D; d >= 0; --d) {
     const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
     for (int t = r.tid; t < nsw * cnt; t += NT) {
@@ -239,15 +275,15 @@ __device__ double residual(const R& r) {
       const int i = rd.lvl_links[l0 + t - sw * cnt];
       const int mm = sw < u ? sw : sw - u;
       const double* src = sw < u ? r.seeds + (long)mm * 16 * N : r.cot;
-      double* X = r.fa(sw, 1);
+      double* X = Xs + sw * NS;
       M4 adj = m4_zero();
-      for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) adj = add(adj, ldm4(X + 16 * rd.ch_list[c]));
+      for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) adj = add(adj, ldm4(X + SMS * rd.ch_list[c]));
       const M4 a = add(adj, ldm4(src + 16 * i));
       stm4(r.fa(sw, 0) + 16 * i, a);
-      const double gi = 0.0 + ddot(ldm4(r.lev(mm) + 16 * i), a);
+      const double gi = 0.0 + ddot(ldm4(Ls + mm * NS + SMS * i), a);
       if (sw < u) r.res[mm * n + i] = gi;
       else r.pg[mm * n + i] = gi;
-      stm4(X + 16 * i, mul_bt(a, ldm4(r.val(mm) + 16 * i)));
+      stm4(X + SMS * i, mul_bt(a, ldm4(Vs + mm * NS + SMS * i)));
     }
     __syncthreads();
   }
@@ -270,7 +306,7 @@ __device__ double residual(const R& r) {
 }
 
 // Jacobian of the residuals (objective.cpp:310-320) into r.J
-__device__ void jacobian(const R& r) {
+__device__ __noinline__ void jacobian(const R& r) {
   const DModel& m = *r.m;
   const DSchedule& sc = *r.sc;
   const ResidDesc& rd = *r.rd;
@@ -283,6 +319,14 @@ __device__ void jacobian(const R& r) {
       r.PH[t] = 0.0;
     }
   }
+  // pass values / levers of every instant and the composite-inertia
+  // contributions Z live in shared memory for the walks below
+  const long NS = (long)SMS * N;
+  double* Vs = r.sm;
+  double* Ls = Vs + u * NS;
+  double* Zs = Ls + u * NS;  // [u*u][N][16]
+  stage_vl(r, Vs, Ls);
+  __syncthreads();
   // correlation_hess_ab(pass_a, pass_b) composite inertias for every pair
   // (a = instant l, b = instant mm), pair = a * u + b (adjoint.cpp:139-141,169-174)
   const int npair = u * u;
@@ -292,15 +336,16 @@ __device__ void jacobian(const R& r) {
       const int pr = t / cnt;
       const int i = rd.lvl_links[l0 + t - pr * cnt];
       const int a = pr / u, b = pr - a * u;
+      double* Z = Zs + pr * NS;
       M4 acc = m4_zero();
-      for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) acc = add(acc, ldm4(r.ha(pr, 3) + 16 * rd.ch_list[c]));
+      for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) acc = add(acc, ldm4(Z + SMS * rd.ch_list[c]));
       const M4 ai = add(acc, ldgm4(m.S + 16 * i));
-      const M4 vb = ldm4(r.val(b) + 16 * i), va = ldm4(r.val(a) + 16 * i);
+      const M4 vb = ldm4(Vs + b * NS + SMS * i), va = ldm4(Vs + a * NS + SMS * i);
       stm4(r.ha(pr, 0) + 16 * i, ai);
       const M4 y = mul(vb, ai);
       stm4(r.ha(pr, 1) + 16 * i, y);
       stm4(r.ha(pr, 2) + 16 * i, mul_bt(ai, va));
-      stm4(r.ha(pr, 3) + 16 * i, mul_bt(y, va));
+      stm4(Z + SMS * i, mul_bt(y, va));
     }
     __syncthreads();
   }
@@ -312,9 +357,11 @@ __device__ void jacobian(const R& r) {
     const int a = pr / u, b = pr - a * u;  // hess_ab(pass_a, pass_b) feeds J block (row b, col a)
     const double* stb = sc.H2 + r.K1 * (2 + b);
     const double ca = r.inv_dt2 * stb[2 + a];
-    const double* la = r.lev(a);
-    const double* lb = r.lev(b);
-    const M4 ua_i = ldm4(la + 16 * i), ub_i = ldm4(lb + 16 * i);
+    const double* la = Ls + a * NS;
+    const double* lb = Ls + b * NS;
+    const double* va = Vs + a * NS;
+    const double* vb = Vs + b * NS;
+    const M4 ua_i = ldm4(la + SMS * i), ub_i = ldm4(lb + SMS * i);
     const long rowb = (long)b * n, cola = (long)a * n;
     {
       const double h = 0.0 + trace_mul(mul_at(ua_i, ub_i), ldm4(r.ha(pr, 0) + 16 * i));
@@ -322,13 +369,13 @@ __device__ void jacobian(const R& r) {
     }
     M4 fwd = ldm4(r.ha(pr, 1) + 16 * i);
     M4 bwd = ldm4(r.ha(pr, 2) + 16 * i);
-    for (int l = m.parent[i]; l >= 0; l = m.parent[l]) {
-      const double t1 = 0.0 + trace_mul(mul_at(ua_i, ldm4(lb + 16 * l)), fwd);   // H(i, l)
-      const double t2 = 0.0 + trace_mul(mul_at(ldm4(la + 16 * l), ub_i), bwd);   // H(l, i)
+    for (int l = r.ss->parent[i]; l >= 0; l = r.ss->parent[l]) {
+      const double t1 = 0.0 + trace_mul(mul_at(ua_i, ldm4(lb + SMS * l)), fwd);   // H(i, l)
+      const double t2 = 0.0 + trace_mul(mul_at(ldm4(la + SMS * l), ub_i), bwd);   // H(l, i)
       r.J[(rowb + l) + U * (cola + i)] = ca * t1;
       r.J[(rowb + i) + U * (cola + l)] = ca * t2;
-      fwd = mul(ldm4(r.val(b) + 16 * l), fwd);
-      bwd = mul_bt(bwd, ldm4(r.val(a) + 16 * l));
+      fwd = mul(ldm4(vb + SMS * l), fwd);
+      bwd = mul_bt(bwd, ldm4(va + SMS * l));
     }
   }
   // functional_hess (adjoint.cpp:66-101) of the inertial seeds and of the
@@ -339,82 +386,136 @@ __device__ void jacobian(const R& r) {
     const int i = rd.walk_order[t - sw * N];
     const int mm = sw < u ? sw : sw - u;
     double* F = (sw < u ? r.FH : r.PH) + (long)mm * n * n;
+    const double* lm = Ls + mm * NS;
+    const double* vm = Vs + mm * NS;
     const M4 a = ldm4(r.fa(sw, 0) + 16 * i);
-    const int p = m.parent[i];
+    const int p = r.ss->parent[i];
     const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
     F[i + (long)n * i] = 0.0 + ddot(mul(pw, ldm4(r.dd2(mm) + 16 * i)), a);
     M4 walk = mul_bt(a, ldm4(r.dd1(mm) + 16 * i));
-    for (int l = p; l >= 0; l = m.parent[l]) {
-      const double h = 0.0 + ddot(ldm4(r.lev(mm) + 16 * l), walk);
+    for (int l = p; l >= 0; l = r.ss->parent[l]) {
+      const double h = 0.0 + ddot(ldm4(lm + SMS * l), walk);
       F[l + (long)n * i] = h;
       F[i + (long)n * l] = h;
-      walk = mul_bt(walk, ldm4(r.val(mm) + 16 * l));
+      walk = mul_bt(walk, ldm4(vm + SMS * l));
     }
   }
   __syncthreads();
   // diagonal blocks: (functional_hess + c_m ab_mm^T) + pot.hess
-  for (long t = r.tid; t < (long)u * n * n; t += NT) {
-    const int mm = (int)(t / ((long)n * n));
-    const long e = t - (long)mm * n * n;
-    const int rr = (int)(e % n), cc = (int)(e / n);
-    double* Jp = r.J + ((long)mm * n + rr) + U * ((long)mm * n + cc);
-    const double ph = r.grav ? 0.0 + r.PH[t] : 0.0;
-    *Jp = (r.FH[t] + *Jp) + ph;
+  {
+    const int warp = r.tid >> 5, lane = r.tid & 31;
+    for (int col = warp; col < u * n; col += NT / 32) {
+      const int mm = col / n, cc = col - mm * n;
+      const long f0 = (long)mm * n * n + (long)n * cc;
+      double* Jc = r.J + (long)mm * n + (long)U * ((long)mm * n + cc);
+      for (int rr = lane; rr < n; rr += 32) {
+        const double ph = r.grav ? 0.0 + r.PH[f0 + rr] : 0.0;
+        Jc[rr] = (r.FH[f0 + rr] + Jc[rr]) + ph;
+      }
+    }
   }
   __syncthreads();
 }
 
 // grad = 2 J^T g (objective.cpp:326-327)
-__device__ void gradient(const R& r) {
+__device__ __noinline__ void gradient(const R& r) {
   const int U = r.U;
+  double* rs = r.sm;
+  for (int k = r.tid; k < U; k += NT) rs[k] = r.res[k];
+  __syncthreads();
   for (int a = r.tid; a < U; a += NT) {
     const double* Jc = r.J + (long)U * a;
-    double acc = (2.0 * Jc[0]) * r.res[0];
-    for (int k = 1; k < U; ++k) acc = fma(2.0 * Jc[k], r.res[k], acc);
+    double acc = (2.0 * Jc[0]) * rs[0];
+    int k = 1;
+    for (; k + 8 <= U; k += 8) {
+      double jv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) jv[q] = Jc[k + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = fma(2.0 * jv[q], rs[k + q], acc);
+    }
+    for (; k < U; ++k) acc = fma(2.0 * Jc[k], rs[k], acc);
     r.grad[a] = acc;
   }
 }
 
-// GN = 0.5 (2 J^T J + (2 J^T J)^T) = 2 J^T J, lower triangle (objective.cpp:328-330)
-__device__ void gauss_newton(const R& r) {
+// GN = 0.5 (2 J^T J + (2 J^T J)^T) = 2 J^T J, lower triangle (objective.cpp:328-330).
+// Double-buffered k-chunks: the next chunk's global loads are in flight while
+// the current one is multiplied out of shared memory.
+__device__ __forceinline__ void gn_load(const R& r, int a0, int b0, int k0, double (&pa)[GK * GB / NT],
+                                        double (&pb)[GK * GB / NT]) {
+  const int U = r.U;
+#pragma unroll
+  for (int q = 0; q < GK * GB / NT; ++q) {
+    const int t = r.tid + NT * q;
+    const int col = t / GK, kk = t - col * GK;
+    const int k = k0 + kk, a = a0 + col, b = b0 + col;
+    pa[q] = (k < U && a < U) ? 2.0 * r.J[k + (long)U * a] : 0.0;
+    pb[q] = (k < U && b < U) ? r.J[k + (long)U * b] : 0.0;
+  }
+}
+__device__ __forceinline__ void gn_store(const R& r, double* As, double* Bs, const double (&pa)[GK * GB / NT],
+                                         const double (&pb)[GK * GB / NT]) {
+#pragma unroll
+  for (int q = 0; q < GK * GB / NT; ++q) {
+    const int t = r.tid + NT * q;
+    const int col = t / GK, kk = t - col * GK;
+    As[kk * GP + col] = pa[q];
+    Bs[kk * GP + col] = pb[q];
+  }
+}
+
+__device__ __noinline__ void gauss_newton(const R& r) {
   const int U = r.U;
   const int nb = (U + GB - 1) / GB;
-  double* As = r.sm;              // [GK][GP] 2 J(k, a-tile)
-  double* Bs = r.sm + GK * GP;    // [GK][GP] J(k, b-tile)
+  const int nk = (U + GK - 1) / GK;
   const int tx = r.tid & 15, ty = r.tid >> 4;
   for (int bi = 0; bi < nb; ++bi)
     for (int bj = 0; bj <= bi; ++bj) {
       const int a0 = bi * GB, b0 = bj * GB;
       double acc[4][4];
-      for (int k0 = 0; k0 < U; k0 += GK) {
-        const int kc = min(GK, U - k0);
+      double pa[GK * GB / NT], pb[GK * GB / NT];
+      gn_load(r, a0, b0, 0, pa, pb);
+      for (int c = 0; c < nk; ++c) {
+        double* As = r.sm + (c & 1) * 2 * GK * GP;
+        double* Bs = As + GK * GP;
+        gn_store(r, As, Bs, pa, pb);
         __syncthreads();
-        for (int t = r.tid; t < GK * GB; t += NT) {
-          const int col = t / GK, kk = t - col * GK;
-          const int a = a0 + col, b = b0 + col;
-          const bool kin = kk < kc;
-          As[kk * GP + col] = (kin && a < U) ? 2.0 * r.J[(k0 + kk) + (long)U * a] : 0.0;
-          Bs[kk * GP + col] = (kin && b < U) ? r.J[(k0 + kk) + (long)U * b] : 0.0;
-        }
-        __syncthreads();
+        if (c + 1 < nk) gn_load(r, a0, b0, (c + 1) * GK, pa, pb);
+        const int kc = min(GK, U - c * GK);
         int kk = 0;
-        if (k0 == 0) {
+        if (c == 0) {
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[i][j] = As[ty + 16 * i] * Bs[tx + 16 * j];
           kk = 1;
         }
-        for (; kk < kc; ++kk) {
-          double av[4], bv[4];
+        if (kc == GK) {
+#pragma unroll 8
+          for (; kk < GK; ++kk) {
+            double av[4], bv[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
+            for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+              for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+          }
+        } else {
+          for (; kk < kc; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+          }
         }
       }
 #pragma unroll
@@ -424,19 +525,42 @@ __device__ void gauss_newton(const R& r) {
           const int a = a0 + ty + 16 * i, b = b0 + tx + 16 * j;
           if (a < U && b <= a) r.GN[a + (long)U * b] = 0.5 * (acc[i][j] + acc[i][j]);
         }
+      __syncthreads();
     }
-  __syncthreads();
 }
+
+#if PBAD_PHASE_TIMING
+#define PT_START() long long pt_t0 = clock64()
+#define PT_MARK(k)                                   \
+  do {                                               \
+    const long long pt_t1 = clock64();               \
+    if (r.tid == 0) r.ss->pt[k] += pt_t1 - pt_t0;    \
+    pt_t0 = pt_t1;                                   \
+  } while (0)
+#else
+#define PT_START() \
+  do {             \
+  } while (0)
+#define PT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 
 // LLT of r.DM (lower, column-major), blocked left-looking; same per-element
 // operation sequence as the right-looking reference (optim.cpp:11-15).
+// The damped matrix gn + lambda I (optim.cpp:105-107) is read from r.GN at
+// each element's first use (left-looking touches every original entry once).
 // false = non-positive pivot.
-__device__ bool cholesky(const R& r) {
+constexpr int CS = CB + 1;  // smem row stride of the diagonal block / panel rows
+#if PBAD_RESID_CHOL_REG
+__device__ __noinline__ bool cholesky(const R& r, double lambda) {
   const int U = r.U;
   double* A = r.DM;
+  const double* G = r.GN;
   double* Ls = r.sm;                 // [LK][LP] panel rows of the k-chunk
   double* Lj = r.sm + LK * LP;       // [CB][CB+1] factored diagonal block
   const int warp = r.tid >> 5, lane = r.tid & 31;
+  PT_START();
   for (int j0 = 0; j0 < U; j0 += CB) {
     const int bw = min(CB, U - j0);
     const int rows = U - j0;
@@ -452,7 +576,9 @@ __device__ bool cholesky(const R& r) {
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const int i = j0 + ty + 32 * ii, j = j0 + tx + 8 * jj;
-          acc[ii][jj] = (ii < ni && i < U && j < j0 + bw && j <= i) ? A[i + (long)U * j] : 0.0;
+          acc[ii][jj] = (ii < ni && i < U && j < j0 + bw && j <= i)
+                            ? (i == j ? G[i + (long)U * j] + lambda : G[i + (long)U * j])
+                            : 0.0;
         }
       for (int k0 = 0; k0 < j0; k0 += LK) {
         const int kc = min(LK, j0 - k0);
@@ -486,11 +612,15 @@ __device__ bool cholesky(const R& r) {
         }
       __syncthreads();
     }
+    PT_MARK(9);
     // 2) diagonal block: one warp, lane l owns row j0 + l
     if (warp == 0) {
       double a[CB];
 #pragma unroll
-      for (int c = 0; c < CB; ++c) a[c] = (lane < bw && c <= lane) ? A[(j0 + lane) + (long)U * (j0 + c)] : 0.0;
+      for (int c = 0; c < CB; ++c) {
+        const long at = (j0 + lane) + (long)U * (j0 + c);
+        a[c] = (lane < bw && c <= lane) ? (j0 > 0 ? A[at] : (c == lane ? G[at] + lambda : G[at])) : 0.0;
+      }
       int ok = 1;
 #pragma unroll
       for (int k = 0; k < CB; ++k) {
@@ -516,7 +646,7 @@ __device__ bool cholesky(const R& r) {
         for (int c = 0; c < CB; ++c)
           if (lane < bw && c <= lane) {
             A[(j0 + lane) + (long)U * (j0 + c)] = a[c];
-            Lj[lane * (CB + 1) + c] = a[c];
+            Lj[lane * CS + c] = a[c];
           }
       }
     }
@@ -525,18 +655,19 @@ __device__ bool cholesky(const R& r) {
       __syncthreads();
       return false;
     }
+    PT_MARK(10);
     // 3) rows below the diagonal block: one thread per row
     for (int i = j0 + bw + r.tid; i < U; i += NT) {
       double a[CB];
 #pragma unroll
-      for (int c = 0; c < CB; ++c) a[c] = c < bw ? A[i + (long)U * (j0 + c)] : 0.0;
+      for (int c = 0; c < CB; ++c) a[c] = c < bw ? (j0 > 0 ? A : G)[i + (long)U * (j0 + c)] : 0.0;
 #pragma unroll
       for (int k = 0; k < CB; ++k) {
         if (k < bw) {
-          a[k] = a[k] / Lj[k * (CB + 1) + k];
+          a[k] = a[k] / Lj[k * CS + k];
 #pragma unroll
           for (int j = k + 1; j < CB; ++j)
-            if (j < bw) a[j] = fma(-a[k], Lj[j * (CB + 1) + k], a[j]);
+            if (j < bw) a[j] = fma(-a[k], Lj[j * CS + k], a[j]);
         }
       }
 #pragma unroll
@@ -544,12 +675,13 @@ __device__ bool cholesky(const R& r) {
         if (c < bw) A[i + (long)U * (j0 + c)] = a[c];
     }
     __syncthreads();
+    PT_MARK(11);
   }
   return true;
 }
 
 // llt_solve (eigen_lite): x = L^-T L^-1 b in place on v (shared, length U)
-__device__ void llt_solve(const R& r, double* v) {
+__device__ __noinline__ void llt_solve(const R& r, double* v) {
   const int U = r.U;
   const double* A = r.DM;
   const int warp = r.tid >> 5, lane = r.tid & 31;
@@ -610,20 +742,217 @@ __device__ void llt_solve(const R& r, double* v) {
   }
 }
 
+#else
+__device__ __noinline__ bool cholesky(const R& r, double lambda) {
+  const int U = r.U;
+  double* A = r.DM;
+  const double* G = r.GN;
+  double* Ls = r.sm;                 // [LK][LP] panel rows of the k-chunk
+  double* Lj = r.sm + LK * LP;       // [CB][CS] diagonal block
+  double* Rs = Lj + CB * CS;         // [MAXU][CS] rows below the diagonal block
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  for (int j0 = 0; j0 < U; j0 += CB) {
+    const int bw = min(CB, U - j0);
+    const int rows = U - j0;
+    // 1) block-column update by columns [0, j0): acc over k ascending
+    if (j0 > 0) {
+      // thread (ty, tx): rows j0 + ty + 32 ii, cols j0 + tx + 8 jj
+      const int tx = r.tid & 7, ty = r.tid >> 3;
+      constexpr int MI = (MAXU + 31) / 32;
+      double acc[MI][4];
+      const int ni = (rows + 31) / 32;
+#pragma unroll
+      for (int ii = 0; ii < MI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int i = j0 + ty + 32 * ii, j = j0 + tx + 8 * jj;
+          acc[ii][jj] = (ii < ni && i < U && j < j0 + bw && j <= i)
+                            ? (i == j ? G[i + (long)U * j] + lambda : G[i + (long)U * j])
+                            : 0.0;
+        }
+      for (int k0 = 0; k0 < j0; k0 += LK) {
+        const int kc = min(LK, j0 - k0);
+        __syncthreads();
+        for (int t = r.tid; t < LK * rows; t += NT) {
+          const int kk = t / rows, rr = t - kk * rows;
+          Ls[kk * LP + rr] = kk < kc ? A[(j0 + rr) + (long)U * (k0 + kk)] : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+          double bv[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) bv[jj] = Ls[kk * LP + tx + 8 * jj];
+#pragma unroll
+          for (int ii = 0; ii < MI; ++ii) {
+            if (ii < ni) {
+              const double av = Ls[kk * LP + min(ty + 32 * ii, rows - 1)];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(-av, bv[jj], acc[ii][jj]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int ii = 0; ii < MI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int i = j0 + ty + 32 * ii, j = j0 + tx + 8 * jj;
+          if (ii < ni && i < U && j < j0 + bw && j <= i) A[i + (long)U * j] = acc[ii][jj];
+        }
+      __syncthreads();
+    }
+    // 2) diagonal block: one warp in shared memory, lane l owns row j0 + l
+    if (warp == 0) {
+      for (int c = 0; c < bw; ++c)
+        if (lane < bw && c <= lane) {
+          const long at = (j0 + lane) + (long)U * (j0 + c);
+          Lj[lane * CS + c] = j0 > 0 ? A[at] : (c == lane ? G[at] + lambda : G[at]);
+        }
+      __syncwarp();
+      int ok = 1;
+      for (int k = 0; k < bw; ++k) {
+        const double akk = Lj[k * CS + k];
+        if (akk <= 0.0) {
+          ok = 0;
+          break;
+        }
+        const double d = sqrt(akk);
+        __syncwarp();
+        if (lane == k) Lj[k * CS + k] = d;
+        else if (lane > k && lane < bw) Lj[lane * CS + k] = Lj[lane * CS + k] / d;
+        __syncwarp();
+        if (lane > k && lane < bw) {
+          const double lik = Lj[lane * CS + k];
+          for (int j = k + 1; j <= lane; ++j) Lj[lane * CS + j] = fma(-lik, Lj[j * CS + k], Lj[lane * CS + j]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) r.ss->flag = ok;
+      if (ok)
+        for (int c = 0; c < bw; ++c)
+          if (lane < bw && c <= lane) A[(j0 + lane) + (long)U * (j0 + c)] = Lj[lane * CS + c];
+    }
+    // stage the rows below the diagonal block meanwhile (other warps)
+    const int nr = U - j0 - bw;
+    for (int t = warp == 0 ? nr * bw : r.tid - 32; t < nr * bw; t += NT - 32) {
+      const int c = t / nr, rr = t - c * nr;
+      const long at = (j0 + bw + rr) + (long)U * (j0 + c);
+      Rs[rr * CS + c] = j0 > 0 ? A[at] : G[at];
+    }
+    __syncthreads();
+    if (!r.ss->flag) {
+      __syncthreads();
+      return false;
+    }
+    // 3) rows below the diagonal block: one thread per row (shared memory)
+    for (int rr = r.tid; rr < nr; rr += NT) {
+      double* row = Rs + rr * CS;
+      for (int k = 0; k < bw; ++k) {
+        const double lik = row[k] / Lj[k * CS + k];
+        row[k] = lik;
+        for (int j = k + 1; j < bw; ++j) row[j] = fma(-lik, Lj[j * CS + k], row[j]);
+      }
+    }
+    __syncthreads();
+    for (int t = r.tid; t < nr * bw; t += NT) {
+      const int c = t / nr, rr = t - c * nr;
+      A[(j0 + bw + rr) + (long)U * (j0 + c)] = Rs[rr * CS + c];
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// llt_solve (eigen_lite): x = L^-T L^-1 b in place on v (global, length U),
+// blocked: one warp solves each diagonal block, all threads apply it to the
+// remaining rows (each element's fma chain keeps the reference order).
+__device__ __noinline__ void llt_solve(const R& r, double* v) {
+  const int U = r.U;
+  const double* A = r.DM;
+  double* Lj = r.sm;            // [CB][CS]
+  double* vs = Lj + CB * CS;    // [U]
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  for (int t = r.tid; t < U; t += NT) vs[t] = v[t];
+  __syncthreads();
+  // forward: x_i -= L(i, j) x_j for i > j, j ascending
+  for (int j0 = 0; j0 < U; j0 += CB) {
+    const int bw = min(CB, U - j0);
+    if (warp == 0) {
+      for (int c = 0; c < bw; ++c)
+        if (lane < bw && c <= lane) Lj[lane * CS + c] = A[(j0 + lane) + (long)U * (j0 + c)];
+      __syncwarp();
+      for (int j = 0; j < bw; ++j) {
+        const double xj = vs[j0 + j] / Lj[j * CS + j];
+        __syncwarp();
+        if (lane == j) vs[j0 + j] = xj;
+        else if (lane > j && lane < bw) vs[j0 + lane] = fma(-Lj[lane * CS + j], xj, vs[j0 + lane]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = j0 + bw + r.tid; i < U; i += NT) {
+      double x = vs[i];
+#pragma unroll 8
+      for (int j = j0; j < j0 + bw; ++j) x = fma(-A[i + (long)U * j], vs[j], x);
+      vs[i] = x;
+    }
+    __syncthreads();
+  }
+  // backward: x_i -= L(j, i) x_j for i < j, j descending
+  const int nbk = (U + CB - 1) / CB;
+  for (int bk = nbk - 1; bk >= 0; --bk) {
+    const int j0 = bk * CB;
+    const int bw = min(CB, U - j0);
+    if (warp == 0) {
+      for (int c = 0; c < bw; ++c)
+        if (lane < bw && c <= lane) Lj[lane * CS + c] = A[(j0 + lane) + (long)U * (j0 + c)];
+      __syncwarp();
+      for (int j = bw - 1; j >= 0; --j) {
+        const double xj = vs[j0 + j] / Lj[j * CS + j];
+        __syncwarp();
+        if (lane == j) vs[j0 + j] = xj;
+        else if (lane < j) vs[j0 + lane] = fma(-Lj[j * CS + lane], xj, vs[j0 + lane]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = r.tid; i < j0; i += NT) {
+      double x = vs[i];
+      const double* Ai = A + (long)U * i;
+#pragma unroll 8
+      for (int j = j0 + bw - 1; j >= j0; --j) x = fma(-Ai[j], vs[j], x);
+      vs[i] = x;
+    }
+    __syncthreads();
+  }
+  for (int t = r.tid; t < U; t += NT) v[t] = vs[t];
+  __syncthreads();
+}
+
+#endif
+
 struct Solver {
   int status, iters, stag, acc;
   double value, lambda, grad0;
 };
 
+
 // full evaluation at r.x: value, residual Jacobian, gradient, GN
-__device__ int full_eval(const R& r, double* value) {
+__device__ __noinline__ int full_eval(const R& r, double* value) {
+  PT_START();
   if (!passes(r, r.x, true)) return TR_NONFINITE_CFG;
   const double v = residual(r);
   *value = v;
+  PT_MARK(5);
   if (!isfinite(v)) return TR_NONFINITE_INIT;
   jacobian(r);
+  PT_MARK(6);
   gradient(r);
+  __syncthreads();
+  PT_MARK(7);
   gauss_newton(r);
+  PT_MARK(8);
   return 0;
 }
 
@@ -632,6 +961,7 @@ __device__ int lm_iterate(const R& r, Solver& S) {
   const DOpt& o = r.sc->opt;
   if (S.status != ST_RUNNING) return S.status;
   if (S.iters >= o.max_iters) return S.status = ST_FAILED;
+  PT_START();
   {
     const double g = infnorm(r, r.grad, r.U);
     const double xn = infnorm(r, r.x, r.U);
@@ -640,25 +970,26 @@ __device__ int lm_iterate(const R& r, Solver& S) {
     if (conv) return S.status = ST_CONVERGED;
   }
   const int U = r.U;
-  for (long t = r.tid; t < (long)U * U; t += NT) {
-    const int a = (int)(t % U), b = (int)(t / U);
-    if (a >= b) r.DM[t] = (a == b) ? r.GN[t] + S.lambda : r.GN[t];
-  }
   double* v = r.step;
   for (int t = r.tid; t < U; t += NT) v[t] = -r.grad[t];
   __syncthreads();
   bool accepted = false;
-  const bool ok = cholesky(r);
+  PT_MARK(0);
+  const bool ok = cholesky(r, S.lambda);
+  PT_MARK(1);
   bool finite = false;
   if (ok) {
     llt_solve(r, v);
     finite = all_finite(r, v, U);
   }
+  PT_MARK(2);
   if (finite) {
     for (int t = r.tid; t < U; t += NT) r.cand[t] = r.x[t] + v[t];
     __syncthreads();
     if (!passes(r, r.cand, false)) return -1;
+    PT_MARK(3);
     const double tv = residual(r);
+    PT_MARK(4);
     if (isfinite(tv) && tv < S.value) {
       const double oldv = S.value;
       for (int t = r.tid; t < U; t += NT) r.x[t] = r.cand[t];
@@ -684,7 +1015,7 @@ __device__ int lm_iterate(const R& r, Solver& S) {
 }
 
 // ForceModel::tau_at (objective.hpp:28-58) for instant mm into dst
-__device__ void tau_at(const R& r, double t, double* dst) {
+__device__ __noinline__ void tau_at(const R& r, double t, double* dst) {
   const DForces& f = *r.f;
   const int n = r.n;
   for (int i = r.tid; i < n; i += NT) {
@@ -752,6 +1083,9 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
     r.step = g + rd.oStep;
   }
   const int n = r.n, u = r.u, U = r.U, N = r.N;
+  for (int i = r.tid; i < N; i += NT) ss.parent[i] = m.parent[i];
+  if (r.tid < 12) ss.pt[r.tid] = 0;
+  __syncthreads();
   int* const ivp = iws + e;
   auto iv = [&](int slot) -> int& { return ivp[(long)slot * B]; };
   const int step = iv(IS_STEP);
@@ -870,26 +1204,39 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
   }
   if (out.q)
     for (int k = r.tid; k < n; k += NT) out.q[(e * S1 + step + 1) * n + k] = xq[k];
+#if PBAD_PHASE_TIMING
+  if (e == 0 && r.tid == 0)
+    printf("phase cycles (block 0, %d iterations, %d accepted): conv %lld chol %lld solve %lld tpass %lld tres %lld "
+           "fpassres %lld jac %lld grad %lld gn %lld | chol: update %lld diag %lld rows %lld\n",
+           S.iters, S.acc, ss.pt[0], ss.pt[1], ss.pt[2], ss.pt[3], ss.pt[4], ss.pt[5], ss.pt[6], ss.pt[7], ss.pt[8],
+           ss.pt[9], ss.pt[10], ss.pt[11]);
+#endif
 }
 
 }  // namespace resid
 
-bool resid_eligible_sizes(int U) { return U >= 1 && U <= resid::MAXU; }
+bool resid_eligible_sizes(int N, int u) {
+  return N * u >= 1 && N * u <= resid::MAXU && resid_smem_bytes(N, u) + sizeof(resid::Smem) <= 227 * 1024;
+}
 
-size_t resid_smem_bytes() {
-  const size_t gemm = 2 * resid::GK * resid::GP;
-  const size_t llt = resid::LK * resid::LP + resid::CB * (resid::CB + 1);
-  return sizeof(double) * (gemm > llt ? gemm : llt);
+size_t resid_smem_bytes(int N, int u) {
+  const size_t N16 = resid::SMS * (size_t)N;
+  size_t b = 4 * resid::GK * resid::GP;                                   // J^T J tiles (double-buffered)
+  b = std::max(b, (size_t)(resid::LK * resid::LP + resid::CB * resid::CS + resid::MAXU * resid::CS));  // Cholesky
+  b = std::max(b, 2 * u * N16);                                           // passes
+  b = std::max(b, 4 * u * N16);                                           // residual sweeps
+  b = std::max(b, (2 * u + u * u) * N16);                                 // Jacobian walks
+  return sizeof(double) * b;
 }
 
 cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out,
                               cudaStream_t s) {
-  const size_t smem = resid_smem_bytes();
-  static bool configured = false;
-  if (!configured) {
+  const size_t smem = resid_smem_bytes(rd.N, rd.u);
+  static size_t configured = 0;
+  if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(resid::k_resid_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured = smem;
   }
   resid::k_resid_step<<<(unsigned)a.B, resid::NT, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, rd, rws, out);
   return cudaGetLastError();

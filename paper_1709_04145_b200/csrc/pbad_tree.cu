@@ -30,6 +30,15 @@
 #include "pbad_launch.h"
 #include "pbad_math.cuh"
 
+#ifndef PBAD_TREE_NOINLINE
+#define PBAD_TREE_NOINLINE 0  // 1: phase functions kept out of line (smaller code, more registers)
+#endif
+#if PBAD_TREE_NOINLINE
+#define TREE_NOINLINE __noinline__
+#else
+#define TREE_NOINLINE
+#endif
+
 namespace pbad_gpu {
 namespace tree {
 
@@ -150,7 +159,7 @@ __device__ __forceinline__ bool all_finite_warp(const W& w, const double* a) {
 
 // forward_pass / ConfigPass::make value+world part (kinematics.cpp:171-181,
 // adjoint.cpp:9-27).  false = non-finite configuration (ModelError).
-__device__ bool fk_world(const W& w, const double* q) {
+__device__ TREE_NOINLINE bool fk_world(const W& w, const double* q) {
   if (!all_finite_warp(w, q)) return false;
   const DModel& m = *w.m;
   for (int i = w.lane; i < w.N; i += 32) {
@@ -174,7 +183,7 @@ __device__ bool fk_world(const W& w, const double* q) {
 }
 
 // levers of ConfigPass::make (adjoint.cpp:20-24): lever = parent_world * d1
-__device__ void fk_levers(const W& w, const double* q) {
+__device__ TREE_NOINLINE void fk_levers(const W& w, const double* q) {
   const DModel& m = *w.m;
   double* d1s = w.scr;  // n x 16 scratch
   for (int i = w.lane; i < w.N; i += 32) {
@@ -217,7 +226,7 @@ __device__ void fk_levers(const W& w, const double* q) {
 
 // StepObjective energy value (objective.cpp:215-226, 237) at the configuration
 // whose world transforms are in w.world; q is that configuration.
-__device__ double value_at(const W& w, const double* q) {
+__device__ TREE_NOINLINE double value_at(const W& w, const double* q) {
   const DModel& m = *w.m;
   for (int i = w.lane; i < w.N; i += 32) {
     const M4 wi = ld16(w.world + MS * i);
@@ -242,7 +251,7 @@ __device__ double value_at(const W& w, const double* q) {
 
 // energy gradient (objective.cpp:227-248): inertial seeds and gravity
 // cotangents through functional_grad (adjoint.cpp:49-64), then (g + pg) - tau.
-__device__ void gradient(const W& w, double* g) {
+__device__ TREE_NOINLINE void gradient(const W& w, double* g) {
   const DModel& m = *w.m;
   const TreeDesc& td = *w.td;
   double* sA = w.scr_k(0);  // inertial seeds -> children contributions
@@ -279,7 +288,7 @@ __device__ void gradient(const W& w, double* g) {
 
 // Gauss-Newton matrix gn = sym(hess_ab(x, x) / dt^2 + pot.gn) (objective.cpp:
 // 249-254, adjoint.cpp:132-176), lower-packed into w.gn (global).
-__device__ void gn_assemble(const W& w) {
+__device__ TREE_NOINLINE void gn_assemble(const W& w) {
   const DModel& m = *w.m;
   const TreeDesc& td = *w.td;
   double* ai = w.scr_k(0);
@@ -345,7 +354,7 @@ __device__ void gn_assemble(const W& w) {
 
 // LLT (optim.cpp:11-15, eigen_lite right-looking) on the lower-packed damped
 // matrix in shared memory.  false = non-positive pivot.
-__device__ bool llt_factor_w(const W& w) {
+__device__ TREE_NOINLINE bool llt_factor_w(const W& w) {
   double* A = w.damped;
   const int n = w.n;
   for (int k = 0; k < n; ++k) {
@@ -387,7 +396,7 @@ __device__ __forceinline__ double sel(const double (&v)[MAXV], int s) {
 
 // llt_solve (eigen_lite): forward then backward substitution, column-oriented;
 // v holds the right-hand side for rows lane + 32 s on entry, the solution on exit.
-__device__ void llt_solve_w(const W& w, double (&v)[MAXV]) {
+__device__ TREE_NOINLINE void llt_solve_w(const W& w, double (&v)[MAXV]) {
   const double* A = w.damped;
   const int n = w.n;
   for (int j = 0; j < n; ++j) {
@@ -499,7 +508,7 @@ __device__ int lm_iterate(const W& w, Solver& S) {
 }
 
 // ForceModel::tau_at (objective.hpp:28-58), element-parallel
-__device__ void tau_at(const W& w, double t, double* dst) {
+__device__ TREE_NOINLINE void tau_at(const W& w, double t, double* dst) {
   const DForces& f = *w.f;
   const int n = w.n;
   for (int i = w.lane; i < n; i += 32) {
@@ -521,7 +530,7 @@ __device__ void tau_at(const W& w, double t, double* dst) {
 }
 
 // copy w.world into a history block and its body products T = hw S
-__device__ void store_history(const W& w, double* hw, double* T) {
+__device__ TREE_NOINLINE void store_history(const W& w, double* hw, double* T) {
   for (int i = w.lane; i < w.N; i += 32) {
     const M4 wi = ld16(w.world + MS * i);
     st16(hw + 16 * i, wi);
