@@ -174,35 +174,48 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(cfg, scene, model_links, n, steps=1, sample=None):
+def cpu_baseline(cfg, scene, model_links, n, steps=1, sample=None, target_s=15.0):
     """The reference's own CPU batch_simulate (oracle/_ref: /root/reference
     sources compiled unmodified, kind "reference", its WorkerPool on all host
     threads) when built, else the C oracle port (kind "port"), over a bounded
-    sample of the workload."""
+    sample of the workload: one calibration round of `cores` environments x
+    `steps` steps, then (if that took under ~10 s) a second round sized to
+    about `target_s` seconds, which is the one reported."""
     import oracle
     cores = os.cpu_count() or 1
-    sample = sample or max(cores, min(cfg["batch"], cores * 4))
     forces = scene.forces()
     use_ref = oracle.ref_available()
     mo = oracle.RefModel(model_links) if use_ref else oracle.Model(model_links)
-    q0 = initial_states(cfg, scene, n, 0, sample)
-    sims = []
-    for b in range(sample):
-        s = sim_config(cfg, steps, 1 << 30)
-        s.q0 = q0[b]
-        s.qdot0 = np.zeros(n)
-        sims.append(s)
     run = oracle.ref_batch_simulate if use_ref else oracle.batch_simulate
-    t = time.perf_counter()
-    trs = run(mo, forces, sims, workers=cores)
-    el = time.perf_counter() - t
-    done = sum(tr.n_samples - 1 for tr in trs)
+
+    def timed(count, steps=steps):
+        q0 = initial_states(cfg, scene, n, 0, count)
+        sims = []
+        for b in range(count):
+            s = sim_config(cfg, steps, 1 << 30)
+            s.q0 = q0[b]
+            s.qdot0 = np.zeros(n)
+            sims.append(s)
+        t = time.perf_counter()
+        trs = run(mo, forces, sims, workers=cores)
+        el = time.perf_counter() - t
+        return sum(tr.n_samples - 1 for tr in trs), el
+
+    count = sample or min(cfg["batch"], cores)
+    done, el = timed(count)
+    if sample is None and el < 10.0 and count < cfg["batch"]:
+        count = int(min(cfg["batch"], max(count + 1, count * target_s / max(el, 1e-3))))
+        count = max(cores, (count // cores) * cores)
+        done, el = timed(count)
+        if el < 5.0:  # the whole batch is cheap: lengthen the rollout instead
+            steps = int(min(50, max(2, steps * target_s / max(el, 1e-3))))
+            done, el = timed(count, steps)
     kind = "reference" if use_ref else "port"
     what = ("reference batch_simulate (stepper.cpp:204-270, WorkerPool)" if use_ref
             else "C oracle batch_simulate")
     return {"value": done / el, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{sample} envs x {steps} step(s) of {cfg['desc'].split(':')[0]}, {what}, "
-                      f"{cores} threads, {el:.2f} s",
+            "sample": f"{count} envs x {steps} step(s) of {cfg['desc'].split(':')[0]} (first envs of the bench "
+                      f"batch), {what}, {cores} threads, {el:.2f} s",
             "seconds": el}
 
 

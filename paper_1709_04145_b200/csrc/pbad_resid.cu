@@ -40,7 +40,7 @@ namespace pbad_gpu {
 namespace resid {
 
 #ifndef PBAD_RESID_CHOL_REG
-#define PBAD_RESID_CHOL_REG 1  // 1: diagonal blocks and solve rows in registers (unrolled); 0: shared memory loops
+#define PBAD_RESID_CHOL_REG 2  // 2: lookahead; 1: diagonal blocks and solve rows in registers (unrolled); 0: shared memory loops
 #endif
 constexpr int NT = 256;  // threads per environment
 constexpr unsigned FULL = 0xffffffffu;
@@ -57,6 +57,9 @@ constexpr int LK = 16;       // k chunk of the block-column update
 constexpr int MAXU = 320;
 constexpr int SMS = 18;      // shared-memory stride of a 4x4 (16 + 2 pad: conflict-free per-link double2 access)
 constexpr int LP = MAXU + 2; // padded smem row of the update panel
+constexpr int LSCAP = 16384; // shared-memory doubles for the Cholesky update panel
+constexpr int LSCAP_A = 12288;  // lookahead variant: panel of warps 1..7
+constexpr int LSCAP_C = 10240;  // lookahead variant: panel of block J's columns
 
 __device__ __forceinline__ M4 ldm4(const double* p) {
   M4 m;
@@ -119,7 +122,15 @@ struct Smem {
   int flag;
   double scal[8];
   int parent[MAXU];
+  short pk32[CB * (CB + 1) / 2];  // packed 32x32 lower triangle, column-major: row | col << 8
 };
+
+// Shared memory is addressed through these namespace-scope symbols (not through
+// pointers stored in R) so the out-of-line phase functions keep LDS/STS
+// addressing instead of generic loads.
+__shared__ Smem rss;
+extern __shared__ __align__(16) double rsm[];
+
 
 // per-environment context (identical in every thread)
 struct R {
@@ -132,8 +143,6 @@ struct R {
   double inv_dt2;
   double *J, *GN, *DM, *FH, *PH, *pass, *hw0, *hw1, *HA, *FA, *seeds, *cot, *x, *grad, *cand, *res, *pg, *tau,
       *step;
-  double* sm;   // dynamic shared memory (tiles)
-  Smem* ss;     // static shared scratch
   __device__ __forceinline__ double* val(int mm) const { return pass + mm * rd->pstride; }
   __device__ __forceinline__ double* wld(int mm) const { return pass + mm * rd->pstride + 16L * N; }
   __device__ __forceinline__ double* dd1(int mm) const { return pass + mm * rd->pstride + 32L * N; }
@@ -150,10 +159,10 @@ __device__ double block_max(const R& r, double v) {
 #pragma unroll
   for (int s = 16; s >= 1; s >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, s));
   __syncthreads();
-  if ((r.tid & 31) == 0) r.ss->red[r.tid >> 5] = v;
+  if ((r.tid & 31) == 0) rss.red[r.tid >> 5] = v;
   __syncthreads();
   double mx = 0.0;
-  for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, r.ss->red[w]);
+  for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, rss.red[w]);
   __syncthreads();
   return mx;
 }
@@ -192,8 +201,8 @@ __device__ __noinline__ bool passes(const R& r, const double* xs, bool want_d2) 
   const ResidDesc& rd = *r.rd;
   const int N = r.N;
   const long NS = (long)SMS * N;
-  double* Vs = r.sm;                 // values [u][N][16]
-  double* Ws = r.sm + r.u * NS;     // worlds [u][N][16]
+  double* Vs = rsm;                 // values [u][N][16]
+  double* Ws = rsm + r.u * NS;     // worlds [u][N][16]
   for (int t = r.tid; t < r.u * N; t += NT) {
     const int mm = t / N, i = t - mm * N;
     const double q = xs[mm * r.n + i];
@@ -210,7 +219,7 @@ __device__ __noinline__ bool passes(const R& r, const double* xs, bool want_d2) 
     for (int t = r.tid; t < r.u * cnt; t += NT) {
       const int mm = t / cnt;
       const int i = rd.lvl_links[l0 + t - mm * cnt];
-      const int p = r.ss->parent[i];
+      const int p = rss.parent[i];
       const M4 v = ldm4(Vs + mm * NS + SMS * i);
       stm4(Ws + mm * NS + SMS * i, p >= 0 ? mul(ldm4(Ws + mm * NS + SMS * p), v) : v);
     }
@@ -218,7 +227,7 @@ __device__ __noinline__ bool passes(const R& r, const double* xs, bool want_d2) 
   }
   for (int t = r.tid; t < r.u * N; t += NT) {
     const int mm = t / N, i = t - mm * N;
-    const int p = r.ss->parent[i];
+    const int p = rss.parent[i];
     stm4(r.wld(mm) + 16 * i, ldm4(Ws + mm * NS + SMS * i));
     const M4 pw = p >= 0 ? ldm4(Ws + mm * NS + SMS * p) : m4_identity();
     stm4(r.lev(mm) + 16 * i, mul(pw, ldm4(r.dd1(mm) + 16 * i)));
@@ -263,8 +272,8 @@ __device__ __noinline__ double residual(const R& r) {
   // gravity cotangent sweeps, level-synchronous from the leaves
   const int nsw = r.grav ? 2 * u : u;
   const long NS = (long)SMS * N;
-  double* Xs = r.sm;                  // children contributions [2u][N][16]
-  double* Ls = r.sm + 2 * u * NS;    // levers [u][N][16]
+  double* Xs = rsm;                  // children contributions [2u][N][16]
+  double* Ls = rsm + 2 * u * NS;    // levers [u][N][16]
   double* Vs = Ls + u * NS;          // values [u][N][16]
   stage_vl(r, Vs, Ls);
   __syncthreads();
@@ -296,11 +305,11 @@ __device__ __noinline__ double residual(const R& r) {
     for (int i = lane; i < n; i += 32) p = fma(r.res[warp * n + i], r.res[warp * n + i], p);
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) p = p + __shfl_xor_sync(FULL, p, s);
-    if (lane == 0) r.ss->scal[warp] = p;
+    if (lane == 0) rss.scal[warp] = p;
   }
   __syncthreads();
   double v = 0.0;
-  for (int mm = 0; mm < u; ++mm) v += r.ss->scal[mm];
+  for (int mm = 0; mm < u; ++mm) v += rss.scal[mm];
   __syncthreads();
   return v;
 }
@@ -322,7 +331,7 @@ __device__ __noinline__ void jacobian(const R& r) {
   // pass values / levers of every instant and the composite-inertia
   // contributions Z live in shared memory for the walks below
   const long NS = (long)SMS * N;
-  double* Vs = r.sm;
+  double* Vs = rsm;
   double* Ls = Vs + u * NS;
   double* Zs = Ls + u * NS;  // [u*u][N][16]
   stage_vl(r, Vs, Ls);
@@ -369,7 +378,7 @@ __device__ __noinline__ void jacobian(const R& r) {
     }
     M4 fwd = ldm4(r.ha(pr, 1) + 16 * i);
     M4 bwd = ldm4(r.ha(pr, 2) + 16 * i);
-    for (int l = r.ss->parent[i]; l >= 0; l = r.ss->parent[l]) {
+    for (int l = rss.parent[i]; l >= 0; l = rss.parent[l]) {
       const double t1 = 0.0 + trace_mul(mul_at(ua_i, ldm4(lb + SMS * l)), fwd);   // H(i, l)
       const double t2 = 0.0 + trace_mul(mul_at(ldm4(la + SMS * l), ub_i), bwd);   // H(l, i)
       r.J[(rowb + l) + U * (cola + i)] = ca * t1;
@@ -389,11 +398,11 @@ __device__ __noinline__ void jacobian(const R& r) {
     const double* lm = Ls + mm * NS;
     const double* vm = Vs + mm * NS;
     const M4 a = ldm4(r.fa(sw, 0) + 16 * i);
-    const int p = r.ss->parent[i];
+    const int p = rss.parent[i];
     const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
     F[i + (long)n * i] = 0.0 + ddot(mul(pw, ldm4(r.dd2(mm) + 16 * i)), a);
     M4 walk = mul_bt(a, ldm4(r.dd1(mm) + 16 * i));
-    for (int l = p; l >= 0; l = r.ss->parent[l]) {
+    for (int l = p; l >= 0; l = rss.parent[l]) {
       const double h = 0.0 + ddot(ldm4(lm + SMS * l), walk);
       F[l + (long)n * i] = h;
       F[i + (long)n * l] = h;
@@ -420,7 +429,7 @@ __device__ __noinline__ void jacobian(const R& r) {
 // grad = 2 J^T g (objective.cpp:326-327)
 __device__ __noinline__ void gradient(const R& r) {
   const int U = r.U;
-  double* rs = r.sm;
+  double* rs = rsm;
   for (int k = r.tid; k < U; k += NT) rs[k] = r.res[k];
   __syncthreads();
   for (int a = r.tid; a < U; a += NT) {
@@ -477,7 +486,7 @@ __device__ __noinline__ void gauss_newton(const R& r) {
       double pa[GK * GB / NT], pb[GK * GB / NT];
       gn_load(r, a0, b0, 0, pa, pb);
       for (int c = 0; c < nk; ++c) {
-        double* As = r.sm + (c & 1) * 2 * GK * GP;
+        double* As = rsm + (c & 1) * 2 * GK * GP;
         double* Bs = As + GK * GP;
         gn_store(r, As, Bs, pa, pb);
         __syncthreads();
@@ -534,7 +543,7 @@ __device__ __noinline__ void gauss_newton(const R& r) {
 #define PT_MARK(k)                                   \
   do {                                               \
     const long long pt_t1 = clock64();               \
-    if (r.tid == 0) r.ss->pt[k] += pt_t1 - pt_t0;    \
+    if (r.tid == 0) rss.pt[k] += pt_t1 - pt_t0;    \
     pt_t0 = pt_t1;                                   \
   } while (0)
 #else
@@ -551,14 +560,256 @@ __device__ __noinline__ void gauss_newton(const R& r) {
 // The damped matrix gn + lambda I (optim.cpp:105-107) is read from r.GN at
 // each element's first use (left-looking touches every original entry once).
 // false = non-positive pivot.
-constexpr int CS = CB + 1;  // smem row stride of the diagonal block / panel rows
-#if PBAD_RESID_CHOL_REG
+#if PBAD_RESID_CHOL_REG == 2
+// ---- lookahead variant ------------------------------------------------------
+// Block column J+1's update by the columns left of block J (warps 1..7) runs
+// while warp 0 factors the diagonal block J; then the rows below block J are
+// solved (all threads) and block column J+1 receives block J's 32 columns.
+// Every element still sees its k updates in ascending order.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+  if (id == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// acc(i, j) for rows i in [c0, U), cols j in [c0, c0 + bw), j <= i:
+//   init (G + lambda I if fromG, else A), then acc = fma(-L(i,k), L(j,k), acc)
+//   for k in [kb, ke) ascending; result to A.  Threads [NT - GS, NT) of the CTA,
+//   thread tile NI rows (stride GS/8) x 4 columns (stride 8).
+template <int GS, int NI>
+__device__ __forceinline__ void bcu_tile(const R& r, double* A, const double* G, double lambda, bool fromG, int c0,
+                                         int bw, int kb, int ke, double* panel, int cap, int bar) {
+  constexpr int RY = GS / 8;
+  const int U = r.U;
+  const int t = r.tid - (NT - GS);
+  const int tx = t & 7, ty = t >> 3;
+  const int rows = U - c0;
+  double acc[NI][4];
+  int ri[NI];
+#pragma unroll
+  for (int ii = 0; ii < NI; ++ii) ri[ii] = min(ty + RY * ii, rows - 1);
+  int cj[4];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) cj[jj] = min(tx + 8 * jj, rows - 1);
+#pragma unroll
+  for (int ii = 0; ii < NI; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int i = c0 + ty + RY * ii, j = c0 + tx + 8 * jj;
+      const long at = i + (long)U * j;
+      acc[ii][jj] = (i < U && j < c0 + bw && j <= i) ? (fromG ? (i == j ? G[at] + lambda : G[at]) : A[at]) : 0.0;
+    }
+  const int kcap = cap / rows;
+  for (int k0 = kb; k0 < ke; k0 += kcap) {
+    const int kc = min(kcap, ke - k0);
+    group_sync(bar, GS);
+    for (int kk = 0; kk < kc; ++kk)
+      for (int rr = t; rr < rows; rr += GS) cp_async8(panel + kk * rows + rr, A + (c0 + rr) + (long)U * (k0 + kk));
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    group_sync(bar, GS);
+#pragma unroll 4
+    for (int kk = 0; kk < kc; ++kk) {
+      const double* pk = panel + kk * rows;
+      double bv[4], av[NI];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) bv[jj] = pk[cj[jj]];
+#pragma unroll
+      for (int ii = 0; ii < NI; ++ii) av[ii] = pk[ri[ii]];
+#pragma unroll
+      for (int ii = 0; ii < NI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(-av[ii], bv[jj], acc[ii][jj]);
+    }
+  }
+#pragma unroll
+  for (int ii = 0; ii < NI; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int i = c0 + ty + RY * ii, j = c0 + tx + 8 * jj;
+      if (i < U && j < c0 + bw && j <= i) A[i + (long)U * j] = acc[ii][jj];
+    }
+}
+template <int GS>
+__device__ __noinline__ void block_col_update(const R& r, double* A, const double* G, double lambda, bool fromG,
+                                              int c0, int bw, int kb, int ke, double* panel, int cap, int bar) {
+  constexpr int RY = GS / 8;
+  const int ni = (r.U - c0 + RY - 1) / RY;
+  if (ni <= 1) bcu_tile<GS, 1>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (ni <= 2) bcu_tile<GS, 2>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (ni <= 3) bcu_tile<GS, 3>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (ni <= 4) bcu_tile<GS, 4>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (ni <= 6) bcu_tile<GS, 6>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (ni <= 8) bcu_tile<GS, 8>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else bcu_tile<GS, (MAXU + RY - 1) / RY>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+}
+
+constexpr int CS = CB + 1;
 __device__ __noinline__ bool cholesky(const R& r, double lambda) {
   const int U = r.U;
   double* A = r.DM;
   const double* G = r.GN;
-  double* Ls = r.sm;                 // [LK][LP] panel rows of the k-chunk
-  double* Lj = r.sm + LK * LP;       // [CB][CB+1] factored diagonal block
+  double* Lj = rsm;                       // [CB][CS] diagonal block
+  double* panelA = Lj + CB * CS;           // lookahead update panel
+  double* panelC = panelA + LSCAP_A;       // block-J update panel [CB][rows]
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  PT_START();
+  for (int j0 = 0; j0 < U; j0 += CB) {
+    const int bw = min(CB, U - j0);
+    const int j1 = j0 + bw;                // next block column
+    const int bw1 = min(CB, U - j1);
+    // A) warp 0: diagonal block j0 | warps 1..7: block column j1 by k in [0, j0)
+    if (warp == 0) {
+      for (int c = 0; c < bw; ++c)
+        if (lane < bw && c <= lane) {
+          const long at = (j0 + lane) + (long)U * (j0 + c);
+          Lj[lane * CS + c] = j0 > 0 ? A[at] : (c == lane ? G[at] + lambda : G[at]);
+        }
+      __syncwarp();
+      // right-looking, the trailing update spread over the packed 32x32
+      // triangle (rss.pk32: row | col << 8, columns ascending)
+      int ok = 1;
+      for (int k = 0; k < bw; ++k) {
+        const double akk = Lj[k * CS + k];
+        if (akk <= 0.0) {
+          ok = 0;
+          break;
+        }
+        const double d = sqrt(akk);
+        if (lane > k && lane < bw) Lj[lane * CS + k] = Lj[lane * CS + k] / d;
+        __syncwarp();
+        if (lane == k) Lj[k * CS + k] = d;
+        const int e0 = (k + 1) * (2 * CB - k - 2) / 2 + k + 1;  // packed index of (k+1, k+1)
+        for (int e = e0 + lane; e < CB * (CB + 1) / 2; e += 64) {
+          const int p0 = rss.pk32[e];
+          const int p1 = e + 32 < CB * (CB + 1) / 2 ? rss.pk32[e + 32] : -1;
+          const int i0 = p0 & 255, c0 = p0 >> 8;
+          const int i1 = p1 & 255, c1 = p1 >> 8;
+          double u0 = 0.0, u1 = 0.0;
+          if (i0 < bw) u0 = fma(-Lj[i0 * CS + k], Lj[c0 * CS + k], Lj[i0 * CS + c0]);
+          if (p1 >= 0 && i1 < bw) u1 = fma(-Lj[i1 * CS + k], Lj[c1 * CS + k], Lj[i1 * CS + c1]);
+          if (i0 < bw) Lj[i0 * CS + c0] = u0;
+          if (p1 >= 0 && i1 < bw) Lj[i1 * CS + c1] = u1;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) rss.flag = ok;
+    } else if (j1 < U) {
+      block_col_update<NT - 32>(r, A, G, lambda, true, j1, bw1, 0, j0, panelA, LSCAP_A, 1);
+    }
+    __syncthreads();
+    PT_MARK(10);
+    if (!rss.flag) {
+      __syncthreads();
+      return false;
+    }
+    // diagonal block to HBM
+    for (int t = r.tid; t < bw * bw; t += NT) {
+      const int rr = t / bw, c = t - rr * bw;
+      if (c <= rr) A[(j0 + rr) + (long)U * (j0 + c)] = Lj[rr * CS + c];
+    }
+    // B) rows below the diagonal block: one thread per row, registers
+    for (int i = j1 + r.tid; i < U; i += NT) {
+      double a[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) a[c] = c < bw ? (j0 > 0 ? A : G)[i + (long)U * (j0 + c)] : 0.0;
+#pragma unroll
+      for (int k = 0; k < CB; ++k) {
+        if (k < bw) {
+          a[k] = a[k] / Lj[k * CS + k];
+#pragma unroll
+          for (int j = k + 1; j < CB; ++j)
+            if (j < bw) a[j] = fma(-a[k], Lj[j * CS + k], a[j]);
+        }
+        asm volatile("" ::: "memory");  // keep the column loads per step (no 496-value hoist)
+      }
+#pragma unroll
+      for (int c = 0; c < CB; ++c)
+        if (c < bw) A[i + (long)U * (j0 + c)] = a[c];
+    }
+    __syncthreads();
+    PT_MARK(11);
+    // C) block column j1 by block j0's columns
+    if (j1 < U) {
+      block_col_update<NT>(r, A, G, lambda, false, j1, bw1, j0, j1, panelC, LSCAP_C, 0);
+      __syncthreads();
+    }
+    PT_MARK(9);
+  }
+  return true;
+}
+
+// llt_solve (eigen_lite): x = L^-T L^-1 b in place on v (global, length U)
+__device__ __noinline__ void llt_solve(const R& r, double* v) {
+  const int U = r.U;
+  const double* A = r.DM;
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  // forward: column-oriented, blocks ascending
+  for (int j0 = 0; j0 < U; j0 += CB) {
+    const int bw = min(CB, U - j0);
+    if (warp == 0) {
+      double x = lane < bw ? v[j0 + lane] : 0.0;
+      double lrow[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) lrow[c] = (lane < bw && c <= lane) ? A[(j0 + lane) + (long)U * (j0 + c)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < CB; ++j) {
+        if (j < bw) {
+          const double xj = __shfl_sync(FULL, x, j) / __shfl_sync(FULL, lrow[j], j);
+          if (lane == j) x = xj;
+          else if (lane > j && lane < bw) x = fma(-lrow[j], xj, x);
+        }
+      }
+      if (lane < bw) v[j0 + lane] = x;
+    }
+    __syncthreads();
+    for (int i = j0 + bw + r.tid; i < U; i += NT) {
+      double x = v[i];
+      for (int j = j0; j < j0 + bw; ++j) x = fma(-A[i + (long)U * j], v[j], x);
+      v[i] = x;
+    }
+    __syncthreads();
+  }
+  // backward: for j descending, x_i -= L(j, i) x_j for i < j
+  const int nbk = (U + CB - 1) / CB;
+  for (int bk = nbk - 1; bk >= 0; --bk) {
+    const int j0 = bk * CB;
+    const int bw = min(CB, U - j0);
+    if (warp == 0) {
+      double x = lane < bw ? v[j0 + lane] : 0.0;
+      // lane l holds column j0 + l of the block: L(j0 + c, j0 + l) for c >= l
+      double lcol[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) lcol[c] = (lane < bw && c >= lane && c < bw) ? A[(j0 + c) + (long)U * (j0 + lane)] : 0.0;
+#pragma unroll
+      for (int jr = CB - 1; jr >= 0; --jr) {
+        if (jr < bw) {
+          const double xj = __shfl_sync(FULL, x, jr) / __shfl_sync(FULL, lcol[jr], jr);
+          if (lane == jr) x = xj;
+          else if (lane < jr) x = fma(-lcol[jr], xj, x);
+        }
+      }
+      if (lane < bw) v[j0 + lane] = x;
+    }
+    __syncthreads();
+    for (int i = r.tid; i < j0; i += NT) {
+      double x = v[i];
+      for (int j = j0 + bw - 1; j >= j0; --j) x = fma(-A[j + (long)U * i], v[j], x);
+      v[i] = x;
+    }
+    __syncthreads();
+  }
+}
+
+#elif PBAD_RESID_CHOL_REG
+constexpr int CS = CB + 1;  // smem row stride of the diagonal block / panel rows
+__device__ __noinline__ bool cholesky(const R& r, double lambda) {
+  const int U = r.U;
+  double* A = r.DM;
+  const double* G = r.GN;
+  double* Lj = rsm;                 // [CB][CS] factored diagonal block
+  double* Ls = rsm + CB * CS;       // [kc][rows] panel rows of the k-chunk (LSCAP doubles)
   const int warp = r.tid >> 5, lane = r.tid & 31;
   PT_START();
   for (int j0 = 0; j0 < U; j0 += CB) {
@@ -580,22 +831,29 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
                             ? (i == j ? G[i + (long)U * j] + lambda : G[i + (long)U * j])
                             : 0.0;
         }
-      for (int k0 = 0; k0 < j0; k0 += LK) {
-        const int kc = min(LK, j0 - k0);
+      // k-chunks as long as the panel fits in shared memory (few, large chunks:
+      // the late block columns have few rows and a long k range)
+      const int kcap = LSCAP / rows;
+      for (int k0 = 0; k0 < j0; k0 += kcap) {
+        const int kc = min(kcap, j0 - k0);
         __syncthreads();
-        for (int t = r.tid; t < LK * rows; t += NT) {
-          const int kk = t / rows, rr = t - kk * rows;
-          Ls[kk * LP + rr] = kk < kc ? A[(j0 + rr) + (long)U * (k0 + kk)] : 0.0;
-        }
+        // cp.async: every thread keeps all its copies in flight
+        for (int kk = 0; kk < kc; ++kk)
+          for (int rr = r.tid; rr < rows; rr += NT) {
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(Ls + kk * rows + rr);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(A + (j0 + rr) + (long)U * (k0 + kk))
+                         : "memory");
+          }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         for (int kk = 0; kk < kc; ++kk) {
           double bv[4];
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) bv[jj] = Ls[kk * LP + tx + 8 * jj];
+          for (int jj = 0; jj < 4; ++jj) bv[jj] = Ls[kk * rows + min(tx + 8 * jj, rows - 1)];
 #pragma unroll
           for (int ii = 0; ii < MI; ++ii) {
             if (ii < ni) {
-              const double av = Ls[kk * LP + min(ty + 32 * ii, rows - 1)];
+              const double av = Ls[kk * rows + min(ty + 32 * ii, rows - 1)];
 #pragma unroll
               for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fma(-av, bv[jj], acc[ii][jj]);
             }
@@ -640,7 +898,7 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
           }
         }
       }
-      if (lane == 0) r.ss->flag = ok;
+      if (lane == 0) rss.flag = ok;
       if (ok) {
 #pragma unroll
         for (int c = 0; c < CB; ++c)
@@ -651,7 +909,7 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
       }
     }
     __syncthreads();
-    if (!r.ss->flag) {
+    if (!rss.flag) {
       __syncthreads();
       return false;
     }
@@ -743,12 +1001,13 @@ __device__ __noinline__ void llt_solve(const R& r, double* v) {
 }
 
 #else
+constexpr int CS = CB + 1;
 __device__ __noinline__ bool cholesky(const R& r, double lambda) {
   const int U = r.U;
   double* A = r.DM;
   const double* G = r.GN;
-  double* Ls = r.sm;                 // [LK][LP] panel rows of the k-chunk
-  double* Lj = r.sm + LK * LP;       // [CB][CS] diagonal block
+  double* Ls = rsm;                 // [LK][LP] panel rows of the k-chunk
+  double* Lj = rsm + LK * LP;       // [CB][CS] diagonal block
   double* Rs = Lj + CB * CS;         // [MAXU][CS] rows below the diagonal block
   const int warp = r.tid >> 5, lane = r.tid & 31;
   for (int j0 = 0; j0 < U; j0 += CB) {
@@ -828,7 +1087,7 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
         }
         __syncwarp();
       }
-      if (lane == 0) r.ss->flag = ok;
+      if (lane == 0) rss.flag = ok;
       if (ok)
         for (int c = 0; c < bw; ++c)
           if (lane < bw && c <= lane) A[(j0 + lane) + (long)U * (j0 + c)] = Lj[lane * CS + c];
@@ -841,7 +1100,7 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
       Rs[rr * CS + c] = j0 > 0 ? A[at] : G[at];
     }
     __syncthreads();
-    if (!r.ss->flag) {
+    if (!rss.flag) {
       __syncthreads();
       return false;
     }
@@ -870,7 +1129,7 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
 __device__ __noinline__ void llt_solve(const R& r, double* v) {
   const int U = r.U;
   const double* A = r.DM;
-  double* Lj = r.sm;            // [CB][CS]
+  double* Lj = rsm;            // [CB][CS]
   double* vs = Lj + CB * CS;    // [U]
   const int warp = r.tid >> 5, lane = r.tid & 31;
   for (int t = r.tid; t < U; t += NT) vs[t] = v[t];
@@ -1038,8 +1297,6 @@ __device__ __noinline__ void tau_at(const R& r, double t, double* dst) {
 
 __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
                                                       int* iws, long B, ResidDesc rd, double* rws, Outputs out) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ Smem ss;
   const long e = blockIdx.x;
   if (e >= B) return;
   if (iws[(long)IS_RUN * B + e] != TR_RUNNING) return;
@@ -1058,8 +1315,6 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
   r.grav = f.gravity_nonzero != 0;
   const double dt = sc.dt;
   r.inv_dt2 = 1.0 / (dt * dt);
-  r.sm = smem;
-  r.ss = &ss;
   {
     double* g = rws + e * rd.gstride;
     r.J = g + rd.oJ;
@@ -1083,8 +1338,11 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
     r.step = g + rd.oStep;
   }
   const int n = r.n, u = r.u, U = r.U, N = r.N;
-  for (int i = r.tid; i < N; i += NT) ss.parent[i] = m.parent[i];
-  if (r.tid < 12) ss.pt[r.tid] = 0;
+  for (int i = r.tid; i < N; i += NT) rss.parent[i] = m.parent[i];
+  for (int c = 0, e = 0; c < CB; ++c)
+    for (int rr = c; rr < CB; ++rr, ++e)
+      if (e % NT == r.tid) rss.pk32[e] = (short)(rr | (c << 8));
+  if (r.tid < 12) rss.pt[r.tid] = 0;
   __syncthreads();
   int* const ivp = iws + e;
   auto iv = [&](int slot) -> int& { return ivp[(long)slot * B]; };
@@ -1208,8 +1466,8 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
   if (e == 0 && r.tid == 0)
     printf("phase cycles (block 0, %d iterations, %d accepted): conv %lld chol %lld solve %lld tpass %lld tres %lld "
            "fpassres %lld jac %lld grad %lld gn %lld | chol: update %lld diag %lld rows %lld\n",
-           S.iters, S.acc, ss.pt[0], ss.pt[1], ss.pt[2], ss.pt[3], ss.pt[4], ss.pt[5], ss.pt[6], ss.pt[7], ss.pt[8],
-           ss.pt[9], ss.pt[10], ss.pt[11]);
+           S.iters, S.acc, rss.pt[0], rss.pt[1], rss.pt[2], rss.pt[3], rss.pt[4], rss.pt[5], rss.pt[6], rss.pt[7], rss.pt[8],
+           rss.pt[9], rss.pt[10], rss.pt[11]);
 #endif
 }
 
@@ -1222,7 +1480,9 @@ bool resid_eligible_sizes(int N, int u) {
 size_t resid_smem_bytes(int N, int u) {
   const size_t N16 = resid::SMS * (size_t)N;
   size_t b = 4 * resid::GK * resid::GP;                                   // J^T J tiles (double-buffered)
-  b = std::max(b, (size_t)(resid::LK * resid::LP + resid::CB * resid::CS + resid::MAXU * resid::CS));  // Cholesky
+  b = std::max(b, (size_t)(resid::LK * resid::LP + resid::CB * (resid::CB + 1) + resid::MAXU * (resid::CB + 1)));  // Cholesky (smem variant)
+  b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP));             // Cholesky update panel
+  b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
   b = std::max(b, 2 * u * N16);                                           // passes
   b = std::max(b, 4 * u * N16);                                           // residual sweeps
   b = std::max(b, (2 * u + u * u) * N16);                                 // Jacobian walks

@@ -33,10 +33,18 @@
 #ifndef PBAD_TREE_NOINLINE
 #define PBAD_TREE_NOINLINE 0  // 1: phase functions kept out of line (smaller code, more registers)
 #endif
+#ifndef PBAD_TREE_NOINLINE_COLD
+#define PBAD_TREE_NOINLINE_COLD 0  // 1: multiply-called kinematics / cold phases out of line (I-cache)
+#endif
 #if PBAD_TREE_NOINLINE
 #define TREE_NOINLINE __noinline__
 #else
 #define TREE_NOINLINE
+#endif
+#if PBAD_TREE_NOINLINE || PBAD_TREE_NOINLINE_COLD
+#define TREE_COLD __noinline__
+#else
+#define TREE_COLD
 #endif
 
 namespace pbad_gpu {
@@ -159,7 +167,7 @@ __device__ __forceinline__ bool all_finite_warp(const W& w, const double* a) {
 
 // forward_pass / ConfigPass::make value+world part (kinematics.cpp:171-181,
 // adjoint.cpp:9-27).  false = non-finite configuration (ModelError).
-__device__ TREE_NOINLINE bool fk_world(const W& w, const double* q) {
+__device__ TREE_COLD bool fk_world(const W& w, const double* q) {
   if (!all_finite_warp(w, q)) return false;
   const DModel& m = *w.m;
   for (int i = w.lane; i < w.N; i += 32) {
@@ -183,7 +191,7 @@ __device__ TREE_NOINLINE bool fk_world(const W& w, const double* q) {
 }
 
 // levers of ConfigPass::make (adjoint.cpp:20-24): lever = parent_world * d1
-__device__ TREE_NOINLINE void fk_levers(const W& w, const double* q) {
+__device__ TREE_COLD void fk_levers(const W& w, const double* q) {
   const DModel& m = *w.m;
   double* d1s = w.scr;  // n x 16 scratch
   for (int i = w.lane; i < w.N; i += 32) {
@@ -288,7 +296,7 @@ __device__ TREE_NOINLINE void gradient(const W& w, double* g) {
 
 // Gauss-Newton matrix gn = sym(hess_ab(x, x) / dt^2 + pot.gn) (objective.cpp:
 // 249-254, adjoint.cpp:132-176), lower-packed into w.gn (global).
-__device__ TREE_NOINLINE void gn_assemble(const W& w) {
+__device__ TREE_COLD void gn_assemble(const W& w) {
   const DModel& m = *w.m;
   const TreeDesc& td = *w.td;
   double* ai = w.scr_k(0);
@@ -425,7 +433,7 @@ __device__ bool full_eval(const W& w, double* value) {
   *value = value_at(w, w.x);
   return true;
 }
-__device__ void derivatives(const W& w) {
+__device__ TREE_COLD void derivatives(const W& w) {
   fk_levers(w, w.x);
   gradient(w, w.grad);
   gn_assemble(w);
@@ -508,7 +516,7 @@ __device__ int lm_iterate(const W& w, Solver& S) {
 }
 
 // ForceModel::tau_at (objective.hpp:28-58), element-parallel
-__device__ TREE_NOINLINE void tau_at(const W& w, double t, double* dst) {
+__device__ TREE_COLD void tau_at(const W& w, double t, double* dst) {
   const DForces& f = *w.f;
   const int n = w.n;
   for (int i = w.lane; i < n; i += 32) {
@@ -530,7 +538,7 @@ __device__ TREE_NOINLINE void tau_at(const W& w, double t, double* dst) {
 }
 
 // copy w.world into a history block and its body products T = hw S
-__device__ TREE_NOINLINE void store_history(const W& w, double* hw, double* T) {
+__device__ TREE_COLD void store_history(const W& w, double* hw, double* T) {
   for (int i = w.lane; i < w.N; i += 32) {
     const M4 wi = ld16(w.world + MS * i);
     st16(hw + 16 * i, wi);
