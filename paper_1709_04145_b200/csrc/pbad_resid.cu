@@ -117,7 +117,7 @@ __device__ __forceinline__ M4 gravity_cot(const DForces& f, const M4& S) {
 #define PBAD_PHASE_TIMING 0  // 1: per-phase clock64 totals printed by block 0 (diagnostic builds only)
 #endif
 struct Smem {
-  long long pt[12];
+  long long pt[16];
   double red[NT];
   int flag;
   double scal[8];
@@ -570,6 +570,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void group_sync(int id, int nthreads) {
   if (id == 0) __syncthreads();
   else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -661,6 +666,9 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
     const int bw1 = min(CB, U - j1);
     // A) warp 0: diagonal block j0 | warps 1..7: block column j1 by k in [0, j0)
     if (warp == 0) {
+#if PBAD_PHASE_TIMING
+      const long long td0 = clock64();
+#endif
       for (int c = 0; c < bw; ++c)
         if (lane < bw && c <= lane) {
           const long at = (j0 + lane) + (long)U * (j0 + c);
@@ -695,8 +703,17 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
         __syncwarp();
       }
       if (lane == 0) rss.flag = ok;
+#if PBAD_PHASE_TIMING
+      if (lane == 0) rss.pt[12] += clock64() - td0;
+#endif
     } else if (j1 < U) {
+#if PBAD_PHASE_TIMING
+      const long long tu0 = clock64();
+#endif
       block_col_update<NT - 32>(r, A, G, lambda, true, j1, bw1, 0, j0, panelA, LSCAP_A, 1);
+#if PBAD_PHASE_TIMING
+      if (r.tid == 32) rss.pt[13] += clock64() - tu0;
+#endif
     }
     __syncthreads();
     PT_MARK(10);
@@ -709,24 +726,44 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
       const int rr = t / bw, c = t - rr * bw;
       if (c <= rr) A[(j0 + rr) + (long)U * (j0 + c)] = Lj[rr * CS + c];
     }
-    // B) rows below the diagonal block: one thread per row, registers
-    for (int i = j1 + r.tid; i < U; i += NT) {
-      double a[CB];
+    // B) rows below the diagonal block: one thread per row, registers; the
+    //    diagonal block's column k is read per step with explicit ld.shared
+    //    (volatile: not hoisted across steps, no generic addressing)
+    {
+      const unsigned ljs = (unsigned)__cvta_generic_to_shared(Lj);
+      for (int i = j1 + r.tid; i < U; i += NT) {
+        double a[CB];
+        const double* src = (j0 > 0 ? A : G) + i + (long)U * j0;
 #pragma unroll
-      for (int c = 0; c < CB; ++c) a[c] = c < bw ? (j0 > 0 ? A : G)[i + (long)U * (j0 + c)] : 0.0;
+        for (int c = 0; c < CB; ++c) a[c] = c < bw ? src[(long)U * c] : 0.0;
+        if (bw == CB) {
 #pragma unroll
-      for (int k = 0; k < CB; ++k) {
-        if (k < bw) {
-          a[k] = a[k] / Lj[k * CS + k];
+          for (int k = 0; k < CB; ++k) {
+            double col[CB];
 #pragma unroll
-          for (int j = k + 1; j < CB; ++j)
-            if (j < bw) a[j] = fma(-a[k], Lj[j * CS + k], a[j]);
+            for (int j = k; j < CB; ++j) col[j] = lds_f64(ljs + 8u * (j * CS + k));
+            a[k] = a[k] / col[k];
+#pragma unroll
+            for (int j = k + 1; j < CB; ++j) a[j] = fma(-a[k], col[j], a[j]);
+          }
+        } else {
+          for (int k = 0; k < bw; ++k) {
+            // short last block: dynamic k, row in registers through a rotation-free select
+#pragma unroll
+            for (int kk = 0; kk < CB; ++kk)
+              if (kk == k) {
+                a[kk] = a[kk] / lds_f64(ljs + 8u * (kk * CS + kk));
+#pragma unroll
+                for (int j = kk + 1; j < CB; ++j)
+                  if (j < bw) a[j] = fma(-a[kk], lds_f64(ljs + 8u * (j * CS + kk)), a[j]);
+              }
+          }
         }
-        asm volatile("" ::: "memory");  // keep the column loads per step (no 496-value hoist)
-      }
+        double* dst = A + i + (long)U * j0;
 #pragma unroll
-      for (int c = 0; c < CB; ++c)
-        if (c < bw) A[i + (long)U * (j0 + c)] = a[c];
+        for (int c = 0; c < CB; ++c)
+          if (c < bw) dst[(long)U * c] = a[c];
+      }
     }
     __syncthreads();
     PT_MARK(11);
@@ -1342,7 +1379,7 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
   for (int c = 0, e = 0; c < CB; ++c)
     for (int rr = c; rr < CB; ++rr, ++e)
       if (e % NT == r.tid) rss.pk32[e] = (short)(rr | (c << 8));
-  if (r.tid < 12) rss.pt[r.tid] = 0;
+  if (r.tid < 16) rss.pt[r.tid] = 0;
   __syncthreads();
   int* const ivp = iws + e;
   auto iv = [&](int slot) -> int& { return ivp[(long)slot * B]; };
@@ -1465,9 +1502,9 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
 #if PBAD_PHASE_TIMING
   if (e == 0 && r.tid == 0)
     printf("phase cycles (block 0, %d iterations, %d accepted): conv %lld chol %lld solve %lld tpass %lld tres %lld "
-           "fpassres %lld jac %lld grad %lld gn %lld | chol: update %lld diag %lld rows %lld\n",
+           "fpassres %lld jac %lld grad %lld gn %lld | chol: C %lld A %lld B %lld | diag-only %lld updA-only %lld\n",
            S.iters, S.acc, rss.pt[0], rss.pt[1], rss.pt[2], rss.pt[3], rss.pt[4], rss.pt[5], rss.pt[6], rss.pt[7], rss.pt[8],
-           rss.pt[9], rss.pt[10], rss.pt[11]);
+           rss.pt[9], rss.pt[10], rss.pt[11], rss.pt[12], rss.pt[13]);
 #endif
 }
 
