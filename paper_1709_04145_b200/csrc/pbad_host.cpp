@@ -907,7 +907,8 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     td.o_hw1 = np2 + N16;
     td.o_t0 = np2 + 2 * N16;
     td.o_t1 = np2 + 3 * N16;
-    td.gstride = np2 + 4 * N16;
+    td.o_gs = np2 + 4 * N16;
+    td.gstride = td.o_gs + 4 * 18L * m.N;
     td.smem_doubles = (int)(tree_smem_bytes(td) / sizeof(double));
     if (tree_smem_bytes(td) > 200 * 1024) c->tree = false;
   }

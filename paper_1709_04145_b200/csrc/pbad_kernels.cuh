@@ -128,6 +128,7 @@ struct TreeDesc {
   int smem_doubles;        // per environment
   long gstride;            // per-env doubles of tws
   long o_hw0, o_hw1, o_t0, o_t1;  // offsets inside one env's tws block (GN at 0)
+  long o_gs;                      // GN composite-inertia scratch [4][N][18] (PBAD_TREE_GN_GLOBAL)
 };
 
 // Residual-form path (pbad_resid.cu): CTA-per-environment LM for hinge

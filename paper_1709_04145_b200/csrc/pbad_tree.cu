@@ -33,6 +33,9 @@
 #ifndef PBAD_TREE_NOINLINE
 #define PBAD_TREE_NOINLINE 0  // 1: phase functions kept out of line (smaller code, more registers)
 #endif
+#ifndef PBAD_TREE_GN_GLOBAL
+#define PBAD_TREE_GN_GLOBAL 1  // 1: GN composite-inertia scratch in the per-env HBM/L2 block (smaller SMEM, more warps)
+#endif
 #ifndef PBAD_TREE_NOINLINE_COLD
 #define PBAD_TREE_NOINLINE_COLD 0  // 1: multiply-called kinematics / cold phases out of line (I-cache)
 #endif
@@ -53,7 +56,8 @@ namespace tree {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAXV = 3;  // dof vectors in registers: n <= 96
 constexpr int MAXN = 96;
-constexpr int MS = 18;  // shared-memory stride of a 4x4 (16 + 2 pad: conflict-free lane-per-link double2 access)
+constexpr int MS = 18;
+constexpr int TREE_SCR_ARRAYS = PBAD_TREE_GN_GLOBAL ? 2 : 4;  // link scratch arrays in SMEM  // shared-memory stride of a 4x4 (16 + 2 pad: conflict-free lane-per-link double2 access)
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
 enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
 
@@ -139,7 +143,7 @@ struct W {
   double *value, *world, *lever, *scr, *damped, *red;
   double *x, *grad, *cand, *vtau, *vtmp;
   // global, this environment's block
-  double *gn, *hw0, *hw1, *T0, *T1;
+  double *gn, *hw0, *hw1, *T0, *T1, *gs;
   __device__ __forceinline__ double* scr_k(int k) const { return scr + (long)k * MS * N; }
 };
 
@@ -299,10 +303,18 @@ __device__ TREE_NOINLINE void gradient(const W& w, double* g) {
 __device__ TREE_COLD void gn_assemble(const W& w) {
   const DModel& m = *w.m;
   const TreeDesc& td = *w.td;
+#if PBAD_TREE_GN_GLOBAL
+  constexpr int GS_ = MS;
+  double* ai = w.gs;
+  double* fwd = w.gs + (long)GS_ * w.N;
+  double* bwd = w.gs + 2L * GS_ * w.N;
+  double* Z = w.gs + 3L * GS_ * w.N;
+#else
   double* ai = w.scr_k(0);
   double* fwd = w.scr_k(1);
   double* bwd = w.scr_k(2);
   double* Z = w.scr_k(3);
+#endif
   for (int d = w.D; d >= 0; --d) {
     for (int t = td.lvl_start[d] + w.lane; t < td.lvl_start[d + 1]; t += 32) {
       const int i = td.lvl_links[t];
@@ -568,7 +580,7 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
   w.inv_dt2 = 1.0 / (dt * dt);
   {
     const int N16 = MS * td.N, nv = (td.n + 1) & ~1;
-    const int scr = (4 * N16 > MS * td.n) ? 4 * N16 : MS * td.n;
+    const int scr = (TREE_SCR_ARRAYS * N16 > MS * td.n) ? TREE_SCR_ARRAYS * N16 : MS * td.n;
     double* p = smem;
     w.value = p; p += N16;
     w.world = p; p += N16;
@@ -587,6 +599,7 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
     w.hw1 = g + td.o_hw1;
     w.T0 = g + td.o_t0;
     w.T1 = g + td.o_t1;
+    w.gs = g + td.o_gs;
   }
   const int n = td.n;
   int* const ivp = iws + e;
@@ -734,7 +747,7 @@ bool tree_eligible_sizes(int N, int n) { return N >= 1 && N <= 255 && n >= 1 && 
 
 static int tree_smem_doubles(const TreeDesc& td) {
   const int N16 = tree::MS * td.N, nv = (td.n + 1) & ~1;
-  const int scr = (4 * N16 > tree::MS * td.n) ? 4 * N16 : tree::MS * td.n;
+  const int scr = (tree::TREE_SCR_ARRAYS * N16 > tree::MS * td.n) ? tree::TREE_SCR_ARRAYS * N16 : tree::MS * td.n;
   return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 5 * nv + 4 * td.N + 32;
 }
 
