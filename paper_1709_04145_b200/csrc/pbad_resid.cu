@@ -117,7 +117,7 @@ __device__ __forceinline__ M4 gravity_cot(const DForces& f, const M4& S) {
 #define PBAD_PHASE_TIMING 0  // 1: per-phase clock64 totals printed by block 0 (diagnostic builds only)
 #endif
 struct Smem {
-  long long pt[16];
+  long long pt[20];
   double red[NT];
   int flag;
   double scal[8];
@@ -130,6 +130,23 @@ struct Smem {
 // addressing instead of generic loads.
 __shared__ Smem rss;
 extern __shared__ __align__(16) double rsm[];
+
+#if PBAD_PHASE_TIMING
+#define PT_START() long long pt_t0 = clock64()
+#define PT_MARK(k)                                   \
+  do {                                               \
+    const long long pt_t1 = clock64();               \
+    if (r.tid == 0) rss.pt[k] += pt_t1 - pt_t0;    \
+    pt_t0 = pt_t1;                                   \
+  } while (0)
+#else
+#define PT_START() \
+  do {             \
+  } while (0)
+#define PT_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 
 
 // per-environment context (identical in every thread)
@@ -314,6 +331,105 @@ __device__ __noinline__ double residual(const R& r) {
   return v;
 }
 
+// ---- hinge-chain walk steps on the non-zero blocks ---------------------------
+// Hinge levers are 3x3 (row 3 and column 3 exact zeros), link values affine
+// (row 3 = e4^T).  The walk quantities of correlation_hess_ab / functional_hess
+// are only ever read through 3x3 traces/ddots with levers, so only their
+// top-left 3x3 is updated; the fourth row (fwd) / column (bwd, walk) is
+// invariant under the affine products (exact copies) and the dropped terms
+// are fma(+-0, x, acc) = acc.  Same values as the full 4x4 reference products.
+struct L3 {
+  double a[9];  // a[r + 3c]
+};
+__device__ __forceinline__ L3 ldl3(const double* p) {
+  L3 m;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) m.a[r + 3 * c] = p[r + 4 * c];
+  return m;
+}
+// trace(mul(mul_at(A, B), F)) over the non-zero 3x3 blocks (adjoint.cpp:150-165)
+__device__ __forceinline__ double trace_at3(const L3& A, const L3& B, const M4& F) {
+  double M[9];
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      double acc = A.a[3 * p] * B.a[3 * q];
+      acc = fma(A.a[1 + 3 * p], B.a[1 + 3 * q], acc);
+      acc = fma(A.a[2 + 3 * p], B.a[2 + 3 * q], acc);
+      M[p + 3 * q] = acc;
+    }
+  double d[3];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    double acc = M[p] * F.a[4 * p];
+    acc = fma(M[p + 3], F.a[1 + 4 * p], acc);
+    acc = fma(M[p + 6], F.a[2 + 4 * p], acc);
+    d[p] = acc;
+  }
+  return (d[0] + d[1]) + d[2];
+}
+// F <- V F on rows 0..2, columns 0..2 (V affine, smem)
+__device__ __forceinline__ void fwd_step3(const double* V, M4& F) {
+  double v[12];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) v[r + 3 * c] = V[r + 4 * c];
+  double o[9];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double acc = v[r] * F.a[4 * c];
+      acc = fma(v[r + 3], F.a[1 + 4 * c], acc);
+      acc = fma(v[r + 6], F.a[2 + 4 * c], acc);
+      acc = fma(v[r + 9], F.a[3 + 4 * c], acc);
+      o[r + 3 * c] = acc;
+    }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) F.a[r + 4 * c] = o[r + 3 * c];
+}
+// B <- B V^T on rows 0..2, columns 0..2 (V affine, smem)
+__device__ __forceinline__ void bwd_step3(M4& Bm, const double* V) {
+  double v[12];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) v[r + 3 * c] = V[r + 4 * c];
+  double o[9];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double acc = Bm.a[r] * v[c];
+      acc = fma(Bm.a[r + 4], v[c + 3], acc);
+      acc = fma(Bm.a[r + 8], v[c + 6], acc);
+      acc = fma(Bm.a[r + 12], v[c + 9], acc);
+      o[r + 3 * c] = acc;
+    }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) Bm.a[r + 4 * c] = o[r + 3 * c];
+}
+// ddot(lever, W) over the non-zero 3x3 block (adjoint.cpp:84-86)
+__device__ __forceinline__ double ddot3(const L3& A, const M4& W) {
+  double rs[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    double acc = A.a[r] * W.a[r];
+    acc = fma(A.a[r + 3], W.a[r + 4], acc);
+    acc = fma(A.a[r + 6], W.a[r + 8], acc);
+    rs[r] = acc;
+  }
+  return (rs[0] + rs[1]) + rs[2];
+}
+
 // Jacobian of the residuals (objective.cpp:310-320) into r.J
 __device__ __noinline__ void jacobian(const R& r) {
   const DModel& m = *r.m;
@@ -321,6 +437,7 @@ __device__ __noinline__ void jacobian(const R& r) {
   const ResidDesc& rd = *r.rd;
   const int N = r.N, n = r.n, u = r.u, U = r.U;
   const long UU = (long)U * U;
+  PT_START();
   if (!rd.chain) {
     for (long t = r.tid; t < UU; t += NT) r.J[t] = 0.0;
     for (long t = r.tid; t < (long)u * n * n; t += NT) {
@@ -358,6 +475,7 @@ __device__ __noinline__ void jacobian(const R& r) {
     }
     __syncthreads();
   }
+  PT_MARK(14);
   // hess_ab entries: own block and the ancestor walk of every (pair, link),
   // written straight into J (transposed, scaled by inv_dt2 * stencil)
   for (int t = r.tid; t < npair * N; t += NT) {
@@ -370,23 +488,24 @@ __device__ __noinline__ void jacobian(const R& r) {
     const double* lb = Ls + b * NS;
     const double* va = Vs + a * NS;
     const double* vb = Vs + b * NS;
-    const M4 ua_i = ldm4(la + SMS * i), ub_i = ldm4(lb + SMS * i);
     const long rowb = (long)b * n, cola = (long)a * n;
     {
-      const double h = 0.0 + trace_mul(mul_at(ua_i, ub_i), ldm4(r.ha(pr, 0) + 16 * i));
+      const double h = 0.0 + trace_mul(mul_at(ldm4(la + SMS * i), ldm4(lb + SMS * i)), ldm4(r.ha(pr, 0) + 16 * i));
       r.J[(rowb + i) + U * (cola + i)] = ca * h;
     }
+    const L3 ua_i = ldl3(la + SMS * i), ub_i = ldl3(lb + SMS * i);
     M4 fwd = ldm4(r.ha(pr, 1) + 16 * i);
     M4 bwd = ldm4(r.ha(pr, 2) + 16 * i);
     for (int l = rss.parent[i]; l >= 0; l = rss.parent[l]) {
-      const double t1 = 0.0 + trace_mul(mul_at(ua_i, ldm4(lb + SMS * l)), fwd);   // H(i, l)
-      const double t2 = 0.0 + trace_mul(mul_at(ldm4(la + SMS * l), ub_i), bwd);   // H(l, i)
+      const double t1 = 0.0 + trace_at3(ua_i, ldl3(lb + SMS * l), fwd);   // H(i, l)
+      const double t2 = 0.0 + trace_at3(ldl3(la + SMS * l), ub_i, bwd);   // H(l, i)
       r.J[(rowb + l) + U * (cola + i)] = ca * t1;
       r.J[(rowb + i) + U * (cola + l)] = ca * t2;
-      fwd = mul(ldm4(vb + SMS * l), fwd);
-      bwd = mul_bt(bwd, ldm4(va + SMS * l));
+      fwd_step3(vb + SMS * l, fwd);
+      bwd_step3(bwd, va + SMS * l);
     }
   }
+  PT_MARK(15);
   // functional_hess (adjoint.cpp:66-101) of the inertial seeds and of the
   // gravity cotangents at every instant
   const int nsw = r.grav ? 2 * u : u;
@@ -403,24 +522,37 @@ __device__ __noinline__ void jacobian(const R& r) {
     F[i + (long)n * i] = 0.0 + ddot(mul(pw, ldm4(r.dd2(mm) + 16 * i)), a);
     M4 walk = mul_bt(a, ldm4(r.dd1(mm) + 16 * i));
     for (int l = p; l >= 0; l = rss.parent[l]) {
-      const double h = 0.0 + ddot(ldm4(lm + SMS * l), walk);
+      const double h = 0.0 + ddot3(ldl3(lm + SMS * l), walk);
       F[l + (long)n * i] = h;
       F[i + (long)n * l] = h;
-      walk = mul_bt(walk, ldm4(vm + SMS * l));
+      bwd_step3(walk, vm + SMS * l);
     }
   }
   __syncthreads();
+  PT_MARK(16);
   // diagonal blocks: (functional_hess + c_m ab_mm^T) + pot.hess
   {
-    const int warp = r.tid >> 5, lane = r.tid & 31;
-    for (int col = warp; col < u * n; col += NT / 32) {
-      const int mm = col / n, cc = col - mm * n;
-      const long f0 = (long)mm * n * n + (long)n * cc;
-      double* Jc = r.J + (long)mm * n + (long)U * ((long)mm * n + cc);
-      for (int rr = lane; rr < n; rr += 32) {
-        const double ph = r.grav ? 0.0 + r.PH[f0 + rr] : 0.0;
-        Jc[rr] = (r.FH[f0 + rr] + Jc[rr]) + ph;
+    // flat over (instant, column, row); 4 independent elements per thread in flight
+    const int nn = n * n;
+    const int tot = u * nn;
+    for (int t0 = r.tid; t0 < tot; t0 += 4 * NT) {
+      double fh[4], jv[4], phv[4];
+      long jat[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = t0 + q * NT;
+        if (t < tot) {
+          const int mm = t / nn, e = t - mm * nn;
+          const int cc = e / n, rr = e - cc * n;
+          jat[q] = ((long)mm * n + rr) + (long)U * ((long)mm * n + cc);
+          fh[q] = r.FH[t];
+          phv[q] = r.grav ? 0.0 + r.PH[t] : 0.0;
+          jv[q] = r.J[jat[q]];
+        }
       }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (t0 + q * NT < tot) r.J[jat[q]] = (fh[q] + jv[q]) + phv[q];
     }
   }
   __syncthreads();
@@ -538,22 +670,6 @@ __device__ __noinline__ void gauss_newton(const R& r) {
     }
 }
 
-#if PBAD_PHASE_TIMING
-#define PT_START() long long pt_t0 = clock64()
-#define PT_MARK(k)                                   \
-  do {                                               \
-    const long long pt_t1 = clock64();               \
-    if (r.tid == 0) rss.pt[k] += pt_t1 - pt_t0;    \
-    pt_t0 = pt_t1;                                   \
-  } while (0)
-#else
-#define PT_START() \
-  do {             \
-  } while (0)
-#define PT_MARK(k) \
-  do {             \
-  } while (0)
-#endif
 
 // LLT of r.DM (lower, column-major), blocked left-looking; same per-element
 // operation sequence as the right-looking reference (optim.cpp:11-15).
@@ -1379,7 +1495,7 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
   for (int c = 0, e = 0; c < CB; ++c)
     for (int rr = c; rr < CB; ++rr, ++e)
       if (e % NT == r.tid) rss.pk32[e] = (short)(rr | (c << 8));
-  if (r.tid < 16) rss.pt[r.tid] = 0;
+  if (r.tid < 20) rss.pt[r.tid] = 0;
   __syncthreads();
   int* const ivp = iws + e;
   auto iv = [&](int slot) -> int& { return ivp[(long)slot * B]; };
@@ -1502,9 +1618,9 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSche
 #if PBAD_PHASE_TIMING
   if (e == 0 && r.tid == 0)
     printf("phase cycles (block 0, %d iterations, %d accepted): conv %lld chol %lld solve %lld tpass %lld tres %lld "
-           "fpassres %lld jac %lld grad %lld gn %lld | chol: C %lld A %lld B %lld | diag-only %lld updA-only %lld\n",
+           "fpassres %lld jac %lld grad %lld gn %lld | chol: C %lld A %lld B %lld | diag-only %lld updA-only %lld | jac: acc %lld walks(t0) %lld fhess(t0)+sync %lld\n",
            S.iters, S.acc, rss.pt[0], rss.pt[1], rss.pt[2], rss.pt[3], rss.pt[4], rss.pt[5], rss.pt[6], rss.pt[7], rss.pt[8],
-           rss.pt[9], rss.pt[10], rss.pt[11], rss.pt[12], rss.pt[13]);
+           rss.pt[9], rss.pt[10], rss.pt[11], rss.pt[12], rss.pt[13], rss.pt[14], rss.pt[15], rss.pt[16]);
 #endif
 }
 
