@@ -581,29 +581,28 @@ __device__ __noinline__ void gradient(const R& r) {
 }
 
 // GN = 0.5 (2 J^T J + (2 J^T J)^T) = 2 J^T J, lower triangle (objective.cpp:328-330).
-// Double-buffered k-chunks: the next chunk's global loads are in flight while
-// the current one is multiplied out of shared memory.
-__device__ __forceinline__ void gn_load(const R& r, int a0, int b0, int k0, double (&pa)[GK * GB / NT],
-                                        double (&pb)[GK * GB / NT]) {
-  const int U = r.U;
-#pragma unroll
-  for (int q = 0; q < GK * GB / NT; ++q) {
-    const int t = r.tid + NT * q;
-    const int col = t / GK, kk = t - col * GK;
-    const int k = k0 + kk, a = a0 + col, b = b0 + col;
-    pa[q] = (k < U && a < U) ? 2.0 * r.J[k + (long)U * a] : 0.0;
-    pb[q] = (k < U && b < U) ? r.J[k + (long)U * b] : 0.0;
-  }
+// k-chunks of J land in shared memory by cp.async one chunk ahead of the
+// multiply (no register staging); each thread doubles its own A elements
+// (2 J exact) once its copies have arrived.
+__device__ __forceinline__ void gn_cpa8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
-__device__ __forceinline__ void gn_store(const R& r, double* As, double* Bs, const double (&pa)[GK * GB / NT],
-                                         const double (&pb)[GK * GB / NT]) {
+__device__ __forceinline__ void gn_issue(const R& r, int a0, int b0, int c) {
+  const int U = r.U;
+  double* As = rsm + (c & 1) * 2 * GK * GP;
+  double* Bs = As + GK * GP;
 #pragma unroll
   for (int q = 0; q < GK * GB / NT; ++q) {
     const int t = r.tid + NT * q;
     const int col = t / GK, kk = t - col * GK;
-    As[kk * GP + col] = pa[q];
-    Bs[kk * GP + col] = pb[q];
+    const int k = c * GK + kk, a = a0 + col, b = b0 + col;
+    if (k < U && a < U) gn_cpa8(As + kk * GP + col, r.J + k + (long)U * a);
+    else As[kk * GP + col] = 0.0;
+    if (k < U && b < U) gn_cpa8(Bs + kk * GP + col, r.J + k + (long)U * b);
+    else Bs[kk * GP + col] = 0.0;
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 __device__ __noinline__ void gauss_newton(const R& r) {
@@ -615,14 +614,24 @@ __device__ __noinline__ void gauss_newton(const R& r) {
     for (int bj = 0; bj <= bi; ++bj) {
       const int a0 = bi * GB, b0 = bj * GB;
       double acc[4][4];
-      double pa[GK * GB / NT], pb[GK * GB / NT];
-      gn_load(r, a0, b0, 0, pa, pb);
+      gn_issue(r, a0, b0, 0);
       for (int c = 0; c < nk; ++c) {
         double* As = rsm + (c & 1) * 2 * GK * GP;
         double* Bs = As + GK * GP;
-        gn_store(r, As, Bs, pa, pb);
+        __syncthreads();  // everyone is done with the buffer chunk c + 1 will overwrite
+        if (c + 1 < nk) {
+          gn_issue(r, a0, b0, c + 1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+#pragma unroll
+        for (int q = 0; q < GK * GB / NT; ++q) {
+          const int t = r.tid + NT * q;
+          const int col = t / GK, kk = t - col * GK;
+          As[kk * GP + col] = 2.0 * As[kk * GP + col];
+        }
         __syncthreads();
-        if (c + 1 < nk) gn_load(r, a0, b0, (c + 1) * GK, pa, pb);
         const int kc = min(GK, U - c * GK);
         int kk = 0;
         if (c == 0) {
@@ -666,8 +675,8 @@ __device__ __noinline__ void gauss_newton(const R& r) {
           const int a = a0 + ty + 16 * i, b = b0 + tx + 16 * j;
           if (a < U && b <= a) r.GN[a + (long)U * b] = 0.5 * (acc[i][j] + acc[i][j]);
         }
-      __syncthreads();
     }
+  __syncthreads();
 }
 
 

@@ -626,10 +626,11 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
     if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
     return;
   }
-  fk_world(w, h0);
-  store_history(w, w.hw0, w.T0);
-  fk_world(w, h1);
-  store_history(w, w.hw1, w.T1);
+#pragma unroll 1
+  for (int hs = 0; hs < 2; ++hs) {  // one inlined copy of the kinematics for both history configurations
+    fk_world(w, hs ? h1 : h0);
+    store_history(w, hs ? w.hw1 : w.hw0, hs ? w.T1 : w.T0);
+  }
   {
     for (int i = w.lane; i < w.N; i += 32) {
       const M4 w0 = ld16(w.hw0 + 16 * i), w1 = ld16(w.hw1 + 16 * i);
@@ -648,33 +649,120 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
     w.histconst = 4.0 * c11 + c00 - 4.0 * c10;
     __syncwarp();
   }
-  // solver construction (optim.cpp:82-93): first evaluation with GN
+  // solver construction (optim.cpp:82-93) and LmSolver::iterate (optim.cpp:95-134)
+  // share one loop body, so the kinematics / value / derivative code is inlined
+  // once (instruction-cache footprint): pass 0 evaluates x0 with the GN matrix,
+  // later passes solve the damped system and evaluate the candidate.
   Solver S;
   S.status = ST_RUNNING;
   S.iters = 0;
   S.stag = 0;
   S.acc = 0;
   S.lambda = sc.opt.lm_lambda0;
+  S.value = 0.0;
+  S.grad0 = 0.0;
   {
-    double v;
-    if (!full_eval(w, &v)) {
-      if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
+    const DOpt& o = sc.opt;
+    int err = 0;
+    bool first = true;
+#pragma unroll 1
+    for (;;) {
+      double* q = w.x;
+      bool do_eval = true;
+      if (!first) {
+        if (S.status != ST_RUNNING) break;
+        if (S.iters >= o.max_iters) {
+          S.status = ST_FAILED;
+          break;
+        }
+        if (grad_converged(w, S)) {
+          S.status = ST_CONVERGED;
+          break;
+        }
+        for (int t = w.lane; t < w.np; t += 32) {
+          const int rc = __ldg(w.td->pk + t);
+          const double g = w.gn[t];
+          w.damped[t] = ((rc & 0xffff) == (rc >> 16)) ? g + S.lambda : g;
+        }
+        double v[MAXV];
+#pragma unroll
+        for (int s = 0; s < MAXV; ++s) {
+          const int i = w.lane + 32 * s;
+          v[s] = i < n ? -w.grad[i] : 0.0;
+        }
+        __syncwarp();
+        bool finite = false;
+        if (llt_factor_w(w)) {
+          llt_solve_w(w, v);
+          bool fin = true;
+#pragma unroll
+          for (int s = 0; s < MAXV; ++s)
+            if (w.lane + 32 * s < n) fin = fin && isfinite(v[s]);
+          finite = __all_sync(FULL, fin);
+        }
+        if (finite) {
+#pragma unroll
+          for (int s = 0; s < MAXV; ++s) {
+            const int i = w.lane + 32 * s;
+            if (i < n) w.cand[i] = w.x[i] + v[s];
+          }
+          __syncwarp();
+          q = w.cand;
+        } else {
+          do_eval = false;
+        }
+      }
+      bool accepted = false;
+      if (do_eval) {
+        if (!fk_world(w, q)) {
+          err = TR_NONFINITE_CFG;
+          break;
+        }
+        const double tv = value_at(w, q);
+        bool take = false;
+        if (first) {
+          if (!isfinite(tv)) {
+            err = TR_NONFINITE_INIT;
+            break;
+          }
+          take = true;
+        } else {
+          take = isfinite(tv) && tv < S.value;
+        }
+        if (take) {
+          const double oldv = S.value;
+          if (!first) {
+            for (int i = w.lane; i < n; i += 32) w.x[i] = w.cand[i];
+            __syncwarp();
+          }
+          derivatives(w);
+          S.value = tv;  // evaluate(x) repeats value(cand) bit for bit
+          if (first) {
+            S.grad0 = infnorm_warp(w, w.grad);
+          } else {
+            S.lambda = fmax(S.lambda / o.lm_lambda_factor, 1e-12);
+            accepted = true;
+            ++S.acc;
+            if (oldv - tv <= o.ftol * fmax(1.0, fabs(oldv))) ++S.stag;
+            else S.stag = 0;
+            if (S.stag >= 2) S.status = ST_CONVERGED;
+          }
+        }
+      }
+      if (!first) {
+        if (!accepted) {
+          S.lambda *= o.lm_lambda_factor;
+          if (S.lambda > o.lm_lambda_max) S.status = ST_FAILED;
+        }
+        ++S.iters;
+        if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
+      }
+      first = false;
+    }
+    if (err) {
+      if (w.lane == 0) iv(IS_RUN) = err;
       return;
     }
-    if (!isfinite(v)) {
-      if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_INIT;
-      return;
-    }
-    S.value = v;
-    derivatives(w);
-    S.grad0 = infnorm_warp(w, w.grad);
-  }
-  int st;
-  while ((st = lm_iterate(w, S)) == ST_RUNNING) {
-  }
-  if (st < 0) {
-    if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
-    return;
   }
 
   // ---- finish_step (stepper.cpp:118-147) ----
