@@ -46,10 +46,16 @@ enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
 enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
 
 constexpr int kE = 8;   // environments per warp
-constexpr int kW = 2;   // warps per block
+#ifndef PBAD_C4_WARPS
+#define PBAD_C4_WARPS 2
+#endif
+#ifndef PBAD_C4_RING
+#define PBAD_C4_RING 3
+#endif
+constexpr int kW = PBAD_C4_WARPS;   // warps per block
 constexpr int kT = 32 * kW;
 constexpr int CL = 8;   // links per chunk
-constexpr int kRing = 3;
+constexpr int kRing = PBAD_C4_RING;
 constexpr int kMaxMem = 16;
 constexpr long kGS = 32;  // vector group stride (doubles)
 constexpr int kU = 8;     // vector-loop unroll
