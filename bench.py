@@ -41,6 +41,9 @@ CONFIGS = {
                desc="C3: 4096 x 200-DOF serial hinge chains (make_chain_scene(100)), L-BFGS, dt=0.1"),
     "C4": dict(scene="humanoid", links=18, dt=0.01, batch=4096, opt="lm", seed=2, lo=-0.1, hi=0.1,
                desc="C4: 4096 x 41-DOF humanoid trees, LM (Gauss-Newton + Cholesky), dt=0.01"),
+    "C4b": dict(scene="humanoid_contact", links=18, dt=0.01, batch=4096, opt="lm", seed=2, lo=-0.1, hi=0.1,
+                desc="C4b: 4096 x 41-DOF humanoid trees with ground contact (plane z=0, D1=2e4, D2=2e2), LM, "
+                     "dt=0.01"),
     "C5": dict(scene="single_hinge", links=100, dt=0.01, batch=256, opt="lm", seed=3, lo=-0.3, hi=0.3, order=4,
                objective="residual",
                desc="C5: high-order collocation PBAD (K=4 residual form, U=300), 100-link chains, LM, dt=0.01, "
@@ -54,14 +57,18 @@ def build_scene(cfg):
         return scenes.make_chain_scene(cfg["links"])
     if cfg["scene"] == "single_hinge":
         return scenes.make_single_hinge_chain_scene(cfg["links"])
-    return scenes.make_humanoid_scene()
+    sc = scenes.make_humanoid_scene()
+    if cfg["scene"] == "humanoid_contact":
+        from paper_1709_04145_b200.types import ContactModel
+        sc.contact = ContactModel(plane_normal=(0.0, 0.0, 1.0), plane_offset=0.0, d1=2e4, d2=2e2)
+    return sc
 
 
 def initial_states(cfg, scene, n, first_env, count):
     """std::mt19937(seed) env-major draws (benchmark.cpp:278-288) for envs
     [first_env, first_env + count) of the global batch."""
     from paper_1709_04145_b200.scenes import mt19937_uniform
-    if cfg["scene"] == "humanoid":
+    if cfg["scene"].startswith("humanoid"):
         draws = mt19937_uniform(cfg["seed"], (first_env + count) * (n - 6), cfg["lo"], cfg["hi"])
         q = np.tile(scene.q0, (count, 1))
         q[:, 6:] = draws[first_env * (n - 6):].reshape(count, n - 6)

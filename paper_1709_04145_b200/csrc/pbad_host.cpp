@@ -607,13 +607,12 @@ bool chain_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
 }
 
 // The tree kernel covers any tree with the energy form and LM (Newton):
-// gravity / constant or sinusoidal actuation (no drag or contact yet).
+// gravity, drag, ground contact, constant or sinusoidal actuation.
 bool tree_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2 || sim->opt.kind != PBAD_LM) return false;
-  if (f->drag_d > 0.0) return false;
-  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
   if (!tree_eligible_sizes(m.N, m.n)) return false;
+  if (m.sample_off[m.N] > 1024) return false;
   for (int i = 0; i < m.N; ++i)
     if (m.dof_cnt[i] > 6) return false;
   return true;
@@ -908,7 +907,12 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     td.o_t0 = np2 + 2 * N16;
     td.o_t1 = np2 + 3 * N16;
     td.o_gs = np2 + 4 * N16;
-    td.gstride = td.o_gs + 4 * 18L * m.N;
+    td.pot = (f->drag_d > 0.0 || (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0))) ? 1 : 0;
+    td.ns = (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) ? m.sample_off[m.N] : 0;
+    td.o_abl = td.o_gs + 4 * 18L * m.N;
+    td.o_abu = td.o_abl + (td.pot ? np2 : 0);
+    td.o_cs = td.o_abu + (td.pot ? np2 : 0);
+    td.gstride = td.o_cs + 4L * m.n * td.ns;
     td.smem_doubles = (int)(tree_smem_bytes(td) / sizeof(double));
     if (tree_smem_bytes(td) > 200 * 1024) c->tree = false;
   }

@@ -129,6 +129,11 @@ struct TreeDesc {
   long gstride;            // per-env doubles of tws
   long o_hw0, o_hw1, o_t0, o_t1;  // offsets inside one env's tws block (GN at 0)
   long o_gs;                      // GN composite-inertia scratch [4][N][18] (PBAD_TREE_GN_GLOBAL)
+  // drag / contact potentials (objective.cpp:60-131)
+  int pot;                        // 1: drag and/or contact present (slow GN path)
+  int ns;                         // total contact samples (0 without contact)
+  long o_abl, o_abu;              // packed ab(col,row) / ab(row,col) [np] (pot path)
+  long o_cs;                      // contact sample scratch [ns][4n]: dd (n), jr (3n)
 };
 
 // Residual-form path (pbad_resid.cu): CTA-per-environment LM for hinge

@@ -144,6 +144,13 @@ struct W {
   double *x, *grad, *cand, *vtau, *vtmp;
   // global, this environment's block
   double *gn, *hw0, *hw1, *T0, *T1, *gs;
+  // potentials: drag scale, contact flags / per-sample scratch
+  bool drag, contact;
+  double scl;                 // drag_d / dt^2
+  double* ctv;                // [ns] contact value term of each sample (shared)
+  int* cact;                  // [ns] sample active at the evaluated configuration (shared)
+  double* cdep;               // [ns][4]: depth, pv0..pv2 (shared)
+  double *abl, *abu, *cs;     // global: packed ab(col,row), ab(row,col); sample dd / jr
   __device__ __forceinline__ double* scr_k(int k) const { return scr + (long)k * MS * N; }
 };
 
@@ -236,6 +243,52 @@ __device__ TREE_COLD void fk_levers(const W& w, const double* q) {
   __syncwarp();
 }
 
+
+// contact sample s of link i at the configuration in w.world (objective.cpp:74-101):
+// active flag, value term, depth and projected velocity
+__device__ __forceinline__ void contact_sample(const W& w, int i, int sidx) {
+  const DModel& m = *w.m;
+  const DForces& f = *w.f;
+  const double* nrm = f.normal;
+  const M4 wi = ld16(w.world + MS * i);
+  const double ph[4] = {m.samples[3 * sidx], m.samples[3 * sidx + 1], m.samples[3 * sidx + 2], 1.0};
+  double x4[4], xp4[4];
+  mul_vec4(wi, ph, x4);
+  const double depth = f.plane_offset - dot3(nrm, x4);
+  if (depth <= 0.0) {
+    w.cact[sidx] = 0;
+    return;
+  }
+  const double dt = w.sc->dt;
+  mul_vec4(ld16(w.hw1 + 16 * i), ph, xp4);
+  double proj[9];
+  for (int c = 0; c < 3; ++c)
+    for (int r = 0; r < 3; ++r) proj[r + 3 * c] = ((r == c) ? 1.0 : 0.0) - nrm[r] * nrm[c];
+  double v[3], pv[3];
+  for (int k = 0; k < 3; ++k) v[k] = (x4[k] - xp4[k]) / dt;
+  for (int r = 0; r < 3; ++r) {
+    double acc = proj[r] * v[0];
+    acc = fma(proj[r + 3], v[1], acc);
+    acc = fma(proj[r + 6], v[2], acc);
+    pv[r] = acc;
+  }
+  const double pv2 = dot3(pv, pv);
+  w.cact[sidx] = 1;
+  w.ctv[sidx] = f.d1 * depth * depth + f.d2 * depth * depth * pv2;
+  w.cdep[4 * sidx] = depth;
+  w.cdep[4 * sidx + 1] = pv[0];
+  w.cdep[4 * sidx + 2] = pv[1];
+  w.cdep[4 * sidx + 3] = pv[2];
+}
+// all samples, lane-parallel; then the drag / contact part of pot.value in
+// the reference order (gravity over links, drag over links, contact samples)
+__device__ __forceinline__ void contact_all(const W& w) {
+  const DModel& m = *w.m;
+  for (int i = 0; i < w.N; ++i)
+    for (int sidx = m.sample_off[i] + w.lane; sidx < m.sample_off[i + 1]; sidx += 32) contact_sample(w, i, sidx);
+  __syncwarp();
+}
+
 // StepObjective energy value (objective.cpp:215-226, 237) at the configuration
 // whose world transforms are in w.world; q is that configuration.
 __device__ TREE_NOINLINE double value_at(const W& w, const double* q) {
@@ -247,15 +300,29 @@ __device__ TREE_NOINLINE double value_at(const W& w, const double* q) {
     w.red[4 * i + 1] = ddot(ld16(w.T1 + 16 * i), wi);
     w.red[4 * i + 2] = ddot(ld16(w.T0 + 16 * i), wi);
     if (w.grav) w.red[4 * i + 3] = ddot(gravity_cot(*w.f, S), wi);
+    if (w.drag) {
+      const M4 diff = sub(wi, ld16(w.hw1 + 16 * i));
+      w.red[4 * w.N + i] = w.scl * ddot(mul(diff, S), diff);
+    }
   }
+  if (w.contact) contact_all(w);
   __syncwarp();
   double s = 0.0;
-  if (w.lane < 4)
-    for (int i = 0; i < w.N; ++i) s += w.red[4 * i + w.lane];
+  if (w.lane < 4) {
+    if (w.lane < 3 || w.grav)
+      for (int i = 0; i < w.N; ++i) s += w.red[4 * i + w.lane];
+    if (w.lane == 3) {
+      if (w.drag)
+        for (int i = 0; i < w.N; ++i) s += w.red[4 * w.N + i];
+      if (w.contact)
+        for (int k = 0; k < w.td->ns; ++k)
+          if (w.cact[k]) s += w.ctv[k];
+    }
+  }
   const double cpp = __shfl_sync(FULL, s, 0) - m.weighted_mass;
   const double c1 = __shfl_sync(FULL, s, 1) - m.weighted_mass;
   const double c0 = __shfl_sync(FULL, s, 2) - m.weighted_mass;
-  const double pot = w.grav ? __shfl_sync(FULL, s, 3) : 0.0;
+  const double pot = (w.grav || w.drag || w.contact) ? __shfl_sync(FULL, s, 3) : 0.0;
   const double inertial = 0.5 * w.inv_dt2 * (cpp - 4.0 * c1 + 2.0 * c0 + w.histconst);
   const double tdot = vdot_warp(w, w.vtau, q);
   return inertial + pot - tdot;
@@ -274,10 +341,46 @@ __device__ TREE_NOINLINE void gradient(const W& w, double* g) {
     d = add(d, ld16(w.hw0 + 16 * i));
     d = scale(w.inv_dt2, d);
     st16(sA + MS * i, mul(d, S));
-    if (w.grav) st16(sB + MS * i, add(m4_zero(), gravity_cot(*w.f, S)));
+    if (w.grav || w.drag || w.contact) {
+      M4 cot = m4_zero();
+      if (w.grav) cot = add(cot, gravity_cot(*w.f, S));
+      if (w.drag) {
+        const M4 diff = sub(ld16(w.world + MS * i), ld16(w.hw1 + 16 * i));
+        cot = add(cot, scale(2.0 * w.scl, mul(diff, S)));
+      }
+      if (w.contact) {
+        const DForces& f = *w.f;
+        const double dtc = w.sc->dt;
+        for (int sidx = m.sample_off[i]; sidx < m.sample_off[i + 1]; ++sidx) {
+          if (!w.cact[sidx]) continue;
+          const double depth = w.cdep[4 * sidx];
+          const double pv[3] = {w.cdep[4 * sidx + 1], w.cdep[4 * sidx + 2], w.cdep[4 * sidx + 3]};
+          const double pv2 = dot3(pv, pv);
+          const double a = -2.0 * f.d1 * depth - 2.0 * f.d2 * depth * pv2;
+          const double b = 2.0 * f.d2 * depth * depth / dtc;
+          double dq[4];
+          for (int k = 0; k < 3; ++k) dq[k] = a * f.normal[k] + b * pv[k];
+          dq[3] = 0.0;
+          const double ph[4] = {m.samples[3 * sidx], m.samples[3 * sidx + 1], m.samples[3 * sidx + 2], 1.0};
+          M4 oc;
+          for (int c = 0; c < 4; ++c)
+            for (int r = 0; r < 4; ++r) oc.a[r + 4 * c] = dq[r] * ph[c];
+          cot = add(cot, oc);
+        }
+      }
+      st16(sB + MS * i, cot);
+    }
   }
   __syncwarp();
-  const int nsw = w.grav ? 2 : 1;
+  // the potential sweep runs when the reference builds a cotangent
+  // (objective.cpp:132-137: gravity, drag, or an active contact sample)
+  bool have_cot = w.grav || w.drag;
+  if (!have_cot && w.contact) {
+    bool any = false;
+    for (int k = w.lane; k < w.td->ns; k += 32) any = any || w.cact[k];
+    have_cot = __any_sync(FULL, any);
+  }
+  const int nsw = have_cot ? 2 : 1;
   for (int d = w.D; d >= 0; --d) {
     const int l0 = td.lvl_start[d], cnt = td.lvl_start[d + 1] - l0;
     for (int t = w.lane; t < nsw * cnt; t += 32) {
@@ -294,7 +397,7 @@ __device__ TREE_NOINLINE void gradient(const W& w, double* g) {
     }
     __syncwarp();
   }
-  for (int k = w.lane; k < w.n; k += 32) g[k] = (g[k] + (w.grav ? w.vtmp[k] : 0.0)) - w.vtau[k];
+  for (int k = w.lane; k < w.n; k += 32) g[k] = (g[k] + (have_cot ? w.vtmp[k] : 0.0)) - w.vtau[k];
   __syncwarp();
 }
 
@@ -330,7 +433,14 @@ __device__ TREE_COLD void gn_assemble(const W& w) {
     }
     __syncwarp();
   }
-  for (int t = w.lane; t < w.np; t += 32) w.gn[t] = 0.0;
+  for (int t = w.lane; t < w.np; t += 32) {
+    if (w.drag || w.contact) {
+      w.abl[t] = 0.0;
+      w.abu[t] = 0.0;
+    } else {
+      w.gn[t] = 0.0;
+    }
+  }
   __syncwarp();
   const int n = w.n;
   for (int s = 0; s <= w.D; ++s) {
@@ -339,25 +449,30 @@ __device__ TREE_COLD void gn_assemble(const W& w) {
       const int i = code & 255, l = (code >> 8) & 255, j = (code >> 16) & 15, k = (code >> 20) & 15;
       const int offi = m.dof_off[i], offl = m.dof_off[l];
       const M4 M = mul_at(ld16(w.lever + MS * (offi + j)), ld16(w.lever + MS * (offl + k)));
-      double grc, gcr;
+      double a1, a2;  // ab(col, row), ab(row, col)
       int row, col;
       if (s == 0) {
         const M4 F = ld16(ai + MS * i);
         const double tjk = trace_mul(M, F);
-        const double tkj = (j == k) ? tjk : trace_tmul(M, F);
-        grc = w.inv_dt2 * tjk + 0.0;
-        gcr = w.inv_dt2 * tkj + 0.0;
+        a1 = tjk;
+        a2 = (j == k) ? tjk : trace_tmul(M, F);
         row = offi + k;
         col = offi + j;
       } else {
-        const double t1 = trace_mul(M, ld16(fwd + MS * i));
-        const double t2 = trace_tmul(M, ld16(bwd + MS * i));
-        grc = w.inv_dt2 * t2 + 0.0;
-        gcr = w.inv_dt2 * t1 + 0.0;
+        a1 = trace_tmul(M, ld16(bwd + MS * i));
+        a2 = trace_mul(M, ld16(fwd + MS * i));
         row = offi + j;
         col = offl + k;
       }
-      w.gn[pidx(n, row, col)] = 0.5 * (grc + gcr);
+      const int e = pidx(n, row, col);
+      if (w.drag || w.contact) {
+        w.abl[e] = 0.0 + a1;
+        w.abu[e] = 0.0 + a2;
+      } else {
+        const double grc = w.inv_dt2 * a1 + 0.0;
+        const double gcr = w.inv_dt2 * a2 + 0.0;
+        w.gn[e] = 0.5 * (grc + gcr);
+      }
     }
     __syncwarp();
     if (s >= 1 && s < w.D) {
@@ -370,6 +485,90 @@ __device__ TREE_COLD void gn_assemble(const W& w) {
       __syncwarp();
     }
   }
+  if (!(w.drag || w.contact)) return;
+  __syncwarp();
+  // contact Jacobian rows of the samples active at x (objective.cpp:103-129):
+  // dd = -n^T jx, jr = pv dd^T + (depth/dt) P jx, one lane per sample
+  const DForces& f = *w.f;
+  if (w.contact) {
+    const double* nrm = f.normal;
+    double proj[9];
+    for (int c = 0; c < 3; ++c)
+      for (int r = 0; r < 3; ++r) proj[r + 3 * c] = ((r == c) ? 1.0 : 0.0) - nrm[r] * nrm[c];
+    for (int i = 0; i < w.N; ++i)
+      for (int sidx = m.sample_off[i] + w.lane; sidx < m.sample_off[i + 1]; sidx += 32) {
+        if (!w.cact[sidx]) continue;
+        double* dd = w.cs + (long)sidx * 4 * n;
+        double* jr = dd + n;  // holds jx first
+        for (int k = 0; k < 3 * n; ++k) jr[k] = 0.0;
+        double y[4] = {m.samples[3 * sidx], m.samples[3 * sidx + 1], m.samples[3 * sidx + 2], 1.0};
+        for (int l = i; l >= 0; l = m.parent[l]) {
+          const int off = m.dof_off[l];
+          for (int j = 0; j < m.dof_cnt[l]; ++j) {
+            double t4[4];
+            mul_vec4(ld16(w.lever + MS * (off + j)), y, t4);
+            for (int r = 0; r < 3; ++r) jr[r + 3 * (off + j)] = t4[r];
+          }
+          double y2[4];
+          mul_vec4(ld16(w.value + MS * l), y, y2);
+          for (int r = 0; r < 4; ++r) y[r] = y2[r];
+        }
+        for (int k = 0; k < n; ++k) {
+          double acc = nrm[0] * jr[3 * k];
+          acc = fma(nrm[1], jr[1 + 3 * k], acc);
+          acc = fma(nrm[2], jr[2 + 3 * k], acc);
+          dd[k] = -acc;
+        }
+        if (f.d2 > 0.0) {
+          const double ddt = w.cdep[4 * sidx] / w.sc->dt;
+          const double pv[3] = {w.cdep[4 * sidx + 1], w.cdep[4 * sidx + 2], w.cdep[4 * sidx + 3]};
+          for (int k = 0; k < n; ++k) {
+            double tmp[3];
+            for (int r = 0; r < 3; ++r) {
+              double acc = proj[r] * jr[3 * k];
+              acc = fma(proj[r + 3], jr[1 + 3 * k], acc);
+              acc = fma(proj[r + 6], jr[2 + 3 * k], acc);
+              tmp[r] = acc;
+            }
+            for (int r = 0; r < 3; ++r) jr[r + 3 * k] = pv[r] * dd[k] + ddt * tmp[r];
+          }
+        }
+      }
+  }
+  __syncwarp();
+  // gn = sym(inv_dt2 ab + pot.gn), pot.gn = 2 scl ab (drag) + contact terms in
+  // sample order (objective.cpp:69-70, 111-126, 249-254)
+  const double s2 = 2.0 * w.scl;
+  const double c2 = 2.0 * f.d1, c3 = 2.0 * f.d2;
+  for (int t = w.lane; t < w.np; t += 32) {
+    const int rc = __ldg(td.pk + t);
+    const int row = rc & 0xffff, col = rc >> 16;
+    const double a1 = w.abl[t], a2 = w.abu[t];
+    double p1 = w.drag ? 0.0 + s2 * a1 : 0.0;  // pot.gn(col, row)
+    double p2 = w.drag ? 0.0 + s2 * a2 : 0.0;  // pot.gn(row, col)
+    if (w.contact)
+      for (int k = 0; k < td.ns; ++k) {
+        if (!w.cact[k]) continue;
+        const double* dd = w.cs + (long)k * 4 * n;
+        const double* jr = dd + n;
+        p1 = p1 + (c2 * dd[col]) * dd[row];
+        p2 = p2 + (c2 * dd[row]) * dd[col];
+        if (f.d2 > 0.0) {
+          double q1 = (c3 * jr[3 * col]) * jr[3 * row];
+          q1 = fma(c3 * jr[1 + 3 * col], jr[1 + 3 * row], q1);
+          q1 = fma(c3 * jr[2 + 3 * col], jr[2 + 3 * row], q1);
+          double q2 = (c3 * jr[3 * row]) * jr[3 * col];
+          q2 = fma(c3 * jr[1 + 3 * row], jr[1 + 3 * col], q2);
+          q2 = fma(c3 * jr[2 + 3 * row], jr[2 + 3 * col], q2);
+          p1 = p1 + q1;
+          p2 = p2 + q2;
+        }
+      }
+    const double grc = w.inv_dt2 * a1 + p1;
+    const double gcr = w.inv_dt2 * a2 + p2;
+    w.gn[t] = 0.5 * (grc + gcr);
+  }
+  __syncwarp();
 }
 
 // LLT (optim.cpp:11-15, eigen_lite right-looking) on the lower-packed damped
@@ -559,6 +758,7 @@ __device__ TREE_COLD void store_history(const W& w, double* hw, double* T) {
   __syncwarp();
 }
 
+template <bool POT>
 __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
                                                   int* iws, long B, TreeDesc td, double* tws, Outputs out) {
   extern __shared__ __align__(16) double smem[];
@@ -578,6 +778,10 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
   w.grav = f.gravity_nonzero != 0;
   const double dt = sc.dt;
   w.inv_dt2 = 1.0 / (dt * dt);
+  // POT = false compiles the drag / contact code out (lean fast path)
+  w.drag = POT && f.drag_d > 0.0;
+  w.scl = w.drag ? f.drag_d / (dt * dt) : 0.0;
+  w.contact = POT && f.has_contact && (f.d1 > 0.0 || f.d2 > 0.0) && td.ns > 0;
   {
     const int N16 = MS * td.N, nv = (td.n + 1) & ~1;
     const int scr = (TREE_SCR_ARRAYS * N16 > MS * td.n) ? TREE_SCR_ARRAYS * N16 : MS * td.n;
@@ -592,7 +796,10 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
     w.cand = p; p += nv;
     w.vtau = p; p += nv;
     w.vtmp = p; p += nv;
-    w.red = p;
+    w.red = p; p += 5 * td.N + 32;
+    w.ctv = p; p += (td.ns + 1) & ~1;
+    w.cdep = p; p += 4 * td.ns;
+    w.cact = reinterpret_cast<int*>(p);
     double* g = tws + e * td.gstride;
     w.gn = g;
     w.hw0 = g + td.o_hw0;
@@ -600,6 +807,9 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
     w.T0 = g + td.o_t0;
     w.T1 = g + td.o_t1;
     w.gs = g + td.o_gs;
+    w.abl = g + td.o_abl;
+    w.abu = g + td.o_abu;
+    w.cs = g + td.o_cs;
   }
   const int n = td.n;
   int* const ivp = iws + e;
@@ -836,7 +1046,8 @@ bool tree_eligible_sizes(int N, int n) { return N >= 1 && N <= 255 && n >= 1 && 
 static int tree_smem_doubles(const TreeDesc& td) {
   const int N16 = tree::MS * td.N, nv = (td.n + 1) & ~1;
   const int scr = (tree::TREE_SCR_ARRAYS * N16 > tree::MS * td.n) ? tree::TREE_SCR_ARRAYS * N16 : tree::MS * td.n;
-  return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 5 * nv + 4 * td.N + 32;
+  return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 5 * nv + 5 * td.N + 32 + ((td.ns + 1) & ~1) +
+         4 * td.ns + (td.ns + 1) / 2 + 2;
 }
 
 size_t tree_smem_bytes(const TreeDesc& td) { return sizeof(double) * (size_t)tree_smem_doubles(td); }
@@ -844,13 +1055,16 @@ size_t tree_smem_bytes(const TreeDesc& td) { return sizeof(double) * (size_t)tre
 cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
                              cudaStream_t s) {
   const size_t smem = tree_smem_bytes(td);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(tree::k_tree_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t configured[2] = {0, 0};
+  const int pot = td.pot ? 1 : 0;
+  if (smem > 48 * 1024 && smem > configured[pot]) {
+    cudaError_t e = pot ? cudaFuncSetAttribute(tree::k_tree_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                        : cudaFuncSetAttribute(tree::k_tree_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured[pot] = smem;
   }
-  tree::k_tree_step<<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
+  if (pot) tree::k_tree_step<true><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
+  else tree::k_tree_step<false><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
   return cudaGetLastError();
 }
 

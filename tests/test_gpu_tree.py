@@ -140,3 +140,74 @@ def test_tree_path_equals_general_kernel(monkeypatch):
         np.testing.assert_array_equal(np.array([s[1] for s in x.samples]), np.array([s[1] for s in y.samples]))
         assert [r.iterations for r in x.solve_reports] == [r.iterations for r in y.solve_reports]
         assert [r.final_value for r in x.solve_reports] == [r.final_value for r in y.solve_reports]
+
+
+# --- potentials on the tree path: drag and ground contact (objective.cpp:60-131) ---
+
+def _humanoid_contact():
+    from paper_1709_04145_b200.types import ContactModel
+    sc = make_humanoid_scene()
+    sc.contact = ContactModel(plane_normal=(0.0, 0.0, 1.0), plane_offset=0.0, d1=2e4, d2=2e2)
+    return sc
+
+
+def test_tree_path_humanoid_contact_c4b():
+    """C4b: the humanoid dropped onto the ground plane (pelvis lowered so the
+    feet are in contact from the first step)."""
+    sc = _humanoid_contact()
+    sim = SimConfig(dt=0.01, duration=0.06)
+    n = 41
+
+    def q0(b):
+        q = sc.q0.copy()
+        q[2] = 0.9
+        q[6:] = mt19937_uniform(60 + b, n - 6, -0.1, 0.1)
+        return q
+    _check(sc, sim, _sims(sim, n, 4, q0))
+
+
+@pytest.mark.parametrize("seed", [51, 52])
+def test_tree_path_drag_contact_random_trees(seed):
+    from paper_1709_04145_b200.types import ContactModel
+    rng = np.random.default_rng(seed)
+    links = random_tree(rng, 6)
+    sc = Scene(links=links, gravity=(0.2, -0.5, -9.81), drag_d=0.8,
+               contact=ContactModel(plane_normal=(0.0, 0.3, 0.95), plane_offset=0.4, d1=5e3, d2=50.0))
+    m = api.build_model(links)
+    n = m.total_dofs
+    sc.q0 = np.zeros(n)
+    sc.qdot0 = np.zeros(n)
+    sim = SimConfig(dt=0.02, duration=0.08)
+    _check(sc, sim, _sims(sim, n, 3, lambda b: rng.uniform(-0.5, 0.5, n)))
+
+
+def test_tree_path_drag_only_zero_gravity():
+    rng = np.random.default_rng(7)
+    links = random_tree(rng, 5)
+    sc = Scene(links=links, gravity=(0.0, 0.0, 0.0), drag_d=2.0)
+    m = api.build_model(links)
+    n = m.total_dofs
+    sc.q0 = np.zeros(n)
+    sc.qdot0 = np.zeros(n)
+    sim = SimConfig(dt=0.02, duration=0.06)
+    _check(sc, sim, _sims(sim, n, 2, lambda b: rng.uniform(-0.4, 0.4, n)))
+
+
+def test_tree_path_contact_equals_general_kernel(monkeypatch):
+    sc = _humanoid_contact()
+    sim = SimConfig(dt=0.01, duration=0.03)
+    n = 41
+    m = api.build_model(sc.links)
+
+    def q0(b):
+        q = sc.q0.copy()
+        q[2] = 0.85
+        q[6:] = mt19937_uniform(80 + b, n - 6, -0.1, 0.1)
+        return q
+    sims = _sims(sim, n, 9, q0)
+    a = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.setenv("PBAD_GPU_FORCE_GENERAL", "1")
+    b = api.batch_simulate(m, sc.forces(), sims)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(np.array([s[1] for s in x.samples]), np.array([s[1] for s in y.samples]))
+        assert [r.iterations for r in x.solve_reports] == [r.iterations for r in y.solve_reports]
