@@ -253,6 +253,21 @@ __device__ __noinline__ bool passes(const R& r, const double* xs, bool want_d2) 
   return true;
 }
 
+// second joint derivatives of the u configurations (joint_jet d2, kinematics.cpp:119-169);
+// the rest of the pass is already current
+__device__ __noinline__ void passes_d2(const R& r, const double* xs) {
+  const DModel& m = *r.m;
+  const int N = r.N;
+  for (int t = r.tid; t < r.u * N; t += NT) {
+    const int mm = t / N, i = t - mm * N;
+    const double q = xs[mm * r.n + i];
+    M4 v, d1, d2;
+    joint_jet(0, m.axis + 3 * i, ldgm4(m.offset + 16 * i), &q, &v, &d1, &d2, true);
+    stm4(r.dd2(mm) + 16 * i, d2);
+  }
+  __syncthreads();
+}
+
 // stage the u passes' values and levers into shared memory
 __device__ void stage_vl(const R& r, double* Vs, double* Ls) {
   const int N8 = 8 * r.N;  // double2 per pass
@@ -1415,8 +1430,22 @@ __device__ int lm_iterate(const R& r, Solver& S) {
       const double oldv = S.value;
       for (int t = r.tid; t < U; t += NT) r.x[t] = r.cand[t];
       __syncthreads();
-      double nv;
-      if (full_eval(r, &nv) == TR_NONFINITE_CFG) return -1;
+      // evaluate(x) at the accepted candidate: its passes, residuals and
+      // adjoint sums are the trial's (same configuration, same operations),
+      // only the second joint derivatives are new
+      const double nv = tv;
+      {
+        PT_START();
+        passes_d2(r, r.x);
+        PT_MARK(5);
+        jacobian(r);
+        PT_MARK(6);
+        gradient(r);
+        __syncthreads();
+        PT_MARK(7);
+        gauss_newton(r);
+        PT_MARK(8);
+      }
       S.value = nv;
       S.lambda = fmax(S.lambda / o.lm_lambda_factor, 1e-12);
       accepted = true;
