@@ -782,7 +782,11 @@ struct Solver {
   int status, iters, stag, acc, h0, hc, trial, phase;
 };
 
-constexpr int kB = 16;  // groups per batch of loads
+#ifndef PBAD_C4_KB
+#define PBAD_C4_KB 16
+#endif
+constexpr int kB = PBAD_C4_KB;  // groups per batch of loads (multiple of 8: dot partial index)
+static_assert(kB % 8 == 0, "batch must keep the 32-partial dot order");
 
 __device__ __forceinline__ bool elem_ok(const Ctx& C, int g) { return g < C.n4 && 4 * g + C.r < C.n; }
 template <int KB>

@@ -42,7 +42,11 @@ namespace resid {
 #ifndef PBAD_RESID_CHOL_REG
 #define PBAD_RESID_CHOL_REG 2  // 2: lookahead; 1: diagonal blocks and solve rows in registers (unrolled); 0: shared memory loops
 #endif
-constexpr int NT = 256;  // threads per environment
+#ifndef PBAD_RESID_NT
+#define PBAD_RESID_NT 256
+#endif
+constexpr int NT = PBAD_RESID_NT;  // threads per environment (256 or 512)
+constexpr int TG = NT / 256;       // concurrent J^T J tiles
 constexpr unsigned FULL = 0xffffffffu;
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
 enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
@@ -603,13 +607,13 @@ __device__ __forceinline__ void gn_cpa8(double* dst, const double* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
-__device__ __forceinline__ void gn_issue(const R& r, int a0, int b0, int c) {
+__device__ __forceinline__ void gn_issue(const R& r, double* buf, int lt, int a0, int b0, int c) {
   const int U = r.U;
-  double* As = rsm + (c & 1) * 2 * GK * GP;
+  double* As = buf + (c & 1) * 2 * GK * GP;
   double* Bs = As + GK * GP;
 #pragma unroll
-  for (int q = 0; q < GK * GB / NT; ++q) {
-    const int t = r.tid + NT * q;
+  for (int q = 0; q < GK * GB / 256; ++q) {
+    const int t = lt + 256 * q;
     const int col = t / GK, kk = t - col * GK;
     const int k = c * GK + kk, a = a0 + col, b = b0 + col;
     if (k < U && a < U) gn_cpa8(As + kk * GP + col, r.J + k + (long)U * a);
@@ -624,65 +628,77 @@ __device__ __noinline__ void gauss_newton(const R& r) {
   const int U = r.U;
   const int nb = (U + GB - 1) / GB;
   const int nk = (U + GK - 1) / GK;
-  const int tx = r.tid & 15, ty = r.tid >> 4;
-  for (int bi = 0; bi < nb; ++bi)
-    for (int bj = 0; bj <= bi; ++bj) {
-      const int a0 = bi * GB, b0 = bj * GB;
-      double acc[4][4];
-      gn_issue(r, a0, b0, 0);
-      for (int c = 0; c < nk; ++c) {
-        double* As = rsm + (c & 1) * 2 * GK * GP;
-        double* Bs = As + GK * GP;
-        __syncthreads();  // everyone is done with the buffer chunk c + 1 will overwrite
-        if (c + 1 < nk) {
-          gn_issue(r, a0, b0, c + 1);
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
+  const int ntile = nb * (nb + 1) / 2;
+  const int grp = r.tid >> 8, lt = r.tid & 255;  // TG groups of 256 threads, one tile each
+  const int tx = lt & 15, ty = lt >> 4;
+  double* buf = rsm + grp * 4 * GK * GP;
+  for (int t0 = 0; t0 < ntile; t0 += TG) {
+    // tile t0 + grp of the lower triangle (row-major over block rows)
+    int tile = t0 + grp, bi = 0;
+    const bool active = tile < ntile;
+    if (!active) tile = ntile - 1;
+    while (tile > bi) {
+      tile -= bi + 1;
+      ++bi;
+    }
+    const int bj = tile;
+    const int a0 = bi * GB, b0 = bj * GB;
+    double acc[4][4];
+    gn_issue(r, buf, lt, a0, b0, 0);
+    for (int c = 0; c < nk; ++c) {
+      double* As = buf + (c & 1) * 2 * GK * GP;
+      double* Bs = As + GK * GP;
+      __syncthreads();  // everyone is done with the buffer chunk c + 1 will overwrite
+      if (c + 1 < nk) {
+        gn_issue(r, buf, lt, a0, b0, c + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
 #pragma unroll
-        for (int q = 0; q < GK * GB / NT; ++q) {
-          const int t = r.tid + NT * q;
-          const int col = t / GK, kk = t - col * GK;
-          As[kk * GP + col] = 2.0 * As[kk * GP + col];
-        }
-        __syncthreads();
-        const int kc = min(GK, U - c * GK);
-        int kk = 0;
-        if (c == 0) {
+      for (int q = 0; q < GK * GB / 256; ++q) {
+        const int t = lt + 256 * q;
+        const int col = t / GK, kk = t - col * GK;
+        As[kk * GP + col] = 2.0 * As[kk * GP + col];
+      }
+      __syncthreads();
+      const int kc = min(GK, U - c * GK);
+      int kk = 0;
+      if (c == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = As[ty + 16 * i] * Bs[tx + 16 * j];
+        kk = 1;
+      }
+      if (kc == GK) {
+#pragma unroll 8
+        for (; kk < GK; ++kk) {
+          double av[4], bv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = As[ty + 16 * i] * Bs[tx + 16 * j];
-          kk = 1;
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
         }
-        if (kc == GK) {
-#pragma unroll 8
-          for (; kk < GK; ++kk) {
-            double av[4], bv[4];
+      } else {
+        for (; kk < kc; ++kk) {
+          double av[4], bv[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
+          for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
+          for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-              for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-          }
-        } else {
-          for (; kk < kc; ++kk) {
-            double av[4], bv[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[kk * GP + ty + 16 * i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk * GP + tx + 16 * j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-          }
+            for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
         }
       }
+    }
+    if (active) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -691,6 +707,7 @@ __device__ __noinline__ void gauss_newton(const R& r) {
           if (a < U && b <= a) r.GN[a + (long)U * b] = 0.5 * (acc[i][j] + acc[i][j]);
         }
     }
+  }
   __syncthreads();
 }
 
@@ -879,12 +896,17 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
         if (bw == CB) {
 #pragma unroll
           for (int k = 0; k < CB; ++k) {
-            double col[CB];
+            a[k] = a[k] / lds_f64(ljs + 8u * (k * CS + k));
 #pragma unroll
-            for (int j = k; j < CB; ++j) col[j] = lds_f64(ljs + 8u * (j * CS + k));
-            a[k] = a[k] / col[k];
+            for (int j0c = k + 1; j0c < CB; j0c += 8) {  // column k in chunks of 8 (register budget)
+              double col[8];
 #pragma unroll
-            for (int j = k + 1; j < CB; ++j) a[j] = fma(-a[k], col[j], a[j]);
+              for (int q = 0; q < 8; ++q)
+                if (j0c + q < CB) col[q] = lds_f64(ljs + 8u * ((j0c + q) * CS + k));
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                if (j0c + q < CB) a[j0c + q] = fma(-a[k], col[q], a[j0c + q]);
+            }
           }
         } else {
           for (int k = 0; k < bw; ++k) {
@@ -1670,7 +1692,7 @@ bool resid_eligible_sizes(int N, int u) {
 
 size_t resid_smem_bytes(int N, int u) {
   const size_t N16 = resid::SMS * (size_t)N;
-  size_t b = 4 * resid::GK * resid::GP;                                   // J^T J tiles (double-buffered)
+  size_t b = resid::TG * 4 * resid::GK * resid::GP;                       // J^T J tiles (double-buffered, TG groups)
   b = std::max(b, (size_t)(resid::LK * resid::LP + resid::CB * (resid::CB + 1) + resid::MAXU * (resid::CB + 1)));  // Cholesky (smem variant)
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP));             // Cholesky update panel
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
