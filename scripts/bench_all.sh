@@ -2,7 +2,7 @@
 # Bench lines for every config (bench.py defaults per config), plus the ncu
 # launch list of the default bench command (C3).  Outputs in gpurun_out/.
 mkdir -p gpurun_out
-for c in C1 C2 C4 C5; do
+for c in C1 C2 C4 C4b C5; do
   timeout 600 python bench.py --config $c --steps ${STEPS:-3} --warmup 3 > gpurun_out/bench_all_$c.json 2> gpurun_out/bench_all_$c.err
 done
 timeout 900 python bench.py > gpurun_out/bench_all_C3.json 2> gpurun_out/bench_all_C3.err
