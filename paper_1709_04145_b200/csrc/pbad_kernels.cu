@@ -1100,28 +1100,31 @@ __global__ void __launch_bounds__(128) k_minimize(DModel m, DForces f, DSchedule
 
 namespace pbad_gpu {
 
-static inline unsigned grid_for(long B) { return (unsigned)((B + 127) / 128); }
+// one thread per environment: blocks of 32 until the batch fills every SM
+// with 128-thread blocks (a 4096 batch would otherwise occupy 32 SMs)
+static inline int block_for(long B) { return B >= 148L * 128 ? 128 : 32; }
+static inline unsigned grid_for(long B) { return (unsigned)((B + block_for(B) - 1) / block_for(B)); }
 
 cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
                         cudaStream_t s) {
-  k_init<<<grid_for(a.B), 128, 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, q0, qdot0, out);
+  k_init<<<grid_for(a.B), block_for(a.B), 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, q0, qdot0, out);
   return cudaGetLastError();
 }
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s) {
-  k_step<<<grid_for(a.B), 128, 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, out);
+  k_step<<<grid_for(a.B), block_for(a.B), 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, out);
   return cudaGetLastError();
 }
 cudaError_t launch_eval(const KernelArgs& a, const double* hist, const double* tau, const double* x,
                         int want_grad, int want_gn, double* value, double* grad, double* gn, int* err,
                         cudaStream_t s) {
-  k_eval<<<grid_for(a.B), 128, 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, hist, tau, x, want_grad,
+  k_eval<<<grid_for(a.B), block_for(a.B), 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, hist, tau, x, want_grad,
                                        want_gn, value, grad, gn, err);
   return cudaGetLastError();
 }
 cudaError_t launch_minimize(const KernelArgs& a, const double* hist, const double* tau, const double* x0,
                             double* xout, int* iters, int* conv, double* fval, double* gnorm, int* err,
                             cudaStream_t s) {
-  k_minimize<<<grid_for(a.B), 128, 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, hist, tau, x0, xout, iters,
+  k_minimize<<<grid_for(a.B), block_for(a.B), 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, hist, tau, x0, xout, iters,
                                            conv, fval, gnorm, err);
   return cudaGetLastError();
 }
