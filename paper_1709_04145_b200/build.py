@@ -25,7 +25,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
               "-Xptxas", "-v"]
-CUDA_SOURCES = ["pbad_kernels.cu", "pbad_chain.cu", "pbad_chain4.cu", "pbad_tree.cu", "pbad_resid.cu"]
+CUDA_SOURCES = ["pbad_kernels.cu", "pbad_chain.cu", "pbad_chain4.cu", "pbad_tree.cu", "pbad_tree_lbfgs.cu", "pbad_resid.cu"]
 HOST_SOURCES = ["pbad_host.cpp"]
 
 
@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if not os.path.exists(s):
                 continue
             o = os.path.join(BUILD, src + ".o")
-            if force or _stale(o, [s] + headers):
+            extra = [os.path.join(CSRC, "pbad_tree.cu")] if src == "pbad_tree_lbfgs.cu" else []
+            if force or _stale(o, [s] + headers + extra):
                 _run([NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o], log)
             objs.append(o)
         for src in HOST_SOURCES:

@@ -606,11 +606,13 @@ bool chain_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
   return true;
 }
 
-// The tree kernel covers any tree with the energy form and LM (Newton):
-// gravity, drag, ground contact, constant or sinusoidal actuation.
+// The tree kernel covers any tree with the energy form, LM (Newton) or
+// L-BFGS: gravity, drag, ground contact, constant or sinusoidal actuation
+// (serial hinge chains with L-BFGS go to the chain kernels first).
 bool tree_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
-  if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2 || sim->opt.kind != PBAD_LM) return false;
+  if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2) return false;
+  if (sim->opt.kind == PBAD_LBFGS && (sim->opt.lbfgs_memory < 1 || sim->opt.lbfgs_memory > 64)) return false;
   if (!tree_eligible_sizes(m.N, m.n)) return false;
   if (m.sample_off[m.N] > 1024) return false;
   for (int i = 0; i < m.N; ++i)
@@ -912,7 +914,13 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     td.o_abl = td.o_gs + 4 * 18L * m.N;
     td.o_abu = td.o_abl + (td.pot ? np2 : 0);
     td.o_cs = td.o_abu + (td.pot ? np2 : 0);
-    td.gstride = td.o_cs + 4L * m.n * td.ns;
+    td.lb = sim->opt.kind == PBAD_LBFGS ? 1 : 0;
+    const long cap = td.lb ? sim->opt.lbfgs_memory + 1 : 0;
+    td.o_hs = td.o_cs + 4L * m.n * td.ns;
+    td.o_hy = td.o_hs + ((cap * m.n + 1) & ~1L);
+    td.o_hsy = td.o_hy + ((cap * m.n + 1) & ~1L);
+    td.o_alpha = td.o_hsy + ((cap + 1) & ~1L);
+    td.gstride = td.o_alpha + ((cap + 1) & ~1L);
     td.smem_doubles = (int)(tree_smem_bytes(td) / sizeof(double));
     if (tree_smem_bytes(td) > 200 * 1024) c->tree = false;
   }

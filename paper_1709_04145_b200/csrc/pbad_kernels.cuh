@@ -134,6 +134,9 @@ struct TreeDesc {
   int ns;                         // total contact samples (0 without contact)
   long o_abl, o_abu;              // packed ab(col,row) / ab(row,col) [np] (pot path)
   long o_cs;                      // contact sample scratch [ns][4n]: dd (n), jr (3n)
+  // L-BFGS on trees (optim.cpp:141-232): s / y ring [(mem+1)][n], s.y and alpha [mem+1]
+  int lb;
+  long o_hs, o_hy, o_hsy, o_alpha;
 };
 
 // Residual-form path (pbad_resid.cu): CTA-per-environment LM for hinge

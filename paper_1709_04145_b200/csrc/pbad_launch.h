@@ -45,6 +45,10 @@ bool tree_eligible_sizes(int N, int n);
 size_t tree_smem_bytes(const TreeDesc& td);
 cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
                              cudaStream_t s);
+// L-BFGS on trees (pbad_tree_lbfgs.cu, same device code compiled as its own
+// translation unit so the LM kernel's register allocation is unaffected)
+cudaError_t launch_tree_lbfgs(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
+                              cudaStream_t s);
 
 // residual-form path (pbad_resid.cu): CTA-per-environment LM, hinge trees
 bool resid_eligible_sizes(int N, int u);

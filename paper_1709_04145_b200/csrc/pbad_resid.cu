@@ -1508,8 +1508,12 @@ __device__ __noinline__ void tau_at(const R& r, double t, double* dst) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_resid_step(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
-                                                      int* iws, long B, ResidDesc rd, double* rws, Outputs out) {
+__global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DModel m,
+                                                      const __grid_constant__ DForces f,
+                                                      const __grid_constant__ DSchedule sc,
+                                                      const __grid_constant__ Layout L, double* ws, int* iws, long B,
+                                                      const __grid_constant__ ResidDesc rd, double* rws,
+                                                      const __grid_constant__ Outputs out) {
   const long e = blockIdx.x;
   if (e >= B) return;
   if (iws[(long)IS_RUN * B + e] != TR_RUNNING) return;

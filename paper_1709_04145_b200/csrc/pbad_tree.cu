@@ -51,7 +51,14 @@
 #endif
 
 namespace pbad_gpu {
-namespace tree {
+// The L-BFGS translation unit (pbad_tree_lbfgs.cu) compiles this file again
+// under its own namespace so the device functions' host stubs do not collide.
+#ifdef PBAD_TREE_LBFGS_TU
+#define PBAD_TREE_NS tree_lbfgs
+#else
+#define PBAD_TREE_NS tree
+#endif
+namespace PBAD_TREE_NS {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAXV = 3;  // dof vectors in registers: n <= 96
@@ -142,6 +149,7 @@ struct W {
   // shared memory
   double *value, *world, *lever, *scr, *damped, *red;
   double *x, *grad, *cand, *vtau, *vtmp;
+  double *q2, *dir, *evg;     // L-BFGS two-loop vector, direction, candidate gradient
   // global, this environment's block
   double *gn, *hw0, *hw1, *T0, *T1, *gs;
   // potentials: drag scale, contact flags / per-sample scratch
@@ -246,7 +254,7 @@ __device__ TREE_COLD void fk_levers(const W& w, const double* q) {
 
 // contact sample s of link i at the configuration in w.world (objective.cpp:74-101):
 // active flag, value term, depth and projected velocity
-__device__ __forceinline__ void contact_sample(const W& w, int i, int sidx) {
+__device__ void contact_sample(const W& w, int i, int sidx) {
   const DModel& m = *w.m;
   const DForces& f = *w.f;
   const double* nrm = f.normal;
@@ -282,7 +290,7 @@ __device__ __forceinline__ void contact_sample(const W& w, int i, int sidx) {
 }
 // all samples, lane-parallel; then the drag / contact part of pot.value in
 // the reference order (gravity over links, drag over links, contact samples)
-__device__ __forceinline__ void contact_all(const W& w) {
+__device__ void contact_all(const W& w) {
   const DModel& m = *w.m;
   for (int i = 0; i < w.N; ++i)
     for (int sidx = m.sample_off[i] + w.lane; sidx < m.sample_off[i + 1]; sidx += 32) contact_sample(w, i, sidx);
@@ -758,9 +766,12 @@ __device__ TREE_COLD void store_history(const W& w, double* hw, double* T) {
   __syncwarp();
 }
 
+#ifndef PBAD_TREE_LBFGS_TU
 template <bool POT>
-__global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
-                                                  int* iws, long B, TreeDesc td, double* tws, Outputs out) {
+__global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel m, const __grid_constant__ DForces f,
+                                                  const __grid_constant__ DSchedule sc, const __grid_constant__ Layout L,
+                                                  double* ws, int* iws, long B, const __grid_constant__ TreeDesc td,
+                                                  double* tws, const __grid_constant__ Outputs out) {
   extern __shared__ __align__(16) double smem[];
   const long e = blockIdx.x;
   if (e >= B) return;
@@ -1039,14 +1050,331 @@ __global__ void __launch_bounds__(32) k_tree_step(DModel m, DForces f, DSchedule
   }
 }
 
-}  // namespace tree
+#else
+template <bool POT>
+__global__ void __launch_bounds__(32) k_tree_lbfgs(const __grid_constant__ DModel m, const __grid_constant__ DForces f,
+                                                  const __grid_constant__ DSchedule sc, const __grid_constant__ Layout L,
+                                                  double* ws, int* iws, long B, const __grid_constant__ TreeDesc td,
+                                                  double* tws, const __grid_constant__ Outputs out) {
+  extern __shared__ __align__(16) double smem[];
+  const long e = blockIdx.x;
+  if (e >= B) return;
+  if (iws[(long)IS_RUN * B + e] != TR_RUNNING) return;
+  W w;
+  w.m = &m;
+  w.f = &f;
+  w.sc = &sc;
+  w.td = &td;
+  w.lane = threadIdx.x;
+  w.N = td.N;
+  w.n = td.n;
+  w.D = td.D;
+  w.np = td.np;
+  w.grav = f.gravity_nonzero != 0;
+  const double dt = sc.dt;
+  w.inv_dt2 = 1.0 / (dt * dt);
+  // POT = false compiles the drag / contact code out (lean fast path)
+  w.drag = POT && f.drag_d > 0.0;
+  w.scl = w.drag ? f.drag_d / (dt * dt) : 0.0;
+  w.contact = POT && f.has_contact && (f.d1 > 0.0 || f.d2 > 0.0) && td.ns > 0;
+  {
+    const int N16 = MS * td.N, nv = (td.n + 1) & ~1;
+    const int scr = (TREE_SCR_ARRAYS * N16 > MS * td.n) ? TREE_SCR_ARRAYS * N16 : MS * td.n;
+    double* p = smem;
+    w.value = p; p += N16;
+    w.world = p; p += N16;
+    w.lever = p; p += MS * td.n;
+    w.scr = p; p += scr;
+    w.damped = p; p += (td.np + 1) & ~1;
+    w.x = p; p += nv;
+    w.grad = p; p += nv;
+    w.cand = p; p += nv;
+    w.vtau = p; p += nv;
+    w.vtmp = p; p += nv;
+    w.q2 = p; p += nv;
+    w.dir = p; p += nv;
+    w.evg = p; p += nv;
+    w.red = p; p += 5 * td.N + 32;
+    w.ctv = p; p += (td.ns + 1) & ~1;
+    w.cdep = p; p += 4 * td.ns;
+    w.cact = reinterpret_cast<int*>(p);
+    double* g = tws + e * td.gstride;
+    w.gn = g;
+    w.hw0 = g + td.o_hw0;
+    w.hw1 = g + td.o_hw1;
+    w.T0 = g + td.o_t0;
+    w.T1 = g + td.o_t1;
+    w.gs = g + td.o_gs;
+    w.abl = g + td.o_abl;
+    w.abu = g + td.o_abu;
+    w.cs = g + td.o_cs;
+  }
+  const int n = td.n;
+  int* const ivp = iws + e;
+  auto iv = [&](int slot) -> int& { return ivp[(long)slot * B]; };
+  const int step = iv(IS_STEP);
 
+  // ---- begin_step (stepper.cpp:83-115) ----
+  double* h0 = w.cand;
+  double* h1 = w.vtmp;
+  for (int k = w.lane; k < n; k += 32) {
+    h0[k] = ws[(L.hist0 + k) * B + e];
+    h1[k] = ws[(L.hist1 + k) * B + e];
+  }
+  const double t0 = step * dt;
+  tau_at(w, t0 + sc.times[2] * dt, w.vtau);
+  {
+    const double span = -sc.times[0];
+    const double tau_m = sc.times[2];
+    for (int k = w.lane; k < n; k += 32) w.x[k] = sc.warm_start ? h1[k] + (tau_m / span) * (h1[k] - h0[k]) : h1[k];
+  }
+  __syncwarp();
+  // StepObjective ctor (objective.cpp:162-185)
+  if (!all_finite_warp(w, h0) || !all_finite_warp(w, h1)) {
+    if (w.lane == 0) iv(IS_RUN) = TR_NONFINITE_CFG;
+    return;
+  }
+#pragma unroll 1
+  for (int hs = 0; hs < 2; ++hs) {  // one inlined copy of the kinematics for both history configurations
+    fk_world(w, hs ? h1 : h0);
+    store_history(w, hs ? w.hw1 : w.hw0, hs ? w.T1 : w.T0);
+  }
+  {
+    for (int i = w.lane; i < w.N; i += 32) {
+      const M4 w0 = ld16(w.hw0 + 16 * i), w1 = ld16(w.hw1 + 16 * i);
+      const M4 T1 = ld16(w.T1 + 16 * i);
+      w.red[4 * i] = ddot(T1, w1);
+      w.red[4 * i + 1] = ddot(ld16(w.T0 + 16 * i), w0);
+      w.red[4 * i + 2] = ddot(T1, w0);
+    }
+    __syncwarp();
+    double s = 0.0;
+    if (w.lane < 3)
+      for (int i = 0; i < w.N; ++i) s += w.red[4 * i + w.lane];
+    const double c11 = __shfl_sync(FULL, s, 0) - m.weighted_mass;
+    const double c00 = __shfl_sync(FULL, s, 1) - m.weighted_mass;
+    const double c10 = __shfl_sync(FULL, s, 2) - m.weighted_mass;
+    w.histconst = 4.0 * c11 + c00 - 4.0 * c10;
+    __syncwarp();
+  }
+  // LbfgsSolver (optim.cpp:141-232): construction evaluates value + gradient,
+  // every iterate runs the two-loop recursion and the Armijo backtracking
+  Solver S;
+  S.status = ST_RUNNING;
+  S.iters = 0;
+  S.stag = 0;
+  S.acc = 0;
+  S.lambda = 0.0;
+  S.value = 0.0;
+  S.grad0 = 0.0;
+  {
+    // LbfgsSolver (optim.cpp:141-232): construction evaluates value + gradient,
+    // every iterate runs the two-loop recursion and the Armijo backtracking
+    const DOpt& o = sc.opt;
+    const int cap = o.mem + 1;
+    double* gtw = tws + e * td.gstride;
+    double* hs = gtw + td.o_hs;
+    double* hy = gtw + td.o_hy;
+    double* hsy = gtw + td.o_hsy;
+    double* alpha = gtw + td.o_alpha;
+    int err = 0;
+    if (!fk_world(w, w.x)) {
+      err = TR_NONFINITE_CFG;
+    } else {
+      const double v0 = value_at(w, w.x);
+      if (!isfinite(v0)) {
+        err = TR_NONFINITE_INIT;
+      } else {
+        S.value = v0;
+        fk_levers(w, w.x);
+        gradient(w, w.grad);
+        S.grad0 = infnorm_warp(w, w.grad);
+      }
+    }
+    int h0 = 0, hc = 0;
+#pragma unroll 1
+    while (!err) {
+      if (S.status != ST_RUNNING) break;
+      if (S.iters >= o.max_iters) {
+        S.status = ST_FAILED;
+        break;
+      }
+      if (grad_converged(w, S)) {
+        S.status = ST_CONVERGED;
+        break;
+      }
+      // two_loop (optim.cpp:213-229): q = H g
+      for (int k = w.lane; k < n; k += 32) w.q2[k] = w.grad[k];
+      __syncwarp();
+      for (int i = hc - 1; i >= 0; --i) {
+        const int slot = (h0 + i) % cap;
+        const double* si = hs + (long)slot * n;
+        const double* yi = hy + (long)slot * n;
+        const double a = vdot_warp(w, si, w.q2) / hsy[slot];
+        if (w.lane == 0) alpha[i] = a;
+        for (int k = w.lane; k < n; k += 32) w.q2[k] = w.q2[k] - a * yi[k];
+        __syncwarp();
+      }
+      if (hc > 0) {
+        const int slot = (h0 + hc - 1) % cap;
+        const double* yl = hy + (long)slot * n;
+        const double scl = hsy[slot] / vdot_warp(w, yl, yl);
+        for (int k = w.lane; k < n; k += 32) w.q2[k] = w.q2[k] * scl;
+        __syncwarp();
+      }
+      for (int i = 0; i < hc; ++i) {
+        const int slot = (h0 + i) % cap;
+        const double* si = hs + (long)slot * n;
+        const double* yi = hy + (long)slot * n;
+        const double beta = vdot_warp(w, yi, w.q2) / hsy[slot];
+        const double c = alpha[i] - beta;
+        for (int k = w.lane; k < n; k += 32) w.q2[k] = w.q2[k] + c * si[k];
+        __syncwarp();
+      }
+      for (int k = w.lane; k < n; k += 32) w.dir[k] = -w.q2[k];
+      __syncwarp();
+      double slope = vdot_warp(w, w.dir, w.grad);
+      if (!(slope < 0.0)) {
+        hc = 0;
+        h0 = 0;
+        for (int k = w.lane; k < n; k += 32) w.dir[k] = -w.grad[k];
+        __syncwarp();
+        slope = vdot_warp(w, w.dir, w.grad);
+      }
+      // Armijo backtracking (optim.cpp:171-205)
+      double t = 1.0;
+      bool accepted = false;
+      const double fval = S.value;
+      for (int trial = 0; trial < o.max_line_search; ++trial) {
+        for (int k = w.lane; k < n; k += 32) w.cand[k] = w.x[k] + t * w.dir[k];
+        __syncwarp();
+        if (all_finite_warp(w, w.cand)) {
+          if (!fk_world(w, w.cand)) {
+            err = TR_NONFINITE_CFG;
+            break;
+          }
+          const double v = value_at(w, w.cand);
+          if (isfinite(v) && v <= fval + o.armijo_c1 * t * slope && v < fval) {
+            fk_levers(w, w.cand);
+            gradient(w, w.evg);  // evaluate(cand): the value repeats v bit for bit
+            const int slot = (h0 + hc) % cap;
+            double* sn = hs + (long)slot * n;
+            double* yn = hy + (long)slot * n;
+            for (int k = w.lane; k < n; k += 32) {
+              sn[k] = t * w.dir[k];
+              yn[k] = w.evg[k] - w.grad[k];
+            }
+            __syncwarp();
+            const double sy = vdot_warp(w, sn, yn);
+            if (sy > 1e-12) {
+              if (w.lane == 0) hsy[slot] = sy;
+              ++hc;
+              if (hc > o.mem) {
+                h0 = (h0 + 1) % cap;
+                --hc;
+              }
+            }
+            for (int k = w.lane; k < n; k += 32) {
+              w.x[k] = w.cand[k];
+              w.grad[k] = w.evg[k];
+            }
+            __syncwarp();
+            S.value = v;
+            accepted = true;
+            ++S.acc;
+            if (fval - v <= o.ftol * fmax(1.0, fabs(fval))) ++S.stag;
+            else S.stag = 0;
+            if (S.stag >= 2) S.status = ST_CONVERGED;
+            break;
+          }
+        }
+        t *= o.backtrack_factor;
+      }
+      if (err) break;
+      if (!accepted) S.status = ST_FAILED;
+      ++S.iters;
+      if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
+    }
+    if (err) {
+      if (w.lane == 0) iv(IS_RUN) = err;
+      return;
+    }
+  }
+
+  // ---- finish_step (stepper.cpp:118-147) ----
+  const bool converged = S.status == ST_CONVERGED;
+  const long Stot = sc.total_steps;
+  const double gnorm = infnorm_warp(w, w.grad);
+  if (w.lane == 0) {
+    if (out.iterations) out.iterations[e * Stot + step] = S.iters;
+    if (out.converged) out.converged[e * Stot + step] = converged;
+    if (out.accepted) out.accepted[e * Stot + step] = S.acc;
+    if (out.final_value) out.final_value[e * Stot + step] = S.value;
+    if (out.final_grad_norm) out.final_grad_norm[e * Stot + step] = gnorm;
+    iv(IS_NREP) = step + 1;
+    iv(IS_ITERS) = S.iters;
+    iv(IS_STATUS) = S.status;
+    iv(IS_ACC) = S.acc;
+  }
+  const int fs = converged ? 0 : iv(IS_FAIL) + 1;
+  __syncwarp();
+  if (w.lane == 0) iv(IS_FAIL) = fs;
+  if (fs > sc.fail_limit) {
+    if (w.lane == 0) iv(IS_RUN) = TR_FAIL_LIMIT;
+    return;
+  }
+  // history shift (order 2): hist0 <- hist1, hist1 <- x
+  for (int k = w.lane; k < n; k += 32) {
+    const double h1k = ws[(L.hist1 + k) * B + e];  // (h1 scratch was reused by the solver)
+    ws[(L.hist0 + k) * B + e] = h1k;
+    ws[(L.hist1 + k) * B + e] = w.x[k];
+  }
+  // energy audit: fd_kinetic(world(hist1_old), world(x)), gravity_potential(world(x))
+  fk_world(w, w.x);
+  for (int i = w.lane; i < w.N; i += 32) {
+    const M4 S_i = ldg16(m.S + 16 * i);
+    const M4 wn = ld16(w.world + MS * i);
+    const M4 td_ = divs(sub(wn, ld16(w.hw1 + 16 * i)), dt);
+    w.red[4 * i] = 0.5 * ddot(mul(td_, S_i), td_);
+    const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
+    const double e4[4] = {0.0, 0.0, 0.0, 1.0};
+    double u[4], vv[4];
+    mul_vec4(S_i, e4, u);
+    mul_vec4(wn, u, vv);
+    w.red[4 * i + 1] = dot4(ghat, vv);
+  }
+  __syncwarp();
+  if (w.lane == 0) {
+    double ke = 0.0, pe = 0.0;
+    for (int i = 0; i < w.N; ++i) {
+      ke += w.red[4 * i];
+      pe -= w.red[4 * i + 1];
+    }
+    const long S1 = Stot + 1;
+    if (out.energy) {
+      out.energy[(e * S1 + step + 1) * 2] = ke;
+      out.energy[(e * S1 + step + 1) * 2 + 1] = pe;
+    }
+    iv(IS_NSAMP) = step + 2;
+    iv(IS_STEP) = step + 1;
+    if (step + 1 >= sc.total_steps) iv(IS_RUN) = TR_OK;
+  }
+  if (out.q) {
+    const long S1 = Stot + 1;
+    for (int k = w.lane; k < n; k += 32) out.q[(e * S1 + step + 1) * n + k] = w.x[k];
+  }
+}
+#endif
+
+}  // namespace PBAD_TREE_NS
+
+#ifndef PBAD_TREE_LBFGS_TU
 bool tree_eligible_sizes(int N, int n) { return N >= 1 && N <= 255 && n >= 1 && n <= tree::MAXN; }
 
 static int tree_smem_doubles(const TreeDesc& td) {
   const int N16 = tree::MS * td.N, nv = (td.n + 1) & ~1;
   const int scr = (tree::TREE_SCR_ARRAYS * N16 > tree::MS * td.n) ? tree::TREE_SCR_ARRAYS * N16 : tree::MS * td.n;
-  return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 5 * nv + 5 * td.N + 32 + ((td.ns + 1) & ~1) +
+  return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 8 * nv + 5 * td.N + 32 + ((td.ns + 1) & ~1) +
          4 * td.ns + (td.ns + 1) / 2 + 2;
 }
 
@@ -1055,6 +1383,7 @@ size_t tree_smem_bytes(const TreeDesc& td) { return sizeof(double) * (size_t)tre
 cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
                              cudaStream_t s) {
   const size_t smem = tree_smem_bytes(td);
+  if (td.lb) return launch_tree_lbfgs(a, td, tws, out, s);
   static size_t configured[2] = {0, 0};
   const int pot = td.pot ? 1 : 0;
   if (smem > 48 * 1024 && smem > configured[pot]) {
@@ -1069,3 +1398,23 @@ cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tw
 }
 
 }  // namespace pbad_gpu
+
+#else  // PBAD_TREE_LBFGS_TU
+
+cudaError_t launch_tree_lbfgs(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
+                              cudaStream_t s) {
+  const size_t smem = tree_smem_bytes(td);
+  static size_t configured[2] = {0, 0};
+  const int pot = td.pot ? 1 : 0;
+  if (smem > 48 * 1024 && smem > configured[pot]) {
+    cudaError_t e = pot ? cudaFuncSetAttribute(PBAD_TREE_NS::k_tree_lbfgs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                        : cudaFuncSetAttribute(PBAD_TREE_NS::k_tree_lbfgs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured[pot] = smem;
+  }
+  if (pot) PBAD_TREE_NS::k_tree_lbfgs<true><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
+  else PBAD_TREE_NS::k_tree_lbfgs<false><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
+  return cudaGetLastError();
+}
+}  // namespace pbad_gpu
+#endif

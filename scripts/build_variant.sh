@@ -8,7 +8,7 @@ name=$1; shift
 mkdir -p build/var_$name
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 F="-O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -Iinclude -Ipaper_1709_04145_b200/csrc"
-for s in pbad_kernels pbad_chain pbad_chain4 pbad_tree pbad_resid; do
+for s in pbad_kernels pbad_chain pbad_chain4 pbad_tree pbad_tree_lbfgs pbad_resid; do
   nvcc $ARCH $F "$@" -c paper_1709_04145_b200/csrc/$s.cu -o build/var_$name/$s.o
 done
 nvcc $ARCH -O2 -std=c++17 -Xcompiler -fPIC,-ffp-contract=off,-mfma -Iinclude -Ipaper_1709_04145_b200/csrc "$@" \

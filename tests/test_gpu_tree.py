@@ -211,3 +211,46 @@ def test_tree_path_contact_equals_general_kernel(monkeypatch):
     for x, y in zip(a, b):
         np.testing.assert_array_equal(np.array([s[1] for s in x.samples]), np.array([s[1] for s in y.samples]))
         assert [r.iterations for r in x.solve_reports] == [r.iterations for r in y.solve_reports]
+
+
+# --- L-BFGS on trees (LbfgsSolver, optim.cpp:141-232) ---
+
+def test_tree_path_humanoid_lbfgs():
+    sc = make_humanoid_scene()
+    sim = SimConfig(dt=0.01, duration=0.04)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    n = 41
+    _check(sc, sim, _sims(sim, n, 4, _humanoid_q0(sc, n, 7)))
+
+
+@pytest.mark.parametrize("seed,mem", [(61, 8), (62, 3)])
+def test_tree_path_lbfgs_random_trees_contact(seed, mem):
+    from paper_1709_04145_b200.types import ContactModel
+    rng = np.random.default_rng(seed)
+    links = random_tree(rng, 6)
+    sc = Scene(links=links, gravity=(0.2, -0.5, -9.81), drag_d=0.5,
+               contact=ContactModel(plane_normal=(0.0, 0.0, 1.0), plane_offset=0.3, d1=5e3, d2=20.0))
+    m = api.build_model(links)
+    n = m.total_dofs
+    sc.q0 = np.zeros(n)
+    sc.qdot0 = np.zeros(n)
+    sim = SimConfig(dt=0.02, duration=0.08)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    sim.optimizer.lbfgs_memory = mem
+    _check(sc, sim, _sims(sim, n, 3, lambda b: rng.uniform(-0.5, 0.5, n)))
+
+
+def test_tree_path_lbfgs_equals_general_kernel(monkeypatch):
+    sc = make_humanoid_scene()
+    sim = SimConfig(dt=0.01, duration=0.03)
+    sim.optimizer.kind = OptimizerKind.lbfgs
+    sim.optimizer.max_iters = 40
+    n = 41
+    m = api.build_model(sc.links)
+    sims = _sims(sim, n, 17, _humanoid_q0(sc, n, 300))
+    a = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.setenv("PBAD_GPU_FORCE_GENERAL", "1")
+    b = api.batch_simulate(m, sc.forces(), sims)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(np.array([s[1] for s in x.samples]), np.array([s[1] for s in y.samples]))
+        assert [r.iterations for r in x.solve_reports] == [r.iterations for r in y.solve_reports]
