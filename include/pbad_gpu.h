@@ -11,6 +11,7 @@
  *   pbad_gpu_sync_outputs   state in HBM (the bench's `value` leg)
  *   pbad_gpu_body_integral  replaces body_integral          model.hpp:100, model.cpp:35-60
  *   pbad_gpu_rotation_vector_matrix                          kinematics.hpp:39
+ *   pbad_gpu_rotation_vector_from_matrix                     scene.cpp:66-86 (scene serialisation)
  *   pbad_gpu_build_scheme   replaces build_scheme           collocation.hpp:39
  *
  * Plain pointers and sizes only.  Matrices are column-major (Eigen's
@@ -160,6 +161,7 @@ int32_t pbad_gpu_model_info(const pbad_gpu_model* model, double* S /*[N][16]*/,
 int32_t pbad_gpu_body_integral(const pbad_link_spec* link, double* S /*[16]*/,
                                double* mass);
 int32_t pbad_gpu_rotation_vector_matrix(const double theta[3], double R[9]);
+int32_t pbad_gpu_rotation_vector_from_matrix(const double R[9], double theta[3]);
 int32_t pbad_gpu_build_scheme(int32_t order, double dt, double* alphas, double* times,
                               double* H, double* H2);
 int32_t pbad_gpu_validate_configuration(const pbad_gpu_model* model, const double* q,

@@ -503,8 +503,36 @@ def ref_lib():
         R.pbr_simulate.argtypes = [vp, C.POINTER(ForcesC), C.POINTER(SimC), C.POINTER(TrajectoryC)]
         R.pbr_batch_simulate.argtypes = [vp, C.POINTER(ForcesC), C.POINTER(SimC), C.c_int, C.c_int,
                                          C.POINTER(TrajectoryC)]
+        R.pbr_scene_roundtrip.restype = C.c_char_p
+        R.pbr_scene_roundtrip.argtypes = [C.c_char_p]
+        R.pbr_bundled_scene.restype = C.c_char_p
+        R.pbr_bundled_scene.argtypes = [C.c_char_p]
+        R.pbr_scene_simulate_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p]
         _ref = R
     return _ref
+
+
+def ref_scene_roundtrip(text):
+    """The reference's parse_scene + serialize_scene; raises OracleError with
+    the reference's exception text."""
+    out = ref_lib().pbr_scene_roundtrip(text.encode())
+    if out is None:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return out.decode()
+
+
+def ref_bundled_scene(name):
+    """serialize_scene of a reference scene builder: chain<N>, single<N>, swimmer, spider."""
+    out = ref_lib().pbr_bundled_scene(name.encode())
+    if out is None:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return out.decode()
+
+
+def ref_scene_simulate_csv(text, traj_csv, energy_csv):
+    """The reference CLI's simulate path: scene text -> trajectory.csv, energy.csv."""
+    if ref_lib().pbr_scene_simulate_csv(text.encode(), traj_csv.encode(), energy_csv.encode()) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
 
 
 class RefModel:

@@ -10,11 +10,13 @@
 
 #include "../pbad_oracle.h"
 #include "pbad/adjoint.hpp"
+#include "pbad/benchmark.hpp"
 #include "pbad/collocation.hpp"
 #include "pbad/kinematics.hpp"
 #include "pbad/model.hpp"
 #include "pbad/objective.hpp"
 #include "pbad/optim.hpp"
+#include "pbad/scene.hpp"
 #include "pbad/stepper.hpp"
 
 using namespace pbad;
@@ -23,6 +25,7 @@ using namespace pbad;
 
 namespace {
 thread_local std::string g_err;
+thread_local std::string g_text;
 
 Mat4 m4(const double* a) {
   Mat4 m;
@@ -291,6 +294,53 @@ API int pbr_batch_simulate(void* mp, const pbo_forces* f, const pbo_sim_config* 
     for (int i = 0; i < count; ++i) v.push_back(sim_of(&sims[i], m.total_dofs));
     const auto trs = batch_simulate(m, forces_of(f, m.total_dofs), v, workers);
     for (int i = 0; i < count; ++i) fill_traj(trs[i], m.total_dofs, &outs[i]);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// ---- scene files and CSV output (scene.cpp, benchmark.cpp:12-36) ----------
+
+// parse_scene + serialize_scene; NULL on error (pbr_last_error has the text)
+API const char* pbr_scene_roundtrip(const char* json) {
+  try {
+    g_text = serialize_scene(parse_scene(json));
+    return g_text.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// serialize_scene of a bundled scene: chain<N>, single<N>, swimmer, spider
+API const char* pbr_bundled_scene(const char* name) {
+  try {
+    const std::string s(name);
+    Scene sc;
+    if (s.rfind("chain", 0) == 0) sc = make_chain_scene(std::stoi(s.substr(5)));
+    else if (s.rfind("single", 0) == 0) sc = make_single_hinge_chain_scene(std::stoi(s.substr(6)));
+    else if (s == "swimmer") sc = make_swimmer_scene();
+    else if (s == "spider") sc = make_spider_scene();
+    else throw std::invalid_argument("unknown bundled scene '" + s + "'");
+    g_text = serialize_scene(sc);
+    return g_text.c_str();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// the pbad_cli `simulate` path (pbad_cli.cpp:41-63) without the overrides:
+// load, build, simulate, write trajectory.csv / energy.csv
+API int pbr_scene_simulate_csv(const char* json, const char* traj_csv, const char* energy_csv) {
+  try {
+    const Scene scene = parse_scene(json);
+    const KinematicModel model = scene_model(scene);
+    const Trajectory traj = simulate(model, scene_forces(scene), scene_sim_config(scene));
+    write_trajectory_csv(traj_csv, traj);
+    write_energy_csv(energy_csv, traj);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

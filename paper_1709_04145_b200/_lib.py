@@ -21,6 +21,7 @@ HEADER_SYMBOLS = [
     "pbad_gpu_abi_version", "pbad_gpu_last_error", "pbad_gpu_error_string", "pbad_gpu_default_optimizer",
     "pbad_gpu_default_sim", "pbad_gpu_model_create", "pbad_gpu_model_destroy", "pbad_gpu_model_dofs",
     "pbad_gpu_model_links", "pbad_gpu_model_info", "pbad_gpu_body_integral", "pbad_gpu_rotation_vector_matrix",
+    "pbad_gpu_rotation_vector_from_matrix",
     "pbad_gpu_build_scheme", "pbad_gpu_validate_configuration", "pbad_gpu_create", "pbad_gpu_destroy",
     "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
     "pbad_gpu_state_device", "pbad_gpu_eval", "pbad_gpu_minimize",
@@ -101,6 +102,7 @@ def load():
         "pbad_gpu_model_info": ([vp, _dp, _dp, _ip, _dp, _ip], C.c_int32),
         "pbad_gpu_body_integral": ([C.POINTER(LinkSpec), _dp, _dp], C.c_int32),
         "pbad_gpu_rotation_vector_matrix": ([_dp, _dp], C.c_int32),
+        "pbad_gpu_rotation_vector_from_matrix": ([_dp, _dp], C.c_int32),
         "pbad_gpu_build_scheme": ([C.c_int32, C.c_double, _dp, _dp, _dp, _dp], C.c_int32),
         "pbad_gpu_validate_configuration": ([vp, _dp, C.c_int32], C.c_int32),
         "pbad_gpu_create": ([vp, C.POINTER(Forces), C.POINTER(SimDesc), C.c_int32, C.c_int32, C.POINTER(vp)],

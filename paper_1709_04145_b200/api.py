@@ -151,6 +151,14 @@ def rotation_vector_matrix(theta) -> np.ndarray:
     return R.reshape(3, 3).T.copy()
 
 
+def rotation_vector_from_matrix(R) -> np.ndarray:
+    """Principal-branch rotation vector of a 3x3 rotation (scene.cpp:66-86)."""
+    th = np.zeros(3)
+    check(_lib.load().pbad_gpu_rotation_vector_from_matrix(_p(_f64(np.asarray(R, dtype=np.float64).T.reshape(9))),
+                                                           _p(th)))
+    return th
+
+
 @dataclass
 class CollocationScheme:
     order: int

@@ -138,6 +138,52 @@ int32_t pbad_gpu_rotation_vector_matrix(const double theta[3], double R[9]) {
   return PBAD_OK;
 }
 
+// rotation_vector_from_matrix, scene.cpp:66-86 (principal branch of the log
+// map; the inverse of pbad_gpu_rotation_vector_matrix).  R column-major.
+int32_t pbad_gpu_rotation_vector_from_matrix(const double R[9], double theta[3]) {
+  auto at = [&](int r, int c) { return R[r + 3 * c]; };
+  const double tr = (at(0, 0) + at(1, 1)) + at(2, 2);
+  const double c = std::min(std::max(0.5 * (tr - 1.0), -1.0), 1.0);
+  const double angle = std::acos(c);
+  const double sv[3] = {at(2, 1) - at(1, 2), at(0, 2) - at(2, 0), at(1, 0) - at(0, 1)};
+  if (angle < 1e-9) {
+    for (int i = 0; i < 3; ++i) theta[i] = 0.5 * sv[i];
+    return PBAD_OK;
+  }
+  if (angle > 3.141592653589793 - 1e-6) {
+    // near pi: axis from the dominant column of R + I, sign from sv
+    double m[9];
+    for (int k = 0; k < 9; ++k) m[k] = R[k];
+    for (int i = 0; i < 3; ++i) m[i + 3 * i] = m[i + 3 * i] + 1.0;
+    int col = 0;
+    double best = 0.0;
+    for (int j = 0; j < 3; ++j) {
+      double acc = 0.0;
+      for (int i = 0; i < 3; ++i) acc = std::fma(m[i + 3 * j], m[i + 3 * j], acc);
+      const double nj = std::sqrt(acc);
+      if (j == 0 || nj > best) { best = nj; col = j; }
+    }
+    const double* a = m + 3 * col;
+    double n2 = a[0] * a[0];
+    n2 = std::fma(a[1], a[1], n2);
+    n2 = std::fma(a[2], a[2], n2);
+    const double n = std::sqrt(n2);
+    double axis[3] = {a[0] / n, a[1] / n, a[2] / n};
+    double d = sv[0] * axis[0];
+    d = std::fma(sv[1], axis[1], d);
+    d = std::fma(sv[2], axis[2], d);
+    if (d < 0.0)
+      for (int i = 0; i < 3; ++i) axis[i] = -axis[i];
+    for (int i = 0; i < 3; ++i) theta[i] = angle * axis[i];
+    return PBAD_OK;
+  }
+  double sn, cs;
+  pbad_sincos(angle, &sn, &cs);
+  const double k = angle * (0.5 / sn);
+  for (int i = 0; i < 3; ++i) theta[i] = k * sv[i];
+  return PBAD_OK;
+}
+
 // build_model, model.cpp:62-112
 int32_t pbad_gpu_model_create(const pbad_link_spec* links, int32_t N, pbad_gpu_model** out) {
   *out = nullptr;

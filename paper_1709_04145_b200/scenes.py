@@ -1,4 +1,4 @@
-"""Benchmark scene builders (inputs only; the scene JSON layer is out of scope).
+"""Benchmark scene builders (the scene JSON layer is scene_io.py).
 
 make_chain_scene / make_single_hinge_chain_scene / make_swimmer_scene /
 make_spider_scene follow /root/reference/proj/src/scene.cpp:430-618;
@@ -39,6 +39,10 @@ class Scene:
     duration: float = 0.0
     q0: Optional[np.ndarray] = None
     qdot0: Optional[np.ndarray] = None
+    # scene-file fields (scene.hpp:20-44): which links listed contact_samples
+    # explicitly, and the integrator kind ("pbad" or a baseline scheme)
+    link_has_samples: Optional[List[bool]] = None
+    integrator_kind: str = "pbad"
 
     def forces(self) -> ForceModel:
         return ForceModel(gravity=self.gravity, drag_d=self.drag_d, contact=self.contact,
