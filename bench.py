@@ -283,7 +283,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if os.environ.get("PBAD_BENCH_BATCH"):  # experiments only: batch-size sweeps
+        cfg["batch"] = int(os.environ["PBAD_BENCH_BATCH"])
     if args.impl == "reference":
         run_reference(args, cfg)
         return

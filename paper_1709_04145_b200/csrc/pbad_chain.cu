@@ -124,7 +124,10 @@ __device__ __forceinline__ void identity_row(int r, double* v) {
 // n = sqrt(q*q); -K^2 has diagonal entries k2 = q*q.
 __device__ __forceinline__ void hinge_cs(double q, double* c, double* s) {
   const double k2 = q * q;
-  const double n = sqrt(k2);
+  // sqrt(fl(q*q)) == |q| in binary64 round-to-nearest barring underflow of
+  // q*q; an underflowed q lands in the Taylor branch where A = 1, B = 1/2
+  // exactly either way, so fabs is bit-identical and saves the DP sqrt.
+  const double n = isinf(k2) ? k2 : fabs(q);
   const double n2 = n * n;
   double A, B;
   if (n < 1e-4) {

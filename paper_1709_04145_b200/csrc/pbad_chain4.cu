@@ -114,7 +114,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // rotation_coeffs (kinematics.cpp:20-45) for a unit-axis angle q: s = A q, c = 1 - B q^2
 __device__ __forceinline__ void hinge_cs(double q, double* c, double* s) {
   const double k2 = q * q;
-  const double n = sqrt(k2);
+  // sqrt(fl(q*q)) == |q| in binary64 round-to-nearest barring underflow of
+  // q*q; an underflowed q lands in the Taylor branch where A = 1, B = 1/2
+  // exactly either way, so fabs is bit-identical and saves the DP sqrt.
+  const double n = isinf(k2) ? k2 : fabs(q);
   const double n2 = n * n;
   double A, B;
   if (n < 1e-4) {
