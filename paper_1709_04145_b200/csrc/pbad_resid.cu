@@ -624,6 +624,105 @@ __device__ __forceinline__ void gn_issue(const R& r, double* buf, int lt, int a0
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+#ifndef PBAD_RESID_GN_DMMA
+#define PBAD_RESID_GN_DMMA 1
+#endif
+#if PBAD_RESID_GN_DMMA
+// FP64 tensor cores: mma.sync.m8n8k4.f64 computes d = fma(a3, b3, fma(a2, b2,
+// fma(a1, b1, fma(a0, b0, c)))) -- the k-ascending fma chain of the numeric
+// contract, bit for bit (scripts/micro/dmma.cu: 1.28 M random elements, 0
+// mismatches) -- so 2 J^T J runs on DMMA unchanged: the chain starts from
+// c = -0 (fma(a0, b0, -0) == a0 * b0, the product's first term) and padded k
+// contribute (-0) * 0 = -0, which leaves every accumulator unchanged.
+// Tile 64 x 64 per 256 threads; warp w owns rows 8w..8w+7 and all eight 8 x 8
+// column blocks.  Staging k-fastest (column stride GQ = 36 = 4 mod 16 doubles:
+// fragment loads and cp.async stores conflict-free).
+constexpr int GQ = GK + 4;
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void gnd_issue(const R& r, double* buf, int lt, int a0, int b0, int c) {
+  const int U = r.U;
+  double* As = buf + (c & 1) * 2 * GB * GQ;
+  double* Bs = As + GB * GQ;
+#pragma unroll
+  for (int q = 0; q < GK * GB / 256; ++q) {
+    const int t = lt + 256 * q;
+    const int col = t / GK, kk = t - col * GK;
+    const int k = c * GK + kk, a = a0 + col, b = b0 + col;
+    if (k < U && a < U) gn_cpa8(As + col * GQ + kk, r.J + k + (long)U * a);
+    else As[col * GQ + kk] = -0.0;
+    if (k < U && b < U) gn_cpa8(Bs + col * GQ + kk, r.J + k + (long)U * b);
+    else Bs[col * GQ + kk] = 0.0;
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __noinline__ void gauss_newton(const R& r) {
+  const int U = r.U;
+  const int nb = (U + GB - 1) / GB;
+  const int nk = (U + GK - 1) / GK;
+  const int ntile = nb * (nb + 1) / 2;
+  const int grp = r.tid >> 8, lt = r.tid & 255;
+  const int w = lt >> 5, lane = lt & 31, g = lane >> 2, t4 = lane & 3;
+  double* buf = rsm + grp * 4 * GB * GQ;
+  for (int t0 = 0; t0 < ntile; t0 += TG) {
+    int tile = t0 + grp, bi = 0;
+    const bool active = tile < ntile;
+    if (!active) tile = ntile - 1;
+    while (tile > bi) {
+      tile -= bi + 1;
+      ++bi;
+    }
+    const int bj = tile;
+    const int a0 = bi * GB, b0 = bj * GB;
+    double d[8][2];
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb) d[cb][0] = d[cb][1] = -0.0;
+    gnd_issue(r, buf, lt, a0, b0, 0);
+    for (int c = 0; c < nk; ++c) {
+      double* As = buf + (c & 1) * 2 * GB * GQ;
+      double* Bs = As + GB * GQ;
+      __syncthreads();
+      if (c + 1 < nk) {
+        gnd_issue(r, buf, lt, a0, b0, c + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+#pragma unroll
+      for (int q = 0; q < GK * GB / 256; ++q) {
+        const int t = lt + 256 * q;
+        const int col = t / GK, kk = t - col * GK;
+        As[col * GQ + kk] = 2.0 * As[col * GQ + kk];
+      }
+      __syncthreads();
+      const double* ap = As + (8 * w + g) * GQ + t4;
+      const double* bp = Bs + g * GQ + t4;
+#pragma unroll
+      for (int ks = 0; ks < GK / 4; ++ks) {
+        const double av = ap[4 * ks];
+        double bv[8];
+#pragma unroll
+        for (int cb = 0; cb < 8; ++cb) bv[cb] = bp[cb * 8 * GQ + 4 * ks];
+#pragma unroll
+        for (int cb = 0; cb < 8; ++cb) dmma884(d[cb][0], d[cb][1], av, bv[cb]);
+      }
+    }
+    if (active) {
+      const int a = a0 + 8 * w + g;
+#pragma unroll
+      for (int cb = 0; cb < 8; ++cb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int b = b0 + 8 * cb + 2 * t4 + h;
+          if (a < U && b <= a) r.GN[a + (long)U * b] = 0.5 * (d[cb][h] + d[cb][h]);
+        }
+    }
+  }
+  __syncthreads();
+}
+#else
 __device__ __noinline__ void gauss_newton(const R& r) {
   const int U = r.U;
   const int nb = (U + GB - 1) / GB;
@@ -711,6 +810,7 @@ __device__ __noinline__ void gauss_newton(const R& r) {
   __syncthreads();
 }
 
+#endif  // PBAD_RESID_GN_DMMA
 
 // LLT of r.DM (lower, column-major), blocked left-looking; same per-element
 // operation sequence as the right-looking reference (optim.cpp:11-15).
@@ -1696,7 +1796,7 @@ bool resid_eligible_sizes(int N, int u) {
 
 size_t resid_smem_bytes(int N, int u) {
   const size_t N16 = resid::SMS * (size_t)N;
-  size_t b = resid::TG * 4 * resid::GK * resid::GP;                       // J^T J tiles (double-buffered, TG groups)
+  size_t b = resid::TG * 4 * resid::GB * (resid::GK + 4);                 // J^T J tiles (double-buffered, TG groups; covers both layouts)
   b = std::max(b, (size_t)(resid::LK * resid::LP + resid::CB * (resid::CB + 1) + resid::MAXU * (resid::CB + 1)));  // Cholesky (smem variant)
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP));             // Cholesky update panel
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
