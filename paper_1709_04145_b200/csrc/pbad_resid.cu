@@ -624,6 +624,12 @@ __device__ __forceinline__ void gn_issue(const R& r, double* buf, int lt, int a0
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// d += a b on the FP64 tensor cores (one 8x8x4 fragment per warp)
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
 #ifndef PBAD_RESID_GN_DMMA
 #define PBAD_RESID_GN_DMMA 1
 #endif
@@ -638,10 +644,6 @@ __device__ __forceinline__ void gn_issue(const R& r, double* buf, int lt, int a0
 // column blocks.  Staging k-fastest (column stride GQ = 36 = 4 mod 16 doubles:
 // fragment loads and cp.async stores conflict-free).
 constexpr int GQ = GK + 4;
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
 __device__ __forceinline__ void gnd_issue(const R& r, double* buf, int lt, int a0, int b0, int c) {
   const int U = r.U;
   double* As = buf + (c & 1) * 2 * GB * GQ;
@@ -893,6 +895,96 @@ __device__ __forceinline__ void bcu_tile(const R& r, double* A, const double* G,
       if (i < U && j < c0 + bw && j <= i) A[i + (long)U * j] = acc[ii][jj];
     }
 }
+#ifndef PBAD_RESID_BCU_DMMA
+#define PBAD_RESID_BCU_DMMA 1
+#endif
+#if PBAD_RESID_BCU_DMMA
+// The same update on FP64 tensor cores: per 8 x 8 block of the output,
+// d = fma(-L(i,k+3), L(j,k+3), ... fma(-L(i,k), L(j,k), d)) is exactly one
+// mma.m8n8k4 with A = -panel rows i, B = panel rows j (DMMA is the
+// k-ascending fma chain).  Panel k-major with row stride RP = 4 (mod 16)
+// doubles: staging stores and fragment loads are both conflict-free; k
+// padded to a multiple of 4 with +0 (a (-0) * 0 product leaves the
+// accumulator unchanged).  Warp wi of the group owns row blocks wi, wi + NW,
+// ... and the four 8-column blocks of the block column.
+template <int GS, int NRB>
+__device__ __forceinline__ void bcu_dmma(const R& r, double* A, const double* G, double lambda, bool fromG, int c0,
+                                         int bw, int kb, int ke, double* panel, int cap, int bar) {
+  constexpr int NW = GS / 32;
+  const int U = r.U;
+  const int t = r.tid - (NT - GS);
+  const int wi = t >> 5, lane = t & 31, g = lane >> 2, t4 = lane & 3;
+  const int rows = U - c0;
+  const int nrb = (rows + 7) >> 3;
+  const int RP = rows + ((20 - (rows & 15)) & 15);  // >= rows, == 4 (mod 16)
+  double d[NRB][4][2];
+#pragma unroll
+  for (int q = 0; q < NRB; ++q) {
+    const int rb = wi + NW * q;
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = c0 + 8 * rb + g, j = c0 + 8 * cb + 2 * t4 + h;
+        const long at = i + (long)U * j;
+        d[q][cb][h] = (rb < nrb && i < U && j < c0 + bw && j <= i)
+                          ? (fromG ? (i == j ? G[at] + lambda : G[at]) : A[at]) : 0.0;
+      }
+  }
+  const int kcap = (cap / RP) & ~3;
+  for (int k0 = kb; k0 < ke; k0 += kcap) {
+    const int kc = min(kcap, ke - k0);
+    const int kc4 = (kc + 3) & ~3;
+    group_sync(bar, GS);
+    for (int kk = 0; kk < kc4; ++kk)
+      for (int rr = t; rr < rows; rr += GS) {
+        if (kk < kc) cp_async8(panel + kk * RP + rr, A + (c0 + rr) + (long)U * (k0 + kk));
+        else panel[kk * RP + rr] = 0.0;
+      }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    group_sync(bar, GS);
+    for (int ks = 0; ks < kc4; ks += 4) {
+      const double* pk = panel + (ks + t4) * RP + g;
+      double bv[4];
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) bv[cb] = pk[8 * cb];
+#pragma unroll
+      for (int q = 0; q < NRB; ++q) {
+        const int rb = wi + NW * q;
+        if (rb < nrb) {
+          const double av = -pk[8 * rb];
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb)
+            if (cb <= rb) dmma884(d[q][cb][0], d[q][cb][1], av, bv[cb]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NRB; ++q) {
+    const int rb = wi + NW * q;
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = c0 + 8 * rb + g, j = c0 + 8 * cb + 2 * t4 + h;
+        if (rb < nrb && i < U && j < c0 + bw && j <= i) A[i + (long)U * j] = d[q][cb][h];
+      }
+  }
+}
+template <int GS>
+__device__ __noinline__ void block_col_update(const R& r, double* A, const double* G, double lambda, bool fromG,
+                                              int c0, int bw, int kb, int ke, double* panel, int cap, int bar) {
+  constexpr int NW = GS / 32;
+  const int q = ((r.U - c0 + 7) / 8 + NW - 1) / NW;  // row blocks per warp
+  if (q <= 1) bcu_dmma<GS, 1>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (q <= 2) bcu_dmma<GS, 2>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (q <= 3) bcu_dmma<GS, 3>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (q <= 4) bcu_dmma<GS, 4>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else if (q <= 6) bcu_dmma<GS, 6>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else bcu_dmma<GS, (MAXU / 8 + NW - 1) / NW>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+}
+#else
 template <int GS>
 __device__ __noinline__ void block_col_update(const R& r, double* A, const double* G, double lambda, bool fromG,
                                               int c0, int bw, int kb, int ke, double* panel, int cap, int bar) {
@@ -906,6 +998,8 @@ __device__ __noinline__ void block_col_update(const R& r, double* A, const doubl
   else if (ni <= 8) bcu_tile<GS, 8>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
   else bcu_tile<GS, (MAXU + RY - 1) / RY>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
 }
+
+#endif  // PBAD_RESID_BCU_DMMA
 
 constexpr int CS = CB + 1;
 __device__ __noinline__ bool cholesky(const R& r, double lambda) {
