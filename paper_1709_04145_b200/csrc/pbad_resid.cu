@@ -643,16 +643,21 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // Tile 64 x 64 per 256 threads; warp w owns rows 8w..8w+7 and all eight 8 x 8
 // column blocks.  Staging k-fastest (column stride GQ = 36 = 4 mod 16 doubles:
 // fragment loads and cp.async stores conflict-free).
-constexpr int GQ = GK + 4;
+#ifndef PBAD_RESID_GDK
+#define PBAD_RESID_GDK 64
+#endif
+constexpr int GDK = PBAD_RESID_GDK;  // k chunk of the DMMA tiles
+constexpr int GQ = GDK + 4;          // = 4 (mod 16)
+static_assert(GQ % 16 == 4, "conflict-free fragment loads");
 __device__ __forceinline__ void gnd_issue(const R& r, double* buf, int lt, int a0, int b0, int c) {
   const int U = r.U;
   double* As = buf + (c & 1) * 2 * GB * GQ;
   double* Bs = As + GB * GQ;
 #pragma unroll
-  for (int q = 0; q < GK * GB / 256; ++q) {
+  for (int q = 0; q < GDK * GB / 256; ++q) {
     const int t = lt + 256 * q;
-    const int col = t / GK, kk = t - col * GK;
-    const int k = c * GK + kk, a = a0 + col, b = b0 + col;
+    const int col = t / GDK, kk = t - col * GDK;
+    const int k = c * GDK + kk, a = a0 + col, b = b0 + col;
     if (k < U && a < U) gn_cpa8(As + col * GQ + kk, r.J + k + (long)U * a);
     else As[col * GQ + kk] = -0.0;
     if (k < U && b < U) gn_cpa8(Bs + col * GQ + kk, r.J + k + (long)U * b);
@@ -663,10 +668,10 @@ __device__ __forceinline__ void gnd_issue(const R& r, double* buf, int lt, int a
 __device__ __noinline__ void gauss_newton(const R& r) {
   const int U = r.U;
   const int nb = (U + GB - 1) / GB;
-  const int nk = (U + GK - 1) / GK;
   const int ntile = nb * (nb + 1) / 2;
   const int grp = r.tid >> 8, lt = r.tid & 255;
   const int w = lt >> 5, lane = lt & 31, g = lane >> 2, t4 = lane & 3;
+  const int nkd = (U + GDK - 1) / GDK;
   double* buf = rsm + grp * 4 * GB * GQ;
   for (int t0 = 0; t0 < ntile; t0 += TG) {
     int tile = t0 + grp, bi = 0;
@@ -682,28 +687,22 @@ __device__ __noinline__ void gauss_newton(const R& r) {
 #pragma unroll
     for (int cb = 0; cb < 8; ++cb) d[cb][0] = d[cb][1] = -0.0;
     gnd_issue(r, buf, lt, a0, b0, 0);
-    for (int c = 0; c < nk; ++c) {
+    for (int c = 0; c < nkd; ++c) {
       double* As = buf + (c & 1) * 2 * GB * GQ;
       double* Bs = As + GB * GQ;
       __syncthreads();
-      if (c + 1 < nk) {
+      if (c + 1 < nkd) {
         gnd_issue(r, buf, lt, a0, b0, c + 1);
         asm volatile("cp.async.wait_group 1;" ::: "memory");
       } else {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
-#pragma unroll
-      for (int q = 0; q < GK * GB / 256; ++q) {
-        const int t = lt + 256 * q;
-        const int col = t / GK, kk = t - col * GK;
-        As[col * GQ + kk] = 2.0 * As[col * GQ + kk];
-      }
       __syncthreads();
       const double* ap = As + (8 * w + g) * GQ + t4;
       const double* bp = Bs + g * GQ + t4;
 #pragma unroll
-      for (int ks = 0; ks < GK / 4; ++ks) {
-        const double av = ap[4 * ks];
+      for (int ks = 0; ks < GDK / 4; ++ks) {
+        const double av = 2.0 * ap[4 * ks];  // 2 J (exact)
         double bv[8];
 #pragma unroll
         for (int cb = 0; cb < 8; ++cb) bv[cb] = bp[cb * 8 * GQ + 4 * ks];
@@ -1890,7 +1889,7 @@ bool resid_eligible_sizes(int N, int u) {
 
 size_t resid_smem_bytes(int N, int u) {
   const size_t N16 = resid::SMS * (size_t)N;
-  size_t b = resid::TG * 4 * resid::GB * (resid::GK + 4);                 // J^T J tiles (double-buffered, TG groups; covers both layouts)
+  size_t b = resid::TG * 4 * resid::GB * std::max(resid::GK + 4, resid::GQ);  // J^T J tiles (double-buffered, TG groups)
   b = std::max(b, (size_t)(resid::LK * resid::LP + resid::CB * (resid::CB + 1) + resid::MAXU * (resid::CB + 1)));  // Cholesky (smem variant)
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP));             // Cholesky update panel
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
