@@ -930,20 +930,59 @@ __device__ __forceinline__ void bcu_dmma(const R& r, double* A, const double* G,
                           ? (fromG ? (i == j ? G[at] + lambda : G[at]) : A[at]) : 0.0;
       }
   }
-  const int kcap = (cap / RP) & ~3;
-  for (int k0 = kb; k0 < ke; k0 += kcap) {
+  // two panel buffers: chunk c + 1 streams in (cp.async) while chunk c is
+  // multiplied; 16-byte copies of row pairs when the column-major rows are
+  // 16-byte aligned (U and c0 even)
+  const int kcap = ((cap / 2) / RP) & ~3;
+  const bool pairs = ((U | c0) & 1) == 0;
+  auto stage = [&](int k0, double* buf) {
     const int kc = min(kcap, ke - k0);
     const int kc4 = (kc + 3) & ~3;
-    group_sync(bar, GS);
-    for (int kk = 0; kk < kc4; ++kk)
-      for (int rr = t; rr < rows; rr += GS) {
-        if (kk < kc) cp_async8(panel + kk * RP + rr, A + (c0 + rr) + (long)U * (k0 + kk));
-        else panel[kk * RP + rr] = 0.0;
+    if (pairs) {
+      const int rp = (rows + 1) >> 1;
+      for (int e = t; e < kc4 * rp; e += GS) {
+        const int kk = e / rp, rr = 2 * (e - kk * rp);
+        double* dst = buf + kk * RP + rr;
+        if (kk < kc) {
+          const double* src = A + (c0 + rr) + (long)U * (k0 + kk);
+          if (rr + 1 < rows) {
+            const unsigned da = (unsigned)__cvta_generic_to_shared(dst);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(da), "l"(src) : "memory");
+          } else {
+            cp_async8(dst, src);
+          }
+        } else {
+          dst[0] = 0.0;
+          if (rr + 1 < rows) dst[1] = 0.0;
+        }
       }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    } else {
+      for (int e = t; e < kc4 * rows; e += GS) {
+        const int kk = e / rows, rr = e - kk * rows;
+        if (kk < kc) cp_async8(buf + kk * RP + rr, A + (c0 + rr) + (long)U * (k0 + kk));
+        else buf[kk * RP + rr] = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double* pbuf[2] = {panel, panel + kcap * RP};
+  if (kb < ke) {
+    group_sync(bar, GS);  // the previous user of the panel is done with it
+    stage(kb, pbuf[0]);
+  }
+  int ci = 0;
+  for (int k0 = kb; k0 < ke; k0 += kcap, ++ci) {
+    const int kc4 = (min(kcap, ke - k0) + 3) & ~3;
+    if (k0 + kcap < ke) {
+      stage(k0 + kcap, pbuf[(ci + 1) & 1]);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     group_sync(bar, GS);
+    const double* cur = pbuf[ci & 1];
     for (int ks = 0; ks < kc4; ks += 4) {
-      const double* pk = panel + (ks + t4) * RP + g;
+      const double* pk = cur + (ks + t4) * RP + g;
       double bv[4];
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) bv[cb] = pk[8 * cb];
@@ -958,6 +997,7 @@ __device__ __forceinline__ void bcu_dmma(const R& r, double* A, const double* G,
         }
       }
     }
+    group_sync(bar, GS);  // buffer ci & 1 is restaged two chunks later
   }
 #pragma unroll
   for (int q = 0; q < NRB; ++q) {
@@ -1000,7 +1040,7 @@ __device__ __noinline__ void block_col_update(const R& r, double* A, const doubl
 
 #endif  // PBAD_RESID_BCU_DMMA
 
-constexpr int CS = CB + 1;
+constexpr int CS = CB + 4;  // = 4 (mod 16): conflict-free DMMA fragments of the diagonal block
 __device__ __noinline__ bool cholesky(const R& r, double lambda) {
   const int U = r.U;
   double* A = r.DM;
@@ -1019,12 +1059,87 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
 #if PBAD_PHASE_TIMING
       const long long td0 = clock64();
 #endif
-      for (int c = 0; c < bw; ++c)
-        if (lane < bw && c <= lane) {
-          const long at = (j0 + lane) + (long)U * (j0 + c);
-          Lj[lane * CS + c] = j0 > 0 ? A[at] : (c == lane ? G[at] + lambda : G[at]);
+      {
+        // the block's rows, 16 loads in flight per lane (a dynamic loop here
+        // exposed one L2 round trip per column)
+        const double* src = (j0 > 0 ? A : G) + (j0 + lane) + (long)U * j0;
+#pragma unroll
+        for (int c0 = 0; c0 < CB; c0 += 16) {
+          double v[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            v[q] = (lane < bw && c0 + q < bw && c0 + q <= lane) ? src[(long)U * (c0 + q)] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (lane < bw && c0 + q < bw && c0 + q <= lane)
+              Lj[lane * CS + c0 + q] = (j0 == 0 && c0 + q == lane) ? v[q] + lambda : v[q];
         }
+      }
       __syncwarp();
+#ifndef PBAD_RESID_DIAG_DMMA
+#define PBAD_RESID_DIAG_DMMA 1
+#endif
+#if PBAD_RESID_DIAG_DMMA
+      // right-looking in 8-column sub-panels: pivots and the updates inside
+      // the sub-panel are scalar (lane = row), the trailing update by the
+      // sub-panel's 8 columns is one DMMA pair per 8 x 8 block (k ascending:
+      // every element still receives its updates in k order)
+      int ok = 1;
+      const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+      for (int p = 0; p < CB / 8; ++p) {
+        if (8 * p < bw && ok) {
+          // lane = row: the sub-panel's 8 entries of the row in registers,
+          // column k of the pivot step broadcast by shuffles
+          double a[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) a[c] = Lj[lane * CS + 8 * p + c];
+#pragma unroll
+          for (int kq = 0; kq < 8; ++kq) {
+            const int k = 8 * p + kq;
+            if (k < bw && ok) {
+              const double akk = __shfl_sync(FULL, a[kq], k);
+              if (akk <= 0.0) {
+                ok = 0;
+              } else {
+                const double d = sqrt(akk);
+                if (lane == k) a[kq] = d;
+                else if (lane > k) a[kq] = a[kq] / d;
+#pragma unroll
+                for (int c = kq + 1; c < 8; ++c) {
+                  const double lck = __shfl_sync(FULL, a[kq], 8 * p + c);
+                  if (lane > k && 8 * p + c <= lane) a[c] = fma(-a[kq], lck, a[c]);
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (8 * p + c <= lane) Lj[lane * CS + 8 * p + c] = a[c];
+          __syncwarp();
+          if (ok) {
+#pragma unroll
+            for (int rb = p + 1; rb < CB / 8; ++rb)
+#pragma unroll
+              for (int cb = p + 1; cb <= rb; ++cb) {
+                if (8 * cb < bw) {
+                  double* cp = Lj + (8 * rb + g) * CS + 8 * cb + 2 * t4;
+                  double c0 = cp[0], c1 = cp[1];
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    const double a = -Lj[(8 * rb + g) * CS + 8 * p + 4 * h + t4];
+                    const double b = Lj[(8 * cb + g) * CS + 8 * p + 4 * h + t4];
+                    dmma884(c0, c1, a, b);
+                  }
+                  cp[0] = c0;
+                  cp[1] = c1;
+                }
+              }
+            __syncwarp();
+          }
+        }
+      }
+#else
       // right-looking, the trailing update spread over the packed 32x32
       // triangle (rss.pk32: row | col << 8, columns ascending)
       int ok = 1;
@@ -1052,6 +1167,7 @@ __device__ __noinline__ bool cholesky(const R& r, double lambda) {
         }
         __syncwarp();
       }
+#endif
       if (lane == 0) rss.flag = ok;
 #if PBAD_PHASE_TIMING
       if (lane == 0) rss.pt[12] += clock64() - td0;
@@ -1892,7 +2008,7 @@ size_t resid_smem_bytes(int N, int u) {
   size_t b = resid::TG * 4 * resid::GB * std::max(resid::GK + 4, resid::GQ);  // J^T J tiles (double-buffered, TG groups)
   b = std::max(b, (size_t)(resid::LK * resid::LP + resid::CB * (resid::CB + 1) + resid::MAXU * (resid::CB + 1)));  // Cholesky (smem variant)
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP));             // Cholesky update panel
-  b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
+  b = std::max(b, (size_t)(resid::CB * (resid::CB + 4) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
   b = std::max(b, 2 * u * N16);                                           // passes
   b = std::max(b, 4 * u * N16);                                           // residual sweeps
   b = std::max(b, (2 * u + u * u) * N16);                                 // Jacobian walks
