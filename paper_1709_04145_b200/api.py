@@ -319,11 +319,16 @@ class GpuContext:
                 setattr(o, k, v.ctypes.data_as(C.POINTER(C.c_float)))
         return o, bufs
 
-    def rollout(self, q0, qdot0, want_q=True, want_energy=True, pinned=False) -> Dict[str, np.ndarray]:
+    def make_outputs(self, B: int, want_q=True, want_energy=True, pinned=False):
+        """Caller-owned host output buffers for rollout(out=...) (the C ABI
+        writes into buffers the caller allocated, stepper.hpp's Trajectory)."""
+        return self._out_struct(B, want_q, want_energy, pinned)
+
+    def rollout(self, q0, qdot0, want_q=True, want_energy=True, pinned=False, out=None) -> Dict[str, np.ndarray]:
         q0 = _f64(q0)
         qdot0 = _f64(qdot0)
         B = q0.shape[0]
-        o, bufs = self._out_struct(B, want_q, want_energy, pinned)
+        o, bufs = out if out is not None else self._out_struct(B, want_q, want_energy, pinned)
         check(_lib.load().pbad_gpu_rollout(self._h, B, _p(q0), _p(qdot0), C.byref(o)))
         return bufs
 
