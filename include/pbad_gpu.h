@@ -7,6 +7,8 @@
  *   pbad_gpu_rollout        replaces batch_simulate/simulate stepper.hpp:49-64, stepper.cpp:151-270
  *   pbad_gpu_eval           replaces StepObjective::evaluate/value objective.hpp:106-132
  *   pbad_gpu_minimize       replaces minimize()             optim.hpp:58-60, optim.cpp:244-250
+ *   pbad_gpu_correlation    replaces correlation_and_grad / hessian_bb / hessian_ab
+ *                                                           adjoint.hpp:80-82, adjoint.cpp:178-192
  *   pbad_gpu_begin/advance/ device-resident stepping for callers that keep
  *   pbad_gpu_sync_outputs   state in HBM (the bench's `value` leg)
  *   pbad_gpu_body_integral  replaces body_integral          model.hpp:100, model.cpp:35-60
@@ -204,6 +206,16 @@ const double* pbad_gpu_state_device(const pbad_gpu_ctx* ctx);
 int32_t pbad_gpu_eval(pbad_gpu_ctx* ctx, int32_t B, const double* history,
                       const double* tau, const double* x, int32_t want_grad,
                       int32_t want_gn, double* value, double* grad, double* gn);
+
+/* Correlation derivatives of a batch of configuration pairs (adjoint.hpp:80-82:
+ * correlation_and_grad, hessian_bb, hessian_ab), qa/qb [B][n];
+ * weight_per_body [n_links] or NULL (all ones, WeightedBody::make); outputs
+ * value [B], grad_b [B][n], hess_bb / hess_ab [B][n][n] column-major, each
+ * optional (NULL = not computed).  Non-finite inputs propagate like the
+ * reference's ConfigPass::make. */
+int32_t pbad_gpu_correlation(pbad_gpu_ctx* ctx, int32_t B, const double* qa, const double* qb,
+                             const double* weight_per_body, double* value, double* grad_b,
+                             double* hess_bb, double* hess_ab);
 
 /* minimize() of a batch of step problems (same inputs as eval, x0 [B][dim]). */
 int32_t pbad_gpu_minimize(pbad_gpu_ctx* ctx, int32_t B, const double* history,

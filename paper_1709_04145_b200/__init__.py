@@ -9,6 +9,8 @@ from .types import (ActuationKind, ActuationSpec, BoxGeometry, ContactModel, Ene
                     JointSpec, LinkSpec, ModelError, ObjectiveKind, OptimizerConfig, OptimizerKind, PointMass,
                     PointMassGeometry, SimConfig, SolveReport, Trajectory)
 from . import scenes
-from .api import (CollocationScheme, GpuContext, KinematicModel, StepObjective, StepProblem, batch_simulate,
-                  body_integral, build_model, build_scheme, legendre_points, rotation_vector_matrix, simulate,
-                  total_steps, validate_configuration)
+from .api import (CollocationScheme, CorrelationDerivatives, CorrelationRequest, GpuContext, KinematicModel,
+                  StepObjective, StepProblem, batch_correlation, batch_simulate, body_integral, build_model,
+                  build_scheme, correlation_and_grad, hessian_ab, hessian_bb, legendre_points,
+                  rotation_vector_from_matrix, rotation_vector_matrix, simulate, total_steps,
+                  validate_configuration)

@@ -363,6 +363,31 @@ class GpuContext:
             gn = gn.transpose(0, 2, 1).copy()  # column-major -> row-major
         return value, grad, gn
 
+    def correlation(self, qa, qb, weight_per_body=None, want=("value", "grad", "bb", "ab")):
+        """Batched correlation derivatives of (qa[b], qb[b]) (adjoint.cpp:178-192):
+        value [B], grad_b [B, n], hess_bb / hess_ab [B, n, n] (None where not
+        wanted)."""
+        qa = _f64(qa)
+        B = qa.shape[0]
+        n = self.n
+        qa = _f64(qa, (B, n))
+        qb = _f64(qb, (B, n))
+        w = None
+        if weight_per_body is not None and len(weight_per_body) != 0:
+            w = _f64(weight_per_body)
+            if len(w) != self.model.link_count():
+                raise ModelError("weight_per_body length does not match link count")
+        v = np.zeros(B) if "value" in want else None
+        g = np.zeros((B, n)) if "grad" in want else None
+        bb = np.zeros((B, n, n)) if "bb" in want else None
+        ab = np.zeros((B, n, n)) if "ab" in want else None
+        check(_lib.load().pbad_gpu_correlation(self._h, B, _p(qa), _p(qb), _p(w), _p(v), _p(g), _p(bb), _p(ab)))
+        if bb is not None:
+            bb = bb.transpose(0, 2, 1).copy()  # column-major -> row-major
+        if ab is not None:
+            ab = ab.transpose(0, 2, 1).copy()
+        return v, g, bb, ab
+
     def minimize(self, history, x0, tau=None):
         history = _f64(history)
         B = history.shape[0]
@@ -494,3 +519,51 @@ class StepObjective:
     def evaluate(self, x, want_gn: bool = False):
         v, g, gn = self._ctx.eval(self._hist, _f64(x)[None], want_grad=True, want_gn=want_gn, tau=self._tau)
         return float(v[0]), g[0], (gn[0] if gn is not None else None)
+
+
+# --- correlation functional (adjoint.hpp:15-82) --------------------------------
+
+@dataclass
+class CorrelationRequest:
+    model: KinematicModel
+    qa: np.ndarray
+    qb: np.ndarray
+    weight_per_body: Optional[np.ndarray] = None  # empty / None = all ones
+
+
+@dataclass
+class CorrelationDerivatives:
+    value: float
+    grad_b: np.ndarray
+    hess_bb: np.ndarray
+    hess_ab: np.ndarray
+
+
+def _corr_ctx(model: KinematicModel, device: int = 0) -> GpuContext:
+    ctx = getattr(model, "_corr_ctx", None)
+    if ctx is None:
+        ctx = GpuContext(model, ForceModel(), SimConfig(dt=0.01, duration=0.01), device=device)
+        model._corr_ctx = ctx
+    return ctx
+
+
+def correlation_and_grad(req: CorrelationRequest) -> Tuple[float, np.ndarray]:
+    v, g, _, _ = _corr_ctx(req.model).correlation(_f64(req.qa)[None], _f64(req.qb)[None], req.weight_per_body,
+                                                    want=("value", "grad"))
+    return float(v[0]), g[0]
+
+
+def hessian_bb(req: CorrelationRequest) -> np.ndarray:
+    return _corr_ctx(req.model).correlation(_f64(req.qa)[None], _f64(req.qb)[None], req.weight_per_body,
+                                            want=("bb",))[2][0]
+
+
+def hessian_ab(req: CorrelationRequest) -> np.ndarray:
+    return _corr_ctx(req.model).correlation(_f64(req.qa)[None], _f64(req.qb)[None], req.weight_per_body,
+                                            want=("ab",))[3][0]
+
+
+def batch_correlation(model: KinematicModel, qa, qb, weight_per_body=None, device: int = 0):
+    """All four derivatives for a batch of pairs in one launch."""
+    v, g, bb, ab = _corr_ctx(model, device).correlation(qa, qb, weight_per_body)
+    return [CorrelationDerivatives(float(v[b]), g[b], bb[b], ab[b]) for b in range(len(v))]

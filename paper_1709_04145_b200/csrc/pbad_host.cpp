@@ -1219,6 +1219,65 @@ int32_t pbad_gpu_eval(pbad_gpu_ctx* c, int32_t B, const double* history, const d
   return PBAD_OK;
 }
 
+// correlation_and_grad / hessian_bb / hessian_ab (adjoint.cpp:178-192) for a
+// batch of (qa, qb) pairs; WeightedBody::make (adjoint.cpp:29-41) on the host
+int32_t pbad_gpu_correlation(pbad_gpu_ctx* c, int32_t B, const double* qa, const double* qb,
+                             const double* weight_per_body, double* value, double* grad_b, double* hess_bb,
+                             double* hess_ab) {
+  if (B < 1) return fail(PBAD_E_ARGUMENT, "batch %d must be >= 1", B);
+  if (!qa || !qb) return fail(PBAD_E_ARGUMENT, "qa and qb are required");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const pbad_gpu_model& m = c->model;
+  const long N = m.N, n = m.n;
+  DModel dm = c->ka.m;
+  double* dS = nullptr;
+  if (weight_per_body) {
+    std::vector<double> wS(16 * N);
+    double wm = 0.0;
+    for (long i = 0; i < N; ++i) {
+      const double w = weight_per_body[i];
+      for (int k = 0; k < 16; ++k) wS[16 * i + k] = w * m.S[16 * i + k];
+      wm += w * m.mass[i];
+    }
+    dS = dalloc<double>(16 * N);
+    if (!dS) return fail(PBAD_E_CUDA, "cudaMalloc of the weighted body integrals failed");
+    CUDA_TRY(cudaMemcpy(dS, wS.data(), sizeof(double) * 16 * N, cudaMemcpyHostToDevice));
+    dm.S = dS;
+    dm.weighted_mass = wm;
+  }
+  Layout L{};
+  L.p_value = 0;
+  L.p_d1 = N * 16;
+  L.p_world = L.p_d1 + n * 16;
+  L.p_lever = L.p_world + N * 16;
+  L.p_d2 = L.p_lever + n * 16;
+  L.pass_stride = L.p_d2 + (long)m.n_d2 * 16;
+  L.pass = 0;
+  L.seeds = 2 * L.pass_stride;
+  L.adj = L.seeds + N * 16;
+  L.total = L.adj + N * 16;
+  double* ws = dalloc<double>((size_t)L.total * B);
+  double* dq = dalloc<double>((size_t)2 * B * n);
+  double* dv = value ? dalloc<double>(B) : nullptr;
+  double* dg = grad_b ? dalloc<double>((size_t)B * n) : nullptr;
+  double* dbb = hess_bb ? dalloc<double>((size_t)B * n * n) : nullptr;
+  double* dab = hess_ab ? dalloc<double>((size_t)B * n * n) : nullptr;
+  cudaError_t e = (ws && dq && (!value || dv) && (!grad_b || dg) && (!hess_bb || dbb) && (!hess_ab || dab))
+                      ? cudaSuccess : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess) e = cudaMemcpy(dq, qa, sizeof(double) * B * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dq + (size_t)B * n, qb, sizeof(double) * B * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_correlation(dm, L, ws, B, dq, dq + (size_t)B * n, dv, dg, dbb, dab, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && dv) e = cudaMemcpy(value, dv, sizeof(double) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && dg) e = cudaMemcpy(grad_b, dg, sizeof(double) * B * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && dbb) e = cudaMemcpy(hess_bb, dbb, sizeof(double) * B * n * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && dab) e = cudaMemcpy(hess_ab, dab, sizeof(double) * B * n * n, cudaMemcpyDeviceToHost);
+  for (void* p : {(void*)dS, (void*)ws, (void*)dq, (void*)dv, (void*)dg, (void*)dbb, (void*)dab})
+    if (p) cudaFree(p);
+  if (e != cudaSuccess) return fail(PBAD_E_CUDA, "correlation: %s", cudaGetErrorString(e));
+  return PBAD_OK;
+}
+
 int32_t pbad_gpu_minimize(pbad_gpu_ctx* c, int32_t B, const double* history, const double* tau,
                           const double* x0, double* x_out, int32_t* iterations, int32_t* converged,
                           double* final_value, double* final_grad_norm) {

@@ -84,9 +84,9 @@ __device__ void forward_pass(const Env& E, const Arr& q, const Arr& world) {
 }
 
 // ConfigPass::make (adjoint.cpp:9-27); returns false for a non-finite q
-__device__ bool pass_make(const Env& E, const Arr& q, const Pass& P, bool want_d2) {
+__device__ bool pass_make(const Env& E, const Arr& q, const Pass& P, bool want_d2, bool check_finite = true) {
   const DModel& m = *E.m;
-  if (!all_finite(q, m.n)) return false;
+  if (check_finite && !all_finite(q, m.n)) return false;
   for (int i = 0; i < m.N; ++i) {
     double ql[6];
     const int off = m.dof_off[i];
@@ -1112,6 +1112,37 @@ cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdo
 }
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s) {
   k_step<<<grid_for(a.B), block_for(a.B), 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, out);
+  return cudaGetLastError();
+}
+// Batched correlation derivatives (adjoint.cpp:113-192: correlation_and_grad,
+// hessian_bb, hessian_ab) of I(qa, qb) with the (weighted) body integrals in
+// m.S / m.weighted_mass; ConfigPass::make does not validate, so neither does
+// this (non-finite inputs propagate).  Outputs per env, Hessians column-major.
+__global__ void __launch_bounds__(128) k_correlation(DModel m, Layout L, double* ws, long B, const double* qa,
+                                                     const double* qb, double* value, double* grad, double* hbb,
+                                                     double* hab) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= B) return;
+  Env E{&m, nullptr, nullptr, &L, ws, nullptr, B, e};
+  const int n = m.n;
+  const Arr qA{const_cast<double*>(qa) + (long)e * n, 1}, qB{const_cast<double*>(qb) + (long)e * n, 1};
+  const Pass pa = pass_at(E, 0), pb = pass_at(E, 1);
+  pass_make(E, qA, pa, false, false);
+  pass_make(E, qB, pb, hbb != nullptr, false);
+  if (value) value[e] = correlation_value(E, pa.world, pb.world);
+  if (grad || hbb) {
+    const Arr seeds = E.arr(L.seeds);
+    for (int i = 0; i < m.N; ++i) stm(seeds, i, mul(ldm(pa.world, i), ldg4(m.S + 16 * i)));
+    if (grad) functional_grad(E, seeds, pb, Arr{grad + (long)e * n, 1});
+    if (hbb) functional_hess(E, seeds, pb, Arr{hbb + (long)e * n * n, 1});
+  }
+  if (hab) correlation_hess_ab(E, pa, pb, Arr{hab + (long)e * n * n, 1});
+}
+
+cudaError_t launch_correlation(const DModel& m, const Layout& L, double* ws, long B, const double* qa,
+                               const double* qb, double* value, double* grad, double* hbb, double* hab,
+                               cudaStream_t s) {
+  k_correlation<<<grid_for(B), block_for(B), 0, s>>>(m, L, ws, B, qa, qb, value, grad, hbb, hab);
   return cudaGetLastError();
 }
 cudaError_t launch_eval(const KernelArgs& a, const double* hist, const double* tau, const double* x,
