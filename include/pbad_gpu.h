@@ -7,6 +7,7 @@
  *   pbad_gpu_rollout        replaces batch_simulate/simulate stepper.hpp:49-64, stepper.cpp:151-270
  *   pbad_gpu_eval           replaces StepObjective::evaluate/value objective.hpp:106-132
  *   pbad_gpu_minimize       replaces minimize()             optim.hpp:58-60, optim.cpp:244-250
+ *   pbad_gpu_simulate_baseline replaces simulate_baseline     stepper.hpp:54-55, stepper.cpp:168-202
  *   pbad_gpu_correlation    replaces correlation_and_grad / hessian_bb / hessian_ab
  *                                                           adjoint.hpp:80-82, adjoint.cpp:178-192
  *   pbad_gpu_begin/advance/ device-resident stepping for callers that keep
@@ -56,8 +57,16 @@ enum {
   PBAD_TRAJ_FAIL_LIMIT = 1,     /* "optimizer failed N consecutive steps around t=..." */
   PBAD_TRAJ_NONFINITE_INIT = 2, /* "objective is non-finite at the initial point" */
   PBAD_TRAJ_NONFINITE_CFG = 3,  /* "configuration contains a non-finite entry" */
-  PBAD_TRAJ_RUNNING = 4
+  PBAD_TRAJ_RUNNING = 4,
+  /* simulate_baseline (pbad_gpu_simulate_baseline) */
+  PBAD_TRAJ_DIVERGED = 5,       /* "diverged to a non-finite state at t=..." */
+  PBAD_TRAJ_SINGULAR_MASS = 6,  /* "step failed: singular generalized mass matrix" */
+  PBAD_TRAJ_STAGE_NONFINITE = 7 /* "step failed: configuration contains a non-finite entry" */
 };
+
+/* BaselineScheme (baseline.hpp:17) */
+enum { PBAD_BASELINE_FORWARD_EULER = 0, PBAD_BASELINE_SEMI_IMPLICIT = 1, PBAD_BASELINE_RK2 = 2,
+       PBAD_BASELINE_RK3 = 3, PBAD_BASELINE_RK4 = 4 };
 
 /* LinkSpec (model.hpp:57-62) with JointSpec and Geometry flattened. */
 typedef struct {
@@ -206,6 +215,14 @@ const double* pbad_gpu_state_device(const pbad_gpu_ctx* ctx);
 int32_t pbad_gpu_eval(pbad_gpu_ctx* ctx, int32_t B, const double* history,
                       const double* tau, const double* x, int32_t want_grad,
                       int32_t want_gn, double* value, double* grad, double* gn);
+
+/* simulate_baseline (stepper.cpp:168-202, baseline.cpp:56-206): explicit
+ * Newton-Euler integration with the context's model, forces (gravity, drag,
+ * contact, constant tau) and dt / duration; q_out [B][S+1][n] and energy
+ * [B][S+1][2] (KE, PE) optional, n_samples / status (PBAD_TRAJ_*) [B]. */
+int32_t pbad_gpu_simulate_baseline(pbad_gpu_ctx* ctx, int32_t scheme, int32_t B, const double* q0,
+                                   const double* qdot0, double* q_out, double* energy,
+                                   int32_t* n_samples, int32_t* status);
 
 /* Correlation derivatives of a batch of configuration pairs (adjoint.hpp:80-82:
  * correlation_and_grad, hessian_bb, hessian_ab), qa/qb [B][n];

@@ -508,6 +508,7 @@ def ref_lib():
         R.pbr_bundled_scene.restype = C.c_char_p
         R.pbr_bundled_scene.argtypes = [C.c_char_p]
         R.pbr_scene_simulate_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p]
+        R.pbr_simulate_baseline.argtypes = [vp, C.POINTER(ForcesC), C.c_int, C.POINTER(SimC), C.POINTER(TrajectoryC)]
         _ref = R
     return _ref
 
@@ -633,3 +634,15 @@ def ref_batch_simulate(model, forces, sims, workers=1):
         tr.c = tarr[i]
         tr.finalize()
     return trs
+
+
+def ref_simulate_baseline(model, forces, scheme, sim):
+    """The reference's simulate_baseline (stepper.cpp:168-202) on a RefModel."""
+    keep = []
+    n = model.n_dofs
+    f = forces_c(forces, n, keep)
+    sc = sim_c(sim, n, keep)
+    tr = OracleTrajectory(n, total_steps(sim))
+    if ref_lib().pbr_simulate_baseline(model.h, C.byref(f), int(scheme), C.byref(sc), C.byref(tr.c)) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return tr.finalize()

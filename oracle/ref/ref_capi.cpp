@@ -10,6 +10,7 @@
 
 #include "../pbad_oracle.h"
 #include "pbad/adjoint.hpp"
+#include "pbad/baseline.hpp"
 #include "pbad/benchmark.hpp"
 #include "pbad/collocation.hpp"
 #include "pbad/kinematics.hpp"
@@ -341,6 +342,21 @@ API int pbr_scene_simulate_csv(const char* json, const char* traj_csv, const cha
     const Trajectory traj = simulate(model, scene_forces(scene), scene_sim_config(scene));
     write_trajectory_csv(traj_csv, traj);
     write_energy_csv(energy_csv, traj);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// simulate_baseline (stepper.cpp:168-202): scheme 0..4 = BaselineScheme order
+API int pbr_simulate_baseline(void* mp, const pbo_forces* f, int scheme, const pbo_sim_config* s,
+                              pbo_trajectory* out) {
+  const KinematicModel& m = *static_cast<KinematicModel*>(mp);
+  try {
+    const Trajectory t = simulate_baseline(m, forces_of(f, m.total_dofs), static_cast<BaselineScheme>(scheme),
+                                           sim_of(s, m.total_dofs));
+    fill_traj(t, m.total_dofs, out);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -25,6 +25,7 @@ HEADER_SYMBOLS = [
     "pbad_gpu_build_scheme", "pbad_gpu_validate_configuration", "pbad_gpu_create", "pbad_gpu_destroy",
     "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
     "pbad_gpu_state_device", "pbad_gpu_eval", "pbad_gpu_minimize", "pbad_gpu_correlation",
+    "pbad_gpu_simulate_baseline",
 ]
 
 
@@ -102,6 +103,7 @@ def load():
         "pbad_gpu_model_info": ([vp, _dp, _dp, _ip, _dp, _ip], C.c_int32),
         "pbad_gpu_body_integral": ([C.POINTER(LinkSpec), _dp, _dp], C.c_int32),
         "pbad_gpu_correlation": ([vp, C.c_int32, _dp, _dp, _dp, _dp, _dp, _dp, _dp], C.c_int32),
+        "pbad_gpu_simulate_baseline": ([vp, C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, _ip, _ip], C.c_int32),
         "pbad_gpu_rotation_vector_matrix": ([_dp, _dp], C.c_int32),
         "pbad_gpu_rotation_vector_from_matrix": ([_dp, _dp], C.c_int32),
         "pbad_gpu_build_scheme": ([C.c_int32, C.c_double, _dp, _dp, _dp, _dp], C.c_int32),

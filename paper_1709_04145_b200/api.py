@@ -363,6 +363,22 @@ class GpuContext:
             gn = gn.transpose(0, 2, 1).copy()  # column-major -> row-major
         return value, grad, gn
 
+    def simulate_baseline(self, scheme, q0, qdot0, want_q=True, want_energy=True) -> Dict[str, np.ndarray]:
+        """Explicit Newton-Euler rollouts (simulate_baseline, stepper.cpp:168-202)
+        with this context's model, forces, dt and duration."""
+        q0 = _f64(q0)
+        B = q0.shape[0]
+        n, S = self.n, self.total_steps
+        q0 = _f64(q0, (B, n))
+        qdot0 = _f64(qdot0, (B, n))
+        q = np.zeros((B, S + 1, n)) if want_q else None
+        en = np.zeros((B, S + 1, 2)) if want_energy else None
+        ns = np.zeros(B, np.int32)
+        st = np.zeros(B, np.int32)
+        check(_lib.load().pbad_gpu_simulate_baseline(self._h, int(scheme), B, _p(q0), _p(qdot0), _p(q), _p(en),
+                                                     _pi(ns), _pi(st)))
+        return dict(q=q, energy=en, n_samples=ns, status=st)
+
     def correlation(self, qa, qb, weight_per_body=None, want=("value", "grad", "bb", "ab")):
         """Batched correlation derivatives of (qa[b], qb[b]) (adjoint.cpp:178-192):
         value [B], grad_b [B, n], hess_bb / hess_ab [B, n, n] (None where not
@@ -567,3 +583,46 @@ def batch_correlation(model: KinematicModel, qa, qb, weight_per_body=None, devic
     """All four derivatives for a batch of pairs in one launch."""
     v, g, bb, ab = _corr_ctx(model, device).correlation(qa, qb, weight_per_body)
     return [CorrelationDerivatives(float(v[b]), g[b], bb[b], ab[b]) for b in range(len(v))]
+
+
+# --- Newton-Euler baselines (stepper.hpp:54-55) -------------------------------
+
+_BL_ERRORS = {6: "step failed: singular generalized mass matrix",
+              7: "step failed: configuration contains a non-finite entry"}
+
+
+def simulate_baseline(model: KinematicModel, forces: ForceModel, scheme, sim: SimConfig,
+                      device: int = 0) -> Trajectory:
+    """stepper.cpp:168-202 on the GPU: samples, analytic KE / PE log, the
+    reference's error texts (no solve reports)."""
+    return batch_simulate_baseline(model, forces, scheme, [sim], device)[0]
+
+
+def batch_simulate_baseline(model: KinematicModel, forces: ForceModel, scheme, sims: Sequence[SimConfig],
+                            device: int = 0) -> List[Trajectory]:
+    """simulate_baseline for trajectories that share dt / duration (one launch)."""
+    sims = list(sims)
+    for sim in sims:
+        validate_configuration(model, sim.q0)
+        if sim.qdot0 is None or len(sim.qdot0) != model.total_dofs:
+            raise ModelError("initial velocity length does not match model DOF count")
+        if not sims[0].same_schedule(sim):
+            raise ValueError("batch_simulate_baseline: trajectories must share dt and duration")
+    ctx = GpuContext(model, forces, sims[0], device=device, max_batch=1)
+    out = ctx.simulate_baseline(scheme, np.stack([_f64(s.q0) for s in sims]),
+                                np.stack([_f64(s.qdot0) for s in sims]))
+    trs = []
+    for b, sim in enumerate(sims):
+        tr = Trajectory()
+        k = int(out["n_samples"][b])
+        for s in range(k):
+            tr.samples.append((s * sim.dt, out["q"][b, s].copy()))
+            tr.energy_log.append(EnergySample(s * sim.dt, float(out["energy"][b, s, 0]),
+                                              float(out["energy"][b, s, 1])))
+        st = int(out["status"][b])
+        if st == 5:
+            tr.error = f"diverged to a non-finite state at t={(k - 1) * sim.dt:f}"
+        elif st in _BL_ERRORS:
+            tr.error = _BL_ERRORS[st]
+        trs.append(tr)
+    return trs

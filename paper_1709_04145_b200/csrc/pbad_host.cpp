@@ -1219,6 +1219,73 @@ int32_t pbad_gpu_eval(pbad_gpu_ctx* c, int32_t B, const double* history, const d
   return PBAD_OK;
 }
 
+// simulate_baseline (stepper.cpp:168-202): explicit Newton-Euler schemes for
+// B trajectories of the context's model/forces with its dt and duration
+int32_t pbad_gpu_simulate_baseline(pbad_gpu_ctx* c, int32_t scheme, int32_t B, const double* q0,
+                                   const double* qdot0, double* q_out, double* energy, int32_t* n_samples,
+                                   int32_t* status) {
+  if (B < 1) return fail(PBAD_E_ARGUMENT, "batch %d must be >= 1", B);
+  if (scheme < 0 || scheme > 4) return fail(PBAD_E_ARGUMENT, "unknown baseline scheme %d", scheme);
+  if (!q0 || !qdot0 || !n_samples || !status) return fail(PBAD_E_ARGUMENT, "q0, qdot0, n_samples, status required");
+  const pbad_gpu_model& m = c->model;
+  const long N = m.N, n = m.n;
+  for (long k = 0; k < (long)B * n; ++k)
+    if (!std::isfinite(q0[k])) return fail(PBAD_E_MODEL, "configuration contains a non-finite entry");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long S = c->ka.sc.total_steps;
+  Layout L{};
+  long o = 0;
+  auto take = [&](long cnt) {
+    const long at = o;
+    o += cnt;
+    return at;
+  };
+  L.p_value = 0;
+  L.p_d1 = N * 16;
+  L.p_world = L.p_d1 + n * 16;
+  L.p_lever = L.p_world + N * 16;
+  L.p_d2 = L.p_lever + n * 16;
+  L.pass_stride = L.p_d2 + (long)m.n_d2 * 16;
+  L.pass = take(L.pass_stride);
+  L.seeds = take(N * 16);
+  L.adj = take(N * 16);
+  L.cot = take(N * 16);
+  L.hw0 = take(N * 16);  // tdot
+  L.hw1 = take(N * 16);  // quad
+  L.gn = take(n * n);    // mass matrix / its factor
+  L.x = take(n);
+  L.grad = take(n);
+  L.cand = take(n);
+  L.dir = take(n);
+  L.potgrad = take(n);   // Coriolis
+  L.g = take(n);         // generalized force
+  L.dd = take(n);        // right-hand side
+  L.hs = take(4 * n);    // stage accelerations
+  L.hy = take(4 * n);    // stage states
+  L.total = o;
+  double* ws = dalloc<double>((size_t)L.total * B);
+  double* dq = dalloc<double>((size_t)2 * B * n);
+  double* doq = q_out ? dalloc<double>((size_t)B * (S + 1) * n) : nullptr;
+  double* doe = energy ? dalloc<double>((size_t)B * (S + 1) * 2) : nullptr;
+  int* dns = dalloc<int>(B);
+  int* dst = dalloc<int>(B);
+  cudaError_t e = (ws && dq && dns && dst && (!q_out || doq) && (!energy || doe)) ? cudaSuccess
+                                                                                   : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess) e = cudaMemcpy(dq, q0, sizeof(double) * B * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dq + (size_t)B * n, qdot0, sizeof(double) * B * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = launch_baseline(c->ka, L, ws, B, scheme, dq, dq + (size_t)B * n, doq, doe, dns, dst, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && doq) e = cudaMemcpy(q_out, doq, sizeof(double) * B * (S + 1) * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && doe) e = cudaMemcpy(energy, doe, sizeof(double) * B * (S + 1) * 2, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(n_samples, dns, sizeof(int) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(status, dst, sizeof(int) * B, cudaMemcpyDeviceToHost);
+  for (void* p : {(void*)ws, (void*)dq, (void*)doq, (void*)doe, (void*)dns, (void*)dst})
+    if (p) cudaFree(p);
+  if (e != cudaSuccess) return fail(PBAD_E_CUDA, "simulate_baseline: %s", cudaGetErrorString(e));
+  return PBAD_OK;
+}
+
 // correlation_and_grad / hessian_bb / hessian_ab (adjoint.cpp:178-192) for a
 // batch of (qa, qb) pairs; WeightedBody::make (adjoint.cpp:29-41) on the host
 int32_t pbad_gpu_correlation(pbad_gpu_ctx* c, int32_t B, const double* qa, const double* qb,

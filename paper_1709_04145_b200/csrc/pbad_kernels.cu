@@ -860,6 +860,258 @@ __device__ double kinetic_energy(const Env& E, const Arr& q, const Arr& qdot) {
   return ke;
 }
 
+// ---------------------------------------------------------------------------
+// Newton-Euler baselines (baseline.cpp:56-206, simulate_baseline
+// stepper.cpp:168-202): explicit integration of M(q) qdd = f(q, qd) - c(q, qd)
+// with M = correlation_hess_ab(q, q) and the trace-form Coriolis vector.
+// Workspace (per env, BaselineLayout offsets in Layout fields): pass 0 with
+// d2, tdot / quad / seeds / cot / adj [N][16], mass [n][n], vectors.
+// ---------------------------------------------------------------------------
+enum { BL_OK = 0, BL_DIVERGED = 5, BL_SINGULAR = 6, BL_NONFINITE_CFG = 7 };
+
+// velocity_pass (baseline.cpp:20-54) into tdot (and quad)
+__device__ void bl_velocity_pass(const Env& E, const Pass& P, const Arr& qd, const Arr& tdot, const Arr* quad) {
+  const DModel& m = *E.m;
+  for (int i = 0; i < m.N; ++i) {
+    const int p = m.parent[i];
+    const int off = m.dof_off[i];
+    const int dof = m.dof_cnt[i];
+    M4 ldot = m4_zero();
+    for (int j = 0; j < dof; ++j) addto(ldot, scale(qd[off + j], ldm(P.d1, off + j)));
+    const M4 ptd = (p >= 0) ? ldm(tdot, p) : m4_zero();
+    const M4 pw = pworld(E, P, i);
+    const M4 V = ldm(P.value, i);
+    stm(tdot, i, add(mul(ptd, V), mul(pw, ldot)));
+    if (quad) {
+      M4 lq = m4_zero();
+      for (int l = 0; l < dof; ++l)
+        for (int j = 0; j < dof; ++j) {
+          const int a = j < l ? j : l, b = j < l ? l : j;  // d2_at(j, l), packed by the larger index
+          addto(lq, scale(qd[off + j] * qd[off + l], ldm(P.d2, m.d2_off[i] + b * (b + 1) / 2 + a)));
+        }
+      const M4 pq = (p >= 0) ? ldm(*quad, p) : m4_zero();
+      stm(*quad, i, add(add(mul(pq, V), mul(scale(2.0, ptd), ldot)), mul(pw, lq)));
+    }
+  }
+}
+
+struct BlArrs {
+  Arr tdot, quad, cot, mass, cor, gf, rhs;
+};
+
+// acceleration (baseline.cpp:137-147): mass_and_coriolis, generalized_force, LLT
+__device__ int bl_accel(const Env& E, const BlArrs& W, const Arr& q, const Arr& qd, const Arr& acc, double dt) {
+  const DModel& m = *E.m;
+  const DForces& f = *E.f;
+  const int n = m.n, N = m.N;
+  if (!all_finite(q, n)) return BL_NONFINITE_CFG;  // validate_configuration (model.cpp:114-123)
+  const Pass P = pass_at(E, 0);
+  pass_make(E, q, P, true, false);
+  bl_velocity_pass(E, P, qd, W.tdot, &W.quad);
+  correlation_hess_ab(E, P, P, W.mass);
+  const Arr seeds = E.arr(E.L->seeds);
+  for (int i = 0; i < N; ++i) stm(seeds, i, mul(ldm(W.quad, i), ldg4(m.S + 16 * i)));
+  functional_grad(E, seeds, P, W.cor);
+  // generalized_force (baseline.cpp:76-133)
+  bool have = false;
+  for (int i = 0; i < N; ++i) stm(W.cot, i, m4_zero());
+  if (f.gravity_nonzero) {
+    const double ghat[4] = {f.gravity[0], f.gravity[1], f.gravity[2], 0.0};
+    const double e4[4] = {0.0, 0.0, 0.0, 1.0};
+    for (int i = 0; i < N; ++i) {
+      double u[4];
+      mul_vec4(ldg4(m.S + 16 * i), e4, u);
+      M4 g;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) g.a[r + 4 * c] = ghat[r] * u[c];
+      stm(W.cot, i, add(ldm(W.cot, i), g));
+    }
+    have = true;
+  }
+  if (f.drag_d > 0.0) {
+    const double sc = 2.0 * f.drag_d / dt;
+    for (int i = 0; i < N; ++i)
+      stm(W.cot, i, sub(ldm(W.cot, i), mul(scale(sc, ldm(W.tdot, i)), ldg4(m.S + 16 * i))));
+    have = true;
+  }
+  if (f.has_contact && (f.d1 > 0.0 || f.d2 > 0.0)) {
+    const double* nr = f.normal;
+    double proj[9];  // I - n n^T, column-major
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int r = 0; r < 3; ++r) proj[r + 3 * c] = (r == c ? 1.0 : 0.0) - nr[r] * nr[c];
+    for (int i = 0; i < N; ++i) {
+      const M4 Wi = ldm(P.world, i);
+      const M4 Ti = ldm(W.tdot, i);
+      for (int sidx = m.sample_off[i]; sidx < m.sample_off[i + 1]; ++sidx) {
+        const double ph[4] = {m.samples[3 * sidx], m.samples[3 * sidx + 1], m.samples[3 * sidx + 2], 1.0};
+        double x[4];
+        mul_vec4(Wi, ph, x);
+        const double depth = f.plane_offset - dot3(nr, x);
+        if (depth <= 0.0) continue;
+        double fv[3];
+        const double k1 = 2.0 * f.d1 * depth;
+        for (int r = 0; r < 3; ++r) fv[r] = k1 * nr[r];
+        if (f.d2 > 0.0) {
+          double v[4], pv[3];
+          mul_vec4(Ti, ph, v);
+          for (int r = 0; r < 3; ++r) {
+            double a = proj[r] * v[0];
+            a = fma(proj[r + 3], v[1], a);
+            pv[r] = fma(proj[r + 6], v[2], a);
+          }
+          const double k2 = 2.0 * f.d2 * depth * dot3(pv, pv);
+          const double k3 = 2.0 * f.d2 * depth * depth / dt;
+          for (int r = 0; r < 3; ++r) fv[r] = fv[r] + (k2 * nr[r] - k3 * pv[r]);
+        }
+        const double fh[4] = {fv[0], fv[1], fv[2], 0.0};
+        M4 o;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) o.a[r + 4 * c] = fh[r] * ph[c];
+        stm(W.cot, i, add(ldm(W.cot, i), o));
+        have = true;
+      }
+    }
+  }
+  if (have) functional_grad(E, W.cot, P, W.gf);
+  else
+    for (int k = 0; k < n; ++k) W.gf[k] = 0.0;
+  if (f.tau_len == n)
+    for (int k = 0; k < n; ++k) W.gf[k] = W.gf[k] + f.tau[k];
+  for (int k = 0; k < n; ++k) W.rhs[k] = W.gf[k] - W.cor[k];
+  if (!llt_factor(W.mass, n)) return BL_SINGULAR;
+  llt_solve(W.mass, n, W.rhs, acc);
+  return BL_OK;
+}
+
+__device__ __forceinline__ bool bl_finite(const Arr& a, int n) { return all_finite(a, n); }
+
+// simulate_baseline, one thread per trajectory
+__global__ void __launch_bounds__(128) k_baseline(DModel m, DForces f, DSchedule sc, Layout L, double* ws, long B,
+                                                  int scheme, const double* q0, const double* qd0, double* oq,
+                                                  double* oe, int* nsamp, int* status) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= B) return;
+  Env E{&m, &f, &sc, &L, ws, nullptr, B, e};
+  const int n = m.n, S = sc.total_steps;
+  const double dt = sc.dt;
+  const BlArrs W{E.arr(L.hw0), E.arr(L.hw1), E.arr(L.cot), E.arr(L.gn), E.arr(L.potgrad), E.arr(L.g),
+                 E.arr(L.dd)};
+  const Arr q = E.arr(L.x), qd = E.arr(L.grad), sq = E.arr(L.cand), sqd = E.arr(L.dir);
+  const Arr a1 = E.arr(L.hs), a2 = E.arr(L.hs + n), a3 = E.arr(L.hs + 2 * n), a4 = E.arr(L.hs + 3 * n);
+  const Arr s2q = E.arr(L.hy), s2qd = E.arr(L.hy + n), s3q = E.arr(L.hy + 2 * n), s3qd = E.arr(L.hy + 3 * n);
+  for (int k = 0; k < n; ++k) {
+    q[k] = q0[(long)e * n + k];
+    qd[k] = qd0[(long)e * n + k];
+  }
+  const long S1 = S + 1;
+  // the initial sample is logged unconditionally (q0 was validated by the
+  // host), later ones with the inf substitution of stepper.cpp:193-198
+  auto record = [&](int k) {
+    double ke, pe;
+    const bool qf = k == 0 || bl_finite(q, n), vf = k == 0 || bl_finite(qd, n);
+    ke = (qf && vf) ? kinetic_energy(E, q, qd) : INFINITY;
+    if (qf) {
+      const Pass P = pass_at(E, 0);
+      pass_make(E, q, P, false, false);
+      pe = gravity_potential(E, P.world);
+    } else {
+      pe = INFINITY;
+    }
+    if (oq)
+      for (int j = 0; j < n; ++j) oq[((long)e * S1 + k) * n + j] = q[j];
+    if (oe) {
+      oe[((long)e * S1 + k) * 2] = ke;
+      oe[((long)e * S1 + k) * 2 + 1] = pe;
+    }
+  };
+  record(0);
+  int st = BL_OK, k = 0;
+  const double h = 0.5 * dt, d6 = dt / 6.0;
+  for (; k < S; ++k) {
+    if (!bl_finite(q, n) || !bl_finite(qd, n)) {
+      st = BL_DIVERGED;
+      break;
+    }
+    int rc = bl_accel(E, W, q, qd, a1, dt);
+    if (rc) { st = rc; break; }
+    if (scheme == 0) {  // forward_euler
+      for (int j = 0; j < n; ++j) {
+        const double qn = q[j] + dt * qd[j];
+        qd[j] = qd[j] + dt * a1[j];
+        q[j] = qn;
+      }
+    } else if (scheme == 1) {  // semi_implicit
+      for (int j = 0; j < n; ++j) {
+        qd[j] = qd[j] + dt * a1[j];
+        q[j] = q[j] + dt * qd[j];
+      }
+    } else if (scheme == 2) {  // rk2
+      for (int j = 0; j < n; ++j) {
+        sq[j] = q[j] + h * qd[j];
+        sqd[j] = qd[j] + h * a1[j];
+      }
+      rc = bl_accel(E, W, sq, sqd, a2, dt);
+      if (rc) { st = rc; break; }
+      for (int j = 0; j < n; ++j) {
+        q[j] = q[j] + dt * sqd[j];
+        qd[j] = qd[j] + dt * a2[j];
+      }
+    } else if (scheme == 3) {  // rk3
+      for (int j = 0; j < n; ++j) {
+        s2q[j] = q[j] + h * qd[j];
+        s2qd[j] = qd[j] + h * a1[j];
+      }
+      rc = bl_accel(E, W, s2q, s2qd, a2, dt);
+      if (rc) { st = rc; break; }
+      for (int j = 0; j < n; ++j) {
+        s3q[j] = q[j] + dt * (2.0 * s2qd[j] - qd[j]);
+        s3qd[j] = qd[j] + dt * (2.0 * a2[j] - a1[j]);
+      }
+      rc = bl_accel(E, W, s3q, s3qd, a3, dt);
+      if (rc) { st = rc; break; }
+      for (int j = 0; j < n; ++j) {
+        const double qn = q[j] + d6 * ((qd[j] + 4.0 * s2qd[j]) + s3qd[j]);
+        qd[j] = qd[j] + d6 * ((a1[j] + 4.0 * a2[j]) + a3[j]);
+        q[j] = qn;
+      }
+    } else {  // rk4
+      for (int j = 0; j < n; ++j) {
+        s2q[j] = q[j] + h * qd[j];
+        s2qd[j] = qd[j] + h * a1[j];
+      }
+      rc = bl_accel(E, W, s2q, s2qd, a2, dt);
+      if (rc) { st = rc; break; }
+      for (int j = 0; j < n; ++j) {
+        s3q[j] = q[j] + h * s2qd[j];
+        s3qd[j] = qd[j] + h * a2[j];
+      }
+      rc = bl_accel(E, W, s3q, s3qd, a3, dt);
+      if (rc) { st = rc; break; }
+      for (int j = 0; j < n; ++j) {  // s4 in (sq, sqd)
+        sq[j] = q[j] + dt * s3qd[j];
+        sqd[j] = qd[j] + dt * a3[j];
+      }
+      rc = bl_accel(E, W, sq, sqd, a4, dt);
+      if (rc) { st = rc; break; }
+      for (int j = 0; j < n; ++j) {
+        const double qn = q[j] + d6 * (((qd[j] + 2.0 * s2qd[j]) + 2.0 * s3qd[j]) + sqd[j]);
+        qd[j] = qd[j] + d6 * (((a1[j] + 2.0 * a2[j]) + 2.0 * a3[j]) + a4[j]);
+        q[j] = qn;
+      }
+    }
+    record(k + 1);
+  }
+  nsamp[e] = (st == BL_OK) ? S + 1 : k + 1;
+  status[e] = st;
+}
+
+
 // ForceModel::tau_at (objective.hpp:28-58) into dst
 __device__ void forces_tau_at(const Env& E, double t, const Arr& dst) {
   const DForces& f = *E.f;
@@ -1145,6 +1397,13 @@ cudaError_t launch_correlation(const DModel& m, const Layout& L, double* ws, lon
   k_correlation<<<grid_for(B), block_for(B), 0, s>>>(m, L, ws, B, qa, qb, value, grad, hbb, hab);
   return cudaGetLastError();
 }
+cudaError_t launch_baseline(const KernelArgs& a, const Layout& L, double* ws, long B, int scheme, const double* q0,
+                            const double* qd0, double* oq, double* oe, int* nsamp, int* status, cudaStream_t s) {
+  k_baseline<<<(unsigned)((B + 31) / 32), 32, 0, s>>>(a.m, a.f, a.sc, L, ws, B, scheme, q0, qd0, oq, oe, nsamp,
+                                                      status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_eval(const KernelArgs& a, const double* hist, const double* tau, const double* x,
                         int want_grad, int want_gn, double* value, double* grad, double* gn, int* err,
                         cudaStream_t s) {

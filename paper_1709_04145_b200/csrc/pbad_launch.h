@@ -59,6 +59,8 @@ cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* 
 cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
                         cudaStream_t s);
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s);
+cudaError_t launch_baseline(const KernelArgs& a, const Layout& L, double* ws, long B, int scheme, const double* q0,
+                            const double* qd0, double* oq, double* oe, int* nsamp, int* status, cudaStream_t s);
 cudaError_t launch_correlation(const DModel& m, const Layout& L, double* ws, long B, const double* qa,
                                const double* qb, double* value, double* grad, double* hbb, double* hab,
                                cudaStream_t s);

@@ -100,6 +100,15 @@ class ForceModel:
     actuation: Optional[ActuationSpec] = None
 
 
+class BaselineScheme(enum.IntEnum):
+    """baseline.hpp:17"""
+    forward_euler = 0
+    semi_implicit = 1
+    rk2 = 2
+    rk3 = 3
+    rk4 = 4
+
+
 class ObjectiveKind(enum.IntEnum):
     energy_form = 0
     residual_form = 1
