@@ -339,7 +339,10 @@ API int pbr_scene_simulate_csv(const char* json, const char* traj_csv, const cha
   try {
     const Scene scene = parse_scene(json);
     const KinematicModel model = scene_model(scene);
-    const Trajectory traj = simulate(model, scene_forces(scene), scene_sim_config(scene));
+    const Trajectory traj = scene_is_pbad(scene)
+                                ? simulate(model, scene_forces(scene), scene_sim_config(scene))
+                                : simulate_baseline(model, scene_forces(scene), scene_baseline_scheme(scene),
+                                                    scene_sim_config(scene));
     write_trajectory_csv(traj_csv, traj);
     write_energy_csv(energy_csv, traj);
     return 0;

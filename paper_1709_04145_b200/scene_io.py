@@ -27,7 +27,7 @@ import numpy as np
 
 from . import api
 from .scenes import Scene
-from .types import (ActuationKind, ActuationSpec, BoxGeometry, ContactModel, ForceModel, JointKind, JointSpec,
+from .types import (ActuationKind, ActuationSpec, BaselineScheme, BoxGeometry, ContactModel, ForceModel, JointKind, JointSpec,
                     LinkSpec, ModelError, ObjectiveKind, OptimizerKind, PointMass, PointMassGeometry, SimConfig,
                     Trajectory)
 
@@ -545,6 +545,15 @@ def scene_is_pbad(scene: Scene) -> bool:
     return getattr(scene, "integrator_kind", "pbad") == "pbad"
 
 
+def scene_baseline_scheme(scene: Scene) -> BaselineScheme:
+    """scene.cpp:420-428."""
+    k = getattr(scene, "integrator_kind", "pbad")
+    try:
+        return BaselineScheme[k]
+    except KeyError:
+        raise SceneError(f"scene: integrator '{k}' is not a baseline scheme") from None
+
+
 # ---------------------------------------------------------------- CSV out ---
 
 def _csv_row(values) -> str:
@@ -582,8 +591,8 @@ def simulate_scene(scene_path: str, out_dir: str, dt: float = 0.0, duration: flo
                    optimizer: str = "", objective: str = "", device: int = 0) -> Trajectory:
     """The reference CLI's `simulate` subcommand (pbad_cli.cpp:25-63) on the GPU
     step API: load the scene, apply the overrides, simulate, write
-    <out_dir>/trajectory.csv and energy.csv.  Baseline integrators are out of
-    scope and raise."""
+    <out_dir>/trajectory.csv and energy.csv; baseline integrator kinds run
+    simulate_baseline on the GPU (pbad_cli.cpp:49-53)."""
     scene = load_scene(scene_path)
     if dt > 0.0:
         scene.dt = dt
@@ -599,11 +608,13 @@ def simulate_scene(scene_path: str, out_dir: str, dt: float = 0.0, duration: flo
         scene.objective = ObjectiveKind.energy_form if objective == "energy" else ObjectiveKind.residual_form
     if scene.objective == ObjectiveKind.energy_form and scene.order != 2:
         raise SceneError("scene: the energy objective requires order 2")
-    if not scene_is_pbad(scene):
-        raise SceneError(f"scene: integrator '{scene.integrator_kind}' is a baseline scheme (not on the GPU path)")
     model = scene_model(scene)
     os.makedirs(out_dir, exist_ok=True)
-    traj = api.simulate(model, scene_forces(scene), scene_sim_config(scene), device=device)
+    if scene_is_pbad(scene):
+        traj = api.simulate(model, scene_forces(scene), scene_sim_config(scene), device=device)
+    else:
+        traj = api.simulate_baseline(model, scene_forces(scene), scene_baseline_scheme(scene),
+                                     scene_sim_config(scene), device=device)
     write_trajectory_csv(os.path.join(out_dir, "trajectory.csv"), traj)
     write_energy_csv(os.path.join(out_dir, "energy.csv"), traj)
     return traj

@@ -226,7 +226,9 @@ def test_csv_writers_byte_identical(tmp_path, name, duration, integ):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,duration,integ", CSV_CASES + [("swimmer", 0.5, {})])
+@pytest.mark.parametrize("name,duration,integ", CSV_CASES + [("swimmer", 0.5, {}),
+                                                              ("single5", 0.05, {"kind": "rk4"}),
+                                                              ("spider", 0.03, {"kind": "semi_implicit"})])
 def test_simulate_scene_on_gpu_matches_reference_csv(tmp_path, name, duration, integ):
     """The reference CLI's `simulate` on a scene file vs the GPU step API
     driven from the same file: trajectory.csv and energy.csv byte-identical."""
