@@ -491,7 +491,6 @@ __device__ __forceinline__ void chain_fk(const CK& K, double* V, double* dst) {
 
 // correlation_value(A, B) over two link arrays (adjoint.cpp:113-120)
 __device__ __forceinline__ double chain_cv(const CK& K, const double* A, const double* Bw) {
-  const DModel& m = K.m;
   double v = 0.0;
   for (int i = 0; i < K.N; ++i) {
     double a[4], b[4], as[4];
@@ -636,7 +635,6 @@ __device__ __forceinline__ double chain_forward(const CK& K, double* X, bool sto
 // Per-link row partials are reduced eight links at a time; lane k writes the
 // gradient entries it owns (index % 4 == k).
 __device__ __forceinline__ void chain_reverse(const CK& K, double* Gv) {
-  const DModel& m = K.m;
   const int N = K.N;
   const double gr = (K.r == 0) ? K.gz[0] : (K.r == 1) ? K.gz[1] : (K.r == 2) ? K.gz[2] : 0.0;
   double cI[4] = {0.0, 0.0, 0.0, 0.0}, cG[4] = {0.0, 0.0, 0.0, 0.0};
@@ -875,7 +873,6 @@ __device__ __forceinline__ void tau_at(const CK& K, const DForces& f, double t) 
 
 // fd_kinetic (stepper.cpp:14-22) + gravity_potential (baseline.cpp:219-229)
 __device__ __forceinline__ void chain_energy(const CK& K, const double* Wp, const double* Wn, double dt, double* ke, double* pe) {
-  const DModel& m = K.m;
   double k = 0.0, p = 0.0;
   const double ghat[4] = {K.gz[0], K.gz[1], K.gz[2], 0.0};
   for (int i = 0; i < K.N; ++i) {
