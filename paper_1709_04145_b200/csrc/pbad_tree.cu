@@ -157,6 +157,7 @@ struct W {
   double scl;                 // drag_d / dt^2
   double* ctv;                // [ns] contact value term of each sample (shared)
   int* cact;                  // [ns] sample active at the evaluated configuration (shared)
+  int* clist;                 // [ns] ascending indices of the active samples (GN assembly)
   double* cdep;               // [ns][4]: depth, pv0..pv2 (shared)
   double *abl, *abu, *cs;     // global: packed ab(col,row), ab(row,col); sample dd / jr
   __device__ __forceinline__ double* scr_k(int k) const { return scr + (long)k * MS * N; }
@@ -548,15 +549,27 @@ __device__ TREE_COLD void gn_assemble(const W& w) {
   // sample order (objective.cpp:69-70, 111-126, 249-254)
   const double s2 = 2.0 * w.scl;
   const double c2 = 2.0 * f.d1, c3 = 2.0 * f.d2;
+  // active samples compacted once (ascending: the reference's sample order),
+  // instead of every GN element scanning all samples
+  int nact = 0;
+  if (w.contact) {
+    for (int base = 0; base < td.ns; base += 32) {
+      const int k = base + w.lane;
+      const bool on = k < td.ns && w.cact[k];
+      const unsigned msk = __ballot_sync(FULL, on);
+      if (on) w.clist[nact + __popc(msk & ((1u << w.lane) - 1u))] = k;
+      nact += __popc(msk);
+    }
+    __syncwarp();
+  }
   for (int t = w.lane; t < w.np; t += 32) {
     const int rc = __ldg(td.pk + t);
     const int row = rc & 0xffff, col = rc >> 16;
     const double a1 = w.abl[t], a2 = w.abu[t];
     double p1 = w.drag ? 0.0 + s2 * a1 : 0.0;  // pot.gn(col, row)
     double p2 = w.drag ? 0.0 + s2 * a2 : 0.0;  // pot.gn(row, col)
-    if (w.contact)
-      for (int k = 0; k < td.ns; ++k) {
-        if (!w.cact[k]) continue;
+    for (int q = 0; q < nact; ++q) {
+        const int k = w.clist[q];
         const double* dd = w.cs + (long)k * 4 * n;
         const double* jr = dd + n;
         p1 = p1 + (c2 * dd[col]) * dd[row];
@@ -811,6 +824,7 @@ __global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel
     w.ctv = p; p += (td.ns + 1) & ~1;
     w.cdep = p; p += 4 * td.ns;
     w.cact = reinterpret_cast<int*>(p);
+    w.clist = w.cact + ((td.ns + 1) & ~1);
     double* g = tws + e * td.gstride;
     w.gn = g;
     w.hw0 = g + td.o_hw0;
@@ -1098,6 +1112,7 @@ __global__ void __launch_bounds__(32) k_tree_lbfgs(const __grid_constant__ DMode
     w.ctv = p; p += (td.ns + 1) & ~1;
     w.cdep = p; p += 4 * td.ns;
     w.cact = reinterpret_cast<int*>(p);
+    w.clist = w.cact + ((td.ns + 1) & ~1);
     double* g = tws + e * td.gstride;
     w.gn = g;
     w.hw0 = g + td.o_hw0;
@@ -1375,7 +1390,7 @@ static int tree_smem_doubles(const TreeDesc& td) {
   const int N16 = tree::MS * td.N, nv = (td.n + 1) & ~1;
   const int scr = (tree::TREE_SCR_ARRAYS * N16 > tree::MS * td.n) ? tree::TREE_SCR_ARRAYS * N16 : tree::MS * td.n;
   return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 8 * nv + 5 * td.N + 32 + ((td.ns + 1) & ~1) +
-         4 * td.ns + (td.ns + 1) / 2 + 2;
+         4 * td.ns + td.ns + 2;  // cact + clist ints
 }
 
 size_t tree_smem_bytes(const TreeDesc& td) { return sizeof(double) * (size_t)tree_smem_doubles(td); }
