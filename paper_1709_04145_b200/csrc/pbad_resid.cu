@@ -653,15 +653,41 @@ __device__ __forceinline__ void gnd_issue(const R& r, double* buf, int lt, int a
   const int U = r.U;
   double* As = buf + (c & 1) * 2 * GB * GQ;
   double* Bs = As + GB * GQ;
+  if ((U & 1) == 0) {
+    // k pairs: 16-byte copies (J column-major, U even: k-pairs are 16-byte aligned)
 #pragma unroll
-  for (int q = 0; q < GDK * GB / 256; ++q) {
-    const int t = lt + 256 * q;
-    const int col = t / GDK, kk = t - col * GDK;
-    const int k = c * GDK + kk, a = a0 + col, b = b0 + col;
-    if (k < U && a < U) gn_cpa8(As + col * GQ + kk, r.J + k + (long)U * a);
-    else As[col * GQ + kk] = -0.0;
-    if (k < U && b < U) gn_cpa8(Bs + col * GQ + kk, r.J + k + (long)U * b);
-    else Bs[col * GQ + kk] = 0.0;
+    for (int q = 0; q < GDK * GB / 512; ++q) {
+      const int t = lt + 256 * q;
+      const int col = t / (GDK / 2), kk = 2 * (t - col * (GDK / 2));
+      const int k = c * GDK + kk, a = a0 + col, b = b0 + col;
+      double* da = As + col * GQ + kk;
+      double* db = Bs + col * GQ + kk;
+      if (k < U && a < U) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(da)),
+                     "l"(r.J + k + (long)U * a) : "memory");
+      } else {
+        da[0] = -0.0;
+        da[1] = -0.0;
+      }
+      if (k < U && b < U) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(db)),
+                     "l"(r.J + k + (long)U * b) : "memory");
+      } else {
+        db[0] = 0.0;
+        db[1] = 0.0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < GDK * GB / 256; ++q) {
+      const int t = lt + 256 * q;
+      const int col = t / GDK, kk = t - col * GDK;
+      const int k = c * GDK + kk, a = a0 + col, b = b0 + col;
+      if (k < U && a < U) gn_cpa8(As + col * GQ + kk, r.J + k + (long)U * a);
+      else As[col * GQ + kk] = -0.0;
+      if (k < U && b < U) gn_cpa8(Bs + col * GQ + kk, r.J + k + (long)U * b);
+      else Bs[col * GQ + kk] = 0.0;
+    }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
