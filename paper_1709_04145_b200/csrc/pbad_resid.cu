@@ -472,6 +472,7 @@ __device__ __noinline__ void jacobian(const R& r) {
   double* Zs = Ls + u * NS;  // [u*u][N][16]
   stage_vl(r, Vs, Ls);
   __syncthreads();
+  PT_MARK(18);
   // correlation_hess_ab(pass_a, pass_b) composite inertias for every pair
   // (a = instant l, b = instant mm), pair = a * u + b (adjoint.cpp:139-141,169-174)
   const int npair = u * u;
@@ -549,32 +550,56 @@ __device__ __noinline__ void jacobian(const R& r) {
   }
   __syncthreads();
   PT_MARK(16);
-  // diagonal blocks: (functional_hess + c_m ab_mm^T) + pot.hess
+  // diagonal blocks: (functional_hess + c_m ab_mm^T) + pot.hess; a warp per
+  // pair of J columns, lanes down the rows (no index divisions, 24 loads in
+  // flight per lane)
   {
-    // flat over (instant, column, row); 4 independent elements per thread in flight
-    const int nn = n * n;
-    const int tot = u * nn;
-    for (int t0 = r.tid; t0 < tot; t0 += 4 * NT) {
-      double fh[4], jv[4], phv[4];
-      long jat[4];
+    const int NW = NT / 32, wid = r.tid >> 5, lane = r.tid & 31;
+    const int ncol = u * n;
+    for (int c0 = 2 * wid; c0 < ncol; c0 += 2 * NW) {
+      double fh[2][4], ph[2][4], jv[2][4];
+      double* jc[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int t = t0 + q * NT;
-        if (t < tot) {
-          const int mm = t / nn, e = t - mm * nn;
-          const int cc = e / n, rr = e - cc * n;
-          jat[q] = ((long)mm * n + rr) + (long)U * ((long)mm * n + cc);
-          fh[q] = r.FH[t];
-          phv[q] = r.grav ? 0.0 + r.PH[t] : 0.0;
-          jv[q] = r.J[jat[q]];
+      for (int h = 0; h < 2; ++h) {
+        const int col = min(c0 + h, ncol - 1);
+        const int mm = col / n, cc = col - mm * n;
+        const long fo = (long)mm * n * n + (long)cc * n;
+        jc[h] = r.J + (long)mm * n + (long)U * ((long)mm * n + cc);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = lane + 32 * q;
+          if (rr < n) {
+            fh[h][q] = r.FH[fo + rr];
+            ph[h][q] = r.grav ? 0.0 + r.PH[fo + rr] : 0.0;
+            jv[h][q] = jc[h][rr];
+          }
         }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (t0 + q * NT < tot) r.J[jat[q]] = (fh[q] + jv[q]) + phv[q];
+      for (int h = 0; h < 2; ++h)
+        if (c0 + h < ncol)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int rr = lane + 32 * q;
+            if (rr < n) jc[h][rr] = (fh[h][q] + jv[h][q]) + ph[h][q];
+          }
+      for (int rb = 128; rb < n; rb += 32) {  // n > 128: remaining rows
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = c0 + h;
+          const int rr = rb + lane;
+          if (col < ncol && rr < n) {
+            const int mm = col / n, cc = col - mm * n;
+            const long fo = (long)mm * n * n + (long)cc * n;
+            const double phv = r.grav ? 0.0 + r.PH[fo + rr] : 0.0;
+            jc[h][rr] = (r.FH[fo + rr] + jc[h][rr]) + phv;
+          }
+        }
+      }
     }
   }
   __syncthreads();
+  PT_MARK(17);
 }
 
 // grad = 2 J^T g (objective.cpp:326-327)
@@ -2017,9 +2042,10 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
 #if PBAD_PHASE_TIMING
   if (e == 0 && r.tid == 0)
     printf("phase cycles (block 0, %d iterations, %d accepted): conv %lld chol %lld solve %lld tpass %lld tres %lld "
-           "fpassres %lld jac %lld grad %lld gn %lld | chol: C %lld A %lld B %lld | diag-only %lld updA-only %lld | jac: acc %lld walks(t0) %lld fhess(t0)+sync %lld\n",
+           "fpassres %lld jac %lld grad %lld gn %lld | chol: C %lld A %lld B %lld | diag-only %lld updA-only %lld | jac: acc %lld walks(t0) %lld fhess(t0)+sync %lld combine %lld stage %lld\n",
            S.iters, S.acc, rss.pt[0], rss.pt[1], rss.pt[2], rss.pt[3], rss.pt[4], rss.pt[5], rss.pt[6], rss.pt[7], rss.pt[8],
-           rss.pt[9], rss.pt[10], rss.pt[11], rss.pt[12], rss.pt[13], rss.pt[14], rss.pt[15], rss.pt[16]);
+           rss.pt[9], rss.pt[10], rss.pt[11], rss.pt[12], rss.pt[13], rss.pt[14], rss.pt[15], rss.pt[16], rss.pt[17],
+           rss.pt[18]);
 #endif
 }
 
