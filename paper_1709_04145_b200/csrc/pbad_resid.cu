@@ -526,6 +526,46 @@ __device__ __noinline__ void jacobian(const R& r) {
     }
   }
   PT_MARK(15);
+  if (rd.chain) {
+    // chains: every entry of a diagonal block is written by exactly one
+    // functional_hess task, so the inertial and gravity walks of (instant,
+    // link) run in one task and finish J's diagonal block in place:
+    // J = (fh + J) + ph, the combine of the general path below
+    for (int t = r.tid; t < u * N; t += NT) {
+      const int mm = t / N;
+      const int i = rd.walk_order[t - mm * N];
+      const double* lm = Ls + mm * NS;
+      const double* vm = Vs + mm * NS;
+      const M4 aF = ldm4(r.fa(mm, 0) + 16 * i);
+      const M4 aP = r.grav ? ldm4(r.fa(u + mm, 0) + 16 * i) : m4_zero();
+      const int p = rss.parent[i];
+      const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
+      const M4 pd = mul(pw, ldm4(r.dd2(mm) + 16 * i));
+      const long jb = (long)mm * n + (long)U * ((long)mm * n);  // block (mm, mm)
+      {
+        const double hF = 0.0 + ddot(pd, aF);
+        const double hP = r.grav ? 0.0 + ddot(pd, aP) : 0.0;
+        double* je = r.J + jb + i + (long)U * i;
+        *je = (hF + *je) + hP;
+      }
+      const M4 d1 = ldm4(r.dd1(mm) + 16 * i);
+      M4 wF = mul_bt(aF, d1);
+      M4 wP = mul_bt(aP, d1);
+      for (int l = p; l >= 0; l = rss.parent[l]) {
+        const L3 ll = ldl3(lm + SMS * l);
+        const double hF = 0.0 + ddot3(ll, wF);
+        const double hP = r.grav ? 0.0 + ddot3(ll, wP) : 0.0;
+        double* e1 = r.J + jb + l + (long)U * i;
+        double* e2 = r.J + jb + i + (long)U * l;
+        *e1 = (hF + *e1) + hP;
+        *e2 = (hF + *e2) + hP;
+        bwd_step3(wF, vm + SMS * l);
+        if (r.grav) bwd_step3(wP, vm + SMS * l);
+      }
+    }
+    __syncthreads();
+    PT_MARK(16);
+  } else {
   // functional_hess (adjoint.cpp:66-101) of the inertial seeds and of the
   // gravity cotangents at every instant
   const int nsw = r.grav ? 2 * u : u;
@@ -597,6 +637,7 @@ __device__ __noinline__ void jacobian(const R& r) {
         }
       }
     }
+  }
   }
   __syncthreads();
   PT_MARK(17);
