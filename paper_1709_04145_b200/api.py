@@ -326,9 +326,19 @@ class GpuContext:
 
     def rollout(self, q0, qdot0, want_q=True, want_energy=True, pinned=False, out=None) -> Dict[str, np.ndarray]:
         q0 = _f64(q0)
-        qdot0 = _f64(qdot0)
         B = q0.shape[0]
-        o, bufs = out if out is not None else self._out_struct(B, want_q, want_energy, pinned)
+        q0 = _f64(q0, (B, self.n))
+        qdot0 = _f64(qdot0, (B, self.n))
+        if out is not None:
+            o, bufs = out
+            S = self.total_steps
+            if bufs["status"].shape[0] != B or bufs["iterations"].shape != (B, S):
+                raise ValueError("rollout: out buffers were allocated for a different batch or step count")
+            for k, tail in (("q", (S + 1, self.n)), ("energy", (S + 1, 2))):
+                if bufs[k] is not None and bufs[k].shape != (B,) + tail:
+                    raise ValueError(f"rollout: out[{k!r}] has shape {bufs[k].shape}, expected {(B,) + tail}")
+        else:
+            o, bufs = self._out_struct(B, want_q, want_energy, pinned)
         check(_lib.load().pbad_gpu_rollout(self._h, B, _p(q0), _p(qdot0), C.byref(o)))
         return bufs
 
@@ -556,10 +566,12 @@ class CorrelationDerivatives:
 
 
 def _corr_ctx(model: KinematicModel, device: int = 0) -> GpuContext:
-    ctx = getattr(model, "_corr_ctx", None)
+    # one cached context per (model, device)
+    per_dev = model.__dict__.setdefault("_corr_ctx", {})
+    ctx = per_dev.get(device)
     if ctx is None:
         ctx = GpuContext(model, ForceModel(), SimConfig(dt=0.01, duration=0.01), device=device)
-        model._corr_ctx = ctx
+        per_dev[device] = ctx
     return ctx
 
 

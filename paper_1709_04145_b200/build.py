@@ -12,6 +12,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -30,10 +31,9 @@ HOST_SOURCES = ["pbad_host.cpp"]
 
 
 def _run(cmd, log):
-    log.write(" ".join(cmd) + "\n")
-    log.flush()
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
-    log.write(r.stdout)
+    if log is not None:
+        log.write(" ".join(cmd) + "\n" + r.stdout)
     if r.returncode != 0:
         sys.stderr.write(r.stdout)
         raise RuntimeError(f"build failed: {' '.join(cmd)}")
@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(INCLUDE, "pbad_gpu.h"))
-    objs = []
+    objs, jobs = [], []
     with open(os.path.join(BUILD, "build.log"), "w") as log:
         for src in CUDA_SOURCES:
             s = os.path.join(CSRC, src)
@@ -60,15 +60,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
             o = os.path.join(BUILD, src + ".o")
             extra = [os.path.join(CSRC, "pbad_tree.cu")] if src == "pbad_tree_lbfgs.cu" else []
             if force or _stale(o, [s] + headers + extra):
-                _run([NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o], log)
+                jobs.append([NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o])
             objs.append(o)
         for src in HOST_SOURCES:
             s = os.path.join(CSRC, src)
             o = os.path.join(BUILD, src + ".o")
             if force or _stale(o, [s] + headers):
-                _run([NVCC, *ARCH, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-mfma",
-                      "-I", INCLUDE, "-I", CSRC, "-x", "cu", "-c", s, "-o", o], log)
+                jobs.append([NVCC, *ARCH, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-mfma",
+                             "-I", INCLUDE, "-I", CSRC, "-x", "cu", "-c", s, "-o", o])
             objs.append(o)
+        # translation units compile independently (ptxas dominates): run them concurrently
+        with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+            outs = list(ex.map(lambda c: _run(c, None), jobs))
+        for c, out in zip(jobs, outs):
+            log.write(" ".join(c) + "\n" + out)
         if force or _stale(LIB, objs):
             _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], log)
         # FP64 microbenchmark used as the roofline denominator (bench.py)

@@ -526,6 +526,9 @@ __device__ __noinline__ void jacobian(const R& r) {
     }
   }
   PT_MARK(15);
+  // the chain walks below read J entries the hess_ab tasks above wrote, from
+  // other threads (the two loops map tasks to threads differently)
+  __syncthreads();
   if (rd.chain) {
     // chains: every entry of a diagonal block is written by exactly one
     // functional_hess task, so the inertial and gravity walks of (instant,
