@@ -122,6 +122,13 @@ def flops_per_env_step(cfg, model, iters, accepted):
     return iters * rej + accepted * acc_extra + overhead + 320 * N + 24 * P
 
 
+def flops_total(cfg, model, iters, acc):
+    """Sum of flops_per_env_step over the [B][K] iteration / accepted counts
+    (one evaluation per distinct pair)."""
+    pairs, counts = np.unique(np.stack([iters.ravel(), acc.ravel()], axis=1), axis=0, return_counts=True)
+    return float(sum(c * flops_per_env_step(cfg, model, int(i), int(a)) for (i, a), c in zip(pairs, counts)))
+
+
 def measured_fp64_peak(device):
     import ctypes as C
     lib = C.CDLL(os.path.join(ROOT, "paper_1709_04145_b200", "libpbad_peak.so"))
@@ -224,22 +231,135 @@ def cpu_baseline(cfg, scene, model_links, n, steps=1, sample=None, target_s=15.0
     kind = "reference" if use_ref else "port"
     what = ("reference batch_simulate (stepper.cpp:204-270, WorkerPool)" if use_ref
             else "C oracle batch_simulate")
-    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{count} envs x {steps} step(s) of {cfg['desc'].split(':')[0]} (first envs of the bench "
-                      f"batch), {what}, {cores} threads, {el:.2f} s",
-            "seconds": el}
+    # the workers = 1 leg: one environment on one worker thread
+    t1 = time.perf_counter()
+    q1 = initial_states(cfg, scene, n, 0, 1)
+    s1 = sim_config(cfg, steps, 1 << 30)
+    s1.q0 = q1[0]
+    s1.qdot0 = np.zeros(n)
+    tr1 = run(mo, forces, [s1], workers=1)
+    el1 = time.perf_counter() - t1
+    one = (tr1[0].n_samples - 1) / el1
+    res = {"value": done / el, "unit": UNIT, "cores": cores, "kind": kind,
+           "sample": f"{count} envs x {steps} step(s) of {cfg['desc'].split(':')[0]} (first envs of the bench "
+                     f"batch), {what}, {cores} threads, {el:.2f} s",
+           "cpu_model": cpu_model(), "workers": cores,
+           "workers_1": {"value": one, "unit": UNIT, "sample": f"env 0 x {steps} step(s), workers = 1, {el1:.2f} s"},
+           "seconds": el}
+    if cfg["opt"] == "lm":
+        res["caveat"] = ("the reference build uses oracle/eigen_lite (Eigen3 is absent from the image): its dense "
+                         "LLT and GEMM are naive loops, slower than real Eigen, so this CPU figure understates the "
+                         "reference on the Newton path")
+    return res
 
 
-def dist_setup(ngpus):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or None
+
+
+def _free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    p = so.getsockname()[1]
+    so.close()
+    return p
+
+
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec this
+    script as N ranks (one process per GPU) on this node and exit with the
+    launcher's code.  Rank 0 prints the JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+class Dist:
+    """One process per GPU (torchrun env).  NCCL when every rank has its own
+    device; when more ranks than visible devices share them (a dry run on a
+    1-GPU box) the ranks map round-robin onto the devices and the
+    collectives run on gloo over host tensors (`oversubscribed`)."""
+
+    def __init__(self, ngpus):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != ngpus:
+            raise SystemExit(f"bench.py: --gpus {ngpus} but WORLD_SIZE={self.world} (launch one rank per GPU)")
+        import torch
+        ndev = torch.cuda.device_count()
+        if ndev < 1:
+            raise SystemExit("bench.py: no CUDA device visible (the PBAD GPU path has no CPU fallback)")
+        self.device = self.local % ndev
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(self.world)))
+        self.oversubscribed = local_world > ndev
+        self.backend = None
+        if self.world > 1:
+            import torch.distributed as dist
+            torch.cuda.set_device(self.device)
+            if self.oversubscribed:
+                dist.init_process_group("gloo")
+                self.backend = "gloo"
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+                self.backend = "nccl"
+
+    def _dev(self):
+        import torch
+        return torch.device("cpu") if self.backend == "gloo" else torch.device("cuda", self.device)
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def reduce(self, x, op="max"):
+        if self.world == 1:
+            return x
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return world, rank, local
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self._dev())
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def gather_final(self, ctx, B, n, stream):
+        """NCCL all-gather of every rank's final configurations [B][n] straight
+        from device memory (pbad_gpu_final_state, no host bounce); returns
+        (ms, gathered rows) or (None, None) at N = 1."""
+        if self.world == 1:
+            return None, None
+        import torch
+        import torch.distributed as dist
+        fin = torch.empty((B, n), dtype=torch.float64, device=f"cuda:{self.device}")
+        ctx.final_state(fin.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        self.barrier()
+        g0 = time.perf_counter()
+        if self.backend == "nccl":
+            allq = torch.empty((self.world * B, n), dtype=torch.float64, device=f"cuda:{self.device}")
+            dist.all_gather_into_tensor(allq, fin)
+            torch.cuda.synchronize()
+        else:
+            parts = [torch.empty((B, n), dtype=torch.float64) for _ in range(self.world)]
+            dist.all_gather(parts, fin.cpu())
+            allq = torch.cat(parts)
+        return (time.perf_counter() - g0) * 1e3, allq.shape[0]
+
+    def close(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
 
 
 def run_reference(args, cfg):
@@ -257,7 +377,7 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(cfg, args, world),
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: v for k, v in cb.items() if k != "seconds"},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": ("reference arm = the reference's own C++ (oracle/_ref: /root/reference/proj/src compiled "
                  "unmodified against oracle/eigen_lite, Eigen3 being absent) on the host cores; falls back "
@@ -266,12 +386,16 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def config_block(cfg, args, world):
-    return {"workload": cfg["desc"], "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world,
-            "n_links": cfg["links"] * (2 if cfg["scene"] == "chain" else 1), "dt": cfg["dt"],
-            "optimizer": cfg["opt"], "max_iters": 512, "consecutive_fail_limit": "unbounded (bench)",
-            "parallelism": f"dp{world} (independent env shards, weak scaling)",
-            "cache": "per-env solver state (~100 KB/env) > L2: inputs larger than L2, no flush needed"}
+def config_block(cfg, args, world, D=None):
+    c = {"workload": cfg["desc"], "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world,
+         "n_links": cfg["links"] * (2 if cfg["scene"] == "chain" else 1), "dt": cfg["dt"],
+         "optimizer": cfg["opt"], "max_iters": 512, "consecutive_fail_limit": "unbounded (bench)",
+         "parallelism": f"dp{world} (independent env shards, weak scaling)",
+         "cache": "per-env solver state (~100 KB/env) > L2: inputs larger than L2, no flush needed"}
+    if D is not None and D.world > 1:
+        c["collective_backend"] = D.backend
+        c["oversubscribed"] = D.oversubscribed
+    return c
 
 
 def main():
@@ -280,19 +404,28 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("PBAD_BENCH_CONFIG", "C3"))
+    ap.add_argument("--links", type=int, default=None,
+                    help="chain configs: override the link count (the metric's 'vs N links' sweep)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if os.environ.get("PBAD_BENCH_BATCH"):  # experiments only: batch-size sweeps
         cfg["batch"] = int(os.environ["PBAD_BENCH_BATCH"])
+    if args.links is not None:
+        if not cfg["scene"] in ("chain", "single_hinge"):
+            raise SystemExit("--links applies to the chain configurations (C1, C2, C3, C5)")
+        cfg["links"] = args.links // 2 if cfg["scene"] == "chain" else args.links
+        cfg["desc"] = cfg["desc"] + f" [link sweep: {args.links} links]"
     if args.impl == "reference":
         run_reference(args, cfg)
         return
+    relaunch_under_torchrun(args)
 
-    world, rank, local = dist_setup(args.gpus)
+    D = Dist(args.gpus)
+    world, rank, dev = D.world, D.rank, D.device
     import torch
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(dev)
     from paper_1709_04145_b200 import api, build as pbuild
     if not os.path.exists(pbuild.LIB):
         pbuild.build()
@@ -304,22 +437,23 @@ def main():
     W, K = args.warmup, args.steps
     total = W + K
     sim = sim_config(cfg, total, 1 << 30)
-    ctx = api.GpuContext(model, scene.forces(), sim, device=local, max_batch=B)
-    q0 = initial_states(cfg, scene, n, rank * B, B)
-    dq0 = torch.from_numpy(q0).to(f"cuda:{local}")
-    dqd = torch.zeros_like(dq0)
+    ctx = api.GpuContext(model, scene.forces(), sim, device=dev, max_batch=B)
+    q0 = initial_states(cfg, scene, n, rank * B, B)  # this rank's contiguous shard of the global batch
     # a dedicated stream: the legacy default stream has handle 0, which the C
-    # ABI reads as "the context's own stream"
-    stream = torch.cuda.Stream()
+    # ABI reads as "the context's own stream"; the inputs are written on it
+    stream = torch.cuda.Stream(device=dev)
     sh = stream.cuda_stream
+    with torch.cuda.stream(stream):
+        dq0 = torch.from_numpy(q0).to(f"cuda:{dev}", non_blocking=False)
+        dqd = torch.zeros_like(dq0)
+    stream.synchronize()
 
     # warm-up steps (untimed)
     ctx.begin(B, dq0.data_ptr(), dqd.data_ptr(), sh)
     ctx.advance(W, sh)
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    clocks = ClockSampler(local)
+    D.barrier()
+    clocks = ClockSampler(dev)
     clocks.start()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -329,88 +463,71 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = D.reduce(ms, "max")  # device time of the slowest rank
     out = ctx.sync_outputs(want_q=False, want_energy=False)
     iters = out["iterations"][:, W:W + K]
     acc = out["accepted"][:, W:W + K]
     st = out["status"]
 
-    # NCCL gather of the final states (outside the timed region)
-    gather_ms = None
-    if world > 1:
-        import ctypes
-        fin = torch.empty((B, n), dtype=torch.float64, device=f"cuda:{local}")
-        host = ctx.sync_outputs(want_q=True, want_energy=False)["q"][:, -1, :]
-        fin.copy_(torch.from_numpy(np.ascontiguousarray(host)))
-        allq = torch.empty((world * B, n), dtype=torch.float64, device=f"cuda:{local}")
-        torch.cuda.synchronize()
-        g0 = time.perf_counter()
-        torch.distributed.all_gather_into_tensor(allq, fin)
-        torch.cuda.synchronize()
-        gather_ms = (time.perf_counter() - g0) * 1e3
+    # NCCL gather of the final states, device to device (outside the timed region)
+    gather_ms, gathered = D.gather_final(ctx, B, n, stream)
 
-    # FLOP accounting for the roofline (per env, summed, this rank's launches)
-    fl = 0.0
-    for b in range(B):
-        fl += sum(flops_per_env_step(cfg, model, int(iters[b, s]), int(acc[b, s])) for s in range(K))
-    if world > 1:
-        t = torch.tensor([fl], dtype=torch.float64, device=f"cuda:{local}")
-        torch.distributed.all_reduce(t)
-        fl = float(t.item())
-
+    # FLOP accounting for the roofline (per env, summed over all ranks' envs)
+    fl = flops_total(cfg, model, iters, acc)
+    fl = D.reduce(fl, "sum")
     value = world * B * K / (ms / 1e3)
 
-    # end-to-end: the public rollout call with host buffers (H2D + kernels + D2H)
-    e2e = None
-    if rank == 0:
-        sim2 = sim_config(cfg, K, 1 << 30)
-        ctx2 = api.GpuContext(model, scene.forces(), sim2, device=local, max_batch=B)
-        pq0 = torch.from_numpy(np.ascontiguousarray(q0)).pin_memory().numpy()
-        pqd0 = torch.zeros(q0.shape, dtype=torch.float64).pin_memory().numpy()
-        out = ctx2.make_outputs(B, want_q=True, want_energy=True, pinned=True)  # caller-owned, outside the clock
-        ctx2.rollout(pq0, pqd0, out=out)  # warm-up: lazy staging allocation, kernel attributes
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        bufs = ctx2.rollout(pq0, pqd0, out=out)
-        el = time.perf_counter() - t0
-        h2d = 2 * q0.nbytes
-        d2h = sum(v.nbytes for v in bufs.values() if v is not None)
-        e2e = {"value": B * K / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d / K),
-               "d2h_bytes_per_step": int(d2h / K), "note": "pbad_gpu_rollout (C ABI) with pinned host q0/qdot0 in and trajectory + reports out into caller-allocated pinned buffers, wall clock, rank 0, after one warm-up rollout"}
-        del ctx2
+    # end-to-end: every rank's public rollout call with host buffers (H2D +
+    # kernels + D2H) started together; the job's time is the slowest rank's
+    sim2 = sim_config(cfg, K, 1 << 30)
+    ctx2 = api.GpuContext(model, scene.forces(), sim2, device=dev, max_batch=B)
+    pq0 = torch.from_numpy(np.ascontiguousarray(q0)).pin_memory().numpy()
+    pqd0 = torch.zeros(q0.shape, dtype=torch.float64).pin_memory().numpy()
+    o2 = ctx2.make_outputs(B, want_q=True, want_energy=True, pinned=True)  # caller-owned, outside the clock
+    ctx2.rollout(pq0, pqd0, out=o2)  # warm-up: lazy staging allocation, kernel attributes
+    torch.cuda.synchronize()
+    D.barrier()
+    t0 = time.perf_counter()
+    bufs = ctx2.rollout(pq0, pqd0, out=o2)
+    el = D.reduce(time.perf_counter() - t0, "max")
+    h2d = world * 2 * q0.nbytes
+    d2h = world * sum(v.nbytes for v in bufs.values() if v is not None)
+    e2e = {"value": world * B * K / el, "unit": UNIT, "h2d_bytes_per_step": int(h2d / K),
+           "d2h_bytes_per_step": int(d2h / K),
+           "note": (f"pbad_gpu_rollout (C ABI) on every rank concurrently: pinned host q0/qdot0 in, trajectory + "
+                    f"solve reports out into caller-allocated pinned buffers; wall clock of the slowest of "
+                    f"{world} rank(s) after one warm-up rollout; bytes summed over ranks")}
+    del ctx2
 
     if rank != 0:
-        if world > 1:
-            torch.distributed.barrier()
-            torch.distributed.destroy_process_group()
+        D.close()
         return
 
-    peak, lat = measured_fp64_peak(local)
+    peak, lat = measured_fp64_peak(dev)
     achieved = fl / (ms / 1e3) / 1e12 / world  # per GPU
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", f"{args.config}_dram_per_launch.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.links is None:
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            traffic = pj.get("dram_bytes_per_launch")
+            traffic_src = "not measured in this run: from " + os.path.relpath(prof, ROOT) + ": " + pj.get("source", "")
         except Exception:
             traffic = None
     cb = None
     if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1, rank-0 measurement
         try:
             cb = cpu_baseline(cfg, scene, scene.links, n)
-            cb = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # the oracle must never block the GPU line
             cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {ex}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": config_block(cfg, args, world),
+        "dtype": "f64", "data": "synthetic", "config": config_block(cfg, args, world, D),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if peak else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": "measured DFMA microbenchmark (paper_1709_04145_b200/csrc/pbad_peak.cu) on this GPU",
                      "flops_model": "SURVEY.md 8(d) canonical FP64 FLOPs per L-BFGS/LM iteration + per-step overhead",
                      "dfma_latency_cycles": lat},
@@ -426,11 +543,10 @@ def main():
         "mean_iterations_per_step": float(iters.mean()),
         "trajectories_ok": int(np.sum((st == 0) | (st == 4))),
         "gather_ms": gather_ms,
+        "gathered_envs": gathered,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    D.close()
 
 
 if __name__ == "__main__":

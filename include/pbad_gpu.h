@@ -194,9 +194,26 @@ int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* ctx);
 int32_t pbad_gpu_path(const pbad_gpu_ctx* ctx);
 
 /* batch_simulate on the GPU: q0/qdot0 host [B][n]; copies in, steps every
- * trajectory to completion, copies the requested outputs back. */
+ * trajectory to completion, copies the requested outputs back.  The device
+ * keeps a window of the trajectory (all of it when B*(S+1)*(n+2) doubles fit
+ * PBAD_TRAJ_WINDOW_MB, default 2048) and drains each window to the host
+ * buffers between launches, so long rollouts do not need B*S*n of HBM.
+ * device_ms: device time from the first step launch to the last (it includes
+ * the drains of all windows but the last when the rollout is windowed). */
 int32_t pbad_gpu_rollout(pbad_gpu_ctx* ctx, int32_t B, const double* q0,
                          const double* qdot0, pbad_rollout_out* out);
+
+/* batch_simulate sharded over several contexts (stepper.cpp:204-270: the
+ * trajectories share only the immutable model), one per device or several
+ * per device: context i steps the contiguous environments
+ * [B*i/n_ctx, B*(i+1)/n_ctx) of the host arrays, all contexts concurrently
+ * (no collective: every trajectory is independent).  The contexts must share
+ * the model's DOF count and the step count; results equal pbad_gpu_rollout
+ * of the whole batch on one context bit for bit.  device_ms = the slowest
+ * context's device time. */
+int32_t pbad_gpu_rollout_sharded(pbad_gpu_ctx* const* ctxs, int32_t n_ctx, int32_t B,
+                                 const double* q0, const double* qdot0,
+                                 pbad_rollout_out* out);
 
 /* device-resident stepping: q0/qdot0 are DEVICE pointers [B][n]; stream is
  * a cudaStream_t (NULL = the ctx stream).  advance() launches n_steps PBAD
@@ -204,8 +221,14 @@ int32_t pbad_gpu_rollout(pbad_gpu_ctx* ctx, int32_t B, const double* q0,
 int32_t pbad_gpu_begin(pbad_gpu_ctx* ctx, int32_t B, const double* d_q0,
                        const double* d_qdot0, void* stream);
 int32_t pbad_gpu_advance(pbad_gpu_ctx* ctx, int32_t n_steps, void* stream);
-/* copy outputs of the current batch to host buffers (synchronises) */
+/* copy outputs of the current batch to host buffers (synchronises the ctx
+ * stream after the stream of the last begin/advance; no device-wide barrier) */
 int32_t pbad_gpu_sync_outputs(pbad_gpu_ctx* ctx, pbad_rollout_out* out);
+/* the latest configuration of every environment of the current batch
+ * (its last recorded sample) into a DEVICE buffer [B][n], env-major, on
+ * `stream` (NULL = ctx stream), without a host round trip: the source of the
+ * multi-GPU final-state gather */
+int32_t pbad_gpu_final_state(pbad_gpu_ctx* ctx, double* d_dst, void* stream);
 /* device pointer of the current configurations hist1 [B][n] */
 const double* pbad_gpu_state_device(const pbad_gpu_ctx* ctx);
 

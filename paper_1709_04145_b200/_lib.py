@@ -25,7 +25,7 @@ HEADER_SYMBOLS = [
     "pbad_gpu_build_scheme", "pbad_gpu_validate_configuration", "pbad_gpu_create", "pbad_gpu_destroy",
     "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
     "pbad_gpu_state_device", "pbad_gpu_eval", "pbad_gpu_minimize", "pbad_gpu_correlation",
-    "pbad_gpu_simulate_baseline",
+    "pbad_gpu_simulate_baseline", "pbad_gpu_rollout_sharded", "pbad_gpu_final_state",
 ]
 
 
@@ -118,6 +118,9 @@ def load():
         "pbad_gpu_advance": ([vp, C.c_int32, vp], C.c_int32),
         "pbad_gpu_sync_outputs": ([vp, C.POINTER(RolloutOut)], C.c_int32),
         "pbad_gpu_state_device": ([vp], vp),
+        "pbad_gpu_rollout_sharded": ([C.POINTER(vp), C.c_int32, C.c_int32, _dp, _dp, C.POINTER(RolloutOut)],
+                                     C.c_int32),
+        "pbad_gpu_final_state": ([vp, vp, vp], C.c_int32),
         "pbad_gpu_eval": ([vp, C.c_int32, _dp, _dp, _dp, C.c_int32, C.c_int32, _dp, _dp, _dp], C.c_int32),
         "pbad_gpu_minimize": ([vp, C.c_int32, _dp, _dp, _dp, _dp, _ip, _ip, _dp, _dp], C.c_int32),
     }

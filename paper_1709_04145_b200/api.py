@@ -359,6 +359,11 @@ class GpuContext:
     def state_device_ptr(self) -> int:
         return _lib.load().pbad_gpu_state_device(self._h)
 
+    def final_state(self, d_dst: int, stream: int = 0):
+        """Latest configuration of every environment of the current batch into
+        the device buffer d_dst [B][n] (no host round trip)."""
+        check(_lib.load().pbad_gpu_final_state(self._h, C.c_void_p(d_dst), C.c_void_p(stream) if stream else None))
+
     def eval(self, history, x, want_grad=True, want_gn=False, tau=None):
         history = _f64(history)
         B = history.shape[0]
@@ -455,6 +460,25 @@ def _trajectories(ctx: GpuContext, sims: Sequence[SimConfig], bufs) -> List[Traj
     return out
 
 
+def rollout_sharded(ctxs: Sequence[GpuContext], q0, qdot0, want_q=True, want_energy=True, pinned=False,
+                    out=None) -> Dict[str, np.ndarray]:
+    """One batch over several contexts (one per device, or several on one):
+    context i steps the contiguous shard [B*i/k, B*(i+1)/k) of the batch,
+    all concurrently (pbad_gpu_rollout_sharded); equal to one context's
+    rollout bit for bit."""
+    if not ctxs:
+        raise ValueError("rollout_sharded needs at least one context")
+    c0 = ctxs[0]
+    q0 = _f64(q0)
+    B = q0.shape[0]
+    q0 = _f64(q0, (B, c0.n))
+    qdot0 = _f64(qdot0, (B, c0.n))
+    o, bufs = out if out is not None else c0._out_struct(B, want_q, want_energy, pinned)
+    arr = (C.c_void_p * len(ctxs))(*[c._h for c in ctxs])
+    check(_lib.load().pbad_gpu_rollout_sharded(arr, len(ctxs), B, _p(q0), _p(qdot0), C.byref(o)))
+    return bufs
+
+
 def _check_sim(model: KinematicModel, sim: SimConfig):
     validate_configuration(model, sim.q0)
     if sim.qdot0 is None or len(sim.qdot0) != model.total_dofs:
@@ -464,10 +488,11 @@ def _check_sim(model: KinematicModel, sim: SimConfig):
 
 
 def batch_simulate(model: KinematicModel, forces: ForceModel, sims: Sequence[SimConfig], workers: int = 1,
-                   device: int = 0) -> List[Trajectory]:
+                   device: int = 0, devices: Optional[Sequence[int]] = None) -> List[Trajectory]:
     """stepper.cpp:204-270: per-trajectory results equal simulate(); errors are
     recorded per trajectory.  `workers` is accepted for signature parity (the
-    GPU grid replaces the WorkerPool)."""
+    GPU grid replaces the WorkerPool).  `devices` shards every group of
+    trajectories over those devices (one context each, contiguous shards)."""
     if workers < 1:
         raise ModelError("worker count must be >= 1")
     results: List[Optional[Trajectory]] = [None] * len(sims)
@@ -485,10 +510,18 @@ def batch_simulate(model: KinematicModel, forces: ForceModel, sims: Sequence[Sim
         else:
             groups.append((sim, [i]))
     for rep, idx in groups:
-        ctx = GpuContext(model, forces, rep, device=device, max_batch=len(idx))
         q0 = np.stack([_f64(sims[i].q0) for i in idx])
         qd = np.stack([_f64(sims[i].qdot0) for i in idx])
-        bufs = ctx.rollout(q0, qd)
+        devs = list(devices) if devices else [device]
+        devs = devs[:len(idx)]
+        if len(devs) > 1:
+            shard = -(-len(idx) // len(devs))
+            ctxs = [GpuContext(model, forces, rep, device=d, max_batch=shard) for d in devs]
+            ctx = ctxs[0]
+            bufs = rollout_sharded(ctxs, q0, qd)
+        else:
+            ctx = GpuContext(model, forces, rep, device=devs[0], max_batch=len(idx))
+            bufs = ctx.rollout(q0, qd)
         for i, tr in zip(idx, _trajectories(ctx, [sims[i] for i in idx], bufs)):
             results[i] = tr
     return results  # type: ignore[return-value]

@@ -994,13 +994,12 @@ __global__ void __launch_bounds__(kThreads) k_chain_init(DModel m, DForces f, DS
     ke += 0.5 * term;
     pe -= d;
   }
-  const long S1 = sc.total_steps + 1;
   for (int k = K.r; k < n; k += 4)
-    if (out.q) out.q[(K.e * S1) * n + k] = vat(K, K.h1, k);
+    if (out.q) out.q[out.qrow(K.e, 0) * n + k] = vat(K, K.h1, k);
   if (K.r == 0) {
     if (out.energy) {
-      out.energy[(K.e * S1) * 2] = ke;
-      out.energy[(K.e * S1) * 2 + 1] = pe;
+      out.energy[out.qrow(K.e, 0) * 2] = ke;
+      out.energy[out.qrow(K.e, 0) * 2 + 1] = pe;
     }
     ival(K, IS_NSAMP) = 1;
     ival(K, IS_RUN) = (sc.total_steps > 0) ? TR_RUNNING : TR_OK;
@@ -1061,11 +1060,11 @@ __global__ void __launch_bounds__(kThreads) k_chain_step(DModel m, DForces f, DS
   const bool converged = s.status == ST_CONVERGED;
   const double gnorm = qinfnorm(K, K.g);
   if (K.r == 0) {
-    if (out.iterations) out.iterations[K.e * S + step] = s.iters;
-    if (out.converged) out.converged[K.e * S + step] = converged;
-    if (out.accepted) out.accepted[K.e * S + step] = s.acc;
-    if (out.final_value) out.final_value[K.e * S + step] = s.value;
-    if (out.final_grad_norm) out.final_grad_norm[K.e * S + step] = gnorm;
+    if (out.iterations) out.iterations[out.rrow(K.e, step)] = s.iters;
+    if (out.converged) out.converged[out.rrow(K.e, step)] = converged;
+    if (out.accepted) out.accepted[out.rrow(K.e, step)] = s.acc;
+    if (out.final_value) out.final_value[out.rrow(K.e, step)] = s.value;
+    if (out.final_grad_norm) out.final_grad_norm[out.rrow(K.e, step)] = gnorm;
     ival(K, IS_NREP) = step + 1;
   }
   const int fs = converged ? 0 : ival(K, IS_FAIL) + 1;
@@ -1083,13 +1082,12 @@ __global__ void __launch_bounds__(kThreads) k_chain_step(DModel m, DForces f, DS
   qsync(K);
   double ke, pe;
   chain_energy(K, K.tk, K.tk1, sc.dt, &ke, &pe);
-  const long S1 = S + 1;
   for (int k = K.r; k < n; k += 4)
-    if (out.q) out.q[(K.e * S1 + step + 1) * n + k] = vat(K, K.h1, k);
+    if (out.q) out.q[out.qrow(K.e, step + 1) * n + k] = vat(K, K.h1, k);
   if (K.r == 0) {
     if (out.energy) {
-      out.energy[(K.e * S1 + step + 1) * 2] = ke;
-      out.energy[(K.e * S1 + step + 1) * 2 + 1] = pe;
+      out.energy[out.qrow(K.e, step + 1) * 2] = ke;
+      out.energy[out.qrow(K.e, step + 1) * 2 + 1] = pe;
     }
     ival(K, IS_STEP) = step + 1;
     ival(K, IS_NSAMP) = step + 2;

@@ -1195,11 +1195,11 @@ __global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedu
   const bool converged = s.status == ST_CONVERGED;
   const double gnorm = qinfnorm(C, C.g);
   if (C.r == 0) {
-    if (out.iterations) out.iterations[C.ge * S + step] = s.iters;
-    if (out.converged) out.converged[C.ge * S + step] = converged;
-    if (out.accepted) out.accepted[C.ge * S + step] = s.acc;
-    if (out.final_value) out.final_value[C.ge * S + step] = s.value;
-    if (out.final_grad_norm) out.final_grad_norm[C.ge * S + step] = gnorm;
+    if (out.iterations) out.iterations[out.rrow(C.ge, step)] = s.iters;
+    if (out.converged) out.converged[out.rrow(C.ge, step)] = converged;
+    if (out.accepted) out.accepted[out.rrow(C.ge, step)] = s.acc;
+    if (out.final_value) out.final_value[out.rrow(C.ge, step)] = s.value;
+    if (out.final_grad_norm) out.final_grad_norm[out.rrow(C.ge, step)] = gnorm;
     ival(C, IS_NREP) = step + 1;
   }
   const int fs = converged ? 0 : ival(C, IS_FAIL) + 1;
@@ -1216,13 +1216,12 @@ __global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedu
   qsync(C);
   qmap2(C, C.h1, C.x, C.x, [](double a, double) { return a; });
   qsync(C);
-  const long S1 = S + 1;
   for (int k = C.r; k < n; k += 4)
-    if (out.q) out.q[(C.ge * S1 + step + 1) * n + k] = vat(C, C.h1, k);
+    if (out.q) out.q[out.qrow(C.ge, step + 1) * n + k] = vat(C, C.h1, k);
   if (C.r == 0) {
     if (out.energy) {
-      out.energy[(C.ge * S1 + step + 1) * 2] = ke;
-      out.energy[(C.ge * S1 + step + 1) * 2 + 1] = pe;
+      out.energy[out.qrow(C.ge, step + 1) * 2] = ke;
+      out.energy[out.qrow(C.ge, step + 1) * 2 + 1] = pe;
     }
     ival(C, IS_STEP) = step + 1;
     ival(C, IS_NSAMP) = step + 2;

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "pbad_launch.h"
@@ -497,8 +498,10 @@ struct pbad_gpu_ctx {
   int steps_done = 0;
   // device outputs for the current batch
   Outputs dout{};
-  long out_cap = 0;
+  long out_q_cap = 0, out_r_cap = 0;  // allocated sample / report slots
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_work = nullptr;       // orders the ctx stream after a caller's stream
+  cudaStream_t work_stream = nullptr;  // stream of the last begin/advance
   double device_ms = 0.0;
   double* d_q0 = nullptr;
   double* d_qd0 = nullptr;
@@ -517,6 +520,7 @@ struct pbad_gpu_ctx {
     if (d_in) cudaFree(d_in);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_work) cudaEventDestroy(ev_work);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -747,29 +751,52 @@ bool ensure_v1(pbad_gpu_ctx* c) {
   return true;
 }
 
-int32_t ensure_outputs(pbad_gpu_ctx* c, long B) {
-  const long S = c->total_steps, n = c->model.n;
-  if (c->out_cap >= B) return PBAD_OK;
-  cudaFree(c->dout.q);
-  cudaFree(c->dout.energy);
-  cudaFree(c->dout.iterations);
-  cudaFree(c->dout.converged);
-  cudaFree(c->dout.accepted);
-  cudaFree(c->dout.final_value);
-  cudaFree(c->dout.final_grad_norm);
-  c->dout = Outputs{};
-  c->dout.q = dalloc<double>(B * (S + 1) * n);
-  c->dout.energy = dalloc<double>(B * (S + 1) * 2);
-  c->dout.iterations = dalloc<int>(B * S);
-  c->dout.converged = dalloc<int>(B * S);
-  c->dout.accepted = dalloc<int>(B * S);
-  c->dout.final_value = dalloc<double>(B * S);
-  c->dout.final_grad_norm = dalloc<double>(B * S);
-  if (!c->dout.q || !c->dout.energy || !c->dout.iterations || !c->dout.converged || !c->dout.accepted ||
-      !c->dout.final_value || !c->dout.final_grad_norm)
-    return fail(PBAD_E_CUDA, "cudaMalloc of rollout outputs failed (B=%ld)", B);
-  c->out_cap = B;
+// Device outputs for B environments and a window of W steps: W + 1 sample
+// slots and W report slots per environment (W = S: the whole trajectory).
+int32_t ensure_outputs(pbad_gpu_ctx* c, long B, long W) {
+  const long n = c->model.n;
+  const long need_q = B * (W + 1), need_r = B * W;
+  if (c->out_q_cap < need_q || c->out_r_cap < need_r) {
+    cudaFree(c->dout.q);
+    cudaFree(c->dout.energy);
+    cudaFree(c->dout.iterations);
+    cudaFree(c->dout.converged);
+    cudaFree(c->dout.accepted);
+    cudaFree(c->dout.final_value);
+    cudaFree(c->dout.final_grad_norm);
+    c->dout = Outputs{};
+    c->out_q_cap = c->out_r_cap = 0;
+    c->dout.q = dalloc<double>(need_q * n);
+    c->dout.energy = dalloc<double>(need_q * 2);
+    c->dout.iterations = dalloc<int>(need_r);
+    c->dout.converged = dalloc<int>(need_r);
+    c->dout.accepted = dalloc<int>(need_r);
+    c->dout.final_value = dalloc<double>(need_r);
+    c->dout.final_grad_norm = dalloc<double>(need_r);
+    if (!c->dout.q || !c->dout.energy || !c->dout.iterations || !c->dout.converged || !c->dout.accepted ||
+        !c->dout.final_value || !c->dout.final_grad_norm)
+      return fail(PBAD_E_CUDA, "cudaMalloc of rollout outputs failed (B=%ld, window %ld steps)", B, W);
+    c->out_q_cap = need_q;
+    c->out_r_cap = need_r;
+  }
+  c->dout.qs = W + 1;
+  c->dout.rs = W;
+  c->dout.qbase = 0;
+  c->dout.rbase = 0;
   return PBAD_OK;
+}
+
+// Steps per output window of a rollout: the whole trajectory when its
+// samples fit the budget (PBAD_TRAJ_WINDOW_MB, default 2048 MB of device
+// memory), else the largest window that does; windows are drained to the
+// host between launches so a rollout's device footprint does not grow with S.
+long window_steps(const pbad_gpu_ctx* c, long B) {
+  const long S = c->total_steps, n = c->model.n;
+  double mb = 2048.0;
+  if (const char* e = std::getenv("PBAD_TRAJ_WINDOW_MB")) mb = std::atof(e);
+  const double per_step = (double)B * (8.0 * (n + 2) + 4.0 * 3 + 16.0);
+  long W = (long)(mb * 1048576.0 / per_step) - 1;
+  return std::max(1L, std::min(S, W));
 }
 
 cudaStream_t pick(pbad_gpu_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
@@ -1062,7 +1089,8 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     c->owned.push_back(c->tws);
   }
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_work, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return fail(PBAD_E_CUDA, "stream/event creation failed");
   }
@@ -1084,25 +1112,29 @@ const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) {
   return c->chain ? c->ca.cw + c->ca.L.h1 : c->ka.ws + c->ka.L.hist1 * c->ka.B;
 }
 
-int32_t pbad_gpu_begin(pbad_gpu_ctx* c, int32_t B, const double* d_q0, const double* d_qdot0, void* stream) {
+}  // extern "C"
+
+namespace {
+
+int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, const double* d_qdot0, cudaStream_t s) {
   if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
   CUDA_TRY(cudaSetDevice(c->device));
-  int32_t rc = ensure_outputs(c, B);
+  int32_t rc = ensure_outputs(c, B, W);
   if (rc) return rc;
   c->B = B;
   c->ka.B = B;
   c->ca.B = B;
   c->steps_done = 0;
   c->device_ms = 0.0;
-  if (c->chain) CUDA_TRY(launch_chain_init(c->ca, d_q0, d_qdot0, c->dout, pick(c, stream)));
-  else CUDA_TRY(launch_init(c->ka, d_q0, d_qdot0, c->dout, pick(c, stream)));
+  c->work_stream = s;
+  if (c->chain) CUDA_TRY(launch_chain_init(c->ca, d_q0, d_qdot0, c->dout, s));
+  else CUDA_TRY(launch_init(c->ka, d_q0, d_qdot0, c->dout, s));
   return PBAD_OK;
 }
 
-int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
-  CUDA_TRY(cudaSetDevice(c->device));
-  const cudaStream_t s = pick(c, stream);
-  for (int k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
+int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
+  c->work_stream = s;
+  for (long k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
     CUDA_TRY(c->chain4  ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain ? launch_chain_step(c->ca, c->dout, s)
              : c->tree  ? launch_tree_step(c->ka, c->td, c->tws, c->dout, s)
@@ -1111,39 +1143,78 @@ int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
   return PBAD_OK;
 }
 
-int32_t pbad_gpu_sync_outputs(pbad_gpu_ctx* c, pbad_rollout_out* o) {
-  CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaDeviceSynchronize());
-  const long B = c->B, S = c->total_steps, n = c->model.n;
-  if (o->q) CUDA_TRY(cudaMemcpy(o->q, c->dout.q, sizeof(double) * B * (S + 1) * n, cudaMemcpyDeviceToHost));
-  if (o->energy)
-    CUDA_TRY(cudaMemcpy(o->energy, c->dout.energy, sizeof(double) * B * (S + 1) * 2, cudaMemcpyDeviceToHost));
-  if (o->iterations)
-    CUDA_TRY(cudaMemcpy(o->iterations, c->dout.iterations, sizeof(int) * B * S, cudaMemcpyDeviceToHost));
-  if (o->converged)
-    CUDA_TRY(cudaMemcpy(o->converged, c->dout.converged, sizeof(int) * B * S, cudaMemcpyDeviceToHost));
-  if (o->accepted)
-    CUDA_TRY(cudaMemcpy(o->accepted, c->dout.accepted, sizeof(int) * B * S, cudaMemcpyDeviceToHost));
-  if (o->final_value)
-    CUDA_TRY(cudaMemcpy(o->final_value, c->dout.final_value, sizeof(double) * B * S, cudaMemcpyDeviceToHost));
-  if (o->final_grad_norm)
-    CUDA_TRY(cudaMemcpy(o->final_grad_norm, c->dout.final_grad_norm, sizeof(double) * B * S,
-                        cudaMemcpyDeviceToHost));
-  const int* iws = c->chain ? c->ca.ci : c->ka.iws;
-  if (o->n_samples) CUDA_TRY(cudaMemcpy(o->n_samples, iws + (long)IS_NSAMP * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
-  if (o->status) CUDA_TRY(cudaMemcpy(o->status, iws + (long)IS_RUN * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
-  if (o->fail_streak) CUDA_TRY(cudaMemcpy(o->fail_streak, iws + (long)IS_FAIL * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
-  if (o->n_reports) CUDA_TRY(cudaMemcpy(o->n_reports, iws + (long)IS_NREP * B, sizeof(int) * B, cudaMemcpyDeviceToHost));
-  if (o->device_ms) o->device_ms[0] = (float)c->device_ms;
+// the ctx stream waits for the caller's stream of the last begin/advance
+int32_t join_work(pbad_gpu_ctx* c) {
+  if (c->work_stream && c->work_stream != c->stream) {
+    CUDA_TRY(cudaEventRecord(c->ev_work, c->work_stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_work, 0));
+  }
   return PBAD_OK;
 }
 
-int32_t pbad_gpu_rollout(pbad_gpu_ctx* c, int32_t B, const double* q0, const double* qdot0,
-                         pbad_rollout_out* out) {
-  if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
-  CUDA_TRY(cudaSetDevice(c->device));
+// Copies samples [s_lo, s_hi] and reports [r_lo, r_hi) held in the current
+// output window to the host buffers of `o`, whose environment 0 is this
+// context's environment env0 (sharded rollouts), on the ctx stream.
+int32_t drain_window(pbad_gpu_ctx* c, const pbad_rollout_out* o, long env0, long s_lo, long s_hi, long r_lo,
+                     long r_hi) {
+  const long B = c->B, S = c->total_steps, n = c->model.n;
+  const Outputs& d = c->dout;
+  const cudaStream_t st = c->stream;
+  if (s_hi >= s_lo) {
+    const long cnt = s_hi - s_lo + 1;
+    if (o->q)
+      CUDA_TRY(cudaMemcpy2DAsync(o->q + (env0 * (S + 1) + s_lo) * n, sizeof(double) * (S + 1) * n,
+                                 d.q + (s_lo - d.qbase) * n, sizeof(double) * d.qs * n, sizeof(double) * cnt * n, B,
+                                 cudaMemcpyDeviceToHost, st));
+    if (o->energy)
+      CUDA_TRY(cudaMemcpy2DAsync(o->energy + (env0 * (S + 1) + s_lo) * 2, sizeof(double) * (S + 1) * 2,
+                                 d.energy + (s_lo - d.qbase) * 2, sizeof(double) * d.qs * 2, sizeof(double) * cnt * 2,
+                                 B, cudaMemcpyDeviceToHost, st));
+  }
+  if (r_hi > r_lo) {
+    const long cnt = r_hi - r_lo;
+    auto rep = [&](auto* host, auto* dev) -> cudaError_t {
+      using T = std::remove_pointer_t<decltype(dev)>;
+      if (!host) return cudaSuccess;
+      return cudaMemcpy2DAsync(host + env0 * S + r_lo, sizeof(T) * S, dev + (r_lo - d.rbase), sizeof(T) * d.rs,
+                               sizeof(T) * cnt, B, cudaMemcpyDeviceToHost, st);
+    };
+    CUDA_TRY(rep(o->iterations, d.iterations));
+    CUDA_TRY(rep(o->converged, d.converged));
+    CUDA_TRY(rep(o->accepted, d.accepted));
+    CUDA_TRY(rep(o->final_value, d.final_value));
+    CUDA_TRY(rep(o->final_grad_norm, d.final_grad_norm));
+  }
+  return PBAD_OK;
+}
+
+// per-environment status words (n_samples, status, fail streak, reports)
+int32_t drain_status(pbad_gpu_ctx* c, const pbad_rollout_out* o, long env0) {
+  const long B = c->B;
+  const int* iws = c->chain ? c->ca.ci : c->ka.iws;
+  const cudaStream_t st = c->stream;
+  if (o->n_samples)
+    CUDA_TRY(cudaMemcpyAsync(o->n_samples + env0, iws + (long)IS_NSAMP * B, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  if (o->status)
+    CUDA_TRY(cudaMemcpyAsync(o->status + env0, iws + (long)IS_RUN * B, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  if (o->fail_streak)
+    CUDA_TRY(cudaMemcpyAsync(o->fail_streak + env0, iws + (long)IS_FAIL * B, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  if (o->n_reports)
+    CUDA_TRY(cudaMemcpyAsync(o->n_reports + env0, iws + (long)IS_NREP * B, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  return PBAD_OK;
+}
+
+// One context's share of a (possibly sharded) rollout, advanced window by
+// window so several devices step concurrently.
+struct RolloutJob {
+  pbad_gpu_ctx* c;
+  long env0, B, W, ws;
+};
+
+int32_t job_start(RolloutJob& j, const double* q0, const double* qdot0) {
+  pbad_gpu_ctx* c = j.c;
   const long n = c->model.n;
+  CUDA_TRY(cudaSetDevice(c->device));
   if (!c->d_q0) {
     c->d_q0 = dalloc<double>((size_t)c->max_batch * n);
     c->d_qd0 = dalloc<double>((size_t)c->max_batch * n);
@@ -1151,19 +1222,171 @@ int32_t pbad_gpu_rollout(pbad_gpu_ctx* c, int32_t B, const double* q0, const dou
     c->owned.push_back(c->d_q0);
     c->owned.push_back(c->d_qd0);
   }
-  CUDA_TRY(cudaMemcpyAsync(c->d_q0, q0, sizeof(double) * B * n, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->d_qd0, qdot0, sizeof(double) * B * n, cudaMemcpyHostToDevice, c->stream));
-  int32_t rc = pbad_gpu_begin(c, B, c->d_q0, c->d_qd0, nullptr);
+  CUDA_TRY(cudaMemcpyAsync(c->d_q0, q0 + j.env0 * n, sizeof(double) * j.B * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_qd0, qdot0 + j.env0 * n, sizeof(double) * j.B * n, cudaMemcpyHostToDevice, c->stream));
+  int32_t rc = begin_batch(c, (int32_t)j.B, j.W, c->d_q0, c->d_qd0, c->stream);
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
-  rc = pbad_gpu_advance(c, c->total_steps, nullptr);
+  j.ws = 0;
+  return PBAD_OK;
+}
+
+// launches the next window's steps; returns 1 while windows remain
+int32_t job_advance(RolloutJob& j) {
+  pbad_gpu_ctx* c = j.c;
+  if (j.ws >= c->total_steps) return 0;
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->dout.qbase = j.ws;
+  c->dout.rbase = j.ws;
+  const long w = std::min(j.W, (long)c->total_steps - j.ws);
+  const int32_t rc = advance_steps(c, w, c->stream);
   if (rc) return rc;
-  CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
-  CUDA_TRY(cudaEventSynchronize(c->ev1));
-  float ms = 0.f;
-  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-  c->device_ms = ms;
-  return pbad_gpu_sync_outputs(c, out);
+  if (j.ws + w >= c->total_steps) CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+  return 1;
+}
+
+int32_t job_drain(RolloutJob& j, const pbad_rollout_out* o) {
+  pbad_gpu_ctx* c = j.c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long w = std::min(j.W, (long)c->total_steps - j.ws);
+  // the window's samples: its own steps' samples, plus sample 0 in window 0
+  const int32_t rc = drain_window(c, o, j.env0, j.ws == 0 ? 0 : j.ws + 1, j.ws + w, j.ws, j.ws + w);
+  j.ws += w;
+  return rc;
+}
+
+int32_t job_finish(RolloutJob& j, const pbad_rollout_out* o) {
+  pbad_gpu_ctx* c = j.c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->total_steps == 0) {
+    const int32_t rc = drain_window(c, o, j.env0, 0, 0, 0, 0);
+    if (rc) return rc;
+  }
+  return drain_status(c, o, j.env0);
+}
+
+int32_t job_wait(RolloutJob& j, float* ms) {
+  pbad_gpu_ctx* c = j.c;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  float t = 0.f;
+  if (c->total_steps > 0) CUDA_TRY(cudaEventElapsedTime(&t, c->ev0, c->ev1));
+  c->device_ms = t;
+  *ms = t;
+  return PBAD_OK;
+}
+
+int32_t run_jobs(std::vector<RolloutJob>& jobs, const double* q0, const double* qdot0, pbad_rollout_out* out) {
+  for (auto& j : jobs) {
+    const int32_t rc = job_start(j, q0, qdot0);
+    if (rc) return rc;
+  }
+  // window by window: every device's steps are queued before the drains, so
+  // devices overlap even when a drain into pageable memory blocks the host
+  for (;;) {
+    bool more = false;
+    std::vector<char> launched(jobs.size(), 0);
+    for (size_t i = 0; i < jobs.size(); ++i) {
+      const int32_t rc = job_advance(jobs[i]);
+      if (rc < 0) return rc;
+      launched[i] = (char)rc;
+      more = more || rc;
+    }
+    if (!more) break;
+    for (size_t i = 0; i < jobs.size(); ++i)
+      if (launched[i]) {
+        const int32_t rc = job_drain(jobs[i], out);
+        if (rc) return rc;
+      }
+  }
+  float worst = 0.f;
+  for (auto& j : jobs) {
+    const int32_t rc = job_finish(j, out);
+    if (rc) return rc;
+  }
+  for (auto& j : jobs) {
+    float ms = 0.f;
+    const int32_t rc = job_wait(j, &ms);
+    if (rc) return rc;
+    worst = std::max(worst, ms);
+  }
+  if (out->device_ms) out->device_ms[0] = worst;
+  return PBAD_OK;
+}
+
+__global__ void k_gather_final(const double* q, long qs, long qbase, const int* nsamp, long B, int n, double* dst) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * n) return;
+  const long e = t / n, k = t - e * n;
+  const long s = (long)nsamp[e] - 1;
+  dst[t] = q[(e * qs + (s - qbase)) * n + k];
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pbad_gpu_begin(pbad_gpu_ctx* c, int32_t B, const double* d_q0, const double* d_qdot0, void* stream) {
+  return begin_batch(c, B, c->total_steps, d_q0, d_qdot0, pick(c, stream));
+}
+
+int32_t pbad_gpu_advance(pbad_gpu_ctx* c, int32_t n_steps, void* stream) {
+  CUDA_TRY(cudaSetDevice(c->device));
+  return advance_steps(c, n_steps, pick(c, stream));
+}
+
+int32_t pbad_gpu_sync_outputs(pbad_gpu_ctx* c, pbad_rollout_out* o) {
+  CUDA_TRY(cudaSetDevice(c->device));
+  int32_t rc = join_work(c);
+  if (rc) return rc;
+  rc = drain_window(c, o, 0, 0, c->total_steps, 0, c->total_steps);
+  if (rc) return rc;
+  rc = drain_status(c, o, 0);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (o->device_ms) o->device_ms[0] = (float)c->device_ms;
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_final_state(pbad_gpu_ctx* c, double* d_dst, void* stream) {
+  if (!c->B) return fail(PBAD_E_ARGUMENT, "no batch has been started on this context");
+  if (c->dout.qbase != 0 || c->dout.qs != c->total_steps + 1)
+    return fail(PBAD_E_ARGUMENT, "final_state needs the whole-trajectory output geometry (pbad_gpu_begin)");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const cudaStream_t s = pick(c, stream);
+  const int* iws = c->chain ? c->ca.ci : c->ka.iws;
+  const long tot = c->B * (long)c->model.n;
+  k_gather_final<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->dout.q, c->dout.qs, c->dout.qbase,
+                                                               iws + (long)IS_NSAMP * c->B, c->B, c->model.n, d_dst);
+  CUDA_TRY(cudaGetLastError());
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_rollout(pbad_gpu_ctx* c, int32_t B, const double* q0, const double* qdot0,
+                         pbad_rollout_out* out) {
+  if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
+  std::vector<RolloutJob> jobs{RolloutJob{c, 0, B, window_steps(c, B), 0}};
+  return run_jobs(jobs, q0, qdot0, out);
+}
+
+int32_t pbad_gpu_rollout_sharded(pbad_gpu_ctx* const* ctxs, int32_t n_ctx, int32_t B, const double* q0,
+                                 const double* qdot0, pbad_rollout_out* out) {
+  if (!ctxs || n_ctx < 1) return fail(PBAD_E_ARGUMENT, "need at least one context");
+  if (B < n_ctx) return fail(PBAD_E_ARGUMENT, "batch %d smaller than the context count %d", B, n_ctx);
+  std::vector<RolloutJob> jobs;
+  for (int i = 0; i < n_ctx; ++i) {
+    pbad_gpu_ctx* c = ctxs[i];
+    if (!c) return fail(PBAD_E_ARGUMENT, "context %d is null", i);
+    for (int k = 0; k < i; ++k)
+      if (ctxs[k] == c) return fail(PBAD_E_ARGUMENT, "context %d appears twice (one context per shard)", i);
+    if (c->model.n != ctxs[0]->model.n || c->total_steps != ctxs[0]->total_steps)
+      return fail(PBAD_E_ARGUMENT, "contexts differ in DOF count or step count");
+    const long lo = (long)B * i / n_ctx, hi = (long)B * (i + 1) / n_ctx;
+    if (hi - lo > c->max_batch)
+      return fail(PBAD_E_ARGUMENT, "shard %d has %ld environments, context max_batch is %ld", i, hi - lo, c->max_batch);
+    jobs.push_back(RolloutJob{c, lo, hi - lo, window_steps(c, hi - lo), 0});
+  }
+  return run_jobs(jobs, q0, qdot0, out);
 }
 
 static int32_t stage_inputs(pbad_gpu_ctx* c, int32_t B, const double* history, const double* tau,

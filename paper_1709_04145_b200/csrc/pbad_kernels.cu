@@ -1138,12 +1138,11 @@ __device__ void forces_tau_at(const Env& E, double t, const Arr& dst) {
 
 __device__ void record_sample(const Env& E, const Outputs& out, int k, const Arr& q, double ke, double pe) {
   const int n = E.m->n;
-  const long S1 = E.sc->total_steps + 1;
   if (out.q)
-    for (int j = 0; j < n; ++j) out.q[((long)E.e * S1 + k) * n + j] = q[j];
+    for (int j = 0; j < n; ++j) out.q[out.qrow(E.e, k) * n + j] = q[j];
   if (out.energy) {
-    out.energy[((long)E.e * S1 + k) * 2] = ke;
-    out.energy[((long)E.e * S1 + k) * 2 + 1] = pe;
+    out.energy[out.qrow(E.e, k) * 2] = ke;
+    out.energy[out.qrow(E.e, k) * 2 + 1] = pe;
   }
   E.iv(IS_NSAMP) = k + 1;
 }
@@ -1173,12 +1172,11 @@ __device__ bool finish_step(const Env& E, const Outputs& out) {
   const Layout& L = *E.L;
   const int step = E.iv(IS_STEP);
   const bool converged = E.iv(IS_STATUS) == ST_CONVERGED;
-  const long S = sc.total_steps;
-  if (out.iterations) out.iterations[(long)E.e * S + step] = E.iv(IS_ITERS);
-  if (out.converged) out.converged[(long)E.e * S + step] = converged;
-  if (out.accepted) out.accepted[(long)E.e * S + step] = E.iv(IS_ACC);
-  if (out.final_value) out.final_value[(long)E.e * S + step] = E.sv(SC_VALUE);
-  if (out.final_grad_norm) out.final_grad_norm[(long)E.e * S + step] = infnorm(E.arr(L.grad), sc.U);
+  if (out.iterations) out.iterations[out.rrow(E.e, step)] = E.iv(IS_ITERS);
+  if (out.converged) out.converged[out.rrow(E.e, step)] = converged;
+  if (out.accepted) out.accepted[out.rrow(E.e, step)] = E.iv(IS_ACC);
+  if (out.final_value) out.final_value[out.rrow(E.e, step)] = E.sv(SC_VALUE);
+  if (out.final_grad_norm) out.final_grad_norm[out.rrow(E.e, step)] = infnorm(E.arr(L.grad), sc.U);
   E.iv(IS_NREP) = step + 1;
   int& fs = E.iv(IS_FAIL);
   fs = converged ? 0 : fs + 1;

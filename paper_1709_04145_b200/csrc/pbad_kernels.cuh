@@ -155,13 +155,18 @@ struct ResidDesc {
 };
 
 struct Outputs {
-  double* q;        // [B][S+1][n]
-  double* energy;   // [B][S+1][2]
-  int* iterations;  // [B][S]
+  double* q;        // [B][qs][n]: sample qbase + j in slot j
+  double* energy;   // [B][qs][2]
+  int* iterations;  // [B][rs]: report of step rbase + j in slot j
   int* converged;
   int* accepted;
   double* final_value;
   double* final_grad_norm;
+  // slot geometry: the whole trajectory (qs = S + 1, rs = S, bases 0), or a
+  // window of it that pbad_gpu_rollout drains to the host between launches
+  long qs, qbase, rs, rbase;
+  __host__ __device__ long qrow(long e, long sample) const { return e * qs + (sample - qbase); }
+  __host__ __device__ long rrow(long e, long step) const { return e * rs + (step - rbase); }
 };
 
 }  // namespace pbad_gpu

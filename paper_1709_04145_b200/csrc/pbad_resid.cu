@@ -2026,16 +2026,15 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
 
   // ---- finish_step (stepper.cpp:118-147) ----
   const bool converged = S.status == ST_CONVERGED;
-  const long Stot = sc.total_steps;
   const double gnorm = infnorm(r, r.grad, U);
   const int fs = converged ? 0 : iv(IS_FAIL) + 1;
   __syncthreads();
   if (r.tid == 0) {
-    if (out.iterations) out.iterations[e * Stot + step] = S.iters;
-    if (out.converged) out.converged[e * Stot + step] = converged;
-    if (out.accepted) out.accepted[e * Stot + step] = S.acc;
-    if (out.final_value) out.final_value[e * Stot + step] = S.value;
-    if (out.final_grad_norm) out.final_grad_norm[e * Stot + step] = gnorm;
+    if (out.iterations) out.iterations[out.rrow(e, step)] = S.iters;
+    if (out.converged) out.converged[out.rrow(e, step)] = converged;
+    if (out.accepted) out.accepted[out.rrow(e, step)] = S.acc;
+    if (out.final_value) out.final_value[out.rrow(e, step)] = S.value;
+    if (out.final_grad_norm) out.final_grad_norm[out.rrow(e, step)] = gnorm;
     iv(IS_NREP) = step + 1;
     iv(IS_ITERS) = S.iters;
     iv(IS_STATUS) = S.status;
@@ -2066,7 +2065,6 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
     r.FA[2 * i + 1] = dot4(ghat, vv);
   }
   __syncthreads();
-  const long S1 = Stot + 1;
   if (r.tid == 0) {
     double ke = 0.0, pe = 0.0;
     for (int i = 0; i < N; ++i) {
@@ -2074,15 +2072,15 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
       pe -= r.FA[2 * i + 1];
     }
     if (out.energy) {
-      out.energy[(e * S1 + step + 1) * 2] = ke;
-      out.energy[(e * S1 + step + 1) * 2 + 1] = pe;
+      out.energy[out.qrow(e, step + 1) * 2] = ke;
+      out.energy[out.qrow(e, step + 1) * 2 + 1] = pe;
     }
     iv(IS_NSAMP) = step + 2;
     iv(IS_STEP) = step + 1;
     if (step + 1 >= sc.total_steps) iv(IS_RUN) = TR_OK;
   }
   if (out.q)
-    for (int k = r.tid; k < n; k += NT) out.q[(e * S1 + step + 1) * n + k] = xq[k];
+    for (int k = r.tid; k < n; k += NT) out.q[out.qrow(e, step + 1) * n + k] = xq[k];
 #if PBAD_PHASE_TIMING
   if (e == 0 && r.tid == 0)
     printf("phase cycles (block 0, %d iterations, %d accepted): conv %lld chol %lld solve %lld tpass %lld tres %lld "

@@ -1002,14 +1002,13 @@ __global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel
 
   // ---- finish_step (stepper.cpp:118-147) ----
   const bool converged = S.status == ST_CONVERGED;
-  const long Stot = sc.total_steps;
   const double gnorm = infnorm_warp(w, w.grad);
   if (w.lane == 0) {
-    if (out.iterations) out.iterations[e * Stot + step] = S.iters;
-    if (out.converged) out.converged[e * Stot + step] = converged;
-    if (out.accepted) out.accepted[e * Stot + step] = S.acc;
-    if (out.final_value) out.final_value[e * Stot + step] = S.value;
-    if (out.final_grad_norm) out.final_grad_norm[e * Stot + step] = gnorm;
+    if (out.iterations) out.iterations[out.rrow(e, step)] = S.iters;
+    if (out.converged) out.converged[out.rrow(e, step)] = converged;
+    if (out.accepted) out.accepted[out.rrow(e, step)] = S.acc;
+    if (out.final_value) out.final_value[out.rrow(e, step)] = S.value;
+    if (out.final_grad_norm) out.final_grad_norm[out.rrow(e, step)] = gnorm;
     iv(IS_NREP) = step + 1;
     iv(IS_ITERS) = S.iters;
     iv(IS_STATUS) = S.status;
@@ -1049,18 +1048,16 @@ __global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel
       ke += w.red[4 * i];
       pe -= w.red[4 * i + 1];
     }
-    const long S1 = Stot + 1;
     if (out.energy) {
-      out.energy[(e * S1 + step + 1) * 2] = ke;
-      out.energy[(e * S1 + step + 1) * 2 + 1] = pe;
+      out.energy[out.qrow(e, step + 1) * 2] = ke;
+      out.energy[out.qrow(e, step + 1) * 2 + 1] = pe;
     }
     iv(IS_NSAMP) = step + 2;
     iv(IS_STEP) = step + 1;
     if (step + 1 >= sc.total_steps) iv(IS_RUN) = TR_OK;
   }
   if (out.q) {
-    const long S1 = Stot + 1;
-    for (int k = w.lane; k < n; k += 32) out.q[(e * S1 + step + 1) * n + k] = w.x[k];
+    for (int k = w.lane; k < n; k += 32) out.q[out.qrow(e, step + 1) * n + k] = w.x[k];
   }
 }
 
@@ -1318,14 +1315,13 @@ __global__ void __launch_bounds__(32) k_tree_lbfgs(const __grid_constant__ DMode
 
   // ---- finish_step (stepper.cpp:118-147) ----
   const bool converged = S.status == ST_CONVERGED;
-  const long Stot = sc.total_steps;
   const double gnorm = infnorm_warp(w, w.grad);
   if (w.lane == 0) {
-    if (out.iterations) out.iterations[e * Stot + step] = S.iters;
-    if (out.converged) out.converged[e * Stot + step] = converged;
-    if (out.accepted) out.accepted[e * Stot + step] = S.acc;
-    if (out.final_value) out.final_value[e * Stot + step] = S.value;
-    if (out.final_grad_norm) out.final_grad_norm[e * Stot + step] = gnorm;
+    if (out.iterations) out.iterations[out.rrow(e, step)] = S.iters;
+    if (out.converged) out.converged[out.rrow(e, step)] = converged;
+    if (out.accepted) out.accepted[out.rrow(e, step)] = S.acc;
+    if (out.final_value) out.final_value[out.rrow(e, step)] = S.value;
+    if (out.final_grad_norm) out.final_grad_norm[out.rrow(e, step)] = gnorm;
     iv(IS_NREP) = step + 1;
     iv(IS_ITERS) = S.iters;
     iv(IS_STATUS) = S.status;
@@ -1365,18 +1361,16 @@ __global__ void __launch_bounds__(32) k_tree_lbfgs(const __grid_constant__ DMode
       ke += w.red[4 * i];
       pe -= w.red[4 * i + 1];
     }
-    const long S1 = Stot + 1;
     if (out.energy) {
-      out.energy[(e * S1 + step + 1) * 2] = ke;
-      out.energy[(e * S1 + step + 1) * 2 + 1] = pe;
+      out.energy[out.qrow(e, step + 1) * 2] = ke;
+      out.energy[out.qrow(e, step + 1) * 2 + 1] = pe;
     }
     iv(IS_NSAMP) = step + 2;
     iv(IS_STEP) = step + 1;
     if (step + 1 >= sc.total_steps) iv(IS_RUN) = TR_OK;
   }
   if (out.q) {
-    const long S1 = Stot + 1;
-    for (int k = w.lane; k < n; k += 32) out.q[(e * S1 + step + 1) * n + k] = w.x[k];
+    for (int k = w.lane; k < n; k += 32) out.q[out.qrow(e, step + 1) * n + k] = w.x[k];
   }
 }
 #endif
