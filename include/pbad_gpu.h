@@ -61,7 +61,10 @@ enum {
   /* simulate_baseline (pbad_gpu_simulate_baseline) */
   PBAD_TRAJ_DIVERGED = 5,       /* "diverged to a non-finite state at t=..." */
   PBAD_TRAJ_SINGULAR_MASS = 6,  /* "step failed: singular generalized mass matrix" */
-  PBAD_TRAJ_STAGE_NONFINITE = 7 /* "step failed: configuration contains a non-finite entry" */
+  PBAD_TRAJ_STAGE_NONFINITE = 7, /* "step failed: configuration contains a non-finite entry" */
+  /* refined_bootstrap (stepper.cpp:46-59): baseline_step threw inside
+   * init_pbad_run, before sample 0 was recorded */
+  PBAD_TRAJ_BOOTSTRAP_SINGULAR = 8 /* "singular generalized mass matrix" */
 };
 
 /* BaselineScheme (baseline.hpp:17) */
@@ -129,7 +132,7 @@ typedef struct {
   int32_t objective;
   pbad_optimizer_config opt;
   int32_t consecutive_fail_limit;
-  int32_t refined_bootstrap; /* must be 0 (RK4 bootstrap is out of scope) */
+  int32_t refined_bootstrap; /* RK4 Newton-Euler history bootstrap (stepper.cpp:46-59) */
   int32_t warm_start;
 } pbad_sim_desc;
 
@@ -148,6 +151,10 @@ typedef struct {
   int32_t* fail_streak;    /* [B] streak at abort (error text) */
   int32_t* n_reports;      /* [B] recorded solve reports */
   float* device_ms;        /* [1] device time of the stepping kernels */
+  double* iteration_values; /* [B][S][max_iters] SolveReport::per_iteration_values
+                               (optim.cpp:30-37, 64-67): the objective value after
+                               each iteration of step s, iterations[b][s] entries;
+                               pbad_gpu_rollout / _sharded only, NULL = off */
 } pbad_rollout_out;
 
 typedef struct pbad_gpu_model pbad_gpu_model;
@@ -156,6 +163,9 @@ typedef struct pbad_gpu_ctx pbad_gpu_ctx;
 int32_t pbad_gpu_abi_version(void);
 const char* pbad_gpu_last_error(void);
 const char* pbad_gpu_error_string(int32_t code);
+
+/* visible CUDA devices (0 when none: the GPU path has no CPU fallback) */
+int32_t pbad_gpu_device_count(void);
 
 void pbad_gpu_default_optimizer(pbad_optimizer_config* cfg);
 void pbad_gpu_default_sim(pbad_sim_desc* sim);

@@ -26,6 +26,7 @@ HEADER_SYMBOLS = [
     "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
     "pbad_gpu_state_device", "pbad_gpu_eval", "pbad_gpu_minimize", "pbad_gpu_correlation",
     "pbad_gpu_simulate_baseline", "pbad_gpu_rollout_sharded", "pbad_gpu_final_state",
+    "pbad_gpu_device_count",
 ]
 
 
@@ -69,7 +70,7 @@ class RolloutOut(C.Structure):
     _fields_ = [
         ("q", _dp), ("energy", _dp), ("iterations", _ip), ("converged", _ip), ("accepted", _ip),
         ("final_value", _dp), ("final_grad_norm", _dp), ("n_samples", _ip), ("status", _ip),
-        ("fail_streak", _ip), ("n_reports", _ip), ("device_ms", _fp),
+        ("fail_streak", _ip), ("n_reports", _ip), ("device_ms", _fp), ("iteration_values", _dp),
     ]
 
 
@@ -121,6 +122,7 @@ def load():
         "pbad_gpu_rollout_sharded": ([C.POINTER(vp), C.c_int32, C.c_int32, _dp, _dp, C.POINTER(RolloutOut)],
                                      C.c_int32),
         "pbad_gpu_final_state": ([vp, vp, vp], C.c_int32),
+        "pbad_gpu_device_count": ([], C.c_int32),
         "pbad_gpu_eval": ([vp, C.c_int32, _dp, _dp, _dp, C.c_int32, C.c_int32, _dp, _dp, _dp], C.c_int32),
         "pbad_gpu_minimize": ([vp, C.c_int32, _dp, _dp, _dp, _dp, _ip, _ip, _dp, _dp], C.c_int32),
     }

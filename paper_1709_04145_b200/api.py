@@ -259,6 +259,7 @@ def total_steps(sim: SimConfig) -> int:
 
 
 TRAJ_OK, TRAJ_FAIL_LIMIT, TRAJ_NONFINITE_INIT, TRAJ_NONFINITE_CFG, TRAJ_RUNNING = 0, 1, 2, 3, 4
+TRAJ_BOOTSTRAP_SINGULAR = 8
 
 
 class GpuContext:
@@ -288,7 +289,7 @@ class GpuContext:
         except Exception:
             pass
 
-    def _out_struct(self, B: int, want_q=True, want_energy=True, pinned=False):
+    def _out_struct(self, B: int, want_q=True, want_energy=True, pinned=False, want_itv=False):
         S, n = self.total_steps, self.n
         if pinned:
             import torch
@@ -306,7 +307,8 @@ class GpuContext:
             accepted=z((B, S), np.int32), final_value=z((B, S)),
             final_grad_norm=z((B, S)), n_samples=z(B, np.int32), status=z(B, np.int32),
             fail_streak=z(B, np.int32), n_reports=z(B, np.int32),
-            device_ms=z(1, np.float32))
+            device_ms=z(1, np.float32),
+            iteration_values=z((B, S, max(1, self.sim.optimizer.max_iters))) if want_itv else None)
         o = _lib.RolloutOut()
         for k, v in bufs.items():
             if v is None:
@@ -319,12 +321,13 @@ class GpuContext:
                 setattr(o, k, v.ctypes.data_as(C.POINTER(C.c_float)))
         return o, bufs
 
-    def make_outputs(self, B: int, want_q=True, want_energy=True, pinned=False):
+    def make_outputs(self, B: int, want_q=True, want_energy=True, pinned=False, want_itv=False):
         """Caller-owned host output buffers for rollout(out=...) (the C ABI
         writes into buffers the caller allocated, stepper.hpp's Trajectory)."""
-        return self._out_struct(B, want_q, want_energy, pinned)
+        return self._out_struct(B, want_q, want_energy, pinned, want_itv)
 
-    def rollout(self, q0, qdot0, want_q=True, want_energy=True, pinned=False, out=None) -> Dict[str, np.ndarray]:
+    def rollout(self, q0, qdot0, want_q=True, want_energy=True, pinned=False, out=None,
+                want_itv=False) -> Dict[str, np.ndarray]:
         q0 = _f64(q0)
         B = q0.shape[0]
         q0 = _f64(q0, (B, self.n))
@@ -338,7 +341,7 @@ class GpuContext:
                 if bufs[k] is not None and bufs[k].shape != (B,) + tail:
                     raise ValueError(f"rollout: out[{k!r}] has shape {bufs[k].shape}, expected {(B,) + tail}")
         else:
-            o, bufs = self._out_struct(B, want_q, want_energy, pinned)
+            o, bufs = self._out_struct(B, want_q, want_energy, pinned, want_itv)
         check(_lib.load().pbad_gpu_rollout(self._h, B, _p(q0), _p(qdot0), C.byref(o)))
         return bufs
 
@@ -444,9 +447,12 @@ def _trajectories(ctx: GpuContext, sims: Sequence[SimConfig], bufs) -> List[Traj
             tr.energy_log.append(EnergySample(s * sim.dt, float(bufs["energy"][b, s, 0]),
                                               float(bufs["energy"][b, s, 1])))
         for s in range(int(bufs["n_reports"][b])):
-            tr.solve_reports.append(SolveReport(int(bufs["iterations"][b, s]), float(bufs["final_value"][b, s]),
+            its = int(bufs["iterations"][b, s])
+            itv = bufs.get("iteration_values")
+            tr.solve_reports.append(SolveReport(its, float(bufs["final_value"][b, s]),
                                                 float(bufs["final_grad_norm"][b, s]),
-                                                bool(bufs["converged"][b, s]), int(bufs["accepted"][b, s])))
+                                                bool(bufs["converged"][b, s]), int(bufs["accepted"][b, s]),
+                                                [] if itv is None else itv[b, s, :its].tolist()))
         st = int(bufs["status"][b])
         if st == TRAJ_FAIL_LIMIT:
             steps = max(0, k - 1)
@@ -456,12 +462,14 @@ def _trajectories(ctx: GpuContext, sims: Sequence[SimConfig], bufs) -> List[Traj
             tr.error = "objective is non-finite at the initial point"
         elif st == TRAJ_NONFINITE_CFG:
             tr.error = "configuration contains a non-finite entry"
+        elif st == TRAJ_BOOTSTRAP_SINGULAR:
+            tr.error = "singular generalized mass matrix"
         out.append(tr)
     return out
 
 
 def rollout_sharded(ctxs: Sequence[GpuContext], q0, qdot0, want_q=True, want_energy=True, pinned=False,
-                    out=None) -> Dict[str, np.ndarray]:
+                    out=None, want_itv=False) -> Dict[str, np.ndarray]:
     """One batch over several contexts (one per device, or several on one):
     context i steps the contiguous shard [B*i/k, B*(i+1)/k) of the batch,
     all concurrently (pbad_gpu_rollout_sharded); equal to one context's
@@ -473,7 +481,7 @@ def rollout_sharded(ctxs: Sequence[GpuContext], q0, qdot0, want_q=True, want_ene
     B = q0.shape[0]
     q0 = _f64(q0, (B, c0.n))
     qdot0 = _f64(qdot0, (B, c0.n))
-    o, bufs = out if out is not None else c0._out_struct(B, want_q, want_energy, pinned)
+    o, bufs = out if out is not None else c0._out_struct(B, want_q, want_energy, pinned, want_itv)
     arr = (C.c_void_p * len(ctxs))(*[c._h for c in ctxs])
     check(_lib.load().pbad_gpu_rollout_sharded(arr, len(ctxs), B, _p(q0), _p(qdot0), C.byref(o)))
     return bufs
@@ -488,7 +496,8 @@ def _check_sim(model: KinematicModel, sim: SimConfig):
 
 
 def batch_simulate(model: KinematicModel, forces: ForceModel, sims: Sequence[SimConfig], workers: int = 1,
-                   device: int = 0, devices: Optional[Sequence[int]] = None) -> List[Trajectory]:
+                   device: int = 0, devices: Optional[Sequence[int]] = None,
+                   record_iteration_values: bool = False) -> List[Trajectory]:
     """stepper.cpp:204-270: per-trajectory results equal simulate(); errors are
     recorded per trajectory.  `workers` is accepted for signature parity (the
     GPU grid replaces the WorkerPool).  `devices` shards every group of
@@ -518,10 +527,10 @@ def batch_simulate(model: KinematicModel, forces: ForceModel, sims: Sequence[Sim
             shard = -(-len(idx) // len(devs))
             ctxs = [GpuContext(model, forces, rep, device=d, max_batch=shard) for d in devs]
             ctx = ctxs[0]
-            bufs = rollout_sharded(ctxs, q0, qd)
+            bufs = rollout_sharded(ctxs, q0, qd, want_itv=record_iteration_values)
         else:
             ctx = GpuContext(model, forces, rep, device=devs[0], max_batch=len(idx))
-            bufs = ctx.rollout(q0, qd)
+            bufs = ctx.rollout(q0, qd, want_itv=record_iteration_values)
         for i, tr in zip(idx, _trajectories(ctx, [sims[i] for i in idx], bufs)):
             results[i] = tr
     return results  # type: ignore[return-value]
@@ -534,7 +543,7 @@ def simulate(model: KinematicModel, forces: ForceModel, sim: SimConfig, device: 
     bufs = ctx.rollout(_f64(sim.q0)[None], _f64(sim.qdot0)[None])
     tr = _trajectories(ctx, [sim], bufs)[0]
     st = int(bufs["status"][0])
-    if st == TRAJ_FAIL_LIMIT:
+    if st in (TRAJ_FAIL_LIMIT, TRAJ_BOOTSTRAP_SINGULAR):
         raise RuntimeError(tr.error)
     if st == TRAJ_NONFINITE_INIT:
         raise ValueError(tr.error)

@@ -746,6 +746,7 @@ __device__ __forceinline__ void chain_reverse(const CK& K, double* Gv) {
 struct SolverState {
   double value, grad0;
   int status, iters, stag, acc, h0, hc;
+  double* itv;  // per_iteration_values row of this step (lane 0 writes), or null
 };
 
 __device__ __forceinline__ bool grad_converged(const CK& K, const SolverState& s) {
@@ -843,6 +844,7 @@ __device__ __forceinline__ int lbfgs_iterate(const CK& K, SolverState& s) {
     t *= o.backtrack_factor;
   }
   if (!accepted) s.status = ST_FAILED;
+  if (s.itv && K.r == 0) s.itv[s.iters] = s.value;
   ++s.iters;
   if (s.status == ST_RUNNING && s.iters >= o.max_iters) s.status = ST_FAILED;
   return s.status;
@@ -910,7 +912,7 @@ __device__ __forceinline__ void chain_energy(const CK& K, const double* Wp, cons
 // init_pbad_run (stepper.cpp:62-80) for the chain path
 __global__ void __launch_bounds__(kThreads) k_chain_init(DModel m, DForces f, DSchedule sc, ChainLayout L, double* cw,
                                                          int* ci, long B, const double* q0, const double* qdot0,
-                                                         Outputs out) {
+                                                         const double* hist0, Outputs out) {
   extern __shared__ __align__(16) double smem[];
   stage_model(m, smem);
   bool valid;
@@ -936,7 +938,8 @@ __global__ void __launch_bounds__(kThreads) k_chain_init(DModel m, DForces f, DS
     return;
   }
   const double tl = sc.times[0] * sc.dt;
-  for (int k = K.r; k < n; k += 4) vat(K, K.h0, k) = vat(K, K.h1, k) + tl * vat(K, K.g, k);
+  for (int k = K.r; k < n; k += 4)  // refined_bootstrap: precomputed (k_refined_bootstrap)
+    vat(K, K.h0, k) = hist0 ? hist0[K.e * n + k] : vat(K, K.h1, k) + tl * vat(K, K.g, k);
   qsync(K);
   // kinetic_energy via the velocity pass (baseline.cpp:20-54,208-217) and
   // gravity_potential (baseline.cpp:219-229) at q0; general joint algebra
@@ -1041,6 +1044,7 @@ __global__ void __launch_bounds__(kThreads) k_chain_step(DModel m, DForces f, DS
   // LbfgsSolver ctor: first evaluation
   SolverState s{};
   s.status = ST_RUNNING;
+  s.itv = out.itv ? out.itv + out.rrow(K.e, step) * out.itv_n : nullptr;
   if (!qallfinite(K, K.x)) {
     if (K.r == 0) ival(K, IS_RUN) = TR_NONFINITE_CFG;
     return;
@@ -1110,12 +1114,12 @@ static cudaError_t chain_smem_attr(int N, size_t* bytes) {
   return cudaSuccess;
 }
 
-cudaError_t launch_chain_init(const ChainArgs& a, const double* q0, const double* qdot0, const Outputs& out,
-                              cudaStream_t s) {
+cudaError_t launch_chain_init(const ChainArgs& a, const double* q0, const double* qdot0, const double* hist0,
+                              const Outputs& out, cudaStream_t s) {
   size_t sm;
   cudaError_t e = chain_smem_attr(a.m.N, &sm);
   if (e != cudaSuccess) return e;
-  k_chain_init<<<chain_grid(a.B), kThreads, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, q0, qdot0, out);
+  k_chain_init<<<chain_grid(a.B), kThreads, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, q0, qdot0, hist0, out);
   return cudaGetLastError();
 }
 cudaError_t launch_chain_step(const ChainArgs& a, const Outputs& out, cudaStream_t s) {

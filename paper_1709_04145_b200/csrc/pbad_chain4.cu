@@ -783,6 +783,7 @@ struct Solver {
   double ginf, xinf;  // |g|_inf, |x|_inf of the current iterate
   double tdx;         // tau . cand of the pending candidate
   int status, iters, stag, acc, h0, hc, trial, phase;
+  double* itv;  // per_iteration_values row of this step (lane 0 writes), or null
 };
 
 #ifndef PBAD_C4_KB
@@ -975,6 +976,7 @@ __device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
     ++s.trial;
   }
   s.status = ST_FAILED;  // no acceptable step
+  if (s.itv && C.r == 0) s.itv[s.iters] = s.value;
   ++s.iters;
   s.phase = PH_DONE;
 }
@@ -1032,6 +1034,7 @@ __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
   if (oldv - v <= C.o.ftol * fmax(1.0, fabs(oldv))) ++s.stag;
   else s.stag = 0;
   if (s.stag >= 2) s.status = ST_CONVERGED;
+  if (s.itv && C.r == 0) s.itv[s.iters] = s.value;
   ++s.iters;
   if (s.status == ST_RUNNING && s.iters >= C.o.max_iters) s.status = ST_FAILED;
   s.phase = (s.status == ST_RUNNING) ? PH_DIR : PH_DONE;
@@ -1149,6 +1152,7 @@ __global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedu
   Solver s{};
   s.status = ST_RUNNING;
   s.phase = PH_DIR;
+  s.itv = (out.itv && C.valid) ? out.itv + out.rrow(C.ge, step) * out.itv_n : nullptr;
   double tdx0 = 0.0;
   if (active) {
     tdx0 = qdot(C, C.tau, C.x);

@@ -59,6 +59,11 @@ struct pbad_gpu_model {
 extern "C" {
 
 int32_t pbad_gpu_abi_version(void) { return PBAD_GPU_ABI_VERSION; }
+
+int32_t pbad_gpu_device_count(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
 const char* pbad_gpu_last_error(void) { return g_last_error.c_str(); }
 const char* pbad_gpu_error_string(int32_t code) {
   switch (code) {
@@ -499,6 +504,15 @@ struct pbad_gpu_ctx {
   // device outputs for the current batch
   Outputs dout{};
   long out_q_cap = 0, out_r_cap = 0;  // allocated sample / report slots
+  double* d_itv = nullptr;             // per_iteration_values slots (on request)
+  bool refined = false;                // refined_bootstrap (stepper.cpp:46-59)
+  double boot_hs = 0.0;                // its RK4 substep span / 32
+  double* d_boot_ws = nullptr;         // bootstrap workspace, hist0 [B][n], status [B]
+  double* d_boot_h0 = nullptr;
+  int* d_boot_st = nullptr;
+  long boot_cap = 0;
+  long itv_cap = 0;
+  int max_iters = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t ev_work = nullptr;       // orders the ctx stream after a caller's stream
   cudaStream_t work_stream = nullptr;  // stream of the last begin/advance
@@ -518,6 +532,10 @@ struct pbad_gpu_ctx {
     if (dout.final_value) cudaFree(dout.final_value);
     if (dout.final_grad_norm) cudaFree(dout.final_grad_norm);
     if (d_in) cudaFree(d_in);
+    if (d_itv) cudaFree(d_itv);
+    if (d_boot_ws) cudaFree(d_boot_ws);
+    if (d_boot_h0) cudaFree(d_boot_h0);
+    if (d_boot_st) cudaFree(d_boot_st);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev_work) cudaEventDestroy(ev_work);
@@ -645,7 +663,7 @@ bool chain4_eligible(const std::vector<int>& ck, int N, int mem) {
 bool chain_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2 || sim->opt.kind != PBAD_LBFGS) return false;
-  if (sim->opt.lbfgs_memory < 1 || sim->opt.lbfgs_memory > chain_max_memory()) return false;
+  if (sim->opt.lbfgs_memory < 0 || sim->opt.lbfgs_memory > chain_max_memory()) return false;
   if (m.N > chain_max_links()) return false;
   if (f->drag_d > 0.0) return false;
   if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
@@ -662,7 +680,7 @@ bool chain_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
 bool tree_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2) return false;
-  if (sim->opt.kind == PBAD_LBFGS && (sim->opt.lbfgs_memory < 1 || sim->opt.lbfgs_memory > 64)) return false;
+  if (sim->opt.kind == PBAD_LBFGS && (sim->opt.lbfgs_memory < 0 || sim->opt.lbfgs_memory > 64)) return false;
   if (!tree_eligible_sizes(m.N, m.n)) return false;
   if (m.sample_off[m.N] > 1024) return false;
   for (int i = 0; i < m.N; ++i)
@@ -753,9 +771,21 @@ bool ensure_v1(pbad_gpu_ctx* c) {
 
 // Device outputs for B environments and a window of W steps: W + 1 sample
 // slots and W report slots per environment (W = S: the whole trajectory).
-int32_t ensure_outputs(pbad_gpu_ctx* c, long B, long W) {
+int32_t ensure_outputs(pbad_gpu_ctx* c, long B, long W, bool want_itv = false) {
   const long n = c->model.n;
   const long need_q = B * (W + 1), need_r = B * W;
+  const long mi = std::max(1, c->max_iters);
+  if (want_itv && c->itv_cap < need_r * mi) {
+    cudaFree(c->d_itv);
+    c->d_itv = dalloc<double>(need_r * mi);
+    if (!c->d_itv) {
+      c->itv_cap = 0;
+      return fail(PBAD_E_CUDA, "cudaMalloc of per_iteration_values failed (B=%ld, window %ld steps)", B, W);
+    }
+    c->itv_cap = need_r * mi;
+  }
+  c->dout.itv = want_itv ? c->d_itv : nullptr;
+  c->dout.itv_n = mi;
   if (c->out_q_cap < need_q || c->out_r_cap < need_r) {
     cudaFree(c->dout.q);
     cudaFree(c->dout.energy);
@@ -764,7 +794,10 @@ int32_t ensure_outputs(pbad_gpu_ctx* c, long B, long W) {
     cudaFree(c->dout.accepted);
     cudaFree(c->dout.final_value);
     cudaFree(c->dout.final_grad_norm);
+    double* itv = c->dout.itv;
     c->dout = Outputs{};
+    c->dout.itv = itv;
+    c->dout.itv_n = mi;
     c->out_q_cap = c->out_r_cap = 0;
     c->dout.q = dalloc<double>(need_q * n);
     c->dout.energy = dalloc<double>(need_q * 2);
@@ -790,11 +823,11 @@ int32_t ensure_outputs(pbad_gpu_ctx* c, long B, long W) {
 // samples fit the budget (PBAD_TRAJ_WINDOW_MB, default 2048 MB of device
 // memory), else the largest window that does; windows are drained to the
 // host between launches so a rollout's device footprint does not grow with S.
-long window_steps(const pbad_gpu_ctx* c, long B) {
+long window_steps(const pbad_gpu_ctx* c, long B, bool want_itv) {
   const long S = c->total_steps, n = c->model.n;
   double mb = 2048.0;
   if (const char* e = std::getenv("PBAD_TRAJ_WINDOW_MB")) mb = std::atof(e);
-  const double per_step = (double)B * (8.0 * (n + 2) + 4.0 * 3 + 16.0);
+  const double per_step = (double)B * (8.0 * (n + 2) + 4.0 * 3 + 16.0 + (want_itv ? 8.0 * std::max(1, c->max_iters) : 0.0));
   long W = (long)(mb * 1048576.0 / per_step) - 1;
   return std::max(1L, std::min(S, W));
 }
@@ -810,16 +843,20 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   *out = nullptr;
   if (!model || !f || !sim) return fail(PBAD_E_ARGUMENT, "null argument");
   if (max_batch < 1) return fail(PBAD_E_ARGUMENT, "max_batch must be >= 1");
-  if (sim->refined_bootstrap)
-    return fail(PBAD_E_UNSUPPORTED, "refined_bootstrap (RK4 Newton-Euler bootstrap) is outside the GPU path");
+  // lbfgs_memory <= 0: the reference pushes and immediately pops every pair
+  // (optim.cpp:183-186), i.e. steepest descent -- the same as memory 0
+  pbad_sim_desc sim_eff = *sim;
+  sim_eff.opt.lbfgs_memory = std::max(0, sim->opt.lbfgs_memory);
+  sim = &sim_eff;
   if (sim->dt <= 0.0 || sim->duration <= 0.0) return fail(PBAD_E_MODEL, "dt and duration must be positive");
-  if (sim->objective == PBAD_ENERGY_FORM && sim->order != 2)
-    return fail(PBAD_E_MODEL, "the energy objective is only defined for order 2");
-  if (sim->opt.kind == PBAD_LBFGS && sim->opt.lbfgs_memory < 1)
-    return fail(PBAD_E_UNSUPPORTED, "lbfgs_memory must be >= 1");
+  // init_pbad_run's build_scheme (stepper.cpp:70) runs before the first
+  // StepObjective (objective.cpp:167-168) checks the energy form's order
   Scheme scheme;
   int32_t rc = build_scheme(sim->order, sim->dt, &scheme);
   if (rc) return rc;
+  if (sim->objective == PBAD_ENERGY_FORM && sim->order != 2)
+    return fail(PBAD_E_MODEL, "the energy objective is only defined for order 2");
+
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(PBAD_E_CUDA, "no CUDA device available (the PBAD GPU path has no CPU fallback)");
@@ -835,6 +872,13 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   c->max_batch = max_batch;
   const pbad_gpu_model& m = c->model;
   c->total_steps = (int)std::ceil(sim->duration / sim->dt - 1e-9);
+  c->max_iters = sim->opt.max_iters;
+  c->refined = sim->refined_bootstrap != 0;
+  {
+    const double t_local_dt = scheme.times[0] * sim->dt;  // stepper.cpp:72, 46-59
+    const double span = -t_local_dt;
+    c->boot_hs = span / 32;
+  }
 
   auto up_i = [&](const std::vector<int>& v) -> const int* {
     int* d = nullptr;
@@ -1116,10 +1160,81 @@ const double* pbad_gpu_state_device(const pbad_gpu_ctx* c) {
 
 namespace {
 
-int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, const double* d_qdot0, cudaStream_t s) {
+// simulate_baseline's general-kernel workspace layout (velocity pass, mass
+// matrix, stage states), shared by pbad_gpu_simulate_baseline and the
+// refined bootstrap
+Layout baseline_layout(const pbad_gpu_model& m) {
+  const long N = m.N, n = m.n;
+  Layout L{};
+  long o = 0;
+  auto take = [&](long cnt) {
+    const long at = o;
+    o += cnt;
+    return at;
+  };
+  L.p_value = 0;
+  L.p_d1 = N * 16;
+  L.p_world = L.p_d1 + n * 16;
+  L.p_lever = L.p_world + N * 16;
+  L.p_d2 = L.p_lever + n * 16;
+  L.pass_stride = L.p_d2 + (long)m.n_d2 * 16;
+  L.pass = take(L.pass_stride);
+  L.seeds = take(N * 16);
+  L.adj = take(N * 16);
+  L.cot = take(N * 16);
+  L.hw0 = take(N * 16);  // tdot
+  L.hw1 = take(N * 16);  // quad
+  L.gn = take(n * n);    // mass matrix / its factor
+  L.x = take(n);
+  L.grad = take(n);
+  L.cand = take(n);
+  L.dir = take(n);
+  L.potgrad = take(n);   // Coriolis
+  L.g = take(n);         // generalized force
+  L.dd = take(n);        // right-hand side
+  L.hs = take(4 * n);    // stage accelerations
+  L.hy = take(4 * n);    // stage states
+  L.total = o;
+  return L;
+}
+
+// bootstrap_history's refined path (stepper.cpp:46-59) for the batch:
+// hist0 into c->d_boot_h0, baseline_step failures into c->d_boot_st
+int32_t refined_bootstrap(pbad_gpu_ctx* c, long B, const double* d_q0, const double* d_qdot0, cudaStream_t s) {
+  const Layout L = baseline_layout(c->model);
+  if (c->boot_cap < B) {
+    cudaFree(c->d_boot_ws);
+    cudaFree(c->d_boot_h0);
+    cudaFree(c->d_boot_st);
+    c->boot_cap = 0;
+    c->d_boot_ws = dalloc<double>((size_t)L.total * B);
+    c->d_boot_h0 = dalloc<double>((size_t)B * c->model.n);
+    c->d_boot_st = dalloc<int>(B);
+    if (!c->d_boot_ws || !c->d_boot_h0 || !c->d_boot_st)
+      return fail(PBAD_E_CUDA, "cudaMalloc of the refined-bootstrap workspace failed (B=%ld)", B);
+    c->boot_cap = B;
+  }
+  CUDA_TRY(launch_refined_bootstrap(c->ka, L, c->d_boot_ws, B, d_q0, d_qdot0, c->boot_hs, c->d_boot_h0,
+                                    c->d_boot_st, s));
+  return PBAD_OK;
+}
+
+// a failed bootstrap throws inside init_pbad_run, before sample 0 is recorded
+__global__ void k_boot_status(const int* st, int* iws, long B) {
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= B || st[e] == 0) return;
+  int& run = iws[(long)IS_RUN * B + e];
+  if (run == PBAD_TRAJ_NONFINITE_CFG && iws[(long)IS_NSAMP * B + e] == 0) return;  // q0 itself non-finite
+  run = st[e] == 6 ? PBAD_TRAJ_BOOTSTRAP_SINGULAR : PBAD_TRAJ_NONFINITE_CFG;  // BL_SINGULAR / BL_NONFINITE_CFG
+  iws[(long)IS_NSAMP * B + e] = 0;
+  iws[(long)IS_NREP * B + e] = 0;
+}
+
+int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, const double* d_qdot0, cudaStream_t s,
+                    bool want_itv = false) {
   if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
   CUDA_TRY(cudaSetDevice(c->device));
-  int32_t rc = ensure_outputs(c, B, W);
+  int32_t rc = ensure_outputs(c, B, W, want_itv);
   if (rc) return rc;
   c->B = B;
   c->ka.B = B;
@@ -1127,8 +1242,18 @@ int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, cons
   c->steps_done = 0;
   c->device_ms = 0.0;
   c->work_stream = s;
-  if (c->chain) CUDA_TRY(launch_chain_init(c->ca, d_q0, d_qdot0, c->dout, s));
-  else CUDA_TRY(launch_init(c->ka, d_q0, d_qdot0, c->dout, s));
+  const double* h0 = nullptr;
+  if (c->refined) {
+    rc = refined_bootstrap(c, B, d_q0, d_qdot0, s);
+    if (rc) return rc;
+    h0 = c->d_boot_h0;
+  }
+  if (c->chain) CUDA_TRY(launch_chain_init(c->ca, d_q0, d_qdot0, h0, c->dout, s));
+  else CUDA_TRY(launch_init(c->ka, d_q0, d_qdot0, h0, c->dout, s));
+  if (c->refined) {
+    k_boot_status<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(c->d_boot_st, c->chain ? c->ca.ci : c->ka.iws, B);
+    CUDA_TRY(cudaGetLastError());
+  }
   return PBAD_OK;
 }
 
@@ -1184,6 +1309,12 @@ int32_t drain_window(pbad_gpu_ctx* c, const pbad_rollout_out* o, long env0, long
     CUDA_TRY(rep(o->accepted, d.accepted));
     CUDA_TRY(rep(o->final_value, d.final_value));
     CUDA_TRY(rep(o->final_grad_norm, d.final_grad_norm));
+    if (o->iteration_values && d.itv) {
+      const long mi = d.itv_n;
+      CUDA_TRY(cudaMemcpy2DAsync(o->iteration_values + (env0 * S + r_lo) * mi, sizeof(double) * S * mi,
+                                 d.itv + (r_lo - d.rbase) * mi, sizeof(double) * d.rs * mi,
+                                 sizeof(double) * cnt * mi, B, cudaMemcpyDeviceToHost, st));
+    }
   }
   return PBAD_OK;
 }
@@ -1211,7 +1342,7 @@ struct RolloutJob {
   long env0, B, W, ws;
 };
 
-int32_t job_start(RolloutJob& j, const double* q0, const double* qdot0) {
+int32_t job_start(RolloutJob& j, const double* q0, const double* qdot0, bool want_itv) {
   pbad_gpu_ctx* c = j.c;
   const long n = c->model.n;
   CUDA_TRY(cudaSetDevice(c->device));
@@ -1224,7 +1355,7 @@ int32_t job_start(RolloutJob& j, const double* q0, const double* qdot0) {
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_q0, q0 + j.env0 * n, sizeof(double) * j.B * n, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->d_qd0, qdot0 + j.env0 * n, sizeof(double) * j.B * n, cudaMemcpyHostToDevice, c->stream));
-  int32_t rc = begin_batch(c, (int32_t)j.B, j.W, c->d_q0, c->d_qd0, c->stream);
+  int32_t rc = begin_batch(c, (int32_t)j.B, j.W, c->d_q0, c->d_qd0, c->stream, want_itv);
   if (rc) return rc;
   CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
   j.ws = 0;
@@ -1278,7 +1409,7 @@ int32_t job_wait(RolloutJob& j, float* ms) {
 
 int32_t run_jobs(std::vector<RolloutJob>& jobs, const double* q0, const double* qdot0, pbad_rollout_out* out) {
   for (auto& j : jobs) {
-    const int32_t rc = job_start(j, q0, qdot0);
+    const int32_t rc = job_start(j, q0, qdot0, out->iteration_values != nullptr);
     if (rc) return rc;
   }
   // window by window: every device's steps are queued before the drains, so
@@ -1365,7 +1496,7 @@ int32_t pbad_gpu_final_state(pbad_gpu_ctx* c, double* d_dst, void* stream) {
 int32_t pbad_gpu_rollout(pbad_gpu_ctx* c, int32_t B, const double* q0, const double* qdot0,
                          pbad_rollout_out* out) {
   if (B < 1 || B > c->max_batch) return fail(PBAD_E_ARGUMENT, "batch %d outside [1, %ld]", B, c->max_batch);
-  std::vector<RolloutJob> jobs{RolloutJob{c, 0, B, window_steps(c, B), 0}};
+  std::vector<RolloutJob> jobs{RolloutJob{c, 0, B, window_steps(c, B, out->iteration_values != nullptr), 0}};
   return run_jobs(jobs, q0, qdot0, out);
 }
 
@@ -1384,7 +1515,7 @@ int32_t pbad_gpu_rollout_sharded(pbad_gpu_ctx* const* ctxs, int32_t n_ctx, int32
     const long lo = (long)B * i / n_ctx, hi = (long)B * (i + 1) / n_ctx;
     if (hi - lo > c->max_batch)
       return fail(PBAD_E_ARGUMENT, "shard %d has %ld environments, context max_batch is %ld", i, hi - lo, c->max_batch);
-    jobs.push_back(RolloutJob{c, lo, hi - lo, window_steps(c, hi - lo), 0});
+    jobs.push_back(RolloutJob{c, lo, hi - lo, window_steps(c, hi - lo, out->iteration_values != nullptr), 0});
   }
   return run_jobs(jobs, q0, qdot0, out);
 }
@@ -1451,41 +1582,12 @@ int32_t pbad_gpu_simulate_baseline(pbad_gpu_ctx* c, int32_t scheme, int32_t B, c
   if (scheme < 0 || scheme > 4) return fail(PBAD_E_ARGUMENT, "unknown baseline scheme %d", scheme);
   if (!q0 || !qdot0 || !n_samples || !status) return fail(PBAD_E_ARGUMENT, "q0, qdot0, n_samples, status required");
   const pbad_gpu_model& m = c->model;
-  const long N = m.N, n = m.n;
+  const long n = m.n;
   for (long k = 0; k < (long)B * n; ++k)
     if (!std::isfinite(q0[k])) return fail(PBAD_E_MODEL, "configuration contains a non-finite entry");
   CUDA_TRY(cudaSetDevice(c->device));
   const long S = c->ka.sc.total_steps;
-  Layout L{};
-  long o = 0;
-  auto take = [&](long cnt) {
-    const long at = o;
-    o += cnt;
-    return at;
-  };
-  L.p_value = 0;
-  L.p_d1 = N * 16;
-  L.p_world = L.p_d1 + n * 16;
-  L.p_lever = L.p_world + N * 16;
-  L.p_d2 = L.p_lever + n * 16;
-  L.pass_stride = L.p_d2 + (long)m.n_d2 * 16;
-  L.pass = take(L.pass_stride);
-  L.seeds = take(N * 16);
-  L.adj = take(N * 16);
-  L.cot = take(N * 16);
-  L.hw0 = take(N * 16);  // tdot
-  L.hw1 = take(N * 16);  // quad
-  L.gn = take(n * n);    // mass matrix / its factor
-  L.x = take(n);
-  L.grad = take(n);
-  L.cand = take(n);
-  L.dir = take(n);
-  L.potgrad = take(n);   // Coriolis
-  L.g = take(n);         // generalized force
-  L.dd = take(n);        // right-hand side
-  L.hs = take(4 * n);    // stage accelerations
-  L.hy = take(4 * n);    // stage states
-  L.total = o;
+  const Layout L = baseline_layout(m);
   double* ws = dalloc<double>((size_t)L.total * B);
   double* dq = dalloc<double>((size_t)2 * B * n);
   double* doq = q_out ? dalloc<double>((size_t)B * (S + 1) * n) : nullptr;

@@ -33,6 +33,7 @@ struct Env {
   int* iws;
   long B;
   int e;
+  double* itv = nullptr;  // this step's per_iteration_values row, or null
   __device__ __forceinline__ Arr arr(long off) const { return Arr{ws + off * B + e, B}; }
   __device__ __forceinline__ int& iv(int slot) const { return iws[(long)slot * B + e]; }
   __device__ __forceinline__ double& sv(int slot) const { return ws[(L->scal + slot) * B + e]; }
@@ -658,7 +659,11 @@ __device__ int solver_init(const Env& E, bool have_tau) {
   return 0;
 }
 
-__device__ __forceinline__ void finish_iteration(const Env& E) { ++E.iv(IS_ITERS); }
+// SolverBase::finish_iteration (optim.cpp:64-67): count, record the value
+__device__ __forceinline__ void finish_iteration(const Env& E) {
+  if (E.itv) E.itv[E.iv(IS_ITERS)] = E.sv(SC_VALUE);
+  ++E.iv(IS_ITERS);
+}
 
 // LmSolver::iterate (optim.cpp:95-134). Returns status or -1 on ModelError.
 __device__ int lm_iterate(const Env& E, bool have_tau) {
@@ -1111,6 +1116,59 @@ __global__ void __launch_bounds__(128) k_baseline(DModel m, DForces f, DSchedule
   status[e] = st;
 }
 
+// bootstrap_history with refined_bootstrap (stepper.cpp:46-59): the history
+// instant before the run start as the state reached from (q0, -qdot0) after
+// 32 RK4 substeps of hs = span / 32 (baseline_step, baseline.cpp:152-206),
+// one thread per trajectory; status BL_OK or the baseline_step failure
+__global__ void __launch_bounds__(128) k_refined_bootstrap(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
+                                                           long B, const double* q0, const double* qd0, double hs,
+                                                           double* hist0, int* status) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= B) return;
+  Env E{&m, &f, &sc, &L, ws, nullptr, B, e};
+  const int n = m.n;
+  const BlArrs W{E.arr(L.hw0), E.arr(L.hw1), E.arr(L.cot), E.arr(L.gn), E.arr(L.potgrad), E.arr(L.g),
+                 E.arr(L.dd)};
+  const Arr q = E.arr(L.x), qd = E.arr(L.grad), sq = E.arr(L.cand), sqd = E.arr(L.dir);
+  const Arr a1 = E.arr(L.hs), a2 = E.arr(L.hs + n), a3 = E.arr(L.hs + 2 * n), a4 = E.arr(L.hs + 3 * n);
+  const Arr s2q = E.arr(L.hy), s2qd = E.arr(L.hy + n), s3q = E.arr(L.hy + 2 * n), s3qd = E.arr(L.hy + 3 * n);
+  for (int k = 0; k < n; ++k) {
+    q[k] = q0[(long)e * n + k];
+    qd[k] = -qd0[(long)e * n + k];
+  }
+  const double h = 0.5 * hs, d6 = hs / 6.0;
+  int st = BL_OK;
+  for (int k = 0; k < 32 && st == BL_OK; ++k) {
+    int rc = bl_accel(E, W, q, qd, a1, hs);
+    if (rc) { st = rc; break; }
+    for (int j = 0; j < n; ++j) {
+      s2q[j] = q[j] + h * qd[j];
+      s2qd[j] = qd[j] + h * a1[j];
+    }
+    rc = bl_accel(E, W, s2q, s2qd, a2, hs);
+    if (rc) { st = rc; break; }
+    for (int j = 0; j < n; ++j) {
+      s3q[j] = q[j] + h * s2qd[j];
+      s3qd[j] = qd[j] + h * a2[j];
+    }
+    rc = bl_accel(E, W, s3q, s3qd, a3, hs);
+    if (rc) { st = rc; break; }
+    for (int j = 0; j < n; ++j) {
+      sq[j] = q[j] + hs * s3qd[j];
+      sqd[j] = qd[j] + hs * a3[j];
+    }
+    rc = bl_accel(E, W, sq, sqd, a4, hs);
+    if (rc) { st = rc; break; }
+    for (int j = 0; j < n; ++j) {
+      const double qn = q[j] + d6 * (((qd[j] + 2.0 * s2qd[j]) + 2.0 * s3qd[j]) + sqd[j]);
+      qd[j] = qd[j] + d6 * (((a1[j] + 2.0 * a2[j]) + 2.0 * a3[j]) + a4[j]);
+      q[j] = qn;
+    }
+  }
+  for (int k = 0; k < n; ++k) hist0[(long)e * n + k] = q[k];
+  status[e] = st;
+}
+
 
 // ForceModel::tau_at (objective.hpp:28-58) into dst
 __device__ void forces_tau_at(const Env& E, double t, const Arr& dst) {
@@ -1204,7 +1262,7 @@ __device__ bool finish_step(const Env& E, const Outputs& out) {
 // init_pbad_run (stepper.cpp:62-80): q0, qdot0 device [B][n]
 __global__ void __launch_bounds__(128) k_init(DModel m, DForces f, DSchedule sc, Layout L, double* ws,
                                               int* iws, long B, const double* q0, const double* qdot0,
-                                              Outputs out) {
+                                              const double* hist0, Outputs out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= B) return;
   Env E{&m, &f, &sc, &L, ws, iws, B, e};
@@ -1223,7 +1281,10 @@ __global__ void __launch_bounds__(128) k_init(DModel m, DForces f, DSchedule sc,
     return;
   }
   const double tl = sc.times[0] * sc.dt;
-  for (int k = 0; k < n; ++k) h0[k] = h1[k] + tl * qd[k];
+  if (hist0)  // refined_bootstrap (k_refined_bootstrap)
+    for (int k = 0; k < n; ++k) h0[k] = hist0[(long)e * n + k];
+  else
+    for (int k = 0; k < n; ++k) h0[k] = h1[k] + tl * qd[k];
   const Arr w1 = E.arr(L.hw1);
   forward_pass(E, h1, w1);
   const double ke = kinetic_energy(E, h1, qd);
@@ -1238,6 +1299,7 @@ __global__ void __launch_bounds__(128) k_step(DModel m, DForces f, DSchedule sc,
   if (e >= B) return;
   Env E{&m, &f, &sc, &L, ws, iws, B, e};
   if (E.iv(IS_RUN) != TR_RUNNING) return;
+  if (out.itv) E.itv = out.itv + out.rrow(e, E.iv(IS_STEP)) * out.itv_n;
   const int rc = begin_step(E);
   if (rc) {
     E.iv(IS_RUN) = rc;
@@ -1355,9 +1417,9 @@ namespace pbad_gpu {
 static inline int block_for(long B) { return B >= 148L * 128 ? 128 : 32; }
 static inline unsigned grid_for(long B) { return (unsigned)((B + block_for(B) - 1) / block_for(B)); }
 
-cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
-                        cudaStream_t s) {
-  k_init<<<grid_for(a.B), block_for(a.B), 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, q0, qdot0, out);
+cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const double* hist0,
+                        const Outputs& out, cudaStream_t s) {
+  k_init<<<grid_for(a.B), block_for(a.B), 0, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, q0, qdot0, hist0, out);
   return cudaGetLastError();
 }
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s) {
@@ -1393,6 +1455,11 @@ cudaError_t launch_correlation(const DModel& m, const Layout& L, double* ws, lon
                                const double* qb, double* value, double* grad, double* hbb, double* hab,
                                cudaStream_t s) {
   k_correlation<<<grid_for(B), block_for(B), 0, s>>>(m, L, ws, B, qa, qb, value, grad, hbb, hab);
+  return cudaGetLastError();
+}
+cudaError_t launch_refined_bootstrap(const KernelArgs& a, const Layout& L, double* ws, long B, const double* q0,
+                                     const double* qd0, double hs, double* hist0, int* status, cudaStream_t s) {
+  k_refined_bootstrap<<<(unsigned)((B + 31) / 32), 32, 0, s>>>(a.m, a.f, a.sc, L, ws, B, q0, qd0, hs, hist0, status);
   return cudaGetLastError();
 }
 cudaError_t launch_baseline(const KernelArgs& a, const Layout& L, double* ws, long B, int scheme, const double* q0,

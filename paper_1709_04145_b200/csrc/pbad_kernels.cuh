@@ -165,6 +165,9 @@ struct Outputs {
   // slot geometry: the whole trajectory (qs = S + 1, rs = S, bases 0), or a
   // window of it that pbad_gpu_rollout drains to the host between launches
   long qs, qbase, rs, rbase;
+  // SolveReport::per_iteration_values [B][rs][itv_n] (itv_n = max_iters), or null
+  double* itv;
+  long itv_n;
   __host__ __device__ long qrow(long e, long sample) const { return e * qs + (sample - qbase); }
   __host__ __device__ long rrow(long e, long step) const { return e * rs + (step - rbase); }
 };

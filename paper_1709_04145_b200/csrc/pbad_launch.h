@@ -27,8 +27,8 @@ struct ChainArgs {
   long B;
 };
 
-cudaError_t launch_chain_init(const ChainArgs& a, const double* q0, const double* qdot0, const Outputs& out,
-                              cudaStream_t s);
+cudaError_t launch_chain_init(const ChainArgs& a, const double* q0, const double* qdot0, const double* hist0,
+                              const Outputs& out, cudaStream_t s);
 cudaError_t launch_chain_step(const ChainArgs& a, const Outputs& out, cudaStream_t s);
 int chain_max_memory();
 int chain_max_links();
@@ -56,9 +56,12 @@ size_t resid_smem_bytes(int N, int u);
 cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out,
                               cudaStream_t s);
 
-cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const Outputs& out,
-                        cudaStream_t s);
+cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const double* hist0,
+                        const Outputs& out, cudaStream_t s);
 cudaError_t launch_step(const KernelArgs& a, const Outputs& out, cudaStream_t s);
+// refined_bootstrap history (stepper.cpp:46-59): hist0 [B][n], status [B]
+cudaError_t launch_refined_bootstrap(const KernelArgs& a, const Layout& L, double* ws, long B, const double* q0,
+                                     const double* qd0, double hs, double* hist0, int* status, cudaStream_t s);
 cudaError_t launch_baseline(const KernelArgs& a, const Layout& L, double* ws, long B, int scheme, const double* q0,
                             const double* qd0, double* oq, double* oe, int* nsamp, int* status, cudaStream_t s);
 cudaError_t launch_correlation(const DModel& m, const Layout& L, double* ws, long B, const double* qa,

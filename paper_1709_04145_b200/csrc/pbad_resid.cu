@@ -1797,6 +1797,7 @@ __device__ __noinline__ void llt_solve(const R& r, double* v) {
 struct Solver {
   int status, iters, stag, acc;
   double value, lambda, grad0;
+  double* itv;  // per_iteration_values row of this step (thread 0 writes), or null
 };
 
 
@@ -1885,6 +1886,7 @@ __device__ int lm_iterate(const R& r, Solver& S) {
     S.lambda *= o.lm_lambda_factor;
     if (S.lambda > o.lm_lambda_max) S.status = ST_FAILED;
   }
+  if (S.itv && r.tid == 0) S.itv[S.iters] = S.value;
   ++S.iters;
   if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
   return S.status;
@@ -2002,6 +2004,7 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
   // solver construction (optim.cpp:82-93)
   Solver S;
   S.status = ST_RUNNING;
+  S.itv = out.itv ? out.itv + out.rrow(e, step) * out.itv_n : nullptr;
   S.iters = 0;
   S.stag = 0;
   S.acc = 0;

@@ -674,6 +674,7 @@ __device__ TREE_COLD void derivatives(const W& w) {
 struct Solver {
   int status, iters, stag, acc;
   double value, lambda, grad0;
+  double* itv;  // per_iteration_values row of this step (lane 0 writes), or null
 };
 
 __device__ __forceinline__ bool grad_converged(const W& w, const Solver& S) {
@@ -742,6 +743,7 @@ __device__ int lm_iterate(const W& w, Solver& S) {
     S.lambda *= o.lm_lambda_factor;
     if (S.lambda > o.lm_lambda_max) S.status = ST_FAILED;
   }
+  if (S.itv && w.lane == 0) S.itv[S.iters] = S.value;
   ++S.iters;
   if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
   return S.status;
@@ -890,6 +892,7 @@ __global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel
   // later passes solve the damped system and evaluate the candidate.
   Solver S;
   S.status = ST_RUNNING;
+  S.itv = out.itv ? out.itv + out.rrow(e, step) * out.itv_n : nullptr;
   S.iters = 0;
   S.stag = 0;
   S.acc = 0;
@@ -989,6 +992,7 @@ __global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel
           S.lambda *= o.lm_lambda_factor;
           if (S.lambda > o.lm_lambda_max) S.status = ST_FAILED;
         }
+        if (S.itv && w.lane == 0) S.itv[S.iters] = S.value;
         ++S.iters;
         if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
       }
@@ -1173,6 +1177,7 @@ __global__ void __launch_bounds__(32) k_tree_lbfgs(const __grid_constant__ DMode
   // every iterate runs the two-loop recursion and the Armijo backtracking
   Solver S;
   S.status = ST_RUNNING;
+  S.itv = out.itv ? out.itv + out.rrow(e, step) * out.itv_n : nullptr;
   S.iters = 0;
   S.stag = 0;
   S.acc = 0;
@@ -1304,6 +1309,7 @@ __global__ void __launch_bounds__(32) k_tree_lbfgs(const __grid_constant__ DMode
       }
       if (err) break;
       if (!accepted) S.status = ST_FAILED;
+      if (S.itv && w.lane == 0) S.itv[S.iters] = S.value;
       ++S.iters;
       if (S.status == ST_RUNNING && S.iters >= o.max_iters) S.status = ST_FAILED;
     }

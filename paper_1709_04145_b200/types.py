@@ -142,6 +142,7 @@ class SolveReport:
     final_grad_norm: float = 0.0
     converged: bool = False
     accepted: int = 0  # accepted iterations (derivable from per_iteration_values)
+    per_iteration_values: List[float] = field(default_factory=list)  # optim.cpp:30-37 (on request)
 
 
 @dataclass
