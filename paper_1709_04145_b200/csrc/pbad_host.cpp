@@ -486,6 +486,7 @@ struct pbad_gpu_ctx {
   ChainArgs ca{};
   bool chain = false;      // rollouts use the quad chain kernels
   bool chain4 = false;     // ... in their warp-synchronous v4 form (pbad_chain4.cu)
+  bool chain5 = false;     // ... or warp per environment, v5 (pbad_chain5.cu)
   int chain4_pat = 0;      // v4 link-pattern instantiation
   long chain4_recw = 0;    // v4 record doubles per warp
   long v1_per_env = 0;     // general-kernel workspace size (allocated lazily)
@@ -945,6 +946,11 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     dm.croff = up_i(roff);
     c->chain4 = chain4_eligible(ck, m.N, sim->opt.lbfgs_memory);
     c->chain4_pat = chain4_pattern(ck.data(), m.N);
+    // v5 (warp per environment) while the batch fits one wave of resident
+    // blocks, else v4 (quad per environment); PBAD_GPU_CHAIN_V5 / _V4 force one
+    const int waves = chain5_waves(m.N, m.n, sim->opt.lbfgs_memory, max_batch, c->chain4_pat, device);
+    c->chain5 = c->chain4 && !std::getenv("PBAD_GPU_CHAIN_V4") &&
+                (std::getenv("PBAD_GPU_CHAIN_V5") ? waves > 0 : waves == 1);
     c->chain4_recw = roff[m.N];
   }
 
@@ -1001,6 +1007,7 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   c->ka = KernelArgs{dm, df, ds, L, nullptr, nullptr, max_batch};
   c->chain = chain_eligible(m, f, sim);
   c->chain4 = c->chain4 && c->chain;
+  c->chain5 = c->chain5 && c->chain4;
   c->tree = !c->chain && tree_eligible(m, f, sim);
   if (c->tree) {
     const TreeHost th = make_tree_host(m);
@@ -1145,7 +1152,8 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
 void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
 int32_t pbad_gpu_path(const pbad_gpu_ctx* c) {
-  return c->chain4 ? PBAD_PATH_CHAIN4
+  return c->chain5 ? PBAD_PATH_CHAIN5
+         : c->chain4 ? PBAD_PATH_CHAIN4
          : c->chain ? PBAD_PATH_CHAIN
          : c->tree  ? PBAD_PATH_TREE
          : c->resid ? PBAD_PATH_RESID
@@ -1260,7 +1268,8 @@ int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, cons
 int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
   c->work_stream = s;
   for (long k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
-    CUDA_TRY(c->chain4  ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
+    CUDA_TRY(c->chain5  ? launch_chain5_step(c->ca, c->chain4_pat, c->chain4_recw / 8, c->dout, s)
+             : c->chain4 ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain ? launch_chain_step(c->ca, c->dout, s)
              : c->tree  ? launch_tree_step(c->ka, c->td, c->tws, c->dout, s)
              : c->resid ? launch_resid_step(c->ka, c->rd, c->rws, c->dout, s)

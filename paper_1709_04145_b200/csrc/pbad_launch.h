@@ -39,6 +39,10 @@ size_t chain4_smem_bytes(int N);
 int chain4_max_memory();
 long chain4_record_doubles(bool massive);
 long chain4_hist_doubles();
+// chain v5 (pbad_chain5.cu): warp per environment, shared-memory-resident L-BFGS
+bool chain5_fits(int N, int n, int mem);
+int chain5_waves(int N, int n, int mem, long B, int pattern, int device);
+cudaError_t launch_chain5_step(const ChainArgs& a, int pattern, long recw, const Outputs& out, cudaStream_t s);
 
 // tree path (pbad_tree.cu): warp-per-environment LM for articulated trees
 bool tree_eligible_sizes(int N, int n);

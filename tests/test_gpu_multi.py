@@ -42,7 +42,7 @@ def _equal(a, b):
 
 
 @pytest.mark.parametrize("name,steps,batch,max_iters,shards", [
-    ("C2", 3, 40, None, 2),    # chain4 path, ragged warps
+    ("C2", 3, 40, None, 2),    # chain path, ragged blocks
     ("C4b", 4, 70, None, 3),   # tree Newton path with contact
     ("C5", 1, 5, 4, 2),        # residual path
 ])

@@ -273,35 +273,47 @@ def _path(scene, sim):
     return api.GpuContext(m, scene.forces(), sim, max_batch=1).path
 
 
-def test_chain4_dispatch_path_ragged_batch():
+CHAIN_KERNELS = [("v5", 5), ("v4", 2)]
+
+
+def _chain_kernel(monkeypatch, version):
+    if version == "v4":
+        monkeypatch.setenv("PBAD_GPU_CHAIN_V4", "1")
+
+
+@pytest.mark.parametrize("version,path", CHAIN_KERNELS)
+def test_chain4_dispatch_path_ragged_batch(version, path, monkeypatch):
     """13 links (a partial last chunk), 11 environments (a padded warp), the
     generic per-link dispatch: bit-exact against the oracle."""
+    _chain_kernel(monkeypatch, version)
     from paper_1709_04145_b200.scenes import Scene
     sc = Scene(links=_axis_chain(21, 13), gravity=(1.0, -2.0, -9.81))
     sc.q0 = np.zeros(13)
     sc.qdot0 = np.zeros(13)
     sim = SimConfig(dt=0.02, duration=0.1)
     sim.optimizer.kind = OptimizerKind.lbfgs
-    assert _path(sc, sim) == 2
+    assert _path(sc, sim) == path
     _rollout_case(sc, sim, B=11, seed=9, lo=-0.5, hi=0.5)
 
 
-def test_chain4_lockstep_divergent_envs():
+@pytest.mark.parametrize("version,path", CHAIN_KERNELS)
+def test_chain4_lockstep_divergent_envs(version, path, monkeypatch):
     """Environments of one warp converge, fail and abort at different
     iterations / steps (max_iters small, fail limit 1)."""
+    _chain_kernel(monkeypatch, version)
     sc = make_single_hinge_chain_scene(10)
     sim = SimConfig(dt=0.01, duration=0.08, consecutive_fail_limit=1)
     sim.optimizer.kind = OptimizerKind.lbfgs
     sim.optimizer.max_iters = 60
-    assert _path(sc, sim) == 2
+    assert _path(sc, sim) == path
     gpu, ref = _rollout_case(sc, sim, B=11, seed=3, lo=-1.0, hi=1.0)
     errs = {g.error for g in gpu}
     assert len(errs) >= 1
 
 
 def test_chain4_matches_chain_v3(monkeypatch):
-    """The v3 quad kernel (PBAD_GPU_CHAIN_V3) and v4 produce identical
-    trajectories (both are pinned to the oracle)."""
+    """The v3 quad kernel (PBAD_GPU_CHAIN_V3), v4 (PBAD_GPU_CHAIN_V4) and
+    v5 produce identical trajectories (all are pinned to the oracle)."""
     sc = make_chain_scene(12)
     sim = SimConfig(dt=0.1, duration=0.3)
     sim.optimizer.kind = OptimizerKind.lbfgs
@@ -313,11 +325,15 @@ def test_chain4_matches_chain_v3(monkeypatch):
         s.q0 = mt19937_uniform(40 + b, n, -0.3, 0.3)
         s.qdot0 = np.zeros(n)
         sims.append(s)
+    assert _path(sc, sim) == 5
+    v5 = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.setenv("PBAD_GPU_CHAIN_V4", "1")
     assert _path(sc, sim) == 2
     v4 = api.batch_simulate(m, sc.forces(), sims)
     monkeypatch.setenv("PBAD_GPU_CHAIN_V3", "1")
     assert _path(sc, sim) == 1
     v3 = api.batch_simulate(m, sc.forces(), sims)
-    for a, b in zip(v4, v3):
-        np.testing.assert_array_equal(np.array([s[1] for s in a.samples]), np.array([s[1] for s in b.samples]))
-        assert [r.iterations for r in a.solve_reports] == [r.iterations for r in b.solve_reports]
+    for a, b, c in zip(v5, v4, v3):
+        for o in (b, c):
+            np.testing.assert_array_equal(np.array([s[1] for s in a.samples]), np.array([s[1] for s in o.samples]))
+            assert [r.iterations for r in a.solve_reports] == [r.iterations for r in o.solve_reports]

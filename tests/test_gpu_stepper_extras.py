@@ -35,7 +35,7 @@ def _ref(scene, sims):
 
 
 @pytest.mark.parametrize("kind,order,objective,path", [
-    (OptimizerKind.lbfgs, 2, ObjectiveKind.energy_form, 2),
+    (OptimizerKind.lbfgs, 2, ObjectiveKind.energy_form, 5),
     (OptimizerKind.lm, 2, ObjectiveKind.energy_form, 3),
     (OptimizerKind.lm, 4, ObjectiveKind.residual_form, 4),
 ])
@@ -66,7 +66,7 @@ def test_refined_bootstrap_tree():
 
 
 @pytest.mark.parametrize("mem", [0, -3])
-@pytest.mark.parametrize("scene,path", [("chain", 2), ("humanoid", 3)])
+@pytest.mark.parametrize("scene,path", [("chain", 5), ("humanoid", 3)])
 def test_lbfgs_memory_nonpositive(mem, scene, path):
     sc = make_chain_scene(6) if scene == "chain" else make_humanoid_scene()
     m = api.build_model(sc.links)
