@@ -487,6 +487,7 @@ struct pbad_gpu_ctx {
   bool chain = false;      // rollouts use the quad chain kernels
   bool chain4 = false;     // ... in their warp-synchronous v4 form (pbad_chain4.cu)
   bool chain5 = false;     // ... or warp per environment, v5 (pbad_chain5.cu)
+  bool chain6 = false;     // ... or two lanes per row, v6 (pbad_chain6.cu)
   int chain4_pat = 0;      // v4 link-pattern instantiation
   long chain4_recw = 0;    // v4 record doubles per warp
   long v1_per_env = 0;     // general-kernel workspace size (allocated lazily)
@@ -613,7 +614,8 @@ ChainLayout make_chain_layout(const pbad_gpu_model& m, int mem, long B, long rec
   // instead of the link arrays
   ChainLayout L{};
   const long N = m.N, n4 = (m.n + 3) / 4, nw = (B + 7) / 8;
-  const long link = rec_w > 0 ? 0 : nw * N * 128, vec = nw * n4 * 32;
+  // vectors: the v3/v4 quad layout or the v6 8-lane layout, whichever is larger
+  const long link = rec_w > 0 ? 0 : nw * N * 128, vec = std::max(nw * n4 * 32, chain6_vector_doubles(B, m.n));
   long o = 0;
   auto take = [&](long cnt) {
     const long at = o;
@@ -947,9 +949,9 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     c->chain4 = chain4_eligible(ck, m.N, sim->opt.lbfgs_memory);
     c->chain4_pat = chain4_pattern(ck.data(), m.N);
     // v5 (warp per environment) while the batch fits one wave of resident
-    // blocks, else v4 (quad per environment); PBAD_GPU_CHAIN_V5 / _V4 force one
+    // blocks, else v6 (two lanes per row); PBAD_GPU_CHAIN_V5 / _V6 / _V4 force one
     const int waves = chain5_waves(m.N, m.n, sim->opt.lbfgs_memory, max_batch, c->chain4_pat, device);
-    c->chain5 = c->chain4 && !std::getenv("PBAD_GPU_CHAIN_V4") &&
+    c->chain5 = c->chain4 && !std::getenv("PBAD_GPU_CHAIN_V4") && !std::getenv("PBAD_GPU_CHAIN_V6") &&
                 (std::getenv("PBAD_GPU_CHAIN_V5") ? waves > 0 : waves == 1);
     c->chain4_recw = roff[m.N];
   }
@@ -1008,6 +1010,9 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   c->chain = chain_eligible(m, f, sim);
   c->chain4 = c->chain4 && c->chain;
   c->chain5 = c->chain5 && c->chain4;
+  // beyond one v5 wave: v6 (two lanes per row) unless PBAD_GPU_CHAIN_V4
+  c->chain6 = c->chain4 && !c->chain5 && !std::getenv("PBAD_GPU_CHAIN_V4") &&
+              chain6_fits(m.N, sim->opt.lbfgs_memory);
   c->tree = !c->chain && tree_eligible(m, f, sim);
   if (c->tree) {
     const TreeHost th = make_tree_host(m);
@@ -1153,6 +1158,7 @@ void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
 int32_t pbad_gpu_path(const pbad_gpu_ctx* c) {
   return c->chain5 ? PBAD_PATH_CHAIN5
+         : c->chain6 ? PBAD_PATH_CHAIN6
          : c->chain4 ? PBAD_PATH_CHAIN4
          : c->chain ? PBAD_PATH_CHAIN
          : c->tree  ? PBAD_PATH_TREE
@@ -1269,6 +1275,7 @@ int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
   c->work_stream = s;
   for (long k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
     CUDA_TRY(c->chain5  ? launch_chain5_step(c->ca, c->chain4_pat, c->chain4_recw / 8, c->dout, s)
+             : c->chain6 ? launch_chain6_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain4 ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain ? launch_chain_step(c->ca, c->dout, s)
              : c->tree  ? launch_tree_step(c->ka, c->td, c->tws, c->dout, s)

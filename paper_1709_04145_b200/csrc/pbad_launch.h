@@ -42,6 +42,10 @@ long chain4_hist_doubles();
 // chain v5 (pbad_chain5.cu): warp per environment, shared-memory-resident L-BFGS
 bool chain5_fits(int N, int n, int mem);
 int chain5_waves(int N, int n, int mem, long B, int pattern, int device);
+// chain v6 (pbad_chain6.cu): v4 with two lanes per row, 4 environments per warp
+bool chain6_fits(int N, int mem);
+long chain6_vector_doubles(long B, int n);
+cudaError_t launch_chain6_step(const ChainArgs& a, int pattern, const Outputs& out, cudaStream_t s);
 cudaError_t launch_chain5_step(const ChainArgs& a, int pattern, long recw, const Outputs& out, cudaStream_t s);
 
 // tree path (pbad_tree.cu): warp-per-environment LM for articulated trees

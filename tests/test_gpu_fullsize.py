@@ -55,7 +55,7 @@ def _check_sample(out, scene, sim, q0, envs):
 
 
 @pytest.mark.parametrize("name,steps,max_iters,expect_path", [
-    ("C3", 1, None, 2),
+    ("C3", 1, None, 6),
     ("C4", 2, None, 3),
     ("C4b", 2, None, 3),
     ("C5", 1, 6, 4),

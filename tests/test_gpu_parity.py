@@ -273,12 +273,14 @@ def _path(scene, sim):
     return api.GpuContext(m, scene.forces(), sim, max_batch=1).path
 
 
-CHAIN_KERNELS = [("v5", 5), ("v4", 2)]
+CHAIN_KERNELS = [("v5", 5), ("v6", 6), ("v4", 2)]
 
 
 def _chain_kernel(monkeypatch, version):
     if version == "v4":
         monkeypatch.setenv("PBAD_GPU_CHAIN_V4", "1")
+    if version == "v6":
+        monkeypatch.setenv("PBAD_GPU_CHAIN_V6", "1")
 
 
 @pytest.mark.parametrize("version,path", CHAIN_KERNELS)
@@ -327,13 +329,17 @@ def test_chain4_matches_chain_v3(monkeypatch):
         sims.append(s)
     assert _path(sc, sim) == 5
     v5 = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.setenv("PBAD_GPU_CHAIN_V6", "1")
+    assert _path(sc, sim) == 6
+    v6 = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.delenv("PBAD_GPU_CHAIN_V6")
     monkeypatch.setenv("PBAD_GPU_CHAIN_V4", "1")
     assert _path(sc, sim) == 2
     v4 = api.batch_simulate(m, sc.forces(), sims)
     monkeypatch.setenv("PBAD_GPU_CHAIN_V3", "1")
     assert _path(sc, sim) == 1
     v3 = api.batch_simulate(m, sc.forces(), sims)
-    for a, b, c in zip(v5, v4, v3):
-        for o in (b, c):
+    for a, b, c, d in zip(v5, v4, v3, v6):
+        for o in (b, c, d):
             np.testing.assert_array_equal(np.array([s[1] for s in a.samples]), np.array([s[1] for s in o.samples]))
             assert [r.iterations for r in a.solve_reports] == [r.iterations for r in o.solve_reports]
