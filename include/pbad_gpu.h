@@ -269,6 +269,25 @@ int32_t pbad_gpu_correlation(pbad_gpu_ctx* ctx, int32_t B, const double* qa, con
                              const double* weight_per_body, double* value, double* grad_b,
                              double* hess_bb, double* hess_ab);
 
+/* parallel_correlation_suite (adjoint.hpp:103-108, adjoint.cpp:241-336): the
+ * same four derivatives as pbad_gpu_correlation for B configuration pairs,
+ * computed the large-N way: one CTA per pair, the reference's per-link work
+ * items (value slot + grad_b, hess_bb block, hess_ab block) spread over its
+ * threads.  grad_b is assigned, as the suite does (pbad_gpu_correlation
+ * accumulates like correlation_grad_b: they differ only in the sign of a
+ * zero).  Same output layouts, each optional. */
+int32_t pbad_gpu_correlation_suite(pbad_gpu_ctx* ctx, int32_t B, const double* qa, const double* qb,
+                                   const double* weight_per_body, double* value, double* grad_b,
+                                   double* hess_bb, double* hess_ab);
+
+/* functional_value / functional_grad / functional_hess (adjoint.hpp:52-60,
+ * adjoint.cpp:43-101) of f(q) = sum_i ddot(C_i, T^i(q)) for B (q, seeds)
+ * pairs: q [B][n], seeds [B][n_links][16] column-major cotangents C_i;
+ * value [B], grad [B][n], hess [B][n][n] column-major, each optional.
+ * One CTA per pair (pbad_corr.cu). */
+int32_t pbad_gpu_functional(pbad_gpu_ctx* ctx, int32_t B, const double* q, const double* seeds,
+                            double* value, double* grad, double* hess);
+
 /* minimize() of a batch of step problems (same inputs as eval, x0 [B][dim]). */
 int32_t pbad_gpu_minimize(pbad_gpu_ctx* ctx, int32_t B, const double* history,
                           const double* tau, const double* x0, double* x_out,

@@ -498,6 +498,8 @@ def ref_lib():
         R.pbr_forward_pass.argtypes = [vp, _dp, _dp]
         R.pbr_correlation.argtypes = [vp, _dp, _dp, _dp, _dp, _dp, _dp]
         R.pbr_build_scheme.argtypes = [C.c_int, C.c_double, _dp, _dp]
+        R.pbr_correlation_suite.argtypes = [vp, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp, _dp]
+        R.pbr_functional.argtypes = [vp, _dp, _dp, _dp, _dp, _dp]
         R.pbr_step_eval.argtypes = [vp, C.POINTER(ForcesC), C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, C.c_int,
                                     C.c_int, _dp, _dp, _dp]
         R.pbr_simulate.argtypes = [vp, C.POINTER(ForcesC), C.POINTER(SimC), C.POINTER(TrajectoryC)]
@@ -587,6 +589,34 @@ def ref_correlation(model, qa, qb):
                                  _ptr(ab)) != 0:
         raise OracleError(ref_lib().pbr_last_error().decode())
     return v.value, g, bb.T.copy(), ab.T.copy()
+
+
+def ref_correlation_suite(model, qa, qb, weights=None, workers=4):
+    """The reference's parallel_correlation_suite (adjoint.cpp:241-336):
+    (value, grad_b, hess_bb, hess_ab), Hessians row-major numpy."""
+    n = model.n_dofs
+    v = C.c_double()
+    g = np.zeros(n)
+    bb = np.zeros((n, n))
+    ab = np.zeros((n, n))
+    w = None if weights is None else _f64(weights)
+    if ref_lib().pbr_correlation_suite(model.h, _ptr(_f64(qa)), _ptr(_f64(qb)), _ptr(w) if w is not None else None,
+                                       int(workers), C.byref(v), _ptr(g), _ptr(bb), _ptr(ab)) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return v.value, g, bb.T.copy(), ab.T.copy()
+
+
+def ref_functional(model, q, seeds):
+    """The reference's functional_value / _grad / _hess (adjoint.cpp:43-101)
+    of seeds [N][4][4] (row-major numpy matrices) at q."""
+    n = model.n_dofs
+    s = np.ascontiguousarray(np.transpose(np.asarray(seeds, float), (0, 2, 1)).reshape(-1))  # column-major
+    v = C.c_double()
+    g = np.zeros(n)
+    h = np.zeros((n, n))
+    if ref_lib().pbr_functional(model.h, _ptr(_f64(q)), _ptr(s), C.byref(v), _ptr(g), _ptr(h)) != 0:
+        raise OracleError(ref_lib().pbr_last_error().decode())
+    return v.value, g, h.T.copy()
 
 
 def ref_build_scheme(order, dt):

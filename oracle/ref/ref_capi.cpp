@@ -227,6 +227,47 @@ API int pbr_correlation(void* mp, const double* qa, const double* qb, double* va
   }
 }
 
+// the reference's parallel_correlation_suite (adjoint.cpp:241-336) on its WorkerPool
+API int pbr_correlation_suite(void* mp, const double* qa, const double* qb, const double* w, int workers,
+                              double* value, double* grad, double* bb, double* ab) {
+  const KinematicModel& m = *static_cast<KinematicModel*>(mp);
+  try {
+    CorrelationRequest req{&m, vec(qa, m.total_dofs), vec(qb, m.total_dofs),
+                           w ? vec(w, m.link_count()) : VecX()};
+    const CorrelationDerivatives d = parallel_correlation_suite(req, workers);
+    if (value) *value = d.value;
+    if (grad)
+      for (int k = 0; k < m.total_dofs; ++k) grad[k] = d.grad_b[k];
+    if (bb) putx(d.hess_bb, bb);
+    if (ab) putx(d.hess_ab, ab);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// functional_value / functional_grad / functional_hess (adjoint.cpp:43-101) of
+// caller seeds [N][16] column-major at q
+API int pbr_functional(void* mp, const double* q, const double* seeds, double* value, double* grad, double* hess) {
+  const KinematicModel& m = *static_cast<KinematicModel*>(mp);
+  try {
+    const ConfigPass pass = ConfigPass::make(m, vec(q, m.total_dofs));
+    std::vector<Mat4> c(m.link_count());
+    for (int i = 0; i < m.link_count(); ++i) c[i] = m4(seeds + 16 * i);
+    if (value) *value = functional_value(c, pass);
+    if (grad) {
+      const VecX g = functional_grad(m, c, pass);
+      for (int k = 0; k < m.total_dofs; ++k) grad[k] = g[k];
+    }
+    if (hess) putx(functional_hess(m, c, pass), hess);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 API int pbr_build_scheme(int order, double dt, double* times, double* H2) {
   try {
     const CollocationScheme s = build_scheme(order, dt);

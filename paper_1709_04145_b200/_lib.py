@@ -26,7 +26,7 @@ HEADER_SYMBOLS = [
     "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
     "pbad_gpu_state_device", "pbad_gpu_eval", "pbad_gpu_minimize", "pbad_gpu_correlation",
     "pbad_gpu_simulate_baseline", "pbad_gpu_rollout_sharded", "pbad_gpu_final_state",
-    "pbad_gpu_device_count",
+    "pbad_gpu_device_count", "pbad_gpu_correlation_suite", "pbad_gpu_functional",
 ]
 
 
@@ -123,6 +123,8 @@ def load():
                                      C.c_int32),
         "pbad_gpu_final_state": ([vp, vp, vp], C.c_int32),
         "pbad_gpu_device_count": ([], C.c_int32),
+        "pbad_gpu_correlation_suite": ([vp, C.c_int32, _dp, _dp, _dp, _dp, _dp, _dp, _dp], C.c_int32),
+        "pbad_gpu_functional": ([vp, C.c_int32, _dp, _dp, _dp, _dp, _dp], C.c_int32),
         "pbad_gpu_eval": ([vp, C.c_int32, _dp, _dp, _dp, C.c_int32, C.c_int32, _dp, _dp, _dp], C.c_int32),
         "pbad_gpu_minimize": ([vp, C.c_int32, _dp, _dp, _dp, _dp, _ip, _ip, _dp, _dp], C.c_int32),
     }

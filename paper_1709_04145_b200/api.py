@@ -422,6 +422,45 @@ class GpuContext:
             ab = ab.transpose(0, 2, 1).copy()
         return v, g, bb, ab
 
+    def correlation_suite(self, qa, qb, weight_per_body=None, want=("value", "grad", "bb", "ab")):
+        """parallel_correlation_suite (adjoint.cpp:241-336) for a batch of pairs:
+        one CTA per pair, the per-link work items over its threads; outputs as
+        correlation()."""
+        qa = _f64(qa)
+        B = qa.shape[0]
+        n = self.n
+        qa = _f64(qa, (B, n))
+        qb = _f64(qb, (B, n))
+        w = None
+        if weight_per_body is not None and len(weight_per_body) != 0:
+            w = _f64(weight_per_body)
+            if len(w) != self.model.link_count():
+                raise ModelError("weight_per_body length does not match link count")
+        v = np.zeros(B) if "value" in want else None
+        g = np.zeros((B, n)) if "grad" in want else None
+        bb = np.zeros((B, n, n)) if "bb" in want else None
+        ab = np.zeros((B, n, n)) if "ab" in want else None
+        check(_lib.load().pbad_gpu_correlation_suite(self._h, B, _p(qa), _p(qb), _p(w), _p(v), _p(g), _p(bb), _p(ab)))
+        t = (lambda a: None if a is None else a.transpose(0, 2, 1).copy())
+        return v, g, t(bb), t(ab)
+
+    def functional(self, q, seeds, want=("value", "grad", "hess")):
+        """functional_value / functional_grad / functional_hess (adjoint.cpp:43-101)
+        of f(q) = sum_i ddot(C_i, T^i(q)): q [B, n], seeds [B, N, 4, 4]."""
+        q = _f64(q)
+        B = q.shape[0]
+        n, N = self.n, self.model.link_count()
+        q = _f64(q, (B, n))
+        sd = np.asarray(seeds, dtype=np.float64)
+        if sd.shape != (B, N, 4, 4):
+            raise ValueError(f"seeds must have shape {(B, N, 4, 4)}")
+        sd = np.ascontiguousarray(sd.transpose(0, 1, 3, 2))  # column-major 4x4 blocks
+        v = np.zeros(B) if "value" in want else None
+        g = np.zeros((B, n)) if "grad" in want else None
+        h = np.zeros((B, n, n)) if "hess" in want else None
+        check(_lib.load().pbad_gpu_functional(self._h, B, _p(q), _p(sd), _p(v), _p(g), _p(h)))
+        return v, g, (None if h is None else h.transpose(0, 2, 1).copy())
+
     def minimize(self, history, x0, tau=None):
         history = _f64(history)
         B = history.shape[0]
@@ -637,6 +676,32 @@ def batch_correlation(model: KinematicModel, qa, qb, weight_per_body=None, devic
     """All four derivatives for a batch of pairs in one launch."""
     v, g, bb, ab = _corr_ctx(model, device).correlation(qa, qb, weight_per_body)
     return [CorrelationDerivatives(float(v[b]), g[b], bb[b], ab[b]) for b in range(len(v))]
+
+
+def parallel_correlation_suite(req: CorrelationRequest, workers: int = 1, device: int = 0) -> CorrelationDerivatives:
+    """adjoint.hpp:103-108: value, grad_b, hess_bb, hess_ab in one launch, the
+    per-link work items spread over one CTA (the large-N mode).  `workers` is
+    validated like the reference (>= 1); the CTA's threads replace the pool."""
+    if workers < 1:
+        raise ModelError("worker count must be >= 1")
+    v, g, bb, ab = _corr_ctx(req.model, device).correlation_suite(_f64(req.qa)[None], _f64(req.qb)[None],
+                                                                  req.weight_per_body)
+    return CorrelationDerivatives(float(v[0]), g[0], bb[0], ab[0])
+
+
+def functional_value(model: KinematicModel, seeds, q, device: int = 0) -> float:
+    """adjoint.hpp:55 on the GPU: sum_i ddot(C_i, T^i(q)), seeds [N, 4, 4]."""
+    return float(_corr_ctx(model, device).functional(_f64(q)[None], np.asarray(seeds)[None], want=("value",))[0][0])
+
+
+def functional_grad(model: KinematicModel, seeds, q, device: int = 0) -> np.ndarray:
+    """adjoint.hpp:56-57 on the GPU."""
+    return _corr_ctx(model, device).functional(_f64(q)[None], np.asarray(seeds)[None], want=("grad",))[1][0]
+
+
+def functional_hess(model: KinematicModel, seeds, q, device: int = 0) -> np.ndarray:
+    """adjoint.hpp:58-59 on the GPU: the exact Hessian of the linear functional."""
+    return _corr_ctx(model, device).functional(_f64(q)[None], np.asarray(seeds)[None], want=("hess",))[2][0]
 
 
 # --- Newton-Euler baselines (stepper.hpp:54-55) -------------------------------

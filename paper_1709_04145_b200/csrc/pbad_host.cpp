@@ -1686,6 +1686,77 @@ int32_t pbad_gpu_correlation(pbad_gpu_ctx* c, int32_t B, const double* qa, const
   return PBAD_OK;
 }
 
+// One CTA per request (pbad_corr.cu): mode 0 parallel_correlation_suite,
+// mode 1 the linear functional of caller seeds.
+static int32_t run_suite(pbad_gpu_ctx* c, int32_t B, int mode, const double* qa, const double* qb,
+                         const double* seeds, const double* weight_per_body, double* value, double* grad,
+                         double* hess_bb, double* hess_ab) {
+  if (B < 1) return fail(PBAD_E_ARGUMENT, "batch %d must be >= 1", B);
+  if (!qb || (mode == 0 && !qa) || (mode == 1 && !seeds)) return fail(PBAD_E_ARGUMENT, "missing input array");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const pbad_gpu_model& m = c->model;
+  const long N = m.N, n = m.n;
+  DModel dm = c->ka.m;
+  std::vector<void*> tmp;
+  auto dev = [&](size_t cnt) {
+    double* p = dalloc<double>(cnt);
+    tmp.push_back(p);
+    return p;
+  };
+  auto release = [&]() {
+    for (void* p : tmp)
+      if (p) cudaFree(p);
+  };
+  cudaError_t e = cudaSuccess;
+  if (mode == 0 && weight_per_body) {  // WeightedBody::make (adjoint.cpp:29-41)
+    std::vector<double> wS(16 * N);
+    double wm = 0.0;
+    for (long i = 0; i < N; ++i) {
+      const double w = weight_per_body[i];
+      for (int k = 0; k < 16; ++k) wS[16 * i + k] = w * m.S[16 * i + k];
+      wm += w * m.mass[i];
+    }
+    double* dS = dev(16 * N);
+    if (dS) e = cudaMemcpy(dS, wS.data(), sizeof(double) * 16 * N, cudaMemcpyHostToDevice);
+    dm.S = dS;
+    dm.weighted_mass = wm;
+  }
+  const SuiteLayout L = suite_layout(m.N, m.n, m.n_d2);
+  double* ws = dev((size_t)L.total * B);
+  double* dqa = mode == 0 ? dev((size_t)B * n) : nullptr;
+  double* dqb = dev((size_t)B * n);
+  double* dseeds = mode == 1 ? dev((size_t)B * N * 16) : nullptr;
+  double* dv = value ? dev(B) : nullptr;
+  double* dg = grad ? dev((size_t)B * n) : nullptr;
+  double* dbb = hess_bb ? dev((size_t)B * n * n) : nullptr;
+  double* dab = (mode == 0 && hess_ab) ? dev((size_t)B * n * n) : nullptr;
+  for (void* p : tmp)
+    if (!p) e = cudaErrorMemoryAllocation;
+  if (e == cudaSuccess && dqa) e = cudaMemcpy(dqa, qa, sizeof(double) * B * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dqb, qb, sizeof(double) * B * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && dseeds) e = cudaMemcpy(dseeds, seeds, sizeof(double) * B * N * 16, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_suite(dm, L, ws, B, dqa, dqb, dseeds, mode, dv, dg, dbb, dab, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && dv) e = cudaMemcpy(value, dv, sizeof(double) * B, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && dg) e = cudaMemcpy(grad, dg, sizeof(double) * B * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && dbb) e = cudaMemcpy(hess_bb, dbb, sizeof(double) * B * n * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && dab) e = cudaMemcpy(hess_ab, dab, sizeof(double) * B * n * n, cudaMemcpyDeviceToHost);
+  release();
+  if (e != cudaSuccess) return fail(PBAD_E_CUDA, "correlation suite: %s", cudaGetErrorString(e));
+  return PBAD_OK;
+}
+
+int32_t pbad_gpu_correlation_suite(pbad_gpu_ctx* c, int32_t B, const double* qa, const double* qb,
+                                   const double* weight_per_body, double* value, double* grad_b, double* hess_bb,
+                                   double* hess_ab) {
+  return run_suite(c, B, 0, qa, qb, nullptr, weight_per_body, value, grad_b, hess_bb, hess_ab);
+}
+
+int32_t pbad_gpu_functional(pbad_gpu_ctx* c, int32_t B, const double* q, const double* seeds, double* value,
+                            double* grad, double* hess) {
+  return run_suite(c, B, 1, nullptr, q, seeds, nullptr, value, grad, hess, nullptr);
+}
+
 int32_t pbad_gpu_minimize(pbad_gpu_ctx* c, int32_t B, const double* history, const double* tau,
                           const double* x0, double* x_out, int32_t* iterations, int32_t* converged,
                           double* final_value, double* final_grad_norm) {

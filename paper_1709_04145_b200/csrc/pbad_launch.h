@@ -72,6 +72,14 @@ cudaError_t launch_refined_bootstrap(const KernelArgs& a, const Layout& L, doubl
                                      const double* qd0, double hs, double* hist0, int* status, cudaStream_t s);
 cudaError_t launch_baseline(const KernelArgs& a, const Layout& L, double* ws, long B, int scheme, const double* q0,
                             const double* qd0, double* oq, double* oe, int* nsamp, int* status, cudaStream_t s);
+// correlation suite / functional derivatives, one CTA per request (pbad_corr.cu)
+struct SuiteLayout {
+  long va, wa, d1a, la, vb, wb, pwb, d1b, lb, d2b, seeds, adj, acc, vslot, total;
+};
+SuiteLayout suite_layout(int N, int n, int n_d2);
+cudaError_t launch_suite(const DModel& m, const SuiteLayout& L, double* ws, long B, const double* qa, const double* qb,
+                         const double* seeds, int mode, double* value, double* grad, double* hbb, double* hab,
+                         cudaStream_t s);
 cudaError_t launch_correlation(const DModel& m, const Layout& L, double* ws, long B, const double* qa,
                                const double* qb, double* value, double* grad, double* hbb, double* hab,
                                cudaStream_t s);
