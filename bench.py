@@ -539,7 +539,8 @@ def main():
                    3: "pbad_gpu::tree::k_tree_step (warp per env, Newton/LM, in-SMEM Cholesky)",
                    4: "pbad_gpu::resid::k_resid_step (CTA per env, residual-form LM, tiled J^T J + blocked Cholesky)",
                    5: "pbad_gpu::c5::k_chain5_step (warp per env, shared-memory-resident L-BFGS, TMA-fed adjoint)",
-                   6: "pbad_gpu::c6::k_chain6_step (8 lanes per env: two per transform row, TMA-fed adjoint)"
+                   6: "pbad_gpu::c6::k_chain6_step (8 lanes per env: two per transform row, TMA-fed adjoint)",
+                   7: "pbad_gpu::c7::k_chain7_step (16 lanes per env: serial FK rows + link-parallel energy terms, TMA-fed adjoint)"
                    }.get(ctx.path),
         "clocks": clk,
         "mean_iterations_per_step": float(iters.mean()),

@@ -203,6 +203,7 @@ int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* ctx);
 #define PBAD_PATH_RESID 4   /* CTA per environment, residual (collocation) form with LM (pbad_resid.cu) */
 #define PBAD_PATH_CHAIN5 5  /* warp per environment, axis-aligned hinge chains, shared-memory L-BFGS (pbad_chain5.cu) */
 #define PBAD_PATH_CHAIN6 6  /* 8 lanes per environment (two per row), axis-aligned hinge chains (pbad_chain6.cu) */
+#define PBAD_PATH_CHAIN7 7  /* 16 lanes per environment, link-parallel energy terms, axis-aligned hinge chains (pbad_chain7.cu) */
 int32_t pbad_gpu_path(const pbad_gpu_ctx* ctx);
 
 /* batch_simulate on the GPU: q0/qdot0 host [B][n]; copies in, steps every

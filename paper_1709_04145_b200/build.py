@@ -26,7 +26,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
               "-Xptxas", "-v"]
-CUDA_SOURCES = ["pbad_kernels.cu", "pbad_chain.cu", "pbad_chain4.cu", "pbad_chain5.cu", "pbad_chain6.cu", "pbad_corr.cu", "pbad_tree.cu", "pbad_tree_lbfgs.cu", "pbad_resid.cu"]
+CUDA_SOURCES = ["pbad_kernels.cu", "pbad_chain.cu", "pbad_chain4.cu", "pbad_chain5.cu", "pbad_chain6.cu", "pbad_chain7.cu", "pbad_corr.cu", "pbad_tree.cu", "pbad_tree_lbfgs.cu", "pbad_resid.cu"]
 HOST_SOURCES = ["pbad_host.cpp"]
 
 

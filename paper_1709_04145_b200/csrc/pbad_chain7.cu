@@ -1,0 +1,1145 @@
+// pbad_chain7.cu -- chain kernel "v7": serial chains of axis-aligned hinges
+// (energy form, L-BFGS) in batches larger than one wave of the v5 kernel
+// (C3: 4096 x 200 DOF), two environments per warp with 16 lanes each.
+//
+// Why: the v6 kernel (pbad_chain6.cu, 4 environments per warp) gives 1024
+// warps for C3 -- one wave -- and every warp executes ~62 k instructions per
+// L-BFGS iteration at ~7.7 cycles each (ncu round 2: issue 25 %): the step
+// time is one warp's instruction latency chain.  v7 halves the environments
+// per warp and, more importantly, stops executing the per-link algebra once
+// per transform row:
+//  * forward sweep, per 16-link chunk:
+//    - rotations: lane j computes hinge_cs of its own link (element 16 c + j)
+//      and stages the history rotations of that link in shared memory;
+//    - phase A (serial, ~14 instructions per link): lanes (chain, row) carry
+//      the three FK recursions T = FK(x), A = FK(hist1), H = FK(hist0) row by
+//      row (kinematics.cpp:171-181) and drop rows 0..2 of every world
+//      transform into shared memory;
+//    - phase B (link-parallel): lane j takes link 16 c + j whole: the energy
+//      terms ddot(T S, T), ddot(A S, T), ddot(H S, T), the gravity term, the
+//      inertial seed S (T - 2A + H)/dt^2 and the lever rows of the reverse
+//      sweep (adjoint.cpp:9-27, objective.cpp:215-256) -- independent work
+//      with plenty of ILP instead of a dependent chain per row;
+//    - the energy sums are taken link by link in link order (4 lanes, one per
+//      term), exactly the reference's summation sequence.
+//  * reverse sweep: the v4/v6 row-local adjoint recursions (lanes (chain,
+//    row)), link records streamed back by TMA bulk copies into a 3-slot
+//    shared-memory ring in descending 8-link chunks.
+//  * vectors: element k of an environment in lane k % 16, the reference's 32
+//    interleaved dot partials as 2 per lane plus a xor-8/4/2/1 butterfly.
+// Row 3 of every world transform is (+-0, +-0, +-0, 1): its energy-term
+// contribution is S(3,3) exactly for a link with S(3,3) != 0 (the host only
+// selects v7 when every massive link has one), its gravity-term contribution a
+// signed zero that cannot change a sum started at +0, and its lever and seed
+// rows are zero (handled as in v4/v6).  Every other value is produced by the
+// reference's operation sequence, so results are bit-identical to v4/v5/v6,
+// oracle/ and the reference build.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pbad_chain_ops.cuh"
+#include "pbad_kernels.cuh"
+#include "pbad_launch.h"
+#include "pbad_math.cuh"
+
+namespace pbad_gpu {
+namespace c7 {
+
+using namespace chain_ops;
+
+enum { PH_DIR = 0, PH_GEN = 1, PH_EVAL = 2, PH_DONE = 3 };
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
+enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
+
+constexpr int kE = 2;    // environments per warp
+constexpr int kL = 16;   // lanes per environment
+#ifndef PBAD_C7_WARPS
+#define PBAD_C7_WARPS 8
+#endif
+constexpr int kW = PBAD_C7_WARPS;  // warps per block
+constexpr int kT = 32 * kW;
+constexpr int CF = 16;  // forward chunk: links (one per lane of an environment)
+constexpr int CR = 8;   // reverse chunk: links per ring slot
+constexpr int kRing = 3;
+constexpr int kMaxMem = 16;
+constexpr long kGS = 32;  // vector group stride (doubles): 16 elements x 2 environments
+// per-link record (doubles, per warp): cs [env][2] | lev [3*env+row][2] | seed [3*env+row][4]
+constexpr int kRecCS = 0, kRecLev = 4, kRecSd = 16;
+constexpr int kRecLight = 16, kRecMass = 40;
+constexpr int kSlot = CR * kRecMass;  // ring slot (doubles)
+// per-warp shared memory (doubles).  Forward buffers:
+constexpr int kRot = 0;                        // rotations [CF][env][6]: c s | c0 s0 | c1 s1 (terms overlay it)
+constexpr int kTrow = kRot + CF * kE * 6;      // T rows 0..2 [CF+1][env][3][4] (entry 0: parent of the chunk)
+constexpr int kAH = kTrow + (CF + 1) * kE * 12;  // A, H rows 0..2 [slot][env][2][3][4]
+__host__ __device__ constexpr int mass_slots(int pat) {
+  // period-2 patterns with one massive kind: the massive links of a chunk are every other one
+  return ((pat & 3) == 2 && (((pat >> 2) & 4) != 0) != (((pat >> 5) & 4) != 0)) ? CF / 2 : CF;
+}
+__host__ __device__ constexpr int fwd_end(int pat) { return kAH + mass_slots(pat) * kE * 24; }
+// reverse buffers (overlay the forward ones)
+constexpr int kRRed = kRing * kSlot;  // gradient row partials [CR][chain][row][env]
+constexpr int kRevEnd = kRRed + CR * 16;
+__host__ __device__ constexpr int area_end(int pat) { return fwd_end(pat) > kRevEnd ? fwd_end(pat) : kRevEnd; }
+constexpr int kHsyW = 40;
+__host__ __device__ constexpr int hsy_off(int pat) { return (area_end(pat) + 1) & ~1; }
+__host__ __device__ constexpr int bar_off(int pat) { return hsy_off(pat) + kE * kHsyW; }
+__host__ __device__ constexpr int warp_doubles(int pat) { return (bar_off(pat) + kRing + 1) & ~1; }
+static_assert(kHsyW >= 2 * kMaxMem + 1, "s.y ring + alpha");
+static_assert(kSlot % 2 == 0 && kRRed % 2 == 0 && kTrow % 2 == 0 && kAH % 2 == 0, "16-byte aligned areas");
+constexpr int kHistW = 6;  // hist record per (link, env): c0 s0 | c1 s1 | cx sx
+
+__host__ __device__ inline size_t smem_bytes(int N, int pat) {
+  return (size_t)(kW * (long)warp_doubles(pat) + 20L * N) * sizeof(double) + (size_t)(2 * N + 1) * sizeof(int);
+}
+
+// ---- context ----------------------------------------------------------------
+struct Ctx {
+  int N, n, n16, j, e, lane;
+  long ge, B, n4q;
+  bool valid;
+  unsigned em;         // this environment's 16 lanes
+  double* ws;          // this warp's shared area
+  uint64_t* bar;       // kRing mbarriers
+  const double* mrec;  // shared model records [N][20]: S (column-major), t, pad
+  const int* kind;     // shared link classes
+  const int* roff;     // shared per-warp record offsets [N+1]
+  double* rec;         // this warp's link records (global)
+  double* hist;        // this warp's history rotations [N][env][6] (global)
+  double *gh0, *gh1;   // hist0 / hist1 in the quad chain layout (pbad_chain.cu)
+  double *x, *g, *cand, *dir, *q, *evg, *tau, *hs, *hy;
+  long VS;
+  double* hsy;    // shared: this env's s.y ring [mem+1] then alpha [mem]
+  double* histc;
+  int* ci;
+  double dt, inv_dt2, wm;
+  double gz[3];
+  double grr;  // gravity component of this lane's reverse-sweep row (0 for row 3)
+  DOpt o;
+  unsigned nload;  // ring chunks consumed (warp-uniform; sets slot and phase)
+};
+
+__device__ __forceinline__ double eshfl(const Ctx& C, double v, int src) { return __shfl_sync(C.em, v, src, kL); }
+__device__ __forceinline__ double eshfl_xor(const Ctx& C, double v, int m) {
+  return __shfl_xor_sync(C.em, v, m, kL);
+}
+__device__ __forceinline__ double wshfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src, kL); }
+__device__ __forceinline__ void esync(const Ctx& C) { __syncwarp(C.em); }
+__device__ __forceinline__ int& ival(const Ctx& C, int slot) { return C.ci[(long)slot * C.B + C.ge]; }
+// element k of this environment: this lane's elements are k = 16 g + j
+__device__ __forceinline__ double& vat(const Ctx& C, double* V, int k) {
+  return V[(long)(k >> 4) * kGS + ((k & 15) - C.j)];
+}
+// element k of this environment in a quad-interleaved chain-layout vector
+__device__ __forceinline__ double& qv(const Ctx& C, double* base, int k) {
+  return base[((C.ge >> 3) * C.n4q + (k >> 2)) * 32 + (C.ge & 7) * 4 + (k & 3)];
+}
+__device__ __forceinline__ bool elem_ok(const Ctx& C, int g) { return g < C.n16 && 16 * g + C.j < C.n; }
+
+// ---- 16-lane vector ops (32-partial canonical dot, optim.cpp) ----------------
+// acc[a] holds partial 16 a + j of the reference's 32 interleaved partials
+__device__ __forceinline__ double dot_finish(const Ctx& C, const double* acc) {
+  double v = acc[0] + acc[1];  // partial tree level xor 16
+  v = v + eshfl_xor(C, v, 8);
+  v = v + eshfl_xor(C, v, 4);
+  v = v + eshfl_xor(C, v, 2);
+  v = v + eshfl_xor(C, v, 1);
+  return v;
+}
+__device__ __forceinline__ double emax(const Ctx& C, double mx) {
+  mx = fmax(mx, eshfl_xor(C, mx, 8));
+  mx = fmax(mx, eshfl_xor(C, mx, 4));
+  mx = fmax(mx, eshfl_xor(C, mx, 2));
+  mx = fmax(mx, eshfl_xor(C, mx, 1));
+  return mx;
+}
+__device__ __forceinline__ double edot(const Ctx& C, const double* A, const double* Bv) {
+  double acc[2] = {0.0, 0.0};
+  for (int g = 0; g < C.n16; ++g)
+    if (elem_ok(C, g)) acc[g & 1] = fma(A[(long)g * kGS], Bv[(long)g * kGS], acc[g & 1]);
+  return dot_finish(C, acc);
+}
+__device__ __forceinline__ double einfnorm(const Ctx& C, const double* A) {
+  double mx = 0.0;
+  for (int g = 0; g < C.n16; ++g)
+    if (elem_ok(C, g)) mx = fmax(mx, fabs(A[(long)g * kGS]));
+  return emax(C, mx);
+}
+__device__ __forceinline__ bool eallfinite(const Ctx& C, const double* A) {
+  bool ok = true;
+  for (int g = 0; g < C.n16; ++g)
+    if (elem_ok(C, g)) ok = ok && isfinite(A[(long)g * kGS]);
+  return __all_sync(C.em, ok);
+}
+__device__ __forceinline__ bool qallfinite(const Ctx& C, double* base) {
+  bool ok = true;
+  for (int k = C.j; k < C.n; k += kL) ok = ok && isfinite(qv(C, base, k));
+  return __all_sync(C.em, ok);
+}
+
+// link-pattern code: P | K0 << 2 | K1 << 5 (P = period 1 or 2; 0 = per-link dispatch)
+template <int PAT, int J>
+struct PatKind {
+  static constexpr int P = PAT & 3;
+  static constexpr int value = (P == 2 && (J & 1)) ? ((PAT >> 5) & 7) : ((PAT >> 2) & 7);
+};
+template <int PAT>
+__device__ __forceinline__ int mslot(int jl) {
+  return mass_slots(PAT) == CF ? jl : (jl >> 1);
+}
+
+__device__ __forceinline__ void ld4(const double* p, double* v) {
+  const double2 a = *reinterpret_cast<const double2*>(p);
+  const double2 b = *reinterpret_cast<const double2*>(p + 2);
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = b.x;
+  v[3] = b.y;
+}
+__device__ __forceinline__ void st4(double* p, const double* v) {
+  *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+}
+
+// ---- forward sweep ------------------------------------------------------------
+// Phase A: one step of the FK recursion of chain `ch` (0: T, 1: A = FK(hist1),
+// 2: H = FK(hist0)) for link jl of the chunk, row r of this lane.
+template <int CK, int PAT>
+__device__ __forceinline__ void fk_step(const Ctx& C, int jl, int i, int ch, int r, int rofs, double* X) {
+  constexpr int JK = CK & 3;
+  constexpr bool SK = (CK >> 2) != 0;
+  const double2 cs = *reinterpret_cast<const double2*>(C.ws + kRot + (jl * kE + C.e) * 6 + rofs);
+  const double* mr = C.mrec + 20 * i;
+  const double2 t01 = *reinterpret_cast<const double2*>(mr + 16);
+  const double t[3] = {t01.x, t01.y, mr[18]};
+  fk<JK>(cs.x, cs.y, t, X);
+  if (r < 3) {
+    if (ch == 0) st4(C.ws + kTrow + ((jl + 1) * kE + C.e) * 12 + 4 * r, X);
+    else if (SK && ch < 3) st4(C.ws + kAH + ((mslot<PAT>(jl) * kE + C.e) * 2 + (ch - 1)) * 12 + 4 * r, X);
+  }
+}
+// Phase B: link i (chunk position jl) whole, in this lane: its record (joint
+// rotation, lever rows, seed rows) and, for a massive link, its four energy
+// terms (objective.cpp:215-239, adjoint.cpp:9-27,113-120).
+template <int CK, int PAT>
+__device__ __forceinline__ void link_terms(const Ctx& C, int jl, int i, double c, double s, double* tv) {
+  constexpr int JK = CK & 3;
+  constexpr bool SK = (CK >> 2) != 0;
+  double* rp = C.rec + C.roff[i];
+  *reinterpret_cast<double2*>(rp + kRecCS + 2 * C.e) = make_double2(c, s);
+  const double* tp = C.ws + kTrow + (jl * kE + C.e) * 12;  // parent's rows
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    double P[4], l0, l1;
+    ld4(tp + 4 * r, P);
+    lever<JK>(c, s, P, l0, l1);  // T_parent row times dL/dq (adjoint.cpp:22-25)
+    *reinterpret_cast<double2*>(rp + kRecLev + 2 * (3 * C.e + r)) = make_double2(l0, l1);
+  }
+  if (SK) {
+    const double* mr = C.mrec + 20 * i;
+    double S[16];
+    lds16(mr, S);
+    const double* tr = C.ws + kTrow + ((jl + 1) * kE + C.e) * 12;
+    const double* ar = C.ws + kAH + ((mslot<PAT>(jl) * kE + C.e) * 2) * 12;
+    const double* hr = ar + 12;
+    // ddot row combination ((r0 + r1) + r2) + r3, accumulated row by row;
+    // row 3's exact value is S(3,3) (energy terms) or a signed zero (gravity)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double T[4], A[4], H[4], p[4];
+      ld4(tr + 4 * r, T);
+      ld4(ar + 4 * r, A);
+      ld4(hr + 4 * r, H);
+      double v[4];
+      row_s(T, S, p);
+      v[0] = ddot_row(p, T);  // T S . T
+      row_s(A, S, p);
+      v[1] = ddot_row(p, T);  // A S . T
+      row_s(H, S, p);
+      v[2] = ddot_row(p, T);  // H S . T
+      const double gr = C.gz[r];
+      double cg[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cg[k] = (-gr) * S[12 + k];
+      v[3] = ddot_row(cg, T);  // gravity
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tv[k] = r == 0 ? v[k] : tv[k] + v[k];
+      double dd[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double d = T[k] - 2.0 * A[k];  // (T - 2A + H) / dt^2
+        d = d + H[k];
+        dd[k] = C.inv_dt2 * d;
+      }
+      row_s(dd, S, p);  // seed row
+      st4(rp + kRecSd + 4 * (3 * C.e + r), p);
+    }
+    tv[0] = tv[0] + S[15];
+    tv[1] = tv[1] + S[15];
+    tv[2] = tv[2] + S[15];
+  }
+}
+
+template <int PAT>
+__device__ __forceinline__ bool link_b(const Ctx& C, int jl, int i, double c, double s, double* tv) {
+  if constexpr ((PAT & 3) == 1) {
+    link_terms<PatKind<PAT, 0>::value, PAT>(C, jl, i, c, s, tv);
+    return (PatKind<PAT, 0>::value >> 2) != 0;
+  } else if constexpr ((PAT & 3) == 2) {
+    if (jl & 1) {
+      link_terms<PatKind<PAT, 1>::value, PAT>(C, jl, i, c, s, tv);
+      return (PatKind<PAT, 1>::value >> 2) != 0;
+    }
+    link_terms<PatKind<PAT, 0>::value, PAT>(C, jl, i, c, s, tv);
+    return (PatKind<PAT, 0>::value >> 2) != 0;
+  } else {
+    const int ck = C.kind[i];
+    switch (ck) {
+      case 1: link_terms<1, PAT>(C, jl, i, c, s, tv); break;
+      case 2: link_terms<2, PAT>(C, jl, i, c, s, tv); break;
+      case 3: link_terms<3, PAT>(C, jl, i, c, s, tv); break;
+      case 5: link_terms<5, PAT>(C, jl, i, c, s, tv); break;
+      case 6: link_terms<6, PAT>(C, jl, i, c, s, tv); break;
+      default: link_terms<7, PAT>(C, jl, i, c, s, tv); break;
+    }
+    return (ck >> 2) != 0;
+  }
+}
+
+template <int PAT, int J>
+struct FkUnroll {
+  static __device__ __forceinline__ void run(const Ctx& C, int lo, int ch, int r, int rofs, double* X) {
+    fk_step<PatKind<PAT, J>::value, PAT>(C, J, lo + J, ch, r, rofs, X);
+    FkUnroll<PAT, J + 1>::run(C, lo, ch, r, rofs, X);
+  }
+};
+template <int PAT>
+struct FkUnroll<PAT, CF> {
+  static __device__ __forceinline__ void run(const Ctx&, int, int, int, int, double*) {}
+};
+template <int PAT>
+__device__ __forceinline__ void fk_step_dyn(const Ctx& C, int jl, int i, int ch, int r, int rofs, double* X) {
+  switch (C.kind[i]) {
+    case 1: fk_step<1, PAT>(C, jl, i, ch, r, rofs, X); break;
+    case 2: fk_step<2, PAT>(C, jl, i, ch, r, rofs, X); break;
+    case 3: fk_step<3, PAT>(C, jl, i, ch, r, rofs, X); break;
+    case 5: fk_step<5, PAT>(C, jl, i, ch, r, rofs, X); break;
+    case 6: fk_step<6, PAT>(C, jl, i, ch, r, rofs, X); break;
+    default: fk_step<7, PAT>(C, jl, i, ch, r, rofs, X); break;
+  }
+}
+
+// StepObjective::value at X (objective.cpp:215-239), storing the reverse
+// sweep's per-link records.  Warp-collective.
+template <int PAT>
+__device__ __forceinline__ double forward(const Ctx& C, const double* X, double tdx) {
+  const int N = C.N;
+  const int nch = (N + CF - 1) / CF;
+  const int ch = C.j >> 2, r = C.j & 3;
+  const int rofs = ch == 1 ? 4 : ch == 2 ? 2 : 0;  // chain 3 replays T (never stored)
+  double R[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) R[k] = (r == k) ? 1.0 : 0.0;
+  double sum = 0.0;  // lane j < 4: running sum of energy term j
+  double xa = 0.0;
+  double2 ha0 = make_double2(0.0, 0.0), ha1 = ha0;
+  auto fetch = [&](int c) {
+    const int la = CF * c + C.j;
+    if (la < N) {
+      xa = X[(long)c * kGS];
+      const double* hp = C.hist + ((long)la * kE + C.e) * kHistW;
+      ha0 = *reinterpret_cast<const double2*>(hp);
+      ha1 = *reinterpret_cast<const double2*>(hp + 2);
+    }
+  };
+  fetch(0);
+  for (int c = 0; c < nch; ++c) {
+    const int lo = CF * c, cnt = min(CF, N - lo);
+    const int la = lo + C.j;
+    // rotations of this lane's link
+    double ca = 1.0, sa = 0.0;
+    if (la < N) hinge_cs(xa, &ca, &sa);
+    const double2 h_a0 = ha0, h_a1 = ha1;
+    if (c + 1 < nch) fetch(c + 1);
+    __syncwarp();  // the previous chunk's term readers are done with the rotation area
+    if (la < N) {
+      double* rb = C.ws + kRot + (C.j * kE + C.e) * 6;
+      *reinterpret_cast<double2*>(rb) = make_double2(ca, sa);
+      *reinterpret_cast<double2*>(rb + 2) = h_a0;
+      *reinterpret_cast<double2*>(rb + 4) = h_a1;
+    }
+    // the chunk's parent rows: the T chain's current row
+    if (ch == 0 && r < 3) st4(C.ws + kTrow + C.e * 12 + 4 * r, R);
+    __syncwarp();
+    // phase A: the three FK recursions over the chunk
+    if constexpr ((PAT & 3) != 0) {
+      if (cnt == CF) FkUnroll<PAT, 0>::run(C, lo, ch, r, rofs, R);
+      else
+        for (int jl = 0; jl < cnt; ++jl) fk_step_dyn<PAT>(C, jl, lo + jl, ch, r, rofs, R);
+    } else {
+      for (int jl = 0; jl < cnt; ++jl) fk_step_dyn<PAT>(C, jl, lo + jl, ch, r, rofs, R);
+    }
+    __syncwarp();
+    // phase B: this lane's link
+    double tv[4] = {0.0, 0.0, 0.0, 0.0};
+    bool massive = false;
+    if (C.j < cnt) massive = link_b<PAT>(C, C.j, la, ca, sa, tv);
+    __syncwarp();  // every lane has read its rotation: the terms overlay the rotation area
+    double* tb = C.ws + kRot + (C.j * kE + C.e) * 4;
+    if (C.j < cnt) {
+      *reinterpret_cast<double2*>(tb) = make_double2(tv[0], tv[1]);
+      *reinterpret_cast<double2*>(tb + 2) = make_double2(tv[2], tv[3]);
+    }
+    const unsigned mm = __ballot_sync(0xffffffffu, massive && C.j < cnt);
+    __syncwarp();
+    // lane t < 4 adds term t of each massive link, link by link (serial order)
+    if (C.j < 4) {
+      const unsigned em = (mm >> (C.e * kL)) & 0xFFFFu;
+      for (int jl = 0; jl < cnt; ++jl)
+        if ((em >> jl) & 1u) sum += C.ws[kRot + (jl * kE + C.e) * 4 + C.j];
+    }
+  }
+  const double s0 = wshfl(sum, 0), s1 = wshfl(sum, 1), s2 = wshfl(sum, 2), sg = wshfl(sum, 3);
+  const double wm = C.wm;
+  const double cpp = s0 - wm, c1p = s1 - wm, c2p = s2 - wm;
+  const double inertial = 0.5 * C.inv_dt2 * (cpp - 4.0 * c1p + 2.0 * c2p + *C.histc);
+  return inertial + sg - tdx;
+}
+
+// ---- reverse sweep ------------------------------------------------------------
+// functional_grad twice (adjoint.cpp:49-64): gradient = inertial adjoint
+// (chain h = 0) + gravity adjoint (h = 1) - tau (objective.cpp:241-250) into Gv.
+template <int CK>
+__device__ __forceinline__ void rev_link(const Ctx& C, const double* rp, int i, int jl, int h, int r, bool act,
+                                         double* cc) {
+  constexpr int JK = CK & 3;
+  constexpr bool SK = (CK >> 2) != 0;
+  const double2 cs = *reinterpret_cast<const double2*>(rp + kRecCS + 2 * C.e);
+  const int row = 3 * C.e + r;
+  const bool own = r < 3;  // row 3 of the lever and of the seed is exactly zero
+  double l0 = 0.0, l1 = 0.0;
+  if (own) {
+    const double2 lv = *reinterpret_cast<const double2*>(rp + kRecLev + 2 * row);
+    l0 = lv.x;
+    l1 = lv.y;
+  }
+  const double* mr = C.mrec + 20 * i;
+  double a[4];
+  if (SK) {
+    double sd[4] = {0.0, 0.0, 0.0, 0.0};
+    if (own && h == 0) {
+      const double2 s01 = *reinterpret_cast<const double2*>(rp + kRecSd + 4 * row);
+      const double2 s23 = *reinterpret_cast<const double2*>(rp + kRecSd + 4 * row + 2);
+      sd[0] = s01.x;
+      sd[1] = s01.y;
+      sd[2] = s23.x;
+      sd[3] = s23.y;
+    }
+    const double2 u01 = *reinterpret_cast<const double2*>(mr + 12);
+    const double2 u23 = *reinterpret_cast<const double2*>(mr + 14);
+    const double u[4] = {u01.x, u01.y, u23.x, u23.y};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = cc[k] + (h ? (0.0 + (-C.grr) * u[k]) : sd[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = cc[k];
+  }
+  if (act) C.ws[kRRed + jl * 16 + h * 8 + r * 2 + C.e] = lever_dot<JK>(l0, l1, a);
+  if (i > 0) {
+    const double2 t01 = *reinterpret_cast<const double2*>(mr + 16);
+    const double t[3] = {t01.x, t01.y, mr[18]};
+    double o[4];
+    transport<JK>(cs.x, cs.y, t, a, o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cc[k] = 0.0 + o[k];
+  }
+}
+
+__device__ __forceinline__ void rev_link_dyn(const Ctx& C, const double* rp, int i, int jl, int h, int r, bool act,
+                                             double* cc) {
+  switch (C.kind[i]) {
+    case 1: rev_link<1>(C, rp, i, jl, h, r, act, cc); break;
+    case 2: rev_link<2>(C, rp, i, jl, h, r, act, cc); break;
+    case 3: rev_link<3>(C, rp, i, jl, h, r, act, cc); break;
+    case 5: rev_link<5>(C, rp, i, jl, h, r, act, cc); break;
+    case 6: rev_link<6>(C, rp, i, jl, h, r, act, cc); break;
+    default: rev_link<7>(C, rp, i, jl, h, r, act, cc); break;
+  }
+}
+
+template <int PAT, int J>
+struct RevUnroll {  // links J, J-1, ..., 0 of a full chunk
+  static __device__ __forceinline__ void run(const Ctx& C, const double* sbase, int lo, int h, int r, bool act,
+                                             double* cc) {
+    rev_link<PatKind<PAT, J>::value>(C, sbase + C.roff[lo + J], lo + J, J, h, r, act, cc);
+    RevUnroll<PAT, J - 1>::run(C, sbase, lo, h, r, act, cc);
+  }
+};
+template <int PAT>
+struct RevUnroll<PAT, -1> {
+  static __device__ __forceinline__ void run(const Ctx&, const double*, int, int, int, bool, double*) {}
+};
+
+template <int PAT>
+__device__ __forceinline__ void rev_chunk(const Ctx& C, const double* sbase, int lo, int cnt, int h, int r, bool act,
+                                          double* cc) {
+  if constexpr ((PAT & 3) != 0) {
+    if (cnt == CR) {
+      RevUnroll<PAT, CR - 1>::run(C, sbase, lo, h, r, act, cc);
+      return;
+    }
+  }
+  for (int jl = cnt - 1; jl >= 0; --jl) rev_link_dyn(C, sbase + C.roff[lo + jl], lo + jl, jl, h, r, act, cc);
+}
+
+__device__ __forceinline__ void issue_chunk(Ctx& C, int c, unsigned k) {
+  const int lo = CR * c, hi = min(C.N, lo + CR);
+  const int slot = (int)(k % kRing);
+  const unsigned bytes = (unsigned)(C.roff[hi] - C.roff[lo]) * 8u;
+  bulk_load(C.ws + slot * kSlot, C.rec + C.roff[lo], bytes, C.bar + slot);
+}
+
+template <int PAT>
+__device__ __forceinline__ void reverse(Ctx& C, double* Gv) {
+  const int N = C.N;
+  const int nch = (N + CR - 1) / CR;
+  fence_async_global();  // this lane's record stores -> the bulk copies below
+  __syncwarp();
+  const unsigned k0 = C.nload;
+  if (C.lane == 0) {
+    fence_async_smem();  // forward-buffer accesses in the ring area before the async writes
+    for (int p = 0; p < kRing && p < nch; ++p) issue_chunk(C, nch - 1 - p, k0 + p);
+  }
+  const int l8 = C.j & 7, h = l8 >> 2, r = l8 & 3;
+  const bool act = C.j < 8;
+  double cc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int idx = 0; idx < nch; ++idx) {
+    const int c = nch - 1 - idx;
+    const int lo = CR * c, cnt = min(CR, N - lo);
+    const unsigned k = k0 + idx;
+    const int slot = (int)(k % kRing);
+    // tau of this lane's link of the chunk (lanes j < 8)
+    const int kl = lo + C.j;
+    const double tau_c = (act && kl < N) ? vat(C, C.tau, kl) : 0.0;
+    mbar_wait(C.bar + slot, (k / kRing) & 1u);
+    const double* sbase = C.ws + slot * kSlot - C.roff[lo];
+    rev_chunk<PAT>(C, sbase, lo, cnt, h, r, act, cc);
+    __syncwarp();
+    // the gradient entry of this lane's link of the chunk
+    if (act && C.j < cnt) {
+      const double* b = C.ws + kRRed + C.j * 16 + C.e;
+      const double gi = 0.0 + (((b[0] + b[2]) + b[4]) + b[6]);
+      const double gp = 0.0 + (((b[8] + b[10]) + b[12]) + b[14]);
+      vat(C, Gv, kl) = (gi + gp) - tau_c;
+    }
+    __syncwarp();
+    if (idx + kRing < nch && C.lane == 0) {
+      fence_async_smem();
+      issue_chunk(C, c - kRing, k + kRing);
+    }
+  }
+  C.nload = k0 + nch;
+}
+
+// ---- per-step history passes (once per PBAD step) ---------------------------
+// joint rotations into hist slot `slot` (0: hist0, 1: hist1, 2: x)
+__device__ __forceinline__ void hist_rotations_q(const Ctx& C, double* base, int slot) {
+  for (int i = C.j; i < C.N; i += kL) {
+    double c, s;
+    hinge_cs(qv(C, base, i), &c, &s);
+    *reinterpret_cast<double2*>(C.hist + ((long)i * kE + C.e) * kHistW + 2 * slot) = make_double2(c, s);
+  }
+  esync(C);
+}
+__device__ __forceinline__ void hist_rotations(const Ctx& C, const double* V, int slot) {
+  for (int i = C.j; i < C.N; i += kL) {
+    double c, s;
+    hinge_cs(V[(long)(i >> 4) * kGS], &c, &s);
+    *reinterpret_cast<double2*>(C.hist + ((long)i * kE + C.e) * kHistW + 2 * slot) = make_double2(c, s);
+  }
+  esync(C);
+}
+
+__device__ __forceinline__ void fk_dyn(int jk, double c, double s, const double* t, double* T) {
+  if (jk == 1) fk<1>(c, s, t, T);
+  else if (jk == 2) fk<2>(c, s, t, T);
+  else fk<3>(c, s, t, T);
+}
+// ((v_0 + v_1) + v_2) + v_3 over the 4 rows (every quad of the 16 lanes computes the same rows)
+__device__ __forceinline__ double rows4(const Ctx& C, double v) {
+  const double v0 = __shfl_sync(C.em, v, 0, 4), v1 = __shfl_sync(C.em, v, 1, 4);
+  const double v2 = __shfl_sync(C.em, v, 2, 4), v3 = __shfl_sync(C.em, v, 3, 4);
+  return ((v0 + v1) + v2) + v3;
+}
+
+// hist_const = 4 cv(tk, tk) + cv(tk1, tk1) - 4 cv(tk, tk1) (objective.cpp:162-185),
+// tk = FK(hist1), tk1 = FK(hist0); massless links add exact zeros and are skipped
+__device__ __forceinline__ double hist_const(const Ctx& C) {
+  const int r = C.j & 3;
+  double A[4], H[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) A[k] = H[k] = (r == k) ? 1.0 : 0.0;
+  double vAA = 0.0, vHH = 0.0, vAH = 0.0;
+  for (int i = 0; i < C.N; ++i) {
+    const int ck = C.kind[i];
+    const double* hp = C.hist + ((long)i * kE + C.e) * kHistW;
+    const double* mr = C.mrec + 20 * i;
+    const double t[3] = {mr[16], mr[17], mr[18]};
+    fk_dyn(ck & 3, hp[2], hp[3], t, A);
+    fk_dyn(ck & 3, hp[0], hp[1], t, H);
+    if (ck >> 2) {
+      double S[16], as[4], hs[4];
+      lds16(mr, S);
+      row_s(A, S, as);
+      row_s(H, S, hs);
+      vAA += rows4(C, ddot_row(as, A));
+      vHH += rows4(C, ddot_row(hs, H));
+      vAH += rows4(C, ddot_row(as, H));
+    }
+  }
+  return 4.0 * (vAA - C.wm) + (vHH - C.wm) - 4.0 * (vAH - C.wm);
+}
+
+// fd_kinetic (stepper.cpp:14-22) + gravity_potential (baseline.cpp:219-229)
+// between FK(hist slot 1) and FK(hist slot 2)
+__device__ __forceinline__ void step_energy(const Ctx& C, double* ke, double* pe) {
+  const int r = C.j & 3;
+  double P[4], W[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) P[k] = W[k] = (r == k) ? 1.0 : 0.0;
+  double kk = 0.0, pp = 0.0;
+  const double ghat[4] = {C.gz[0], C.gz[1], C.gz[2], 0.0};
+  for (int i = 0; i < C.N; ++i) {
+    const int ck = C.kind[i];
+    const double* hp = C.hist + ((long)i * kE + C.e) * kHistW;
+    const double* mr = C.mrec + 20 * i;
+    const double t[3] = {mr[16], mr[17], mr[18]};
+    fk_dyn(ck & 3, hp[2], hp[3], t, P);
+    fk_dyn(ck & 3, hp[4], hp[5], t, W);
+    if (ck >> 2) {
+      double S[16], td[4], tds[4];
+      lds16(mr, S);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) td[c] = (W[c] - P[c]) / C.dt;
+      row_s(td, S, tds);
+      double wu = W[0] * S[12];
+      wu = fma(W[1], S[13], wu);
+      wu = fma(W[2], S[14], wu);
+      wu = fma(W[3], S[15], wu);
+      const double term = rows4(C, ddot_row(tds, td));
+      const double u0 = __shfl_sync(C.em, wu, 0, 4), u1 = __shfl_sync(C.em, wu, 1, 4);
+      const double u2 = __shfl_sync(C.em, wu, 2, 4), u3 = __shfl_sync(C.em, wu, 3, 4);
+      double d = ghat[0] * u0;
+      d = fma(ghat[1], u1, d);
+      d = fma(ghat[2], u2, d);
+      d = fma(ghat[3], u3, d);
+      kk += 0.5 * term;
+      pp -= d;
+    }
+  }
+  *ke = kk;
+  *pe = pp;
+}
+
+// ForceModel::tau_at (objective.hpp:28-58)
+__device__ __forceinline__ void tau_at(const Ctx& C, const DForces& f, double t) {
+  const int n = C.n;
+  for (int i = C.j; i < n; i += kL) {
+    double v;
+    if (f.has_act && f.act_len == n) {
+      if (f.act_kind == 0) {
+        v = f.act_amp[i];
+      } else {
+        const double ph = i < f.act_phase_len ? f.act_phase[i] : 0.0;
+        double s, c;
+        pbad_sincos(2.0 * 3.141592653589793 * f.act_freq * t + ph, &s, &c);
+        v = f.act_amp[i] * s;
+      }
+    } else if (f.tau_len == n) {
+      v = f.tau[i];
+    } else {
+      v = 0.0;
+    }
+    vat(C, C.tau, i) = v;
+  }
+}
+
+// ---- L-BFGS (LbfgsSolver, optim.cpp:141-232) ------------------------------
+// The v4 kernel's fused vector passes (one per reduction of the two-loop
+// recursion, one for the candidate, one for the accepted step) over this
+// lane's elements 16 g + j; every dot keeps its 32-partial order.
+struct Solver {
+  double value, grad0, t, slope, fval;
+  double ginf, xinf;  // |g|_inf, |x|_inf of the current iterate
+  double tdx;         // tau . cand of the pending candidate
+  int status, iters, stag, acc, h0, hc, trial, phase;
+  double* itv;        // per_iteration_values row of this step (lane j = 0 writes), or null
+};
+
+#ifndef PBAD_C7_KB
+#define PBAD_C7_KB 8
+#endif
+constexpr int kB = PBAD_C7_KB;  // groups per batch of loads (even: dot partial index)
+static_assert(kB % 2 == 0, "batch must keep the 32-partial dot order");
+
+template <int KB>
+__device__ __forceinline__ void ldb(const Ctx& C, const double* V, int g0, double* out) {
+#pragma unroll
+  for (int jj = 0; jj < KB; ++jj) {
+    const int g = g0 + jj;
+    out[jj] = (g < C.n16) ? V[(long)g * kGS] : 0.0;
+  }
+}
+__device__ __forceinline__ void l2_prefetch(const Ctx& C, const double* V) {
+  if (C.lane == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V - C.lane),
+                 "r"((unsigned)(C.n16 * kGS * sizeof(double)))
+                 : "memory");
+}
+
+// two-loop passes: q' = op(q, w); then DOT 0: z . q'; 1: z . z; 2: dir = -q', dir . g
+enum { M_COPY = 0, M_SUB = 1, M_SCALE = 2, M_ADD = 3 };
+template <int MODE, int DOT>
+__device__ __forceinline__ double tl_pass(const Ctx& C, const double* w, double a, const double* z, bool store_q) {
+  double acc[2] = {0.0, 0.0};
+  for (int g0 = 0; g0 < C.n16; g0 += kB) {
+    double qv_[kB], wv[kB], zv[kB];
+    if (MODE != M_COPY) ldb<kB>(C, C.q, g0, qv_);
+    if (MODE != M_SCALE) ldb<kB>(C, w, g0, wv);
+    if (DOT == 2) ldb<kB>(C, C.g, g0, zv);
+    else ldb<kB>(C, z, g0, zv);
+#pragma unroll
+    for (int jj = 0; jj < kB; ++jj) {
+      const int g = g0 + jj;
+      if (!elem_ok(C, g)) continue;
+      double qn;
+      if (MODE == M_COPY) qn = wv[jj];
+      else if (MODE == M_SUB) qn = qv_[jj] - a * wv[jj];
+      else if (MODE == M_SCALE) qn = qv_[jj] * a;
+      else qn = qv_[jj] + a * wv[jj];
+      if (DOT == 2) {
+        const double d = -qn;
+        C.dir[(long)g * kGS] = d;
+        acc[jj & 1] = fma(d, zv[jj], acc[jj & 1]);
+      } else {
+        if (store_q) C.q[(long)g * kGS] = qn;
+        if (DOT == 0) acc[jj & 1] = fma(zv[jj], qn, acc[jj & 1]);
+        else acc[jj & 1] = fma(zv[jj], zv[jj], acc[jj & 1]);
+      }
+    }
+  }
+  return dot_finish(C, acc);
+}
+
+// ring slot of deque entry i: (h0 + i) mod (mem + 1) with h0, i <= mem
+__device__ __forceinline__ int hslot(const Ctx& C, const Solver& s, int i) {
+  const int k = s.h0 + i;
+  return k > C.o.mem ? k - (C.o.mem + 1) : k;
+}
+__device__ __forceinline__ const double* hist_s(const Ctx& C, const Solver& s, int i) {
+  return C.hs + hslot(C, s, i) * C.VS;
+}
+__device__ __forceinline__ const double* hist_y(const Ctx& C, const Solver& s, int i) {
+  return C.hy + hslot(C, s, i) * C.VS;
+}
+__device__ __forceinline__ double hist_sy(const Ctx& C, const Solver& s, int i) { return C.hsy[hslot(C, s, i)]; }
+
+// two_loop (optim.cpp:213-229) fused with dir = -q and slope = dir . g
+// (optim.cpp:162-170); returns the slope
+__device__ __forceinline__ double direction(const Ctx& C, const Solver& s) {
+  const int hc = s.hc;
+  if (hc == 0) return tl_pass<M_COPY, 2>(C, C.g, 0.0, nullptr, false);
+  l2_prefetch(C, hist_s(C, s, hc - 1));
+  l2_prefetch(C, hist_y(C, s, hc - 1));
+  if (hc > 1) l2_prefetch(C, hist_s(C, s, hc - 2));
+  double* alpha = C.hsy + kMaxMem + 1;
+  double d = tl_pass<M_COPY, 0>(C, C.g, 0.0, hist_s(C, s, hc - 1), true);  // q = g; s . q
+  double yy = 0.0;
+  for (int i = hc - 1; i >= 0; --i) {
+    const double a = d / hist_sy(C, s, i);
+    alpha[i] = a;
+    if (i >= 2) {
+      l2_prefetch(C, hist_y(C, s, i - 1));
+      l2_prefetch(C, hist_s(C, s, i - 2));
+    } else if (i == 1) {
+      l2_prefetch(C, hist_y(C, s, 0));
+    }
+    if (i > 0) d = tl_pass<M_SUB, 0>(C, hist_y(C, s, i), a, hist_s(C, s, i - 1), true);
+    else yy = tl_pass<M_SUB, 1>(C, hist_y(C, s, 0), a, hist_y(C, s, hc - 1), true);
+  }
+  l2_prefetch(C, hist_s(C, s, 0));
+  if (hc > 1) l2_prefetch(C, hist_y(C, s, 1));
+  const double scl = hist_sy(C, s, hc - 1) / yy;
+  d = tl_pass<M_SCALE, 0>(C, nullptr, scl, hist_y(C, s, 0), true);  // q *= scl; y_0 . q
+  double slope = 0.0;
+  for (int i = 0; i < hc; ++i) {
+    const double beta = d / hist_sy(C, s, i);
+    const double c = alpha[i] - beta;
+    if (i + 2 < hc) {
+      l2_prefetch(C, hist_s(C, s, i + 1));
+      l2_prefetch(C, hist_y(C, s, i + 2));
+    } else if (i + 1 < hc) {
+      l2_prefetch(C, hist_s(C, s, i + 1));
+    }
+    if (i + 1 < hc) d = tl_pass<M_ADD, 0>(C, hist_s(C, s, i), c, hist_y(C, s, i + 1), true);
+    else slope = tl_pass<M_ADD, 2>(C, hist_s(C, s, i), c, nullptr, false);  // dir = -q; dir . g
+  }
+  return slope;
+}
+
+// start of LbfgsSolver::iterate: termination tests, direction, slope
+__device__ __forceinline__ void begin_iteration(const Ctx& C, Solver& s) {
+  if (s.iters >= C.o.max_iters) {
+    s.status = ST_FAILED;
+    s.phase = PH_DONE;
+    return;
+  }
+  // grad_converged (optim.cpp:35-41) on the norms of the current iterate
+  if (s.ginf <= C.o.grad_tol * fmax(1.0, s.xinf) || (C.o.grad_rtol > 0.0 && s.ginf <= C.o.grad_rtol * s.grad0)) {
+    s.status = ST_CONVERGED;
+    s.phase = PH_DONE;
+    return;
+  }
+  double slope = direction(C, s);
+  if (!(slope < 0.0)) {
+    s.hc = 0;
+    s.h0 = 0;
+    slope = tl_pass<M_COPY, 2>(C, C.g, 0.0, nullptr, false);  // dir = -g
+  }
+  s.slope = slope;
+  s.t = 1.0;
+  s.trial = 0;
+  s.fval = s.value;
+  s.phase = PH_GEN;
+}
+
+// next finite candidate x + t dir of the backtracking line search, with
+// tau . cand for its objective value
+__device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
+  while (s.trial < C.o.max_line_search) {
+    const double t = s.t;
+    double acc[2] = {0.0, 0.0};
+    bool fin = true;
+    for (int g0 = 0; g0 < C.n16; g0 += kB) {
+      double xv[kB], dv[kB], tv[kB];
+      ldb<kB>(C, C.x, g0, xv);
+      ldb<kB>(C, C.dir, g0, dv);
+      ldb<kB>(C, C.tau, g0, tv);
+#pragma unroll
+      for (int jj = 0; jj < kB; ++jj) {
+        const int g = g0 + jj;
+        if (!elem_ok(C, g)) continue;
+        const double cv = xv[jj] + t * dv[jj];
+        C.cand[(long)g * kGS] = cv;
+        fin = fin && isfinite(cv);
+        acc[jj & 1] = fma(tv[jj], cv, acc[jj & 1]);
+      }
+    }
+    const double tdx = dot_finish(C, acc);
+    if (__all_sync(C.em, fin)) {
+      s.tdx = tdx;
+      s.phase = PH_EVAL;
+      return;
+    }
+    s.t *= C.o.backtrack_factor;
+    ++s.trial;
+  }
+  s.status = ST_FAILED;  // no acceptable step
+  if (s.itv && C.j == 0) s.itv[s.iters] = s.value;
+  ++s.iters;
+  s.phase = PH_DONE;
+}
+
+// accepted step (optim.cpp:176-205) in one pass: s = t dir, y = evg - g,
+// s . y, x = cand, g = evg, and the norms of the new iterate
+__device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
+  const int cap = C.o.mem + 1;
+  const int slot = (s.h0 + s.hc) % cap;
+  double* sv = C.hs + slot * C.VS;
+  double* yv = C.hy + slot * C.VS;
+  const double t = s.t;
+  double acc[2] = {0.0, 0.0};
+  double gm = 0.0, xm = 0.0;
+  for (int g0 = 0; g0 < C.n16; g0 += kB) {
+    double dv[kB], ev[kB], gv[kB], cv[kB];
+    ldb<kB>(C, C.dir, g0, dv);
+    ldb<kB>(C, C.evg, g0, ev);
+    ldb<kB>(C, C.g, g0, gv);
+    ldb<kB>(C, C.cand, g0, cv);
+#pragma unroll
+    for (int jj = 0; jj < kB; ++jj) {
+      const int g = g0 + jj;
+      if (!elem_ok(C, g)) continue;
+      const long o = (long)g * kGS;
+      const double sj = t * dv[jj];
+      const double yj = ev[jj] - gv[jj];
+      sv[o] = sj;
+      yv[o] = yj;
+      C.x[o] = cv[jj];
+      C.g[o] = ev[jj];
+      acc[jj & 1] = fma(sj, yj, acc[jj & 1]);
+      gm = fmax(gm, fabs(ev[jj]));
+      xm = fmax(xm, fabs(cv[jj]));
+    }
+  }
+  const double sy = dot_finish(C, acc);
+  s.ginf = emax(C, gm);
+  s.xinf = emax(C, xm);
+  if (sy > 1e-12) {
+    if (C.j == 0) C.hsy[slot] = sy;
+    ++s.hc;
+    if (s.hc > C.o.mem) {
+      s.h0 = (s.h0 + 1) % cap;
+      --s.hc;
+    }
+  }
+  esync(C);
+  const double oldv = s.fval;
+  s.value = v;
+  ++s.acc;
+  if (oldv - v <= C.o.ftol * fmax(1.0, fabs(oldv))) ++s.stag;
+  else s.stag = 0;
+  if (s.stag >= 2) s.status = ST_CONVERGED;
+  if (s.itv && C.j == 0) s.itv[s.iters] = s.value;
+  ++s.iters;
+  if (s.status == ST_RUNNING && s.iters >= C.o.max_iters) s.status = ST_FAILED;
+  s.phase = (s.status == ST_RUNNING) ? PH_DIR : PH_DONE;
+}
+
+template <int PAT>
+__device__ __forceinline__ Ctx make_ctx(const DModel& m, const DForces& f, const DSchedule& sc, const ChainLayout& L,
+                                        double* cw, int* ci, long B, double* smem) {
+  Ctx C;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  C.lane = lane;
+  C.N = m.N;
+  C.n = m.n;
+  C.n16 = (m.n + 15) >> 4;
+  C.n4q = (m.n + 3) >> 2;
+  C.e = lane >> 4;
+  C.j = lane & 15;
+  const long w = (long)blockIdx.x * kW + wib;
+  C.ge = w * kE + C.e;
+  C.B = B;
+  C.valid = C.ge < B;
+  C.em = 0xFFFFu << (lane & ~15);
+  C.ws = smem + (long)wib * warp_doubles(PAT);
+  C.bar = reinterpret_cast<uint64_t*>(C.ws + bar_off(PAT));
+  C.mrec = smem + (long)kW * warp_doubles(PAT);
+  C.kind = reinterpret_cast<const int*>(C.mrec + 20L * m.N);
+  C.roff = C.kind + m.N;
+  C.rec = cw + L.rec + w * (long)C.roff[m.N];
+  C.hist = cw + L.hist + w * (long)m.N * kE * kHistW;
+  C.gh0 = cw + L.h0;
+  C.gh1 = cw + L.h1;
+  const long vl = w * (long)C.n16 * kGS + lane;
+  C.x = cw + L.x + vl;
+  C.g = cw + L.g + vl;
+  C.cand = cw + L.cand + vl;
+  C.dir = cw + L.dir + vl;
+  C.q = cw + L.q + vl;
+  C.evg = cw + L.evg + vl;
+  C.tau = cw + L.tau + vl;
+  C.hs = cw + L.hs + vl;
+  C.hy = cw + L.hy + vl;
+  C.VS = L.vstride;
+  // per-env scalars; padded environments (ge >= B) point at env 0 and never write
+  const long es = C.valid ? C.ge : 0;
+  C.hsy = C.ws + hsy_off(PAT) + C.e * kHsyW;
+  C.histc = cw + L.histc + es;
+  C.ci = ci;
+  C.dt = sc.dt;
+  C.inv_dt2 = 1.0 / (sc.dt * sc.dt);
+  C.wm = m.weighted_mass;
+  C.gz[0] = f.gravity[0];
+  C.gz[1] = f.gravity[1];
+  C.gz[2] = f.gravity[2];
+  {
+    const int rr = lane & 3;  // reverse-sweep row of this lane
+    C.grr = (rr == 0) ? f.gravity[0] : (rr == 1) ? f.gravity[1] : (rr == 2) ? f.gravity[2] : 0.0;
+  }
+  C.o = sc.opt;
+  C.nload = 0;
+  return C;
+}
+
+template <int PAT>
+__device__ __forceinline__ void stage(const DModel& m, double* smem) {
+  double* rec = smem + (long)kW * warp_doubles(PAT);
+  int* kind = reinterpret_cast<int*>(rec + 20L * m.N);
+  int* roff = kind + m.N;
+  const double2* src = reinterpret_cast<const double2*>(m.crec);
+  double2* dst = reinterpret_cast<double2*>(rec);
+  for (int k = threadIdx.x; k < 10 * m.N; k += blockDim.x) dst[k] = __ldg(src + k);
+  for (int k = threadIdx.x; k < m.N; k += blockDim.x) kind[k] = __ldg(m.ckind + k);
+  // record offsets per 2-environment warp (the v4 offsets are per 8 environments)
+  for (int k = threadIdx.x; k <= m.N; k += blockDim.x) roff[k] = __ldg(m.croff + k) / 4;
+  if ((threadIdx.x & 31) == 0) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (long)(threadIdx.x >> 5) * warp_doubles(PAT) + bar_off(PAT));
+    for (int s = 0; s < kRing; ++s) mbar_init(bar + s);
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
+
+// One PBAD step for both environments of the warp: begin_step, L-BFGS to
+// completion in lockstep rounds, finish_step (stepper.cpp:83-147).
+template <int PAT>
+__global__ void __launch_bounds__(kT, 2) k_chain7_step(DModel m, DForces f, DSchedule sc, ChainLayout L, double* cw,
+                                                       int* ci, long B, Outputs out) {
+  extern __shared__ __align__(16) double smem[];
+  stage<PAT>(m, smem);
+  Ctx C = make_ctx<PAT>(m, f, sc, L, cw, ci, B, smem);
+  // a warp with no running environment has nothing to do (warp-uniform exit)
+  bool active = C.valid && ival(C, IS_RUN) == TR_RUNNING;
+  if (!__any_sync(0xffffffffu, active)) return;
+  const int n = m.n;
+  const int step = C.valid ? ival(C, IS_STEP) : 0;
+  if (active) {
+    // StepObjective ctor validates the history (objective.cpp:176-177)
+    if (!qallfinite(C, C.gh0) || !qallfinite(C, C.gh1)) {
+      if (C.j == 0) ival(C, IS_RUN) = TR_NONFINITE_CFG;
+      active = false;
+    }
+  }
+  if (active) {
+    // begin_step: actuation at the step end, warm start (stepper.cpp:83-115)
+    tau_at(C, f, step * sc.dt + sc.times[2] * sc.dt);
+    const double span = -sc.times[0];
+    const double tau_m = sc.times[2];
+    const bool ws = sc.warm_start != 0;
+    for (int k = C.j; k < n; k += kL) {
+      const double h1 = qv(C, C.gh1, k), h0 = qv(C, C.gh0, k);
+      vat(C, C.x, k) = ws ? h1 + (tau_m / span) * (h1 - h0) : h1;
+    }
+    esync(C);
+    hist_rotations_q(C, C.gh0, 0);
+    hist_rotations_q(C, C.gh1, 1);
+    const double hc = hist_const(C);
+    if (C.j == 0) *C.histc = hc;
+    esync(C);
+    if (!eallfinite(C, C.x)) {
+      if (C.j == 0) ival(C, IS_RUN) = TR_NONFINITE_CFG;
+      active = false;
+    }
+  }
+  __syncwarp();
+  // LbfgsSolver ctor: first evaluation (warp-collective sweeps)
+  Solver s{};
+  s.status = ST_RUNNING;
+  s.phase = PH_DIR;
+  s.itv = (out.itv && C.valid) ? out.itv + out.rrow(C.ge, step) * out.itv_n : nullptr;
+  double tdx0 = 0.0;
+  if (active) {
+    tdx0 = edot(C, C.tau, C.x);
+    s.xinf = einfnorm(C, C.x);
+  }
+  __syncwarp();
+  const double v0 = forward<PAT>(C, C.x, tdx0);
+  reverse<PAT>(C, C.g);
+  if (active && !isfinite(v0)) {
+    if (C.j == 0) ival(C, IS_RUN) = TR_NONFINITE_INIT;
+    active = false;
+  }
+  if (active) {
+    s.value = v0;
+    s.grad0 = einfnorm(C, C.g);
+    s.ginf = s.grad0;
+  } else {
+    s.phase = PH_DONE;
+  }
+  for (;;) {
+    if (s.phase == PH_DIR) begin_iteration(C, s);
+    if (s.phase == PH_GEN) next_candidate(C, s);
+    __syncwarp();
+    const bool eval = s.phase == PH_EVAL;
+    if (!__any_sync(0xffffffffu, eval)) break;
+    const double v = forward<PAT>(C, C.cand, s.tdx);
+    bool acc = false;
+    if (eval) {
+      if (isfinite(v) && v <= s.fval + C.o.armijo_c1 * s.t * s.slope && v < s.fval) {
+        acc = true;
+      } else {
+        s.t *= C.o.backtrack_factor;
+        ++s.trial;
+        s.phase = PH_GEN;
+      }
+    }
+    if (__any_sync(0xffffffffu, acc)) reverse<PAT>(C, C.evg);
+    if (acc) accept_step(C, s, v);
+    __syncwarp();
+  }
+  if (!active) return;
+  // finish_step
+  const bool converged = s.status == ST_CONVERGED;
+  const double gnorm = einfnorm(C, C.g);
+  if (C.j == 0) {
+    if (out.iterations) out.iterations[out.rrow(C.ge, step)] = s.iters;
+    if (out.converged) out.converged[out.rrow(C.ge, step)] = converged;
+    if (out.accepted) out.accepted[out.rrow(C.ge, step)] = s.acc;
+    if (out.final_value) out.final_value[out.rrow(C.ge, step)] = s.value;
+    if (out.final_grad_norm) out.final_grad_norm[out.rrow(C.ge, step)] = gnorm;
+    ival(C, IS_NREP) = step + 1;
+  }
+  const int fs = converged ? 0 : ival(C, IS_FAIL) + 1;
+  esync(C);
+  if (C.j == 0) ival(C, IS_FAIL) = fs;
+  if (fs > sc.fail_limit) {
+    if (C.j == 0) ival(C, IS_RUN) = TR_FAIL_LIMIT;
+    return;
+  }
+  hist_rotations(C, C.x, 2);
+  double ke, pe;
+  step_energy(C, &ke, &pe);
+  for (int k = C.j; k < n; k += kL) {
+    const double xk = vat(C, C.x, k);
+    qv(C, C.gh0, k) = qv(C, C.gh1, k);
+    qv(C, C.gh1, k) = xk;
+    if (out.q) out.q[out.qrow(C.ge, step + 1) * n + k] = xk;
+  }
+  if (C.j == 0) {
+    if (out.energy) {
+      out.energy[out.qrow(C.ge, step + 1) * 2] = ke;
+      out.energy[out.qrow(C.ge, step + 1) * 2 + 1] = pe;
+    }
+    ival(C, IS_STEP) = step + 1;
+    ival(C, IS_NSAMP) = step + 2;
+    if (step + 1 >= sc.total_steps) ival(C, IS_RUN) = TR_OK;
+  }
+}
+
+template <int PAT>
+cudaError_t launch(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
+  const size_t sm = smem_bytes(a.m.N, PAT);
+  static size_t configured = 0;
+  if (sm > configured) {
+    const cudaError_t e = cudaFuncSetAttribute(k_chain7_step<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  const long nw = (a.B + kE - 1) / kE;
+  const unsigned grid = (unsigned)((nw + kW - 1) / kW);
+  k_chain7_step<PAT><<<grid, kT, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, out);
+  return cudaGetLastError();
+}
+
+constexpr int pat(int P, int K0, int K1) { return P | (K0 << 2) | (K1 << 5); }
+
+}  // namespace c7
+
+bool chain7_fits(int N, int mem, int pattern) {
+  const int p = (pattern == c7::pat(1, 6, 0) || pattern == c7::pat(2, 3, 6)) ? pattern : 0;
+  return mem <= c7::kMaxMem && c7::smem_bytes(N, p) <= 227 * 1024;
+}
+// vector doubles per warp-group layout: ceil(B / 2) warps x ceil(n / 16) groups x 32
+long chain7_vector_doubles(long B, int n) { return (B + c7::kE - 1) / c7::kE * (long)((n + 15) / 16) * c7::kGS; }
+
+cudaError_t launch_chain7_step(const ChainArgs& a, int pattern, const Outputs& out, cudaStream_t s) {
+  switch (pattern) {
+    case c7::pat(1, 6, 0): return c7::launch<c7::pat(1, 6, 0)>(a, out, s);
+    case c7::pat(2, 3, 6): return c7::launch<c7::pat(2, 3, 6)>(a, out, s);
+    default: return c7::launch<0>(a, out, s);
+  }
+}
+
+}  // namespace pbad_gpu

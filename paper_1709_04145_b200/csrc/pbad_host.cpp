@@ -488,6 +488,7 @@ struct pbad_gpu_ctx {
   bool chain4 = false;     // ... in their warp-synchronous v4 form (pbad_chain4.cu)
   bool chain5 = false;     // ... or warp per environment, v5 (pbad_chain5.cu)
   bool chain6 = false;     // ... or two lanes per row, v6 (pbad_chain6.cu)
+  bool chain7 = false;     // ... or 16 lanes per environment, link-parallel terms, v7 (pbad_chain7.cu)
   int chain4_pat = 0;      // v4 link-pattern instantiation
   long chain4_recw = 0;    // v4 record doubles per warp
   long v1_per_env = 0;     // general-kernel workspace size (allocated lazily)
@@ -615,7 +616,7 @@ ChainLayout make_chain_layout(const pbad_gpu_model& m, int mem, long B, long rec
   ChainLayout L{};
   const long N = m.N, n4 = (m.n + 3) / 4, nw = (B + 7) / 8;
   // vectors: the v3/v4 quad layout or the v6 8-lane layout, whichever is larger
-  const long link = rec_w > 0 ? 0 : nw * N * 128, vec = std::max(nw * n4 * 32, chain6_vector_doubles(B, m.n));
+  const long link = rec_w > 0 ? 0 : nw * N * 128, vec = std::max(std::max(nw * n4 * 32, chain6_vector_doubles(B, m.n)), chain7_vector_doubles(B, m.n));
   long o = 0;
   auto take = [&](long cnt) {
     const long at = o;
@@ -952,6 +953,7 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     // blocks, else v6 (two lanes per row); PBAD_GPU_CHAIN_V5 / _V6 / _V4 force one
     const int waves = chain5_waves(m.N, m.n, sim->opt.lbfgs_memory, max_batch, c->chain4_pat, device);
     c->chain5 = c->chain4 && !std::getenv("PBAD_GPU_CHAIN_V4") && !std::getenv("PBAD_GPU_CHAIN_V6") &&
+                !std::getenv("PBAD_GPU_CHAIN_V7") &&
                 (std::getenv("PBAD_GPU_CHAIN_V5") ? waves > 0 : waves == 1);
     c->chain4_recw = roff[m.N];
   }
@@ -1013,6 +1015,20 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
   // beyond one v5 wave: v6 (two lanes per row) unless PBAD_GPU_CHAIN_V4
   c->chain6 = c->chain4 && !c->chain5 && !std::getenv("PBAD_GPU_CHAIN_V4") &&
               chain6_fits(m.N, sim->opt.lbfgs_memory);
+  // v7 (16 lanes per environment, link-parallel energy terms) only on request
+  // (PBAD_GPU_CHAIN_V7): it is bit-exact but measured slower than v6 on C3
+  // (DESIGN.md 3).  It takes a massive link's row-3 energy term as S(3,3)
+  // exactly, which needs S(3,3) != 0 (pbad_chain7.cu)
+  if (c->chain6 && std::getenv("PBAD_GPU_CHAIN_V7") && chain7_fits(m.N, sim->opt.lbfgs_memory, c->chain4_pat)) {
+    bool s33 = true;
+    for (int i = 0; i < m.N; ++i) {
+      bool massive = false;
+      for (int k = 0; k < 16; ++k) massive = massive || m.S[16 * i + k] != 0.0;
+      if (massive && m.S[16 * i + 15] == 0.0) s33 = false;
+    }
+    c->chain7 = s33;
+    c->chain6 = !s33;
+  }
   c->tree = !c->chain && tree_eligible(m, f, sim);
   if (c->tree) {
     const TreeHost th = make_tree_host(m);
@@ -1159,6 +1175,7 @@ int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
 int32_t pbad_gpu_path(const pbad_gpu_ctx* c) {
   return c->chain5 ? PBAD_PATH_CHAIN5
          : c->chain6 ? PBAD_PATH_CHAIN6
+         : c->chain7 ? PBAD_PATH_CHAIN7
          : c->chain4 ? PBAD_PATH_CHAIN4
          : c->chain ? PBAD_PATH_CHAIN
          : c->tree  ? PBAD_PATH_TREE
@@ -1276,6 +1293,7 @@ int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
   for (long k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
     CUDA_TRY(c->chain5  ? launch_chain5_step(c->ca, c->chain4_pat, c->chain4_recw / 8, c->dout, s)
              : c->chain6 ? launch_chain6_step(c->ca, c->chain4_pat, c->dout, s)
+             : c->chain7 ? launch_chain7_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain4 ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain ? launch_chain_step(c->ca, c->dout, s)
              : c->tree  ? launch_tree_step(c->ka, c->td, c->tws, c->dout, s)

@@ -47,6 +47,10 @@ bool chain6_fits(int N, int mem);
 long chain6_vector_doubles(long B, int n);
 cudaError_t launch_chain6_step(const ChainArgs& a, int pattern, const Outputs& out, cudaStream_t s);
 cudaError_t launch_chain5_step(const ChainArgs& a, int pattern, long recw, const Outputs& out, cudaStream_t s);
+// chain v7 (pbad_chain7.cu): 16 lanes per environment, link-parallel energy terms
+bool chain7_fits(int N, int mem, int pattern);
+long chain7_vector_doubles(long B, int n);
+cudaError_t launch_chain7_step(const ChainArgs& a, int pattern, const Outputs& out, cudaStream_t s);
 
 // tree path (pbad_tree.cu): warp-per-environment LM for articulated trees
 bool tree_eligible_sizes(int N, int n);

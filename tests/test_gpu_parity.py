@@ -273,7 +273,7 @@ def _path(scene, sim):
     return api.GpuContext(m, scene.forces(), sim, max_batch=1).path
 
 
-CHAIN_KERNELS = [("v5", 5), ("v6", 6), ("v4", 2)]
+CHAIN_KERNELS = [("v5", 5), ("v7", 7), ("v6", 6), ("v4", 2)]
 
 
 def _chain_kernel(monkeypatch, version):
@@ -281,6 +281,8 @@ def _chain_kernel(monkeypatch, version):
         monkeypatch.setenv("PBAD_GPU_CHAIN_V4", "1")
     if version == "v6":
         monkeypatch.setenv("PBAD_GPU_CHAIN_V6", "1")
+    if version == "v7":
+        monkeypatch.setenv("PBAD_GPU_CHAIN_V7", "1")
 
 
 @pytest.mark.parametrize("version,path", CHAIN_KERNELS)
@@ -314,7 +316,7 @@ def test_chain4_lockstep_divergent_envs(version, path, monkeypatch):
 
 
 def test_chain4_matches_chain_v3(monkeypatch):
-    """The v3 quad kernel (PBAD_GPU_CHAIN_V3), v4 (PBAD_GPU_CHAIN_V4) and
+    """The v3 quad kernel (PBAD_GPU_CHAIN_V3), v4 (PBAD_GPU_CHAIN_V4), v6, v7 and
     v5 produce identical trajectories (all are pinned to the oracle)."""
     sc = make_chain_scene(12)
     sim = SimConfig(dt=0.1, duration=0.3)
@@ -329,6 +331,10 @@ def test_chain4_matches_chain_v3(monkeypatch):
         sims.append(s)
     assert _path(sc, sim) == 5
     v5 = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.setenv("PBAD_GPU_CHAIN_V7", "1")
+    assert _path(sc, sim) == 7
+    v7 = api.batch_simulate(m, sc.forces(), sims)
+    monkeypatch.delenv("PBAD_GPU_CHAIN_V7")
     monkeypatch.setenv("PBAD_GPU_CHAIN_V6", "1")
     assert _path(sc, sim) == 6
     v6 = api.batch_simulate(m, sc.forces(), sims)
@@ -339,7 +345,7 @@ def test_chain4_matches_chain_v3(monkeypatch):
     monkeypatch.setenv("PBAD_GPU_CHAIN_V3", "1")
     assert _path(sc, sim) == 1
     v3 = api.batch_simulate(m, sc.forces(), sims)
-    for a, b, c, d in zip(v5, v4, v3, v6):
-        for o in (b, c, d):
+    for a, b, c, d, e in zip(v5, v4, v3, v6, v7):
+        for o in (b, c, d, e):
             np.testing.assert_array_equal(np.array([s[1] for s in a.samples]), np.array([s[1] for s in o.samples]))
             assert [r.iterations for r in a.solve_reports] == [r.iterations for r in o.solve_reports]
