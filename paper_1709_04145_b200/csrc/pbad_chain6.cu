@@ -82,7 +82,7 @@ __host__ __device__ inline size_t smem_bytes(int N) {
 
 // ---- context ----------------------------------------------------------------
 struct Ctx {
-  int N, n, n8, r, h, j, e;
+  int N, n, n8, nf, r, h, j, e;  // nf: groups whose 8 elements all exist (8 g + 7 < n)
   long ge, B, n4q;
   bool valid;
   unsigned em;         // this environment's 8 lanes
@@ -173,8 +173,15 @@ struct Rows {
   double X1[4], X2[4];
 };
 
+// predicated 16-byte global store without a branch around it
+__device__ __forceinline__ void stg2_if(bool p, double* a, double x, double y) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.global.v2.f64 [%1], {%2, %3};\n}" ::"r"((int)p),
+               "l"(a), "d"(x), "d"(y)
+               : "memory");
+}
+
 template <int CK>
-__device__ __forceinline__ void fwd_link(const Ctx& C, int jl, int i, Rows& R) {
+__device__ __forceinline__ void fwd_link(const Ctx& C, int jl, int i, Rows& R, double* rp) {
   constexpr int JK = CK & 3;
   constexpr bool SK = (CK >> 2) != 0;
   const double* rb = C.ws + kFwdC + (jl * kE + C.e) * 8;
@@ -185,11 +192,11 @@ __device__ __forceinline__ void fwd_link(const Ctx& C, int jl, int i, Rows& R) {
   const double* mr = C.mrec + 20 * i;
   const double2 t01 = *reinterpret_cast<const double2*>(mr + 16);
   const double t[3] = {t01.x, t01.y, mr[18]};
-  double* rp = C.rec + C.roff[i];
   const int row = 3 * C.e + C.r;
+  const bool rec_lane = C.h == 0 && C.r < 3;
   double l0, l1;
   lever<JK>(c1, s1, R.X1, l0, l1);  // h = 0: T_parent row times dL/dq (adjoint.cpp:22-25)
-  if (C.h == 0 && C.r < 3) *reinterpret_cast<double2*>(rp + kRecLev + 2 * row) = make_double2(l0, l1);
+  stg2_if(rec_lane, rp + kRecLev + 2 * row, l0, l1);
   fk<JK>(c1, s1, t, R.X1);
   fk<JK>(hc0.x, hc0.y, t, R.X2);
   if (SK) {
@@ -215,22 +222,20 @@ __device__ __forceinline__ void fwd_link(const Ctx& C, int jl, int i, Rows& R) {
     double* fr = C.ws + kFwdR + jl * 64 + C.r * 4 + C.e;
     fr[C.h ? 16 : 0] = ddot_row(p1, tr);   // term 0 (T S . T) / term 1 (A S . T)
     fr[C.h ? 32 : 48] = ddot_row(cg, tr);  // term 3 (gravity) / term 2 (H S . T)
-    if (C.h == 0 && C.r < 3) {
-      double* sp = rp + kRecSd + 4 * row;
-      *reinterpret_cast<double2*>(sp) = make_double2(p2[0], p2[1]);
-      *reinterpret_cast<double2*>(sp + 2) = make_double2(p2[2], p2[3]);
-    }
+    double* sp = rp + kRecSd + 4 * row;
+    stg2_if(rec_lane, sp, p2[0], p2[1]);
+    stg2_if(rec_lane, sp + 2, p2[2], p2[3]);
   }
 }
 
 __device__ __forceinline__ void fwd_link_dyn(const Ctx& C, int jl, int i, Rows& R) {
   switch (C.kind[i]) {
-    case 1: fwd_link<1>(C, jl, i, R); break;
-    case 2: fwd_link<2>(C, jl, i, R); break;
-    case 3: fwd_link<3>(C, jl, i, R); break;
-    case 5: fwd_link<5>(C, jl, i, R); break;
-    case 6: fwd_link<6>(C, jl, i, R); break;
-    default: fwd_link<7>(C, jl, i, R); break;
+    case 1: fwd_link<1>(C, jl, i, R, C.rec + C.roff[i]); break;
+    case 2: fwd_link<2>(C, jl, i, R, C.rec + C.roff[i]); break;
+    case 3: fwd_link<3>(C, jl, i, R, C.rec + C.roff[i]); break;
+    case 5: fwd_link<5>(C, jl, i, R, C.rec + C.roff[i]); break;
+    case 6: fwd_link<6>(C, jl, i, R, C.rec + C.roff[i]); break;
+    default: fwd_link<7>(C, jl, i, R, C.rec + C.roff[i]); break;
   }
 }
 
@@ -240,23 +245,34 @@ struct PatKind {
   static constexpr int P = PAT & 3;
   static constexpr int value = (P == 2 && (J & 1)) ? ((PAT >> 5) & 7) : ((PAT >> 2) & 7);
 };
+// record offset of chunk link J from the chunk's first record (compile-time
+// for a link pattern: the chunk starts at a multiple of the period)
+template <int PAT, int J>
+struct RecOff {
+  static constexpr int value =
+      RecOff<PAT, J - 1>::value + (((PatKind<PAT, J - 1>::value >> 2) != 0) ? kRecMass : kRecLight);
+};
+template <int PAT>
+struct RecOff<PAT, 0> {
+  static constexpr int value = 0;
+};
 template <int PAT, int J>
 struct FwdUnroll {
-  static __device__ __forceinline__ void run(const Ctx& C, int lo, Rows& R) {
-    fwd_link<PatKind<PAT, J>::value>(C, J, lo + J, R);
-    FwdUnroll<PAT, J + 1>::run(C, lo, R);
+  static __device__ __forceinline__ void run(const Ctx& C, int lo, Rows& R, double* rc) {
+    fwd_link<PatKind<PAT, J>::value>(C, J, lo + J, R, rc + RecOff<PAT, J>::value);
+    FwdUnroll<PAT, J + 1>::run(C, lo, R, rc);
   }
 };
 template <int PAT>
 struct FwdUnroll<PAT, CL> {
-  static __device__ __forceinline__ void run(const Ctx&, int, Rows&) {}
+  static __device__ __forceinline__ void run(const Ctx&, int, Rows&, double*) {}
 };
 
 template <int PAT>
 __device__ __forceinline__ void fwd_chunk(const Ctx& C, int lo, int cnt, Rows& R) {
   if constexpr ((PAT & 3) != 0) {
     if (cnt == CL) {
-      FwdUnroll<PAT, 0>::run(C, lo, R);
+      FwdUnroll<PAT, 0>::run(C, lo, R, C.rec + C.roff[lo]);
       return;
     }
   }
@@ -306,10 +322,22 @@ __device__ __forceinline__ double forward(const Ctx& C, const double* X, double 
     __syncwarp();
     // lane t < 4 adds term t of each massive link, link by link (serial order)
     if (C.j < 4) {
-      for (int jl = 0; jl < cnt; ++jl) {
-        if (C.kind[lo + jl] >> 2) {
-          const double* b = C.ws + kFwdR + jl * 64 + C.j * 16 + C.e;
-          sum += ((b[0] + b[4]) + b[8]) + b[12];
+      const double* b0 = C.ws + kFwdR + C.j * 16 + C.e;
+      if ((PAT & 3) != 0 && cnt == CL) {
+#pragma unroll
+        for (int jl = 0; jl < CL; ++jl) {
+          const int ck = ((PAT & 3) == 2 && (jl & 1)) ? ((PAT >> 5) & 7) : ((PAT >> 2) & 7);
+          if (ck >> 2) {
+            const double* b = b0 + jl * 64;
+            sum += ((b[0] + b[4]) + b[8]) + b[12];
+          }
+        }
+      } else {
+        for (int jl = 0; jl < cnt; ++jl) {
+          if (C.kind[lo + jl] >> 2) {
+            const double* b = b0 + jl * 64;
+            sum += ((b[0] + b[4]) + b[8]) + b[12];
+          }
         }
       }
     }
@@ -340,20 +368,20 @@ __device__ __forceinline__ void rev_link(const Ctx& C, const double* rp, int i, 
   const double* mr = C.mrec + 20 * i;
   double a[4];
   if (SK) {
-    double sd[4] = {0.0, 0.0, 0.0, 0.0};
-    if (own && C.h == 0) {
-      const double2 s01 = *reinterpret_cast<const double2*>(rp + kRecSd + 4 * row);
-      const double2 s23 = *reinterpret_cast<const double2*>(rp + kRecSd + 4 * row + 2);
-      sd[0] = s01.x;
-      sd[1] = s01.y;
-      sd[2] = s23.x;
-      sd[3] = s23.y;
-    }
-    const double2 u01 = *reinterpret_cast<const double2*>(mr + 12);
-    const double2 u23 = *reinterpret_cast<const double2*>(mr + 14);
-    const double u[4] = {u01.x, u01.y, u23.x, u23.y};
+    // inertial chain (h = 0, rows 0..2): a = cc + seed; gravity chain: a = cc +
+    // (0.0 + (-g_r) u) with u = S column 3.  Both as cc + fma(m, v, 0.0): the
+    // product m v is exact for m = 1, and fma(x, y, 0.0) == 0.0 + x * y.  The
+    // only difference, the sign of a zero addend, cannot reach a: cc is never
+    // -0 (it starts at +0 and is 0.0 + o afterwards), and row 3 (no seed)
+    // takes m = 0.
+    const bool sd_lane = own && C.h == 0;
+    const double* vp = sd_lane ? rp + kRecSd + 4 * row : mr + 12;
+    const double mlt = sd_lane ? 1.0 : (C.h ? -C.gr : 0.0);
+    const double2 v01 = *reinterpret_cast<const double2*>(vp);
+    const double2 v23 = *reinterpret_cast<const double2*>(vp + 2);
+    const double v[4] = {v01.x, v01.y, v23.x, v23.y};
 #pragma unroll
-    for (int k = 0; k < 4; ++k) a[k] = cc[k] + (C.h ? (0.0 + (-C.gr) * u[k]) : sd[k]);
+    for (int k = 0; k < 4; ++k) a[k] = cc[k] + fma(mlt, v[k], 0.0);
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k) a[k] = cc[k];
@@ -383,7 +411,7 @@ __device__ __forceinline__ void rev_link_dyn(const Ctx& C, const double* rp, int
 template <int PAT, int J>
 struct RevUnroll {  // links J, J-1, ..., 0 of a full chunk
   static __device__ __forceinline__ void run(const Ctx& C, const double* sbase, int lo, double* cc) {
-    rev_link<PatKind<PAT, J>::value>(C, sbase + C.roff[lo + J], lo + J, J, cc);
+    rev_link<PatKind<PAT, J>::value>(C, sbase + RecOff<PAT, J>::value, lo + J, J, cc);
     RevUnroll<PAT, J - 1>::run(C, sbase, lo, cc);
   }
 };
@@ -396,7 +424,7 @@ template <int PAT>
 __device__ __forceinline__ void rev_chunk(const Ctx& C, const double* sbase, int lo, int cnt, double* cc) {
   if constexpr ((PAT & 3) != 0) {
     if (cnt == CL) {
-      RevUnroll<PAT, CL - 1>::run(C, sbase, lo, cc);
+      RevUnroll<PAT, CL - 1>::run(C, sbase + C.roff[lo], lo, cc);
       return;
     }
   }
@@ -590,14 +618,17 @@ struct Solver {
 constexpr int kB = PBAD_C6_KB;  // groups per batch of loads (multiple of 4: dot partial index)
 static_assert(kB % 4 == 0, "batch must keep the 32-partial dot order");
 
-template <int KB>
+// Vector passes run in batches of kB groups.  Batches of groups below nf
+// hold an element in every lane and run unpredicated from one base address
+// (F = true); the tail batch checks every group (F = false).
+template <bool F>
 __device__ __forceinline__ void ldb(const Ctx& C, const double* V, int g0, double* out) {
+  const double* p = V + (long)g0 * kGS;
 #pragma unroll
-  for (int jj = 0; jj < KB; ++jj) {
-    const int g = g0 + jj;
-    out[jj] = (g < C.n8) ? V[(long)g * kGS] : 0.0;
-  }
+  for (int jj = 0; jj < kB; ++jj) out[jj] = (F || g0 + jj < C.n8) ? p[jj * kGS] : 0.0;
 }
+template <bool F>
+__device__ __forceinline__ bool gok(const Ctx& C, int g) { return F || elem_ok(C, g); }
 __device__ __forceinline__ void l2_prefetch(const Ctx& C, const double* V) {
   if ((threadIdx.x & 31) == 0)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V - (threadIdx.x & 31)),
@@ -607,35 +638,41 @@ __device__ __forceinline__ void l2_prefetch(const Ctx& C, const double* V) {
 
 // two-loop passes: q' = op(q, w); then DOT 0: z . q'; 1: z . z; 2: dir = -q', dir . g
 enum { M_COPY = 0, M_SUB = 1, M_SCALE = 2, M_ADD = 3 };
+template <bool F, int MODE, int DOT>
+__device__ __forceinline__ void tl_batch(const Ctx& C, const double* w, double a, const double* z, bool store_q, int g0,
+                                         double* acc) {
+  double qv_[kB], wv[kB], zv[kB];
+  if (MODE != M_COPY) ldb<F>(C, C.q, g0, qv_);
+  if (MODE != M_SCALE) ldb<F>(C, w, g0, wv);
+  if (DOT == 2) ldb<F>(C, C.g, g0, zv);
+  else ldb<F>(C, z, g0, zv);
+  double* qo = C.q + (long)g0 * kGS;
+  double* dout = C.dir + (long)g0 * kGS;
+#pragma unroll
+  for (int jj = 0; jj < kB; ++jj) {
+    if (!gok<F>(C, g0 + jj)) continue;
+    double qn;
+    if (MODE == M_COPY) qn = wv[jj];
+    else if (MODE == M_SUB) qn = qv_[jj] - a * wv[jj];
+    else if (MODE == M_SCALE) qn = qv_[jj] * a;
+    else qn = qv_[jj] + a * wv[jj];
+    if (DOT == 2) {
+      const double d = -qn;
+      dout[jj * kGS] = d;
+      acc[jj & 3] = fma(d, zv[jj], acc[jj & 3]);
+    } else {
+      if (store_q) qo[jj * kGS] = qn;
+      if (DOT == 0) acc[jj & 3] = fma(zv[jj], qn, acc[jj & 3]);
+      else acc[jj & 3] = fma(zv[jj], zv[jj], acc[jj & 3]);
+    }
+  }
+}
 template <int MODE, int DOT>
 __device__ __forceinline__ double tl_pass(const Ctx& C, const double* w, double a, const double* z, bool store_q) {
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int g0 = 0; g0 < C.n8; g0 += kB) {
-    double qv_[kB], wv[kB], zv[kB];
-    if (MODE != M_COPY) ldb<kB>(C, C.q, g0, qv_);
-    if (MODE != M_SCALE) ldb<kB>(C, w, g0, wv);
-    if (DOT == 2) ldb<kB>(C, C.g, g0, zv);
-    else ldb<kB>(C, z, g0, zv);
-#pragma unroll
-    for (int jj = 0; jj < kB; ++jj) {
-      const int g = g0 + jj;
-      if (!elem_ok(C, g)) continue;
-      double qn;
-      if (MODE == M_COPY) qn = wv[jj];
-      else if (MODE == M_SUB) qn = qv_[jj] - a * wv[jj];
-      else if (MODE == M_SCALE) qn = qv_[jj] * a;
-      else qn = qv_[jj] + a * wv[jj];
-      if (DOT == 2) {
-        const double d = -qn;
-        C.dir[(long)g * kGS] = d;
-        acc[jj & 3] = fma(d, zv[jj], acc[jj & 3]);
-      } else {
-        if (store_q) C.q[(long)g * kGS] = qn;
-        if (DOT == 0) acc[jj & 3] = fma(zv[jj], qn, acc[jj & 3]);
-        else acc[jj & 3] = fma(zv[jj], zv[jj], acc[jj & 3]);
-      }
-    }
-  }
+  int g0 = 0;
+  for (; g0 + kB <= C.nf; g0 += kB) tl_batch<true, MODE, DOT>(C, w, a, z, store_q, g0, acc);
+  for (; g0 < C.n8; g0 += kB) tl_batch<false, MODE, DOT>(C, w, a, z, store_q, g0, acc);
   return dot_finish(C, acc);
 }
 
@@ -721,6 +758,23 @@ __device__ __forceinline__ void begin_iteration(const Ctx& C, Solver& s) {
   s.phase = PH_GEN;
 }
 
+template <bool F>
+__device__ __forceinline__ void cand_batch(const Ctx& C, double t, int g0, double* acc, bool& fin) {
+  double xv[kB], dv[kB], tv[kB];
+  ldb<F>(C, C.x, g0, xv);
+  ldb<F>(C, C.dir, g0, dv);
+  ldb<F>(C, C.tau, g0, tv);
+  double* co = C.cand + (long)g0 * kGS;
+#pragma unroll
+  for (int jj = 0; jj < kB; ++jj) {
+    if (!gok<F>(C, g0 + jj)) continue;
+    const double cv = xv[jj] + t * dv[jj];
+    co[jj * kGS] = cv;
+    fin = fin && isfinite(cv);
+    acc[jj & 3] = fma(tv[jj], cv, acc[jj & 3]);
+  }
+}
+
 // next finite candidate x + t dir of the backtracking line search, with
 // tau . cand for its objective value
 __device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
@@ -728,21 +782,9 @@ __device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
     const double t = s.t;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     bool fin = true;
-    for (int g0 = 0; g0 < C.n8; g0 += kB) {
-      double xv[kB], dv[kB], tv[kB];
-      ldb<kB>(C, C.x, g0, xv);
-      ldb<kB>(C, C.dir, g0, dv);
-      ldb<kB>(C, C.tau, g0, tv);
-#pragma unroll
-      for (int jj = 0; jj < kB; ++jj) {
-        const int g = g0 + jj;
-        if (!elem_ok(C, g)) continue;
-        const double cv = xv[jj] + t * dv[jj];
-        C.cand[(long)g * kGS] = cv;
-        fin = fin && isfinite(cv);
-        acc[jj & 3] = fma(tv[jj], cv, acc[jj & 3]);
-      }
-    }
+    int g0 = 0;
+    for (; g0 + kB <= C.nf; g0 += kB) cand_batch<true>(C, t, g0, acc, fin);
+    for (; g0 < C.n8; g0 += kB) cand_batch<false>(C, t, g0, acc, fin);
     const double tdx = dot_finish(C, acc);
     if (__all_sync(C.em, fin)) {
       s.tdx = tdx;
@@ -758,6 +800,31 @@ __device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
   s.phase = PH_DONE;
 }
 
+template <bool F>
+__device__ __forceinline__ void acc_batch(const Ctx& C, double t, double* sv, double* yv, int g0, double* acc, double& gm,
+                                          double& xm) {
+  double dv[kB], ev[kB], gv[kB], cv[kB];
+  ldb<F>(C, C.dir, g0, dv);
+  ldb<F>(C, C.evg, g0, ev);
+  ldb<F>(C, C.g, g0, gv);
+  ldb<F>(C, C.cand, g0, cv);
+  const long o0 = (long)g0 * kGS;
+#pragma unroll
+  for (int jj = 0; jj < kB; ++jj) {
+    if (!gok<F>(C, g0 + jj)) continue;
+    const long o = o0 + jj * kGS;
+    const double sj = t * dv[jj];
+    const double yj = ev[jj] - gv[jj];
+    sv[o] = sj;
+    yv[o] = yj;
+    C.x[o] = cv[jj];
+    C.g[o] = ev[jj];
+    acc[jj & 3] = fma(sj, yj, acc[jj & 3]);
+    gm = fmax(gm, fabs(ev[jj]));
+    xm = fmax(xm, fabs(cv[jj]));
+  }
+}
+
 // accepted step (optim.cpp:176-205) in one pass: s = t dir, y = evg - g,
 // s . y, x = cand, g = evg, and the norms of the new iterate
 __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
@@ -768,28 +835,9 @@ __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
   const double t = s.t;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   double gm = 0.0, xm = 0.0;
-  for (int g0 = 0; g0 < C.n8; g0 += kB) {
-    double dv[kB], ev[kB], gv[kB], cv[kB];
-    ldb<kB>(C, C.dir, g0, dv);
-    ldb<kB>(C, C.evg, g0, ev);
-    ldb<kB>(C, C.g, g0, gv);
-    ldb<kB>(C, C.cand, g0, cv);
-#pragma unroll
-    for (int jj = 0; jj < kB; ++jj) {
-      const int g = g0 + jj;
-      if (!elem_ok(C, g)) continue;
-      const long o = (long)g * kGS;
-      const double sj = t * dv[jj];
-      const double yj = ev[jj] - gv[jj];
-      sv[o] = sj;
-      yv[o] = yj;
-      C.x[o] = cv[jj];
-      C.g[o] = ev[jj];
-      acc[jj & 3] = fma(sj, yj, acc[jj & 3]);
-      gm = fmax(gm, fabs(ev[jj]));
-      xm = fmax(xm, fabs(cv[jj]));
-    }
-  }
+  int g0 = 0;
+  for (; g0 + kB <= C.nf; g0 += kB) acc_batch<true>(C, t, sv, yv, g0, acc, gm, xm);
+  for (; g0 < C.n8; g0 += kB) acc_batch<false>(C, t, sv, yv, g0, acc, gm, xm);
   const double sy = dot_finish(C, acc);
   s.ginf = emax(C, gm);
   s.xinf = emax(C, xm);
@@ -821,6 +869,7 @@ __device__ __forceinline__ Ctx make_ctx(const DModel& m, const DForces& f, const
   C.N = m.N;
   C.n = m.n;
   C.n8 = (m.n + 7) >> 3;
+  C.nf = m.n >> 3;
   C.n4q = (m.n + 3) >> 2;
   C.e = lane >> 3;
   C.j = lane & 7;
