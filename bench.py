@@ -39,6 +39,9 @@ CONFIGS = {
                desc="C2: 1024 x 50-link single-hinge chains, L-BFGS, dt=0.033"),
     "C3": dict(scene="chain", links=100, dt=0.1, batch=4096, opt="lbfgs", seed=1, lo=-0.3, hi=0.3,
                desc="C3: 4096 x 200-DOF serial hinge chains (make_chain_scene(100)), L-BFGS, dt=0.1"),
+    "C3LM": dict(scene="chain", links=100, dt=0.1, batch=4096, opt="lm", seed=1, lo=-0.3, hi=0.3,
+                 desc="C3-LM: 4096 x 200-DOF serial hinge chains (make_chain_scene(100)), LM (Gauss-Newton + "
+                      "Cholesky; the C3 'LM as variant' of SURVEY 8(d)), dt=0.1"),
     "C4": dict(scene="humanoid", links=18, dt=0.01, batch=4096, opt="lm", seed=2, lo=-0.1, hi=0.1,
                desc="C4: 4096 x 41-DOF humanoid trees, LM (Gauss-Newton + Cholesky), dt=0.01"),
     "C4b": dict(scene="humanoid_contact", links=18, dt=0.01, batch=4096, opt="lm", seed=2, lo=-0.1, hi=0.1,

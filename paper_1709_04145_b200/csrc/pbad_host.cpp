@@ -705,6 +705,19 @@ bool resid_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
   return resid_eligible_sizes(m.N, sim->order - 1);
 }
 
+// ... and the energy form with LM on hinge trees the warp-per-environment tree
+// kernel cannot hold (n > 96 or its shared-memory footprint): the same CTA per
+// environment, u = 1 (pbad_resid.cu "energy form")
+bool resid_energy_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
+  if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
+  if (sim->objective != PBAD_ENERGY_FORM || sim->order != 2 || sim->opt.kind != PBAD_LM) return false;
+  if (f->drag_d > 0.0) return false;
+  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
+  for (int i = 0; i < m.N; ++i)
+    if (m.kind[i] != PBAD_HINGE) return false;
+  return resid_eligible_sizes(m.N, 1);
+}
+
 // Host-side structure of the tree kernel: depth levels, children in
 // descending index (the reference's accumulation order, adjoint.cpp:54-62),
 // ancestor table and the GN task list (adjoint.cpp:132-176 loop nest).
@@ -1029,7 +1042,10 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     c->chain7 = s33;
     c->chain6 = !s33;
   }
-  c->tree = !c->chain && tree_eligible(m, f, sim);
+  // PBAD_GPU_RESID_ENERGY: energy-form LM on the CTA kernel even where the
+  // tree kernel fits (tests compare the two)
+  c->tree = !c->chain && tree_eligible(m, f, sim) &&
+            !(std::getenv("PBAD_GPU_RESID_ENERGY") && resid_energy_eligible(m, f, sim));
   if (c->tree) {
     const TreeHost th = make_tree_host(m);
     TreeDesc& td = c->td;
@@ -1093,7 +1109,7 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     delete c;
     return fail(PBAD_E_CUDA, "cudaMalloc failed (workspace %.1f MB)", per_env * 8.0 * max_batch / 1e6);
   }
-  c->resid = !c->chain && !c->tree && resid_eligible(m, f, sim);
+  c->resid = !c->chain && !c->tree && (resid_eligible(m, f, sim) || resid_energy_eligible(m, f, sim));
   if (c->resid) {
     const TreeHost th = make_tree_host(m);
     ResidDesc& rd = c->rd;
@@ -1124,8 +1140,9 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     rd.oJ = take(U * U);
     rd.oGN = take(U * U);
     rd.oDM = take(U * U);
-    rd.oFH = take(u * n * n);
-    rd.oPH = take(u * n * n);
+    const bool energy = sim->objective == PBAD_ENERGY_FORM;  // no functional_hess blocks
+    rd.oFH = take(energy ? 0 : u * n * n);
+    rd.oPH = take(energy ? 0 : u * n * n);
     rd.oPass = take(u * rd.pstride);
     rd.oHW0 = take(16 * N);
     rd.oHW1 = take(16 * N);

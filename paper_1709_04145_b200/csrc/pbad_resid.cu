@@ -161,6 +161,8 @@ struct R {
   const ResidDesc* rd;
   int tid, N, n, u, U, D, K1;
   bool grav;
+  bool energy;    // energy form (K = 2, u = 1): the large-n Newton path of the energy objective
+  double histc;   // energy form: hist_const (objective.cpp:178-184)
   double inv_dt2;
   double *J, *GN, *DM, *FH, *PH, *pass, *hw0, *hw1, *HA, *FA, *seeds, *cot, *x, *grad, *cand, *res, *pg, *tau,
       *step;
@@ -285,6 +287,8 @@ __device__ void stage_vl(const R& r, double* Vs, double* Ls) {
   }
 }
 
+__device__ __noinline__ void adjoint_sweeps(const R& r);
+
 // residuals g_m (objective.cpp:281-308) of the configuration whose passes are
 // current; returns value = sum_m |g_m|^2 (objective.cpp:323-324).  Leaves the
 // adjoint sums a of every sweep in fa(sw, 0) for functional_hess.
@@ -304,8 +308,32 @@ __device__ __noinline__ double residual(const R& r) {
     stm4(r.seeds + (long)mm * 16 * N + 16 * i, mul(scale(r.inv_dt2, acc), ldgm4(m.S + 16 * i)));
   }
   __syncthreads();
-  // functional_grad (adjoint.cpp:49-64) of the u inertial seeds and the u
-  // gravity cotangent sweeps, level-synchronous from the leaves
+  adjoint_sweeps(r);
+  for (int t = r.tid; t < r.U; t += NT) r.res[t] = r.res[t] + ((r.grav ? r.pg[t] : 0.0) - r.tau[t]);
+  __syncthreads();
+  // value: sum over instants of vdot32(g_m, g_m), warp mm computes instant mm
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  if (warp < u) {
+    double p = 0.0;
+    for (int i = lane; i < n; i += 32) p = fma(r.res[warp * n + i], r.res[warp * n + i], p);
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) p = p + __shfl_xor_sync(FULL, p, s);
+    if (lane == 0) rss.scal[warp] = p;
+  }
+  __syncthreads();
+  double v = 0.0;
+  for (int mm = 0; mm < u; ++mm) v += rss.scal[mm];
+  __syncthreads();
+  return v;
+}
+
+// functional_grad (adjoint.cpp:49-64) of the u inertial seeds (r.seeds) and
+// the u gravity cotangent sweeps, level-synchronous from the leaves: the
+// inertial sums into r.res, the gravity sums into r.pg, the adjoints a of
+// every sweep into fa(sw, 0)
+__device__ __noinline__ void adjoint_sweeps(const R& r) {
+  const ResidDesc& rd = *r.rd;
+  const int N = r.N, n = r.n, u = r.u;
   const int nsw = r.grav ? 2 * u : u;
   const long NS = (long)SMS * N;
   double* Xs = rsm;                  // children contributions [2u][N][16]
@@ -332,22 +360,117 @@ __device__ __noinline__ double residual(const R& r) {
     }
     __syncthreads();
   }
-  for (int t = r.tid; t < r.U; t += NT) r.res[t] = r.res[t] + ((r.grav ? r.pg[t] : 0.0) - r.tau[t]);
-  __syncthreads();
-  // value: sum over instants of vdot32(g_m, g_m), warp mm computes instant mm
-  const int warp = r.tid >> 5, lane = r.tid & 31;
-  if (warp < u) {
-    double p = 0.0;
-    for (int i = lane; i < n; i += 32) p = fma(r.res[warp * n + i], r.res[warp * n + i], p);
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) p = p + __shfl_xor_sync(FULL, p, s);
-    if (lane == 0) rss.scal[warp] = p;
+}
+
+// ---- energy form (objective.cpp:162-256), K = 2 (u = 1) --------------------
+// The large-n Newton path of the energy objective on this kernel's CTA: the
+// value from per-link correlation terms summed link by link by one thread
+// (correlation_value's loop, adjoint.cpp:113-120), the gradient from the
+// shared adjoint sweeps, the Gauss-Newton matrix from the hess_ab walks of
+// jacobian() (pair (0, 0), scale inv_dt2) symmetrised like the reference.
+
+// hist_const = 4 cv(A, A) + cv(H, H) - 4 cv(A, H), A = FK(hist1), H = FK(hist0)
+// (objective.cpp:178-184); hw0/hw1 are current
+__device__ __noinline__ double energy_hist_const(const R& r) {
+  const DModel& m = *r.m;
+  const int N = r.N;
+  double* tt = rsm;  // [N][3]
+  for (int i = r.tid; i < N; i += NT) {
+    const M4 S = ldgm4(m.S + 16 * i);
+    const M4 A = ldm4(r.hw1 + 16 * i), H = ldm4(r.hw0 + 16 * i);
+    const M4 AS = mul(A, S);
+    tt[3 * i] = ddot(AS, A);
+    tt[3 * i + 1] = ddot(mul(H, S), H);
+    tt[3 * i + 2] = ddot(AS, H);
   }
   __syncthreads();
-  double v = 0.0;
-  for (int mm = 0; mm < u; ++mm) v += rss.scal[mm];
+  if (r.tid == 0) {
+    double aa = 0.0, hh = 0.0, ah = 0.0;
+    for (int i = 0; i < N; ++i) {
+      aa += tt[3 * i];
+      hh += tt[3 * i + 1];
+      ah += tt[3 * i + 2];
+    }
+    const double wm = m.weighted_mass;
+    rss.scal[0] = 4.0 * (aa - wm) + (hh - wm) - 4.0 * (ah - wm);
+  }
+  __syncthreads();
+  const double hc = rss.scal[0];
+  __syncthreads();
+  return hc;
+}
+
+// StepObjective::value at xs (objective.cpp:215-239) from its current pass
+__device__ __noinline__ double energy_value(const R& r, const double* xs) {
+  const DModel& m = *r.m;
+  const DForces& f = *r.f;
+  const int N = r.N, n = r.n;
+  double* tt = rsm;  // [N][4]
+  for (int i = r.tid; i < N; i += NT) {
+    const M4 S = ldgm4(m.S + 16 * i);
+    const M4 T = ldm4(r.wld(0) + 16 * i);
+    tt[4 * i] = ddot(mul(T, S), T);                            // cv(pass, pass)
+    tt[4 * i + 1] = ddot(mul(ldm4(r.hw1 + 16 * i), S), T);     // cv(prev1, pass)
+    tt[4 * i + 2] = ddot(mul(ldm4(r.hw0 + 16 * i), S), T);     // cv(prev2, pass)
+    tt[4 * i + 3] = r.grav ? ddot(gravity_cot(f, S), T) : 0.0;  // gravity (objective.cpp:48-58)
+  }
+  // tau . x: the 32-partial dot (numeric contract) in warp 0
+  if (r.tid < 32) {
+    double p = 0.0;
+    for (int i = r.tid; i < n; i += 32) p = fma(r.tau[i], xs[i], p);
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) p = p + __shfl_xor_sync(FULL, p, s);
+    if (r.tid == 0) rss.scal[1] = p;
+  }
+  __syncthreads();
+  if (r.tid == 0) {
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, pv = 0.0;
+    for (int i = 0; i < N; ++i) {
+      c0 += tt[4 * i];
+      c1 += tt[4 * i + 1];
+      c2 += tt[4 * i + 2];
+    }
+    if (r.grav)
+      for (int i = 0; i < N; ++i) pv += tt[4 * i + 3];
+    const double wm = m.weighted_mass;
+    const double inertial = 0.5 * r.inv_dt2 * ((c0 - wm) - 4.0 * (c1 - wm) + 2.0 * (c2 - wm) + r.histc);
+    rss.scal[0] = inertial + pv - rss.scal[1];
+  }
+  __syncthreads();
+  const double v = rss.scal[0];
   __syncthreads();
   return v;
+}
+
+// gradient (objective.cpp:241-250): functional_grad of the seeds
+// inv_dt2 (T - 2 A + H) S plus the gravity potential's, minus tau
+__device__ __noinline__ void energy_grad(const R& r) {
+  const DModel& m = *r.m;
+  const int N = r.N;
+  for (int i = r.tid; i < N; i += NT) {
+    const M4 T = ldm4(r.wld(0) + 16 * i);
+    const M4 d = add(sub(T, scale(2.0, ldm4(r.hw1 + 16 * i))), ldm4(r.hw0 + 16 * i));
+    stm4(r.seeds + 16 * i, mul(scale(r.inv_dt2, d), ldgm4(m.S + 16 * i)));
+  }
+  __syncthreads();
+  adjoint_sweeps(r);
+  for (int t = r.tid; t < r.n; t += NT) r.grad[t] = (r.res[t] + (r.grav ? r.pg[t] : 0.0)) - r.tau[t];
+  __syncthreads();
+}
+
+// gn_matrix = 0.5 (gn + gn^T), gn = inv_dt2 ab + pot.gn (pot.gn = 0 without
+// drag / contact; objective.cpp:251-254), lower triangle into r.GN; jacobian()
+// left J(l, i) = inv_dt2 ab(i, l)
+__device__ __noinline__ void energy_gn(const R& r) {
+  const int U = r.U;
+  for (long t = r.tid; t < (long)U * U; t += NT) {
+    const int b = (int)(t / U), a = (int)(t - (long)b * U);
+    if (a >= b) {
+      const double g_ab = r.J[b + (long)U * a] + 0.0, g_ba = r.J[a + (long)U * b] + 0.0;
+      r.GN[a + (long)U * b] = 0.5 * (g_ab + g_ba);
+    }
+  }
+  __syncthreads();
 }
 
 // ---- hinge-chain walk steps on the non-zero blocks ---------------------------
@@ -459,10 +582,11 @@ __device__ __noinline__ void jacobian(const R& r) {
   PT_START();
   if (!rd.chain) {
     for (long t = r.tid; t < UU; t += NT) r.J[t] = 0.0;
-    for (long t = r.tid; t < (long)u * n * n; t += NT) {
-      r.FH[t] = 0.0;
-      r.PH[t] = 0.0;
-    }
+    if (!r.energy)
+      for (long t = r.tid; t < (long)u * n * n; t += NT) {
+        r.FH[t] = 0.0;
+        r.PH[t] = 0.0;
+      }
   }
   // pass values / levers of every instant and the composite-inertia
   // contributions Z live in shared memory for the walks below
@@ -503,7 +627,7 @@ __device__ __noinline__ void jacobian(const R& r) {
     const int i = rd.walk_order[t - pr * N];
     const int a = pr / u, b = pr - a * u;  // hess_ab(pass_a, pass_b) feeds J block (row b, col a)
     const double* stb = sc.H2 + r.K1 * (2 + b);
-    const double ca = r.inv_dt2 * stb[2 + a];
+    const double ca = r.energy ? r.inv_dt2 : r.inv_dt2 * stb[2 + a];
     const double* la = Ls + a * NS;
     const double* lb = Ls + b * NS;
     const double* va = Vs + a * NS;
@@ -529,6 +653,7 @@ __device__ __noinline__ void jacobian(const R& r) {
   // the chain walks below read J entries the hess_ab tasks above wrote, from
   // other threads (the two loops map tasks to threads differently)
   __syncthreads();
+  if (r.energy) return;  // energy form: J holds inv_dt2 ab^T, no functional_hess terms
   if (rd.chain) {
     // chains: every entry of a diagonal block is written by exactly one
     // functional_hess task, so the inertial and gravity walks of (instant,
@@ -1803,6 +1928,16 @@ struct Solver {
 
 // full evaluation at r.x: value, residual Jacobian, gradient, GN
 __device__ __noinline__ int full_eval(const R& r, double* value) {
+  if (r.energy) {
+    if (!passes(r, r.x, false)) return TR_NONFINITE_CFG;
+    const double v = energy_value(r, r.x);
+    *value = v;
+    if (!isfinite(v)) return TR_NONFINITE_INIT;
+    energy_grad(r);
+    jacobian(r);
+    energy_gn(r);
+    return 0;
+  }
   PT_START();
   if (!passes(r, r.x, true)) return TR_NONFINITE_CFG;
   const double v = residual(r);
@@ -1851,7 +1986,7 @@ __device__ int lm_iterate(const R& r, Solver& S) {
     __syncthreads();
     if (!passes(r, r.cand, false)) return -1;
     PT_MARK(3);
-    const double tv = residual(r);
+    const double tv = r.energy ? energy_value(r, r.cand) : residual(r);
     PT_MARK(4);
     if (isfinite(tv) && tv < S.value) {
       const double oldv = S.value;
@@ -1861,7 +1996,11 @@ __device__ int lm_iterate(const R& r, Solver& S) {
       // adjoint sums are the trial's (same configuration, same operations),
       // only the second joint derivatives are new
       const double nv = tv;
-      {
+      if (r.energy) {
+        energy_grad(r);
+        jacobian(r);
+        energy_gn(r);
+      } else {
         PT_START();
         passes_d2(r, r.x);
         PT_MARK(5);
@@ -1936,6 +2075,8 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
   r.D = rd.D;
   r.K1 = sc.K1;
   r.grav = f.gravity_nonzero != 0;
+  r.energy = sc.objective == 0;  // PBAD_ENERGY_FORM (include/pbad_gpu.h)
+  r.histc = 0.0;
   const double dt = sc.dt;
   r.inv_dt2 = 1.0 / (dt * dt);
   {
@@ -1997,6 +2138,7 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
   }
   fk_config(r, h0, r.hw0);
   fk_config(r, h1, r.hw1);
+  if (r.energy) r.histc = energy_hist_const(r);
   // gravity cotangents (objective.cpp:48-58), the same at every instant
   if (r.grav)
     for (int i = r.tid; i < N; i += NT) stm4(r.cot + 16 * i, add(m4_zero(), gravity_cot(f, ldgm4(m.S + 16 * i))));
