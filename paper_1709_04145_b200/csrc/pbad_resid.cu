@@ -1997,9 +1997,13 @@ __device__ int lm_iterate(const R& r, Solver& S) {
       // only the second joint derivatives are new
       const double nv = tv;
       if (r.energy) {
+        PT_START();
         energy_grad(r);
+        PT_MARK(7);
         jacobian(r);
+        PT_MARK(6);
         energy_gn(r);
+        PT_MARK(8);
       } else {
         PT_START();
         passes_d2(r, r.x);
