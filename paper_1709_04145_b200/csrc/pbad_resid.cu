@@ -200,6 +200,42 @@ __device__ bool all_finite(const R& r, const double* a, int len) {
   return __syncthreads_and(ok) != 0;
 }
 
+// Serial chain recursions (rd.chain): one 16-lane group per recursion, lane
+// e16 = row + 4 col holding that element of a 4x4, the operand rows/columns
+// gathered by shuffles inside the group.  Every element keeps the contract's
+// product sequence (pbad_math.cuh mul / mul_bt: first product, then fma in
+// ascending k), so the values equal the level-synchronous block version; the
+// chain depth no longer costs a block barrier per link.
+// (the other half-warp may be outside any group: the mask names this group only)
+__device__ __forceinline__ double gsh(double v, int src) {
+  return __shfl_sync(0xFFFFu << (threadIdx.x & 16), v, src, 16);
+}
+// element (ri, cj) of A B, A held by the group (lane ri + 4 k), B(k, cj) = Bm[k + 4 cj]
+__device__ __forceinline__ double g_mul_left(double a_el, const double* Bm, int ri, int cj) {
+  const double a0 = gsh(a_el, ri), a1 = gsh(a_el, ri + 4), a2 = gsh(a_el, ri + 8), a3 = gsh(a_el, ri + 12);
+  double acc = a0 * Bm[4 * cj];
+  acc = fma(a1, Bm[1 + 4 * cj], acc);
+  acc = fma(a2, Bm[2 + 4 * cj], acc);
+  return fma(a3, Bm[3 + 4 * cj], acc);
+}
+// element (ri, cj) of A B^T, A held by the group, B(cj, k) = Bm[cj + 4 k]
+__device__ __forceinline__ double g_mul_bt(double a_el, const double* Bm, int ri, int cj) {
+  const double a0 = gsh(a_el, ri), a1 = gsh(a_el, ri + 4), a2 = gsh(a_el, ri + 8), a3 = gsh(a_el, ri + 12);
+  double acc = a0 * Bm[cj];
+  acc = fma(a1, Bm[cj + 4], acc);
+  acc = fma(a2, Bm[cj + 8], acc);
+  return fma(a3, Bm[cj + 12], acc);
+}
+// element (ri, cj) of A B, A(ri, k) = Am[ri + 4 k] in memory, B held by the group (lane k + 4 cj)
+__device__ __forceinline__ double g_mul_right(const double* Am, double b_el, int ri, int cj) {
+  const double b0 = gsh(b_el, 4 * cj), b1 = gsh(b_el, 1 + 4 * cj), b2 = gsh(b_el, 2 + 4 * cj),
+               b3 = gsh(b_el, 3 + 4 * cj);
+  double acc = Am[ri] * b0;
+  acc = fma(Am[ri + 4], b1, acc);
+  acc = fma(Am[ri + 8], b2, acc);
+  return fma(Am[ri + 12], b3, acc);
+}
+
 // forward_pass (kinematics.cpp:171-181) of one configuration into world
 __device__ __noinline__ void fk_config(const R& r, const double* q, double* world) {
   const DModel& m = *r.m;
@@ -237,16 +273,30 @@ __device__ __noinline__ bool passes(const R& r, const double* xs, bool want_d2) 
     if (want_d2) stm4(r.dd2(mm) + 16 * i, d2);
   }
   __syncthreads();
-  for (int d = 0; d <= r.D; ++d) {
-    const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
-    for (int t = r.tid; t < r.u * cnt; t += NT) {
-      const int mm = t / cnt;
-      const int i = rd.lvl_links[l0 + t - mm * cnt];
-      const int p = rss.parent[i];
-      const M4 v = ldm4(Vs + mm * NS + SMS * i);
-      stm4(Ws + mm * NS + SMS * i, p >= 0 ? mul(ldm4(Ws + mm * NS + SMS * p), v) : v);
+  if (rd.chain) {
+    // W_i = W_{i-1} V_i, group mm = instant mm
+    const int g = r.tid >> 4, e16 = r.tid & 15, ri = e16 & 3, cj = e16 >> 2;
+    if (g < r.u) {
+      double w = 0.0;
+      for (int i = 0; i < N; ++i) {
+        const double* V = Vs + g * NS + SMS * i;
+        w = (i == 0) ? V[e16] : g_mul_left(w, V, ri, cj);
+        Ws[g * NS + SMS * i + e16] = w;
+      }
     }
     __syncthreads();
+  } else {
+    for (int d = 0; d <= r.D; ++d) {
+      const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
+      for (int t = r.tid; t < r.u * cnt; t += NT) {
+        const int mm = t / cnt;
+        const int i = rd.lvl_links[l0 + t - mm * cnt];
+        const int p = rss.parent[i];
+        const M4 v = ldm4(Vs + mm * NS + SMS * i);
+        stm4(Ws + mm * NS + SMS * i, p >= 0 ? mul(ldm4(Ws + mm * NS + SMS * p), v) : v);
+      }
+      __syncthreads();
+    }
   }
   for (int t = r.tid; t < r.u * N; t += NT) {
     const int mm = t / N, i = t - mm * N;
@@ -341,6 +391,34 @@ __device__ __noinline__ void adjoint_sweeps(const R& r) {
   double* Vs = Ls + u * NS;          // values [u][N][16]
   stage_vl(r, Vs, Ls);
   __syncthreads();
+  if (rd.chain) {
+    // a_i = (0 + a_{i+1} V_{i+1}^T) + seed_i from the leaf, group sw = sweep sw;
+    // the adjoints land in fa(sw, 0) and in shared memory (Xs, free here)
+    const int g = r.tid >> 4, e16 = r.tid & 15, ri = e16 & 3, cj = e16 >> 2;
+    if (g < nsw) {
+      const int mm = g < u ? g : g - u;
+      const double* src = g < u ? r.seeds + (long)mm * 16 * N : r.cot;
+      double* fa = r.fa(g, 0);
+      double x = 0.0;  // element of a_{i+1} V_{i+1}^T
+      for (int i = N - 1; i >= 0; --i) {
+        const double adj = (i == N - 1) ? 0.0 : 0.0 + x;
+        const double a = adj + src[16 * i + e16];
+        fa[16 * i + e16] = a;
+        Xs[g * NS + SMS * i + e16] = a;
+        if (i > 0) x = g_mul_bt(a, Vs + mm * NS + SMS * i, ri, cj);
+      }
+    }
+    __syncthreads();
+    for (int t = r.tid; t < nsw * N; t += NT) {
+      const int sw = t / N, i = t - sw * N;
+      const int mm = sw < u ? sw : sw - u;
+      const double gi = 0.0 + ddot(ldm4(Ls + mm * NS + SMS * i), ldm4(Xs + sw * NS + SMS * i));
+      if (sw < u) r.res[mm * n + i] = gi;
+      else r.pg[mm * n + i] = gi;
+    }
+    __syncthreads();
+    return;
+  }
   for (int d = r.D; d >= 0; --d) {
     const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
     for (int t = r.tid; t < nsw * cnt; t += NT) {
@@ -600,6 +678,31 @@ __device__ __noinline__ void jacobian(const R& r) {
   // correlation_hess_ab(pass_a, pass_b) composite inertias for every pair
   // (a = instant l, b = instant mm), pair = a * u + b (adjoint.cpp:139-141,169-174)
   const int npair = u * u;
+  if (rd.chain) {
+    // ai = (0 + Z_{i+1}) + S_i, y = V_b ai, Z_i = y V_a^T from the leaf, group = pair
+    const int g = r.tid >> 4, e16 = r.tid & 15, ri = e16 & 3, cj = e16 >> 2;
+    if (g < npair) {
+      const int a = g / u, b = g - a * u;
+      double* h0 = r.ha(g, 0);
+      double* h1 = r.ha(g, 1);
+      double z = 0.0;
+      for (int i = N - 1; i >= 0; --i) {
+        const double acc = (i == N - 1) ? 0.0 : 0.0 + z;
+        const double ai = acc + __ldg(m.S + 16 * i + e16);
+        h0[16 * i + e16] = ai;
+        const double y = g_mul_right(Vs + b * NS + SMS * i, ai, ri, cj);
+        h1[16 * i + e16] = y;
+        z = g_mul_bt(y, Vs + a * NS + SMS * i, ri, cj);
+      }
+    }
+    __syncthreads();
+    for (int t = r.tid; t < npair * N; t += NT) {
+      const int pr = t / N, i = t - pr * N;
+      const int a = pr / u;
+      stm4(r.ha(pr, 2) + 16 * i, mul_bt(ldm4(r.ha(pr, 0) + 16 * i), ldm4(Vs + a * NS + SMS * i)));
+    }
+    __syncthreads();
+  } else
   for (int d = r.D; d >= 0; --d) {
     const int l0 = rd.lvl_start[d], cnt = rd.lvl_start[d + 1] - l0;
     for (int t = r.tid; t < npair * cnt; t += NT) {
@@ -633,6 +736,43 @@ __device__ __noinline__ void jacobian(const R& r) {
     const double* va = Vs + a * NS;
     const double* vb = Vs + b * NS;
     const long rowb = (long)b * n, cola = (long)a * n;
+    if (rd.chain && !r.energy && a == b) {
+      // chains, diagonal block (mm, mm): every entry of it is one (i, l) of
+      // this walk, so the inertial and gravity functional_hess walks of
+      // (mm, i) (adjoint.cpp:66-101) run here too and the block is finished
+      // in registers, J = (fh + c_m ab^T) + ph, without a second pass over J
+      const int mm = a;
+      const double h = 0.0 + trace_mul(mul_at(ldm4(la + SMS * i), ldm4(lb + SMS * i)), ldm4(r.ha(pr, 0) + 16 * i));
+      const M4 aF = ldm4(r.fa(mm, 0) + 16 * i);
+      const M4 aP = r.grav ? ldm4(r.fa(u + mm, 0) + 16 * i) : m4_zero();
+      const int p = rss.parent[i];
+      const M4 pd = mul(p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity(), ldm4(r.dd2(mm) + 16 * i));
+      {
+        const double hF = 0.0 + ddot(pd, aF);
+        const double hP = r.grav ? 0.0 + ddot(pd, aP) : 0.0;
+        r.J[(rowb + i) + U * (cola + i)] = (hF + ca * h) + hP;
+      }
+      const L3 u_i = ldl3(la + SMS * i);
+      M4 fwd = ldm4(r.ha(pr, 1) + 16 * i);
+      M4 bwd = ldm4(r.ha(pr, 2) + 16 * i);
+      const M4 d1 = ldm4(r.dd1(mm) + 16 * i);
+      M4 wF = mul_bt(aF, d1);
+      M4 wP = mul_bt(aP, d1);
+      for (int l = p; l >= 0; l = rss.parent[l]) {
+        const L3 u_l = ldl3(la + SMS * l);
+        const double t1 = 0.0 + trace_at3(u_i, u_l, fwd);  // H(i, l)
+        const double t2 = 0.0 + trace_at3(u_l, u_i, bwd);  // H(l, i)
+        const double hF = 0.0 + ddot3(u_l, wF);
+        const double hP = r.grav ? 0.0 + ddot3(u_l, wP) : 0.0;
+        r.J[(rowb + l) + U * (cola + i)] = (hF + ca * t1) + hP;
+        r.J[(rowb + i) + U * (cola + l)] = (hF + ca * t2) + hP;
+        fwd_step3(va + SMS * l, fwd);
+        bwd_step3(bwd, va + SMS * l);
+        bwd_step3(wF, va + SMS * l);
+        if (r.grav) bwd_step3(wP, va + SMS * l);
+      }
+      continue;
+    }
     {
       const double h = 0.0 + trace_mul(mul_at(ldm4(la + SMS * i), ldm4(lb + SMS * i)), ldm4(r.ha(pr, 0) + 16 * i));
       r.J[(rowb + i) + U * (cola + i)] = ca * h;
@@ -655,43 +795,8 @@ __device__ __noinline__ void jacobian(const R& r) {
   __syncthreads();
   if (r.energy) return;  // energy form: J holds inv_dt2 ab^T, no functional_hess terms
   if (rd.chain) {
-    // chains: every entry of a diagonal block is written by exactly one
-    // functional_hess task, so the inertial and gravity walks of (instant,
-    // link) run in one task and finish J's diagonal block in place:
-    // J = (fh + J) + ph, the combine of the general path below
-    for (int t = r.tid; t < u * N; t += NT) {
-      const int mm = t / N;
-      const int i = rd.walk_order[t - mm * N];
-      const double* lm = Ls + mm * NS;
-      const double* vm = Vs + mm * NS;
-      const M4 aF = ldm4(r.fa(mm, 0) + 16 * i);
-      const M4 aP = r.grav ? ldm4(r.fa(u + mm, 0) + 16 * i) : m4_zero();
-      const int p = rss.parent[i];
-      const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
-      const M4 pd = mul(pw, ldm4(r.dd2(mm) + 16 * i));
-      const long jb = (long)mm * n + (long)U * ((long)mm * n);  // block (mm, mm)
-      {
-        const double hF = 0.0 + ddot(pd, aF);
-        const double hP = r.grav ? 0.0 + ddot(pd, aP) : 0.0;
-        double* je = r.J + jb + i + (long)U * i;
-        *je = (hF + *je) + hP;
-      }
-      const M4 d1 = ldm4(r.dd1(mm) + 16 * i);
-      M4 wF = mul_bt(aF, d1);
-      M4 wP = mul_bt(aP, d1);
-      for (int l = p; l >= 0; l = rss.parent[l]) {
-        const L3 ll = ldl3(lm + SMS * l);
-        const double hF = 0.0 + ddot3(ll, wF);
-        const double hP = r.grav ? 0.0 + ddot3(ll, wP) : 0.0;
-        double* e1 = r.J + jb + l + (long)U * i;
-        double* e2 = r.J + jb + i + (long)U * l;
-        *e1 = (hF + *e1) + hP;
-        *e2 = (hF + *e2) + hP;
-        bwd_step3(wF, vm + SMS * l);
-        if (r.grav) bwd_step3(wP, vm + SMS * l);
-      }
-    }
-    __syncthreads();
+    // chains: the functional_hess walks ran fused with the diagonal-block
+    // hess_ab walks above
     PT_MARK(16);
   } else {
   // functional_hess (adjoint.cpp:66-101) of the inertial seeds and of the
