@@ -394,17 +394,25 @@ __device__ __noinline__ void adjoint_sweeps(const R& r) {
   if (rd.chain) {
     // a_i = (0 + a_{i+1} V_{i+1}^T) + seed_i from the leaf, group sw = sweep sw;
     // the adjoints land in fa(sw, 0) and in shared memory (Xs, free here)
+    // the seeds / cotangents staged in Xs first: the serial loop then reads
+    // shared memory, not global loads ordered behind its own global stores
+    for (int t = r.tid; t < nsw * N * 16; t += NT) {
+      const int sw = t / (16 * N), k = t - sw * 16 * N;
+      const double* src = sw < u ? r.seeds + (long)sw * 16 * N : r.cot;
+      Xs[sw * NS + SMS * (k >> 4) + (k & 15)] = src[k];
+    }
+    __syncthreads();
     const int g = r.tid >> 4, e16 = r.tid & 15, ri = e16 & 3, cj = e16 >> 2;
     if (g < nsw) {
       const int mm = g < u ? g : g - u;
-      const double* src = g < u ? r.seeds + (long)mm * 16 * N : r.cot;
       double* fa = r.fa(g, 0);
+      double* xg = Xs + g * NS + e16;
       double x = 0.0;  // element of a_{i+1} V_{i+1}^T
       for (int i = N - 1; i >= 0; --i) {
         const double adj = (i == N - 1) ? 0.0 : 0.0 + x;
-        const double a = adj + src[16 * i + e16];
+        const double a = adj + xg[SMS * i];
         fa[16 * i + e16] = a;
-        Xs[g * NS + SMS * i + e16] = a;
+        xg[SMS * i] = a;
         if (i > 0) x = g_mul_bt(a, Vs + mm * NS + SMS * i, ri, cj);
       }
     }
