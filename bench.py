@@ -540,7 +540,7 @@ def main():
         "kernel": {0: "pbad_gpu::k_step (general, thread per env)", 1: "pbad_gpu::k_chain_step (quad per env)",
                    2: "pbad_gpu::c4::k_chain4_step (warp-synchronous quads, TMA-fed adjoint)",
                    3: "pbad_gpu::tree::k_tree_step (warp per env, Newton/LM, in-SMEM Cholesky)",
-                   4: "pbad_gpu::resid::k_resid_step (CTA per env, residual-form LM, tiled J^T J + blocked Cholesky)",
+                   4: "pbad_gpu::resid::k_resid_step (CTA per env, LM: residual form or large-n energy form, DMMA J^T J + blocked Cholesky)",
                    5: "pbad_gpu::c5::k_chain5_step (warp per env, shared-memory-resident L-BFGS, TMA-fed adjoint)",
                    6: "pbad_gpu::c6::k_chain6_step (8 lanes per env: two per transform row, TMA-fed adjoint)",
                    7: "pbad_gpu::c7::k_chain7_step (16 lanes per env: serial FK rows + link-parallel energy terms, TMA-fed adjoint)"
