@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "pbad_chain_ops.cuh"
 #include "pbad_kernels.cuh"
@@ -1001,6 +1002,9 @@ __global__ void __launch_bounds__(kT) k_chain6_step(DModel m, DForces f, DSchedu
   } else {
     s.phase = PH_DONE;
   }
+#ifdef PBAD_C6_STATS
+  int st_eval = 0, st_acc = 0, st_acc0 = 0;
+#endif
   for (;;) {
     if (s.phase == PH_DIR) begin_iteration(C, s);
     if (s.phase == PH_GEN) next_candidate(C, s);
@@ -1019,9 +1023,22 @@ __global__ void __launch_bounds__(kT) k_chain6_step(DModel m, DForces f, DSchedu
       }
     }
     if (__any_sync(0xffffffffu, acc)) reverse<PAT>(C, C.evg);
+#ifdef PBAD_C6_STATS
+    if (eval) {
+      ++st_eval;
+      if (acc) {
+        ++st_acc;
+        if (s.trial == 0) ++st_acc0;
+      }
+    }
+#endif
     if (acc) accept_step(C, s, v);
     __syncwarp();
   }
+#ifdef PBAD_C6_STATS
+  if (C.j == 0 && (C.ge % 512) == 0)
+    printf("env %ld: evals %d accepted %d accepted-at-first-trial %d\n", C.ge, st_eval, st_acc, st_acc0);
+#endif
   if (!active) return;
   // finish_step
   const bool converged = s.status == ST_CONVERGED;
