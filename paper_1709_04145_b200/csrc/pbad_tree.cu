@@ -639,22 +639,36 @@ __device__ __forceinline__ double sel(const double (&v)[MAXV], int s) {
 __device__ TREE_NOINLINE void llt_solve_w(const W& w, double (&v)[MAXV]) {
   const double* A = w.damped;
   const int n = w.n;
+  const int nv = (n + 31) >> 5;  // live register slots (warp-uniform)
+  // forward: column j of the packed factor starts at pidx(n, 0, j)
   for (int j = 0; j < n; ++j) {
-    const double xj = __shfl_sync(FULL, sel(v, j >> 5), j & 31) / A[pidx(n, j, j)];
+    const int cs = j * (2 * n - j - 1) / 2;
+    const double xj = __shfl_sync(FULL, sel(v, j >> 5), j & 31) / A[cs + j];
 #pragma unroll
     for (int s = 0; s < MAXV; ++s) {
-      const int i = w.lane + 32 * s;
-      if (i == j) v[s] = xj;
-      else if (i > j && i < n) v[s] = fma(-A[pidx(n, i, j)], xj, v[s]);
+      if (s < nv) {
+        const int i = w.lane + 32 * s;
+        if (i == j) v[s] = xj;
+        else if (i > j && i < n) v[s] = fma(-A[cs + i], xj, v[s]);
+      }
     }
+  }
+  // backward: L(j, i) of this lane's rows i = lane + 32 s lies in column i
+  int ci[MAXV];
+#pragma unroll
+  for (int s = 0; s < MAXV; ++s) {
+    const int i = w.lane + 32 * s;
+    ci[s] = i * (2 * n - i - 1) / 2;
   }
   for (int j = n - 1; j >= 0; --j) {
     const double xj = __shfl_sync(FULL, sel(v, j >> 5), j & 31) / A[pidx(n, j, j)];
 #pragma unroll
     for (int s = 0; s < MAXV; ++s) {
-      const int i = w.lane + 32 * s;
-      if (i == j) v[s] = xj;
-      else if (i < j) v[s] = fma(-A[pidx(n, j, i)], xj, v[s]);
+      if (s < nv) {
+        const int i = w.lane + 32 * s;
+        if (i == j) v[s] = xj;
+        else if (i < j) v[s] = fma(-A[ci[s] + j], xj, v[s]);
+      }
     }
   }
 }
