@@ -51,6 +51,10 @@ constexpr int kRing = 3;  // reverse ring slots
 constexpr int kRecMass = 20;  // per-link record doubles: cs | lev[3][2] | seed[3][4] (massless links: 8)
 constexpr int kMaxMem = 32;
 constexpr int kHistW = 6;  // hist record per link: c0 s0 | c1 s1 | cx sx
+#ifndef PBAD_C5_UNROLL
+#define PBAD_C5_UNROLL 4
+#endif
+constexpr int kUnroll = PBAD_C5_UNROLL;  // forward links unrolled per loop trip (single-kind chains)
 
 // per-warp shared-memory layout (doubles); n2 = n rounded up to even
 struct WarpLayout {
@@ -278,9 +282,20 @@ __device__ double forward(W& w, const double* X, double tdx) {
       *reinterpret_cast<double2*>(w.rec + w.roff[i]) = make_double2(c, s);
     }
     __syncwarp();
-    for (int j = 0; j < cnt; ++j) {
-      fwd_any<PAT>(w, j, lo + j, R, sum, par);
-      par ^= (w.kind[lo + j] >> 2);
+    if constexpr ((PAT & 3) == 1) {
+      // one link kind: the massive flag is a compile-time constant; unrolled so
+      // consecutive links' independent work can overlap
+      constexpr int PK = ((PAT >> 2) & 7) >> 2;
+#pragma unroll kUnroll
+      for (int j = 0; j < cnt; ++j) {
+        fwd_any<PAT>(w, j, lo + j, R, sum, par);
+        par ^= PK;
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        fwd_any<PAT>(w, j, lo + j, R, sum, par);
+        par ^= (w.kind[lo + j] >> 2);
+      }
     }
   }
   const double sa = __shfl_sync(0xffffffffu, sum, 0), sb = __shfl_sync(0xffffffffu, sum, 4);
