@@ -797,7 +797,10 @@ __device__ TREE_COLD void store_history(const W& w, double* hw, double* T) {
 
 #ifndef PBAD_TREE_LBFGS_TU
 template <bool POT>
-__global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel m, const __grid_constant__ DForces f,
+#ifndef PBAD_TREE_MINB
+#define PBAD_TREE_MINB 11  // 168 registers: 12 single-warp blocks per SM by registers, ~10 by shared memory
+#endif
+__global__ void __launch_bounds__(32, PBAD_TREE_MINB) k_tree_step(const __grid_constant__ DModel m, const __grid_constant__ DForces f,
                                                   const __grid_constant__ DSchedule sc, const __grid_constant__ Layout L,
                                                   double* ws, int* iws, long B, const __grid_constant__ TreeDesc td,
                                                   double* tws, const __grid_constant__ Outputs out) {
@@ -828,9 +831,13 @@ __global__ void __launch_bounds__(32) k_tree_step(const __grid_constant__ DModel
     double* p = smem;
     w.value = p; p += N16;
     w.world = p; p += N16;
-    w.lever = p; p += MS * td.n;
-    w.scr = p; p += scr;
-    w.damped = p; p += (td.np + 1) & ~1;
+    // the damped matrix is live only from its rebuild to the end of the
+    // solve, the levers and the link scratch only inside the derivatives
+    // (fk_levers, gradient, GN assembly): one region serves both
+    w.lever = p;
+    w.scr = p + MS * td.n;
+    w.damped = p;
+    p += (MS * td.n + scr) > ((td.np + 1) & ~1) ? (MS * td.n + scr) : ((td.np + 1) & ~1);
     w.x = p; p += nv;
     w.grad = p; p += nv;
     w.cand = p; p += nv;
@@ -1112,9 +1119,13 @@ __global__ void __launch_bounds__(32) k_tree_lbfgs(const __grid_constant__ DMode
     double* p = smem;
     w.value = p; p += N16;
     w.world = p; p += N16;
-    w.lever = p; p += MS * td.n;
-    w.scr = p; p += scr;
-    w.damped = p; p += (td.np + 1) & ~1;
+    // the damped matrix is live only from its rebuild to the end of the
+    // solve, the levers and the link scratch only inside the derivatives
+    // (fk_levers, gradient, GN assembly): one region serves both
+    w.lever = p;
+    w.scr = p + MS * td.n;
+    w.damped = p;
+    p += (MS * td.n + scr) > ((td.np + 1) & ~1) ? (MS * td.n + scr) : ((td.np + 1) & ~1);
     w.x = p; p += nv;
     w.grad = p; p += nv;
     w.cand = p; p += nv;
@@ -1403,7 +1414,9 @@ bool tree_eligible_sizes(int N, int n) { return N >= 1 && N <= 255 && n >= 1 && 
 static int tree_smem_doubles(const TreeDesc& td) {
   const int N16 = tree::MS * td.N, nv = (td.n + 1) & ~1;
   const int scr = (tree::TREE_SCR_ARRAYS * N16 > tree::MS * td.n) ? tree::TREE_SCR_ARRAYS * N16 : tree::MS * td.n;
-  return 2 * N16 + tree::MS * td.n + scr + ((td.np + 1) & ~1) + 8 * nv + 5 * td.N + 32 + ((td.ns + 1) & ~1) +
+  const int np2 = (td.np + 1) & ~1, ls = tree::MS * td.n + scr;
+  // dof vectors: x, grad, cand, vtau, vtmp (+ q2, dir, evg for L-BFGS)
+  return 2 * N16 + (ls > np2 ? ls : np2) + (td.lb ? 8 : 5) * nv + 5 * td.N + 32 + ((td.ns + 1) & ~1) +
          4 * td.ns + td.ns + 2;  // cact + clist ints
 }
 
