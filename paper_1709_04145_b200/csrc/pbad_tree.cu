@@ -63,7 +63,10 @@ namespace PBAD_TREE_NS {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int MAXV = 3;  // dof vectors in registers: n <= 96
 constexpr int MAXN = 96;
-constexpr int MS = 18;
+#ifndef PBAD_TREE_MS
+#define PBAD_TREE_MS 18
+#endif
+constexpr int MS = PBAD_TREE_MS;
 constexpr int TREE_SCR_ARRAYS = PBAD_TREE_GN_GLOBAL ? 2 : 4;  // link scratch arrays in SMEM  // shared-memory stride of a 4x4 (16 + 2 pad: conflict-free lane-per-link double2 access)
 enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_FAILED = 2 };
 enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3, TR_RUNNING = 4 };
@@ -837,13 +840,20 @@ __global__ void __launch_bounds__(32, PBAD_TREE_MINB) k_tree_step(const __grid_c
     w.lever = p;
     w.scr = p + MS * td.n;
     w.damped = p;
-    p += (MS * td.n + scr) > ((td.np + 1) & ~1) ? (MS * td.n + scr) : ((td.np + 1) & ~1);
+    // the per-link value terms (value_at, hist_const, the energy audit) are
+    // consumed before the derivatives run and after the solve: same region
+    w.red = p;
+    {
+      int rs = MS * td.n + scr;
+      if (((td.np + 1) & ~1) > rs) rs = (td.np + 1) & ~1;
+      if (5 * td.N + 32 > rs) rs = 5 * td.N + 32;
+      p += rs;
+    }
     w.x = p; p += nv;
     w.grad = p; p += nv;
     w.cand = p; p += nv;
     w.vtau = p; p += nv;
     w.vtmp = p; p += nv;
-    w.red = p; p += 5 * td.N + 32;
     w.ctv = p; p += (td.ns + 1) & ~1;
     w.cdep = p; p += 4 * td.ns;
     w.cact = reinterpret_cast<int*>(p);
@@ -1414,9 +1424,12 @@ bool tree_eligible_sizes(int N, int n) { return N >= 1 && N <= 255 && n >= 1 && 
 static int tree_smem_doubles(const TreeDesc& td) {
   const int N16 = tree::MS * td.N, nv = (td.n + 1) & ~1;
   const int scr = (tree::TREE_SCR_ARRAYS * N16 > tree::MS * td.n) ? tree::TREE_SCR_ARRAYS * N16 : tree::MS * td.n;
-  const int np2 = (td.np + 1) & ~1, ls = tree::MS * td.n + scr;
-  // dof vectors: x, grad, cand, vtau, vtmp (+ q2, dir, evg for L-BFGS)
-  return 2 * N16 + (ls > np2 ? ls : np2) + (td.lb ? 8 : 5) * nv + 5 * td.N + 32 + ((td.ns + 1) & ~1) +
+  const int np2 = (td.np + 1) & ~1, ls = tree::MS * td.n + scr, rd = 5 * td.N + 32;
+  // one region for the damped matrix, the levers + link scratch and (LM) the
+  // value terms; dof vectors x, grad, cand, vtau, vtmp (+ q2, dir, evg for L-BFGS)
+  int region = ls > np2 ? ls : np2;
+  if (!td.lb && rd > region) region = rd;
+  return 2 * N16 + region + (td.lb ? 8 * nv + rd : 5 * nv) + ((td.ns + 1) & ~1) +
          4 * td.ns + td.ns + 2;  // cact + clist ints
 }
 
