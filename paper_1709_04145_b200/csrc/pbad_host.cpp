@@ -698,7 +698,11 @@ bool resid_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_RESIDUAL_FORM || sim->opt.kind != PBAD_LM) return false;
   if (sim->order < 2 || sim->order - 1 > 8) return false;
-  if (f->drag_d > 0.0) return false;
+  if (f->drag_d > 0.0) {
+    // drag: serial chains (its pot.hess term joins the fused diagonal-block walks)
+    for (int i = 0; i < m.N; ++i)
+      if (m.parent[i] != i - 1) return false;
+  }
   if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
   for (int i = 0; i < m.N; ++i)
     if (m.kind[i] != PBAD_HINGE) return false;
@@ -1149,7 +1153,7 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     rd.oHA = take(u * u * 4 * 16 * N);
     rd.oFA = take(2 * u * 2 * 16 * N);
     rd.oSeeds = take(u * 16 * N);
-    rd.oCot = take(16 * N);
+    rd.oCot = take((f->drag_d > 0.0 ? u : 1) * 16 * N);  // per-instant cotangents with drag
     rd.oX = take(U);
     rd.oGrad = take(U);
     rd.oCand = take(std::max(U, 2 * n));

@@ -161,6 +161,9 @@ struct R {
   const ResidDesc* rd;
   int tid, N, n, u, U, D, K1;
   bool grav;
+  bool drag;      // residual form with drag (chains): per-instant cotangents, pot.hess adds 2 scale ab
+  bool have_cot;  // potential cotangents exist (gravity or drag: PotentialEval::have_cot)
+  double s2[8];   // drag: 2 D / (t_m dt)^2 per unknown instant (objective.cpp:62-68)
   bool energy;    // energy form (K = 2, u = 1): the large-n Newton path of the energy objective
   double histc;   // energy form: hist_const (objective.cpp:178-184)
   double inv_dt2;
@@ -356,10 +359,18 @@ __device__ __noinline__ double residual(const R& r) {
       addto(acc, scale(st[j], ldm4(W + 16 * i)));
     }
     stm4(r.seeds + (long)mm * 16 * N + 16 * i, mul(scale(r.inv_dt2, acc), ldgm4(m.S + 16 * i)));
+    if (r.drag) {
+      // potential_terms' cotangents at instant mm (objective.cpp:45-68):
+      // cot = (0 + gravity) + (2 D / (t_m dt)^2) (T_m - T_hist1) S
+      const M4 S = ldgm4(m.S + 16 * i);
+      const M4 base = r.grav ? add(m4_zero(), gravity_cot(*r.f, S)) : m4_zero();
+      const M4 diff_s = mul(sub(ldm4(r.wld(mm) + 16 * i), ldm4(r.hw1 + 16 * i)), S);
+      stm4(r.cot + (long)mm * 16 * N + 16 * i, add(base, scale(r.s2[mm], diff_s)));
+    }
   }
   __syncthreads();
   adjoint_sweeps(r);
-  for (int t = r.tid; t < r.U; t += NT) r.res[t] = r.res[t] + ((r.grav ? r.pg[t] : 0.0) - r.tau[t]);
+  for (int t = r.tid; t < r.U; t += NT) r.res[t] = r.res[t] + ((r.have_cot ? r.pg[t] : 0.0) - r.tau[t]);
   __syncthreads();
   // value: sum over instants of vdot32(g_m, g_m), warp mm computes instant mm
   const int warp = r.tid >> 5, lane = r.tid & 31;
@@ -384,7 +395,7 @@ __device__ __noinline__ double residual(const R& r) {
 __device__ __noinline__ void adjoint_sweeps(const R& r) {
   const ResidDesc& rd = *r.rd;
   const int N = r.N, n = r.n, u = r.u;
-  const int nsw = r.grav ? 2 * u : u;
+  const int nsw = r.have_cot ? 2 * u : u;
   const long NS = (long)SMS * N;
   double* Xs = rsm;                  // children contributions [2u][N][16]
   double* Ls = rsm + 2 * u * NS;    // levers [u][N][16]
@@ -398,7 +409,7 @@ __device__ __noinline__ void adjoint_sweeps(const R& r) {
     // shared memory, not global loads ordered behind its own global stores
     for (int t = r.tid; t < nsw * N * 16; t += NT) {
       const int sw = t / (16 * N), k = t - sw * 16 * N;
-      const double* src = sw < u ? r.seeds + (long)sw * 16 * N : r.cot;
+      const double* src = sw < u ? r.seeds + (long)sw * 16 * N : r.cot + (r.drag ? (long)(sw - u) * 16 * N : 0L);
       Xs[sw * NS + SMS * (k >> 4) + (k & 15)] = src[k];
     }
     __syncthreads();
@@ -433,7 +444,7 @@ __device__ __noinline__ void adjoint_sweeps(const R& r) {
       const int sw = t / cnt;
       const int i = rd.lvl_links[l0 + t - sw * cnt];
       const int mm = sw < u ? sw : sw - u;
-      const double* src = sw < u ? r.seeds + (long)mm * 16 * N : r.cot;
+      const double* src = sw < u ? r.seeds + (long)mm * 16 * N : r.cot + (r.drag ? (long)mm * 16 * N : 0L);
       double* X = Xs + sw * NS;
       M4 adj = m4_zero();
       for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) adj = add(adj, ldm4(X + SMS * rd.ch_list[c]));
@@ -752,12 +763,16 @@ __device__ __noinline__ void jacobian(const R& r) {
       const int mm = a;
       const double h = 0.0 + trace_mul(mul_at(ldm4(la + SMS * i), ldm4(lb + SMS * i)), ldm4(r.ha(pr, 0) + 16 * i));
       const M4 aF = ldm4(r.fa(mm, 0) + 16 * i);
-      const M4 aP = r.grav ? ldm4(r.fa(u + mm, 0) + 16 * i) : m4_zero();
+      const M4 aP = r.have_cot ? ldm4(r.fa(u + mm, 0) + 16 * i) : m4_zero();
       const int p = rss.parent[i];
       const M4 pd = mul(p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity(), ldm4(r.dd2(mm) + 16 * i));
+      // pot.hess = (0 + 2 scale ab) + functional_hess(cot) with drag
+      // (objective.cpp:70-71,131-134), functional_hess(cot) otherwise
+      const double s2 = r.drag ? r.s2[mm] : 0.0;
       {
         const double hF = 0.0 + ddot(pd, aF);
-        const double hP = r.grav ? 0.0 + ddot(pd, aP) : 0.0;
+        double hP = r.have_cot ? 0.0 + ddot(pd, aP) : 0.0;
+        if (r.drag) hP = (0.0 + s2 * h) + hP;
         r.J[(rowb + i) + U * (cola + i)] = (hF + ca * h) + hP;
       }
       const L3 u_i = ldl3(la + SMS * i);
@@ -771,13 +786,16 @@ __device__ __noinline__ void jacobian(const R& r) {
         const double t1 = 0.0 + trace_at3(u_i, u_l, fwd);  // H(i, l)
         const double t2 = 0.0 + trace_at3(u_l, u_i, bwd);  // H(l, i)
         const double hF = 0.0 + ddot3(u_l, wF);
-        const double hP = r.grav ? 0.0 + ddot3(u_l, wP) : 0.0;
-        r.J[(rowb + l) + U * (cola + i)] = (hF + ca * t1) + hP;
-        r.J[(rowb + i) + U * (cola + l)] = (hF + ca * t2) + hP;
+        const double hP = r.have_cot ? 0.0 + ddot3(u_l, wP) : 0.0;
+        // J(l, i) takes pot.hess(l, i) = ... ab(l, i) = t2, J(i, l) ab(i, l) = t1
+        const double p_li = r.drag ? (0.0 + s2 * t2) + hP : hP;
+        const double p_il = r.drag ? (0.0 + s2 * t1) + hP : hP;
+        r.J[(rowb + l) + U * (cola + i)] = (hF + ca * t1) + p_li;
+        r.J[(rowb + i) + U * (cola + l)] = (hF + ca * t2) + p_il;
         fwd_step3(va + SMS * l, fwd);
         bwd_step3(bwd, va + SMS * l);
         bwd_step3(wF, va + SMS * l);
-        if (r.grav) bwd_step3(wP, va + SMS * l);
+        if (r.have_cot) bwd_step3(wP, va + SMS * l);
       }
       continue;
     }
@@ -809,7 +827,7 @@ __device__ __noinline__ void jacobian(const R& r) {
   } else {
   // functional_hess (adjoint.cpp:66-101) of the inertial seeds and of the
   // gravity cotangents at every instant
-  const int nsw = r.grav ? 2 * u : u;
+  const int nsw = r.have_cot ? 2 * u : u;
   for (int t = r.tid; t < nsw * N; t += NT) {
     const int sw = t / N;
     const int i = rd.walk_order[t - sw * N];
@@ -851,7 +869,7 @@ __device__ __noinline__ void jacobian(const R& r) {
           const int rr = lane + 32 * q;
           if (rr < n) {
             fh[h][q] = r.FH[fo + rr];
-            ph[h][q] = r.grav ? 0.0 + r.PH[fo + rr] : 0.0;
+            ph[h][q] = r.have_cot ? 0.0 + r.PH[fo + rr] : 0.0;
             jv[h][q] = jc[h][rr];
           }
         }
@@ -872,7 +890,7 @@ __device__ __noinline__ void jacobian(const R& r) {
           if (col < ncol && rr < n) {
             const int mm = col / n, cc = col - mm * n;
             const long fo = (long)mm * n * n + (long)cc * n;
-            const double phv = r.grav ? 0.0 + r.PH[fo + rr] : 0.0;
+            const double phv = r.have_cot ? 0.0 + r.PH[fo + rr] : 0.0;
             jc[h][rr] = (r.FH[fo + rr] + jc[h][rr]) + phv;
           }
         }
@@ -2192,7 +2210,14 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
   r.D = rd.D;
   r.K1 = sc.K1;
   r.grav = f.gravity_nonzero != 0;
+  r.drag = f.drag_d > 0.0;
+  r.have_cot = r.grav || r.drag;
   r.energy = sc.objective == 0;  // PBAD_ENERGY_FORM (include/pbad_gpu.h)
+  for (int mm = 0; mm < 8; ++mm) {
+    // potential_terms(..., dt = t_local dt): scale = D / (dt dt) (objective.cpp:62)
+    const double dtl = mm < rd.u ? sc.times[2 + mm] * sc.dt : 1.0;
+    r.s2[mm] = r.drag ? 2.0 * (f.drag_d / (dtl * dtl)) : 0.0;
+  }
   r.histc = 0.0;
   const double dt = sc.dt;
   r.inv_dt2 = 1.0 / (dt * dt);
@@ -2257,7 +2282,7 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
   fk_config(r, h1, r.hw1);
   if (r.energy) r.histc = energy_hist_const(r);
   // gravity cotangents (objective.cpp:48-58), the same at every instant
-  if (r.grav)
+  if (r.grav && !r.drag)
     for (int i = r.tid; i < N; i += NT) stm4(r.cot + 16 * i, add(m4_zero(), gravity_cot(f, ldgm4(m.S + 16 * i))));
   __syncthreads();
   // solver construction (optim.cpp:82-93)

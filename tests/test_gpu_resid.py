@@ -96,3 +96,56 @@ def test_resid_equals_general_kernel(monkeypatch):
     for x, y in zip(a, b):
         np.testing.assert_array_equal(np.array([s[1] for s in x.samples]), np.array([s[1] for s in y.samples]))
         assert [r.iterations for r in x.solve_reports] == [r.iterations for r in y.solve_reports]
+
+
+# --- drag in the residual form (serial chains): per-instant cotangents and the
+# pot.hess term 2 D / (t_m dt)^2 hess_ab in the fused diagonal-block walks
+# (objective.cpp:60-71,131-134, 296-313)
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_resid_drag_chain(order):
+    sc = make_single_hinge_chain_scene(6)
+    sc.drag_d = 1.5
+    sim = SimConfig(dt=0.01, duration=0.05, order=order, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, 6, 3, lambda b: mt19937_uniform(b + 50, 6, -0.4, 0.4)))
+
+
+def test_resid_drag_no_gravity_actuated():
+    """Drag alone (no gravity cotangent) plus sinusoidal actuation, tilted
+    hinge axes and rotated offsets on a serial chain."""
+    rng = np.random.default_rng(12)
+    base = random_tree(rng, 7, chain=True)
+    links = []
+    for l in base:
+        ax = rng.uniform(-1, 1, 3)
+        links.append(LinkSpec(l.parent, JointSpec(JointKind.hinge, tuple(ax / np.linalg.norm(ax)), l.joint.offset),
+                              l.geometry))
+    sc = Scene(links=links, gravity=(0.0, 0.0, 0.0))
+    sc.drag_d = 3.0
+    sc.actuation = ActuationSpec(ActuationKind.sinusoidal, np.linspace(-2, 2, 7), 2.0, np.linspace(0, 1, 7))
+    sim = SimConfig(dt=0.02, duration=0.06, order=3, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, 7, 2, lambda b: rng.uniform(-0.4, 0.4, 7)))
+
+
+def test_resid_drag_c5_shape_bounded_iterations():
+    """The C5 shape with drag (U = 300), a small iteration cap."""
+    sc = make_single_hinge_chain_scene(100)
+    sc.drag_d = 0.8
+    sim = SimConfig(dt=0.01, duration=0.02, order=4, objective=ObjectiveKind.residual_form,
+                    consecutive_fail_limit=10)
+    sim.optimizer.max_iters = 10
+    _check(sc, sim, _sims(sim, 100, 2, lambda b: mt19937_uniform(7, 200, -0.3, 0.3)[100 * b:100 * (b + 1)]))
+
+
+def test_resid_drag_tree_stays_general():
+    """Drag on a branched tree in the residual form is not on this kernel."""
+    rng = np.random.default_rng(5)
+    base = random_tree(rng, 5)
+    links = [LinkSpec(l.parent, JointSpec(JointKind.hinge, (0.0, 1.0, 0.0), l.joint.offset), l.geometry) for l in base]
+    if all(l.parent == (None if i == 0 else i - 1) for i, l in enumerate(links)):
+        pytest.skip("random tree came out a chain")
+    sc = Scene(links=links, gravity=(0.0, 0.0, -9.81))
+    sc.drag_d = 1.0
+    sim = SimConfig(dt=0.01, duration=0.02, order=3, objective=ObjectiveKind.residual_form)
+    m = api.build_model(sc.links)
+    assert api.GpuContext(m, sc.forces(), sim, max_batch=1).path == 0
