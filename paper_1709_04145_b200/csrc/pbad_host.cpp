@@ -698,11 +698,7 @@ bool resid_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_si
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_RESIDUAL_FORM || sim->opt.kind != PBAD_LM) return false;
   if (sim->order < 2 || sim->order - 1 > 8) return false;
-  if (f->drag_d > 0.0) {
-    // drag: serial chains (its pot.hess term joins the fused diagonal-block walks)
-    for (int i = 0; i < m.N; ++i)
-      if (m.parent[i] != i - 1) return false;
-  }
+
   if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
   for (int i = 0; i < m.N; ++i)
     if (m.kind[i] != PBAD_HINGE) return false;

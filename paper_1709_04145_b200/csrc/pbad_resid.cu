@@ -799,9 +799,13 @@ __device__ __noinline__ void jacobian(const R& r) {
       }
       continue;
     }
+    // trees with drag: the diagonal pair's raw ab also lands in PH, where the
+    // cotangent functional_hess walk below turns it into pot.hess
+    double* abm = (r.drag && a == b) ? r.PH + (long)a * n * n : nullptr;
     {
       const double h = 0.0 + trace_mul(mul_at(ldm4(la + SMS * i), ldm4(lb + SMS * i)), ldm4(r.ha(pr, 0) + 16 * i));
       r.J[(rowb + i) + U * (cola + i)] = ca * h;
+      if (abm) abm[i + (long)n * i] = h;
     }
     const L3 ua_i = ldl3(la + SMS * i), ub_i = ldl3(lb + SMS * i);
     M4 fwd = ldm4(r.ha(pr, 1) + 16 * i);
@@ -811,6 +815,10 @@ __device__ __noinline__ void jacobian(const R& r) {
       const double t2 = 0.0 + trace_at3(ldl3(la + SMS * l), ub_i, bwd);   // H(l, i)
       r.J[(rowb + l) + U * (cola + i)] = ca * t1;
       r.J[(rowb + i) + U * (cola + l)] = ca * t2;
+      if (abm) {
+        abm[i + (long)n * l] = t1;
+        abm[l + (long)n * i] = t2;
+      }
       fwd_step3(vb + SMS * l, fwd);
       bwd_step3(bwd, va + SMS * l);
     }
@@ -838,12 +846,24 @@ __device__ __noinline__ void jacobian(const R& r) {
     const M4 a = ldm4(r.fa(sw, 0) + 16 * i);
     const int p = rss.parent[i];
     const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
-    F[i + (long)n * i] = 0.0 + ddot(mul(pw, ldm4(r.dd2(mm) + 16 * i)), a);
+    // drag (cotangent sweeps): pot.hess = (0 + 2 scale ab) + functional_hess(cot),
+    // ab left in PH by the hess_ab walk above
+    const bool dr = r.drag && sw >= u;
+    const double s2 = dr ? r.s2[mm] : 0.0;
+    {
+      const double h = 0.0 + ddot(mul(pw, ldm4(r.dd2(mm) + 16 * i)), a);
+      F[i + (long)n * i] = dr ? (0.0 + s2 * F[i + (long)n * i]) + h : h;
+    }
     M4 walk = mul_bt(a, ldm4(r.dd1(mm) + 16 * i));
     for (int l = p; l >= 0; l = rss.parent[l]) {
       const double h = 0.0 + ddot3(ldl3(lm + SMS * l), walk);
-      F[l + (long)n * i] = h;
-      F[i + (long)n * l] = h;
+      if (dr) {
+        F[l + (long)n * i] = (0.0 + s2 * F[l + (long)n * i]) + h;
+        F[i + (long)n * l] = (0.0 + s2 * F[i + (long)n * l]) + h;
+      } else {
+        F[l + (long)n * i] = h;
+        F[i + (long)n * l] = h;
+      }
       bwd_step3(walk, vm + SMS * l);
     }
   }

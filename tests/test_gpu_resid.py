@@ -137,15 +137,19 @@ def test_resid_drag_c5_shape_bounded_iterations():
     _check(sc, sim, _sims(sim, 100, 2, lambda b: mt19937_uniform(7, 200, -0.3, 0.3)[100 * b:100 * (b + 1)]))
 
 
-def test_resid_drag_tree_stays_general():
-    """Drag on a branched tree in the residual form is not on this kernel."""
-    rng = np.random.default_rng(5)
-    base = random_tree(rng, 5)
-    links = [LinkSpec(l.parent, JointSpec(JointKind.hinge, (0.0, 1.0, 0.0), l.joint.offset), l.geometry) for l in base]
-    if all(l.parent == (None if i == 0 else i - 1) for i, l in enumerate(links)):
-        pytest.skip("random tree came out a chain")
-    sc = Scene(links=links, gravity=(0.0, 0.0, -9.81))
-    sc.drag_d = 1.0
-    sim = SimConfig(dt=0.01, duration=0.02, order=3, objective=ObjectiveKind.residual_form)
-    m = api.build_model(sc.links)
-    assert api.GpuContext(m, sc.forces(), sim, max_batch=1).path == 0
+@pytest.mark.parametrize("seed", [5, 6])
+def test_resid_drag_tree(seed):
+    """Drag on a branched hinge tree in the residual form: the diagonal pair's
+    ab goes through PH into pot.hess (zero blocks between unrelated links)."""
+    rng = np.random.default_rng(seed)
+    base = random_tree(rng, 7)
+    links = []
+    for l in base:
+        ax = rng.uniform(-1, 1, 3)
+        links.append(LinkSpec(l.parent, JointSpec(JointKind.hinge, tuple(ax / np.linalg.norm(ax)), l.joint.offset),
+                              l.geometry))
+    assert not all(l.parent == (None if i == 0 else i - 1) for i, l in enumerate(links))
+    sc = Scene(links=links, gravity=(0.3, -1.0, -9.81))
+    sc.drag_d = 1.2
+    sim = SimConfig(dt=0.02, duration=0.06, order=3, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, 7, 2, lambda b: rng.uniform(-0.4, 0.4, 7)))
