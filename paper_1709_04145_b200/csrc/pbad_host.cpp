@@ -693,13 +693,12 @@ bool tree_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim
 }
 
 // The residual-form kernel covers hinge trees with the residual objective and
-// LM (the high-order collocation Newton path), gravity / actuation.
+// LM (the high-order collocation Newton path), gravity / drag / actuation.
 bool resid_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_RESIDUAL_FORM || sim->opt.kind != PBAD_LM) return false;
   if (sim->order < 2 || sim->order - 1 > 8) return false;
-
-  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;
+  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;  // drag is covered
   for (int i = 0; i < m.N; ++i)
     if (m.kind[i] != PBAD_HINGE) return false;
   return resid_eligible_sizes(m.N, sim->order - 1);
