@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 
 #include "pbad_chain_ops.cuh"
@@ -48,11 +49,9 @@ enum { TR_OK = 0, TR_FAIL_LIMIT = 1, TR_NONFINITE_INIT = 2, TR_NONFINITE_CFG = 3
 
 constexpr int kE = 4;   // environments per warp
 constexpr int kL = 8;   // lanes per environment
-#ifndef PBAD_C6_WARPS
-#define PBAD_C6_WARPS 4
-#endif
-constexpr int kW = PBAD_C6_WARPS;  // warps per block
-constexpr int kT = 32 * kW;
+// warps per block: a launch-time choice among 4, 7 and 8 (launch()): one
+// block per SM of up to 8 warps shares the per-block model records and leaves
+// the most L1 beside the warps' shared areas (C3: 4 -> 7 warps, 118 -> 106 ms)
 constexpr int CL = 8;   // links per chunk (one per lane of an environment)
 constexpr int kRing = 3;
 constexpr int kMaxMem = 16;
@@ -77,8 +76,8 @@ static_assert(kHsyW >= 2 * kMaxMem + 1, "s.y ring + alpha");
 static_assert(kWarpD % 2 == 0, "16-byte aligned warp areas");
 constexpr int kHistW = 6;  // hist record per (link, env): c0 s0 | c1 s1 | cx sx
 
-__host__ __device__ inline size_t smem_bytes(int N) {
-  return (size_t)(kW * kWarpD + 20L * N) * sizeof(double) + (size_t)(2 * N + 1) * sizeof(int);
+__host__ __device__ inline size_t smem_bytes(int N, int kw) {
+  return (size_t)(kw * kWarpD + 20L * N) * sizeof(double) + (size_t)(2 * N + 1) * sizeof(int);
 }
 
 // ---- context ----------------------------------------------------------------
@@ -863,6 +862,7 @@ __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
   s.phase = (s.status == ST_RUNNING) ? PH_DIR : PH_DONE;
 }
 
+template <int KW>
 __device__ __forceinline__ Ctx make_ctx(const DModel& m, const DForces& f, const DSchedule& sc, const ChainLayout& L,
                                         double* cw, int* ci, long B, double* smem) {
   Ctx C;
@@ -876,14 +876,14 @@ __device__ __forceinline__ Ctx make_ctx(const DModel& m, const DForces& f, const
   C.j = lane & 7;
   C.h = C.j >> 2;
   C.r = lane & 3;
-  const long w = (long)blockIdx.x * kW + wib;
+  const long w = (long)blockIdx.x * KW + wib;
   C.ge = w * kE + C.e;
   C.B = B;
   C.valid = C.ge < B;
   C.em = 0xFFu << (lane & ~7);
   C.ws = smem + (long)wib * kWarpD;
   C.bar = reinterpret_cast<uint64_t*>(C.ws + kBar);
-  C.mrec = smem + (long)kW * kWarpD;
+  C.mrec = smem + (long)KW * kWarpD;
   C.kind = reinterpret_cast<const int*>(C.mrec + 20L * m.N);
   C.roff = C.kind + m.N;
   C.rec = cw + L.rec + w * (long)C.roff[m.N];
@@ -918,8 +918,9 @@ __device__ __forceinline__ Ctx make_ctx(const DModel& m, const DForces& f, const
   return C;
 }
 
+template <int KW>
 __device__ __forceinline__ void stage(const DModel& m, double* smem) {
-  double* rec = smem + (long)kW * kWarpD;
+  double* rec = smem + (long)KW * kWarpD;
   int* kind = reinterpret_cast<int*>(rec + 20L * m.N);
   int* roff = kind + m.N;
   const double2* src = reinterpret_cast<const double2*>(m.crec);
@@ -938,12 +939,12 @@ __device__ __forceinline__ void stage(const DModel& m, double* smem) {
 
 // One PBAD step for every environment of the warp: begin_step, L-BFGS to
 // completion in lockstep rounds, finish_step (stepper.cpp:83-147).
-template <int PAT>
-__global__ void __launch_bounds__(kT) k_chain6_step(DModel m, DForces f, DSchedule sc, ChainLayout L, double* cw,
-                                                    int* ci, long B, Outputs out) {
+template <int PAT, int KW>
+__global__ void __launch_bounds__(32 * KW) k_chain6_step(DModel m, DForces f, DSchedule sc, ChainLayout L,
+                                                         double* cw, int* ci, long B, Outputs out) {
   extern __shared__ __align__(16) double smem[];
-  stage(m, smem);
-  Ctx C = make_ctx(m, f, sc, L, cw, ci, B, smem);
+  stage<KW>(m, smem);
+  Ctx C = make_ctx<KW>(m, f, sc, L, cw, ci, B, smem);
   // a warp with no running environment has nothing to do (warp-uniform exit)
   bool active = C.valid && ival(C, IS_RUN) == TR_RUNNING;
   if (!__any_sync(0xffffffffu, active)) return;
@@ -1078,26 +1079,48 @@ __global__ void __launch_bounds__(kT) k_chain6_step(DModel m, DForces f, DSchedu
   }
 }
 
-template <int PAT>
-cudaError_t launch(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
-  const size_t sm = smem_bytes(a.m.N);
+template <int PAT, int KW>
+cudaError_t launch_kw(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
+  const size_t sm = smem_bytes(a.m.N, KW);
   static size_t configured = 0;
   if (sm > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(k_chain6_step<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_chain6_step<PAT, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     configured = sm;
   }
   const long nw = (a.B + kE - 1) / kE;
-  const unsigned grid = (unsigned)((nw + kW - 1) / kW);
-  k_chain6_step<PAT><<<grid, kT, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, out);
+  const unsigned grid = (unsigned)((nw + KW - 1) / KW);
+  k_chain6_step<PAT, KW><<<grid, 32 * KW, sm, s>>>(a.m, a.f, a.sc, a.L, a.cw, a.ci, a.B, out);
   return cudaGetLastError();
+}
+
+// Block size: the warps of the batch spread one block per SM where a block of
+// 7 or 8 warps fits (shared model records, more L1), else blocks of 4 (two per
+// SM).  PBAD_C6_WARPS = 4 / 7 / 8 forces one.
+template <int PAT>
+cudaError_t launch(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  static const int forced = std::getenv("PBAD_C6_WARPS") ? std::atoi(std::getenv("PBAD_C6_WARPS")) : 0;
+  const long nw = (a.B + kE - 1) / kE;
+  int kw = forced;
+  if (kw != 4 && kw != 7 && kw != 8) kw = nw <= 4L * sms ? 4 : nw <= 7L * sms ? 7 : 8;
+  if (kw != 4 && smem_bytes(a.m.N, kw) > 227 * 1024) kw = 4;
+  if (kw == 7) return launch_kw<PAT, 7>(a, out, s);
+  if (kw == 8) return launch_kw<PAT, 8>(a, out, s);
+  return launch_kw<PAT, 4>(a, out, s);
 }
 
 constexpr int pat(int P, int K0, int K1) { return P | (K0 << 2) | (K1 << 5); }
 
 }  // namespace c6
 
-bool chain6_fits(int N, int mem) { return mem <= c6::kMaxMem && c6::smem_bytes(N) <= 227 * 1024; }
+bool chain6_fits(int N, int mem) { return mem <= c6::kMaxMem && c6::smem_bytes(N, 4) <= 227 * 1024; }
 // vector doubles per warp-group layout: ceil(B / 4) warps x ceil(n / 8) groups x 32
 long chain6_vector_doubles(long B, int n) { return (B + c6::kE - 1) / c6::kE * (long)((n + 7) / 8) * c6::kGS; }
 
