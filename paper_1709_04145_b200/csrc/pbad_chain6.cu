@@ -53,7 +53,10 @@ constexpr int kL = 8;   // lanes per environment
 // block per SM of up to 8 warps shares the per-block model records and leaves
 // the most L1 beside the warps' shared areas (C3: 4 -> 7 warps, 118 -> 106 ms)
 constexpr int CL = 8;   // links per chunk (one per lane of an environment)
-constexpr int kRing = 3;
+#ifndef PBAD_C6_RING
+#define PBAD_C6_RING 3
+#endif
+constexpr int kRing = PBAD_C6_RING;
 constexpr int kMaxMem = 16;
 constexpr long kGS = 32;  // vector group stride (doubles): 8 elements x 4 environments
 // per-link record (doubles, per warp): cs [env][2] | lev [3*env+row][2] | seed [3*env+row][4]
@@ -62,11 +65,16 @@ constexpr int kRecLight = 32, kRecMass = 80;
 constexpr int kSlot = CL * kRecMass;  // ring slot (doubles)
 static_assert(kRecLight == kRecSd && kRecMass == kRecSd + 12 * kE, "record layout");
 // per-warp shared memory (doubles)
-constexpr int kFwdC = 0;                       // rotations of the chunk [CL][env]: c s | c0 s0 | c1 s1 | pad
-constexpr int kFwdR = kFwdC + CL * kE * 8;     // energy row partials [CL][term][row][env]
-constexpr int kFwdEnd = kFwdR + CL * 64;       // (the forward buffers overlay the ring)
-constexpr int kRRed = kRing * kSlot;           // gradient row partials [CL][chain][row][env]
-constexpr int kQScr = kRRed + CL * 32;         // per-environment scratch [env][16]
+// Shared-memory strides padded against bank conflicts (ncu round 2: 5.7 G
+// excess wavefronts per C3 launch at strides 8 / 16 / 32):
+constexpr int kRotS = 10;   // rotation record (c s | c0 s0 | c1 s1 | pad): 80 B apart
+constexpr int kTermS = 18;  // energy-term row partials: 4 rows x 4 envs + 2 pad
+constexpr int kRedS = 34;   // gradient row partials of one link: 2 chains x 4 rows x 4 envs + 2 pad
+constexpr int kFwdC = 0;                            // rotations of the chunk [CL][env]
+constexpr int kFwdR = kFwdC + CL * kE * kRotS;      // energy row partials [CL][term][row][env]
+constexpr int kFwdEnd = kFwdR + CL * 4 * kTermS;    // (the forward buffers overlay the ring)
+constexpr int kRRed = kRing * kSlot;                // gradient row partials [CL][chain][row][env]
+constexpr int kQScr = kRRed + CL * kRedS;           // per-environment scratch [env][16]
 constexpr int kHsy = kQScr + kE * 16;          // per-environment s.y ring and alpha [env][kHsyW]
 constexpr int kHsyW = 40;
 constexpr int kBar = kHsy + kE * kHsyW;        // mbarriers
@@ -184,7 +192,7 @@ template <int CK>
 __device__ __forceinline__ void fwd_link(const Ctx& C, int jl, int i, Rows& R, double* rp) {
   constexpr int JK = CK & 3;
   constexpr bool SK = (CK >> 2) != 0;
-  const double* rb = C.ws + kFwdC + (jl * kE + C.e) * 8;
+  const double* rb = C.ws + kFwdC + (jl * kE + C.e) * kRotS;
   // X1's rotation: the iterate's (h = 0) or hist1's (h = 1); X2's: hist0's
   const double2 cs1 = *reinterpret_cast<const double2*>(rb + 4 * C.h);
   const double2 hc0 = *reinterpret_cast<const double2*>(rb + 2);
@@ -219,9 +227,9 @@ __device__ __forceinline__ void fwd_link(const Ctx& C, int jl, int i, Rows& R, d
     row_s(y, S, p2);     // h = 0: seed row, h = 1: H S
 #pragma unroll
     for (int k = 0; k < 4; ++k) cg[k] = C.h ? p2[k] : (-C.gr) * S[12 + k];
-    double* fr = C.ws + kFwdR + jl * 64 + C.r * 4 + C.e;
-    fr[C.h ? 16 : 0] = ddot_row(p1, tr);   // term 0 (T S . T) / term 1 (A S . T)
-    fr[C.h ? 32 : 48] = ddot_row(cg, tr);  // term 3 (gravity) / term 2 (H S . T)
+    double* fr = C.ws + kFwdR + jl * 4 * kTermS + C.r * 4 + C.e;
+    fr[C.h ? kTermS : 0] = ddot_row(p1, tr);           // term 0 (T S . T) / term 1 (A S . T)
+    fr[C.h ? 2 * kTermS : 3 * kTermS] = ddot_row(cg, tr);  // term 3 (gravity) / term 2 (H S . T)
     double* sp = rp + kRecSd + 4 * row;
     stg2_if(rec_lane, sp, p2[0], p2[1]);
     stg2_if(rec_lane, sp + 2, p2[2], p2[3]);
@@ -310,7 +318,7 @@ __device__ __forceinline__ double forward(const Ctx& C, const double* X, double 
     if (c + 1 < nch) fetch(c + 1);
     __syncwarp();  // previous chunk's readers are done with the buffers
     if (la < N) {
-      double* rb = C.ws + kFwdC + (C.j * kE + C.e) * 8;
+      double* rb = C.ws + kFwdC + (C.j * kE + C.e) * kRotS;
       *reinterpret_cast<double2*>(rb) = make_double2(ca, sa);
       *reinterpret_cast<double2*>(rb + 2) = h_a0;
       *reinterpret_cast<double2*>(rb + 4) = h_a1;
@@ -322,20 +330,20 @@ __device__ __forceinline__ double forward(const Ctx& C, const double* X, double 
     __syncwarp();
     // lane t < 4 adds term t of each massive link, link by link (serial order)
     if (C.j < 4) {
-      const double* b0 = C.ws + kFwdR + C.j * 16 + C.e;
+      const double* b0 = C.ws + kFwdR + C.j * kTermS + C.e;
       if ((PAT & 3) != 0 && cnt == CL) {
 #pragma unroll
         for (int jl = 0; jl < CL; ++jl) {
           const int ck = ((PAT & 3) == 2 && (jl & 1)) ? ((PAT >> 5) & 7) : ((PAT >> 2) & 7);
           if (ck >> 2) {
-            const double* b = b0 + jl * 64;
+            const double* b = b0 + jl * 4 * kTermS;
             sum += ((b[0] + b[4]) + b[8]) + b[12];
           }
         }
       } else {
         for (int jl = 0; jl < cnt; ++jl) {
           if (C.kind[lo + jl] >> 2) {
-            const double* b = b0 + jl * 64;
+            const double* b = b0 + jl * 4 * kTermS;
             sum += ((b[0] + b[4]) + b[8]) + b[12];
           }
         }
@@ -386,7 +394,7 @@ __device__ __forceinline__ void rev_link(const Ctx& C, const double* rp, int i, 
 #pragma unroll
     for (int k = 0; k < 4; ++k) a[k] = cc[k];
   }
-  C.ws[kRRed + jl * 32 + C.h * 16 + C.r * 4 + C.e] = lever_dot<JK>(l0, l1, a);
+  C.ws[kRRed + jl * kRedS + C.h * 16 + C.r * 4 + C.e] = lever_dot<JK>(l0, l1, a);
   if (i > 0) {
     const double2 t01 = *reinterpret_cast<const double2*>(mr + 16);
     const double t[3] = {t01.x, t01.y, mr[18]};
@@ -465,7 +473,7 @@ __device__ __forceinline__ void reverse(Ctx& C, double* Gv) {
     __syncwarp();
     // the gradient entry of this lane's link of the chunk
     if (C.j < cnt) {
-      const double* b = C.ws + kRRed + C.j * 32 + C.e;
+      const double* b = C.ws + kRRed + C.j * kRedS + C.e;
       const double gi = 0.0 + (((b[0] + b[4]) + b[8]) + b[12]);
       const double gp = 0.0 + (((b[16] + b[20]) + b[24]) + b[28]);
       Gv[(long)c * kGS] = (gi + gp) - tau_c;
