@@ -30,6 +30,7 @@
 // bit-identical to oracle/ and to the reference build.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "pbad_chain_ops.cuh"
@@ -691,7 +692,7 @@ __device__ __forceinline__ void stage(const DModel& m, double* smem) {
 // One PBAD step for this warp's environment: begin_step, L-BFGS to
 // completion, finish_step (stepper.cpp:83-147).
 template <int PAT>
-__global__ void __launch_bounds__(128, 1) k_chain5_step(DModel m, DForces f, DSchedule sc, ChainLayout CL, double* cw,
+__global__ void __launch_bounds__(256, 1) k_chain5_step(DModel m, DForces f, DSchedule sc, ChainLayout CL, double* cw,
                                                      int* ci, long B, long recw, Outputs out) {
   extern __shared__ __align__(16) double smem[];
   stage(m, smem);
@@ -862,10 +863,30 @@ inline int warps_per_block(int N, int n, int mem) {
     if (block_smem_bytes(N, n, mem, wpb) + 64 <= 227 * 1024) return wpb;
   return 0;
 }
+// Warps per block for a batch of B environments on `sms` SMs: the batch spread
+// evenly, one block per SM (up to 8 warps, as shared memory allows), so no SM
+// runs more warps than the mean (C2: 7 warps per SM instead of 8 on 108 SMs
+// and 4 on 40), at least the 4 of warps_per_block
+inline int launch_wpb(int N, int n, int mem, long B, int sms) {
+  const int base = warps_per_block(N, n, mem);
+  if (base < 4) return base;
+  int w = (int)std::min<long>(8, std::max<long>(4, (B + sms - 1) / sms));
+  while (w > 4 && block_smem_bytes(N, n, mem, w) + 64 > 227 * 1024) --w;
+  return w;
+}
+inline int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
 
 template <int PAT>
 cudaError_t launch(const ChainArgs& a, long recw, const Outputs& out, cudaStream_t s) {
-  const int wpb = warps_per_block(a.m.N, a.m.n, a.sc.opt.mem);
+  const int wpb = launch_wpb(a.m.N, a.m.n, a.sc.opt.mem, a.B, sm_count());
   const size_t sm = block_smem_bytes(a.m.N, a.m.n, a.sc.opt.mem, wpb) + 64;
   static size_t configured = 0;
   if (sm > configured) {
@@ -885,11 +906,11 @@ bool chain5_fits(int N, int n, int mem) { return mem <= c5::kMaxMem && c5::warps
 namespace {
 constexpr int p16 = 1 | (6 << 2), p2 = 2 | (3 << 2) | (6 << 5);
 template <int PAT>
-int c5_blocks_per_sm(size_t sm) {
+int c5_blocks_per_sm(size_t sm, int threads) {
   if (cudaFuncSetAttribute(c5::k_chain5_step<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
     return 0;
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, c5::k_chain5_step<PAT>, 128, sm) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, c5::k_chain5_step<PAT>, threads, sm) != cudaSuccess) return 0;
   return nb;
 }
 }  // namespace
@@ -900,13 +921,15 @@ int c5_blocks_per_sm(size_t sm) {
 // quad-per-environment v4 kernel, eight environments per warp, does more
 // useful work per instruction.
 int chain5_waves(int N, int n, int mem, long B, int pattern, int device) {
-  const int wpb = c5::warps_per_block(N, n, mem);
-  if (wpb != 4 || mem > c5::kMaxMem) return 0;
-  const size_t sm = c5::block_smem_bytes(N, n, mem, wpb) + 64;
-  const int nb = pattern == p16 ? c5_blocks_per_sm<p16>(sm) : pattern == p2 ? c5_blocks_per_sm<p2>(sm)
-                                                                              : c5_blocks_per_sm<0>(sm);
+  if (c5::warps_per_block(N, n, mem) != 4 || mem > c5::kMaxMem) return 0;
   int sms = 0;
-  if (nb < 1 || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+  const int wpb = c5::launch_wpb(N, n, mem, B, sms);  // what launch() will use
+  const size_t sm = c5::block_smem_bytes(N, n, mem, wpb) + 64;
+  const int th = 32 * wpb;
+  const int nb = pattern == p16 ? c5_blocks_per_sm<p16>(sm, th) : pattern == p2 ? c5_blocks_per_sm<p2>(sm, th)
+                                                                                  : c5_blocks_per_sm<0>(sm, th);
+  if (nb < 1) return 0;
   const long blocks = (B + wpb - 1) / wpb;
   return (int)((blocks + (long)nb * sms - 1) / ((long)nb * sms));
 }
