@@ -68,7 +68,8 @@ static_assert(kRecLight == kRecSd && kRecMass == kRecSd + 12 * kE, "record layou
 // Shared-memory strides padded against bank conflicts (ncu round 2: 5.7 G
 // excess wavefronts per C3 launch at strides 8 / 16 / 32):
 constexpr int kRotS = 10;   // rotation record (c s | c0 s0 | c1 s1 | pad): 80 B apart
-constexpr int kTermS = 18;  // energy-term row partials: 4 rows x 4 envs + 2 pad
+constexpr int kTermS = 20;  // energy-term row partials: 4 rows x 4 envs + 4 pad (term readers in distinct banks)
+constexpr int kRedH = 18;   // gravity-chain offset inside a link's gradient partials (16 + 2 pad)
 constexpr int kRedS = 34;   // gradient row partials of one link: 2 chains x 4 rows x 4 envs + 2 pad
 constexpr int kFwdC = 0;                            // rotations of the chunk [CL][env]
 constexpr int kFwdR = kFwdC + CL * kE * kRotS;      // energy row partials [CL][term][row][env]
@@ -394,7 +395,7 @@ __device__ __forceinline__ void rev_link(const Ctx& C, const double* rp, int i, 
 #pragma unroll
     for (int k = 0; k < 4; ++k) a[k] = cc[k];
   }
-  C.ws[kRRed + jl * kRedS + C.h * 16 + C.r * 4 + C.e] = lever_dot<JK>(l0, l1, a);
+  C.ws[kRRed + jl * kRedS + C.h * kRedH + C.r * 4 + C.e] = lever_dot<JK>(l0, l1, a);
   if (i > 0) {
     const double2 t01 = *reinterpret_cast<const double2*>(mr + 16);
     const double t[3] = {t01.x, t01.y, mr[18]};
@@ -475,7 +476,7 @@ __device__ __forceinline__ void reverse(Ctx& C, double* Gv) {
     if (C.j < cnt) {
       const double* b = C.ws + kRRed + C.j * kRedS + C.e;
       const double gi = 0.0 + (((b[0] + b[4]) + b[8]) + b[12]);
-      const double gp = 0.0 + (((b[16] + b[20]) + b[24]) + b[28]);
+      const double gp = 0.0 + (((b[kRedH] + b[kRedH + 4]) + b[kRedH + 8]) + b[kRedH + 12]);
       Gv[(long)c * kGS] = (gi + gp) - tau_c;
     }
     __syncwarp();
