@@ -923,25 +923,67 @@ __device__ __noinline__ void jacobian(const R& r) {
 }
 
 // grad = 2 J^T g (objective.cpp:326-327)
+// 32-row chunk c of J into a shared tile (one column per 33-double row) by
+// 8-byte cp.async, the warps column by column (coalesced)
+__device__ __forceinline__ void grad_issue(const R& r, double* tile, int c) {
+  constexpr int KC = 32, TS = KC + 1;
+  const int U = r.U, k0 = c * KC, kc = min(KC, U - k0);
+  const int warp = r.tid >> 5, lane = r.tid & 31;
+  if (lane < kc)
+    for (int a = warp; a < U; a += NT / 32) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(tile + a * TS + lane);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(r.J + (k0 + lane) + (long)U * a)
+                   : "memory");
+    }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 __device__ __noinline__ void gradient(const R& r) {
+  // Thread t owns columns t and t + NT (two independent fma chains, k
+  // ascending: acc = (2 J(0,a)) g0, then fma(2 J(k,a), g_k, acc)); J arrives
+  // in 32-row chunks, double-buffered, one chunk ahead of the products
+  constexpr int KC = 32, TS = KC + 1;
   const int U = r.U;
   double* rs = rsm;
+  const long tsz = (long)U * TS;
+  double* tiles = rsm + ((U + 1) & ~1);
   for (int k = r.tid; k < U; k += NT) rs[k] = r.res[k];
-  __syncthreads();
-  for (int a = r.tid; a < U; a += NT) {
-    const double* Jc = r.J + (long)U * a;
-    double acc = (2.0 * Jc[0]) * rs[0];
-    int k = 1;
-    for (; k + 8 <= U; k += 8) {
-      double jv[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) jv[q] = Jc[k + q];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc = fma(2.0 * jv[q], rs[k + q], acc);
+  const int nc = (U + KC - 1) / KC;
+  const int a0 = r.tid, a1 = r.tid + NT;
+  double acc0 = 0.0, acc1 = 0.0;
+  grad_issue(r, tiles, 0);
+  for (int c = 0; c < nc; ++c) {
+    const int k0 = c * KC, kc = min(KC, U - k0);
+    if (c + 1 < nc) {
+      grad_issue(r, tiles + ((c + 1) & 1) * tsz, c + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    for (; k < U; ++k) acc = fma(2.0 * Jc[k], rs[k], acc);
-    r.grad[a] = acc;
+    __syncthreads();  // chunk c landed for every thread (and rs is written)
+    const double* tile = tiles + (c & 1) * tsz;
+    if (a0 < U) {
+      const double* t = tile + a0 * TS;
+      int kk = 0;
+      if (c == 0) {
+        acc0 = (2.0 * t[0]) * rs[0];
+        kk = 1;
+      }
+      for (; kk < kc; ++kk) acc0 = fma(2.0 * t[kk], rs[k0 + kk], acc0);
+    }
+    if (a1 < U) {
+      const double* t = tile + a1 * TS;
+      int kk = 0;
+      if (c == 0) {
+        acc1 = (2.0 * t[0]) * rs[0];
+        kk = 1;
+      }
+      for (; kk < kc; ++kk) acc1 = fma(2.0 * t[kk], rs[k0 + kk], acc1);
+    }
+    __syncthreads();  // chunk c consumed before its buffer takes chunk c + 2
   }
+  if (a0 < U) r.grad[a0] = acc0;
+  if (a1 < U) r.grad[a1] = acc1;
 }
 
 // GN = 0.5 (2 J^T J + (2 J^T J)^T) = 2 J^T J, lower triangle (objective.cpp:328-330).
@@ -2411,6 +2453,7 @@ size_t resid_smem_bytes(int N, int u) {
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP));             // Cholesky update panel
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 4) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
   b = std::max(b, 2 * u * N16);                                           // passes
+  b = std::max(b, (size_t)(N * u + 2 + 2 * 33 * N * u));                  // gradient: g + two 32-row J tiles
   b = std::max(b, 4 * u * N16);                                           // residual sweeps
   b = std::max(b, (2 * u + u * u) * N16);                                 // Jacobian walks
   return sizeof(double) * b;
