@@ -1693,16 +1693,27 @@ __device__ __noinline__ void llt_solve(const R& r, double* v) {
     __syncthreads();
   }
   // backward: for j descending, x_i -= L(j, i) x_j for i < j
+  // The block row L(j0 .. j0+bw-1, 0 .. j0+bw-1) is staged in shared memory
+  // first (warp per column, coalesced; column c at tile + 33 c), so the
+  // per-column reads of the diagonal solve and of the update come from
+  // shared memory instead of one L2 line per thread.
+  constexpr int TS = CB + 1;
+  double* tile = rsm;
   const int nbk = (U + CB - 1) / CB;
   for (int bk = nbk - 1; bk >= 0; --bk) {
     const int j0 = bk * CB;
     const int bw = min(CB, U - j0);
+    if (lane < bw)
+      for (int c = warp; c < j0 + bw; c += NT / 32) cp_async8(tile + c * TS + lane, A + (j0 + lane) + (long)U * c);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
     if (warp == 0) {
       double x = lane < bw ? v[j0 + lane] : 0.0;
       // lane l holds column j0 + l of the block: L(j0 + c, j0 + l) for c >= l
       double lcol[CB];
+      const double* tc = tile + (j0 + lane) * TS;
 #pragma unroll
-      for (int c = 0; c < CB; ++c) lcol[c] = (lane < bw && c >= lane && c < bw) ? A[(j0 + c) + (long)U * (j0 + lane)] : 0.0;
+      for (int c = 0; c < CB; ++c) lcol[c] = (lane < bw && c >= lane && c < bw) ? tc[c] : 0.0;
 #pragma unroll
       for (int jr = CB - 1; jr >= 0; --jr) {
         if (jr < bw) {
@@ -1716,7 +1727,8 @@ __device__ __noinline__ void llt_solve(const R& r, double* v) {
     __syncthreads();
     for (int i = r.tid; i < j0; i += NT) {
       double x = v[i];
-      for (int j = j0 + bw - 1; j >= j0; --j) x = fma(-A[j + (long)U * i], v[j], x);
+      const double* ti = tile + i * TS;
+      for (int j = bw - 1; j >= 0; --j) x = fma(-ti[j], v[j0 + j], x);
       v[i] = x;
     }
     __syncthreads();
@@ -2453,7 +2465,7 @@ size_t resid_smem_bytes(int N, int u) {
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 1) + resid::LSCAP));             // Cholesky update panel
   b = std::max(b, (size_t)(resid::CB * (resid::CB + 4) + resid::LSCAP_A + resid::LSCAP_C));  // lookahead panels
   b = std::max(b, 2 * u * N16);                                           // passes
-  b = std::max(b, (size_t)(N * u + 2 + 2 * 33 * N * u));                  // gradient: g + two 32-row J tiles
+  b = std::max(b, (size_t)(N * u + 2 + 2 * 33 * N * u));                  // gradient: g + two 32-row J tiles (covers the solve's 33 U block-row tile)
   b = std::max(b, 4 * u * N16);                                           // residual sweeps
   b = std::max(b, (2 * u + u * u) * N16);                                 // Jacobian walks
   return sizeof(double) * b;
