@@ -693,12 +693,20 @@ bool tree_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim
 }
 
 // The residual-form kernel covers hinge trees with the residual objective and
-// LM (the high-order collocation Newton path), gravity / drag / actuation.
+// LM (the high-order collocation Newton path), gravity / drag / actuation /
+// contact.
 bool resid_eligible(const pbad_gpu_model& m, const pbad_forces* f, const pbad_sim_desc* sim) {
   if (std::getenv("PBAD_GPU_FORCE_GENERAL")) return false;
   if (sim->objective != PBAD_RESIDUAL_FORM || sim->opt.kind != PBAD_LM) return false;
   if (sim->order < 2 || sim->order - 1 > 8) return false;
-  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) return false;  // drag is covered
+  // contact: the per-sample terms of potential_terms (objective.cpp:74-126)
+  // with a cotangent every instant (gravity or drag present, so have_cot is
+  // constant) and a bounded sample count (the per-sample Jacobian buffer)
+  if (f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0)) {
+    const bool grav = f->gravity[0] != 0.0 || f->gravity[1] != 0.0 || f->gravity[2] != 0.0;
+    if (!grav && !(f->drag_d > 0.0)) return false;
+    if (m.sample_off[m.N] > 1024) return false;
+  }
   for (int i = 0; i < m.N; ++i)
     if (m.kind[i] != PBAD_HINGE) return false;
   return resid_eligible_sizes(m.N, sim->order - 1);
@@ -1118,9 +1126,11 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     rd.u = (int)u;
     rd.U = (int)U;
     rd.D = th.D;
-    bool chain = true;
+    const bool contact = f->has_contact && (f->contact_d1 > 0.0 || f->contact_d2 > 0.0);
+    bool chain = !contact;  // contact terms run on the tree walks (pot.hess before functional_hess)
     for (int i = 0; i < m.N; ++i) chain = chain && m.parent[i] == i - 1;
     rd.chain = chain;
+    rd.ns = contact ? m.sample_off[m.N] : 0;
     rd.lvl_start = up_i(th.lvl_start);
     rd.lvl_links = up_i(th.lvl_links);
     rd.ch_start = up_i(th.ch_start);
@@ -1148,7 +1158,8 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
     rd.oHA = take(u * u * 4 * 16 * N);
     rd.oFA = take(2 * u * 2 * 16 * N);
     rd.oSeeds = take(u * 16 * N);
-    rd.oCot = take((f->drag_d > 0.0 ? u : 1) * 16 * N);  // per-instant cotangents with drag
+    rd.oCot = take((f->drag_d > 0.0 || rd.ns ? u : 1) * 16 * N);  // per-instant cotangents with drag / contact
+    rd.oCJ = take(u * rd.ns * (3 * n + 10));  // contact: per (instant, sample) hxx, active flag, 3 x n Jacobian
     rd.oX = take(U);
     rd.oGrad = take(U);
     rd.oCand = take(std::max(U, 2 * n));

@@ -152,6 +152,8 @@ struct ResidDesc {
   long pstride;            // doubles per link pass (value, world, d1, d2, lever: 5 x 16N)
   long gstride;
   long oJ, oGN, oDM, oFH, oPH, oPass, oHW0, oHW1, oHA, oFA, oSeeds, oCot, oX, oGrad, oCand, oRes, oPg, oTau, oStep;
+  int ns;    // contact samples (0: no contact terms)
+  long oCJ;  // contact: [u][ns][3n + 10] (hxx, active, jx column-major 3 x n)
 };
 
 struct Outputs {

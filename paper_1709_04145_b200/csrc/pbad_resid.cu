@@ -163,12 +163,14 @@ struct R {
   bool grav;
   bool drag;      // residual form with drag (chains): per-instant cotangents, pot.hess adds 2 scale ab
   bool have_cot;  // potential cotangents exist (gravity or drag: PotentialEval::have_cot)
+  bool contact;   // residual form with contact samples (hinge trees, walks path)
+  bool cot_pi;    // cotangents per instant (drag or contact), else the gravity cotangent once
   double s2[8];   // drag: 2 D / (t_m dt)^2 per unknown instant (objective.cpp:62-68)
   bool energy;    // energy form (K = 2, u = 1): the large-n Newton path of the energy objective
   double histc;   // energy form: hist_const (objective.cpp:178-184)
   double inv_dt2;
   double *J, *GN, *DM, *FH, *PH, *pass, *hw0, *hw1, *HA, *FA, *seeds, *cot, *x, *grad, *cand, *res, *pg, *tau,
-      *step;
+      *step, *CJ;
   __device__ __forceinline__ double* val(int mm) const { return pass + mm * rd->pstride; }
   __device__ __forceinline__ double* wld(int mm) const { return pass + mm * rd->pstride + 16L * N; }
   __device__ __forceinline__ double* dd1(int mm) const { return pass + mm * rd->pstride + 32L * N; }
@@ -342,6 +344,38 @@ __device__ void stage_vl(const R& r, double* Vs, double* Ls) {
 
 __device__ __noinline__ void adjoint_sweeps(const R& r);
 
+// contact sample sidx of link i at instant mm (objective.cpp:77-90, dt = t_m dt):
+// false = inactive (depth <= 0); else ph, the projected velocity and depth
+__device__ __forceinline__ bool contact_state(const R& r, int mm, int i, int sidx, double (&ph)[4], double (&pv)[3],
+                                              double* depth_out) {
+  const DModel& m = *r.m;
+  const DForces& f = *r.f;
+  const double* nrm = f.normal;
+  ph[0] = m.samples[3 * sidx];
+  ph[1] = m.samples[3 * sidx + 1];
+  ph[2] = m.samples[3 * sidx + 2];
+  ph[3] = 1.0;
+  double x4[4], xp4[4];
+  mul_vec4(ldm4(r.wld(mm) + 16 * i), ph, x4);
+  const double depth = f.plane_offset - dot3(nrm, x4);
+  if (depth <= 0.0) return false;
+  const double dtm = r.sc->times[2 + mm] * r.sc->dt;
+  mul_vec4(ldm4(r.hw1 + 16 * i), ph, xp4);
+  double proj[9];
+  for (int c = 0; c < 3; ++c)
+    for (int rr = 0; rr < 3; ++rr) proj[rr + 3 * c] = ((rr == c) ? 1.0 : 0.0) - nrm[rr] * nrm[c];
+  double v[3];
+  for (int k = 0; k < 3; ++k) v[k] = (x4[k] - xp4[k]) / dtm;
+  for (int rr = 0; rr < 3; ++rr) {
+    double acc = proj[rr] * v[0];
+    acc = fma(proj[rr + 3], v[1], acc);
+    acc = fma(proj[rr + 6], v[2], acc);
+    pv[rr] = acc;
+  }
+  *depth_out = depth;
+  return true;
+}
+
 // residuals g_m (objective.cpp:281-308) of the configuration whose passes are
 // current; returns value = sum_m |g_m|^2 (objective.cpp:323-324).  Leaves the
 // adjoint sums a of every sweep in fa(sw, 0) for functional_hess.
@@ -359,13 +393,37 @@ __device__ __noinline__ double residual(const R& r) {
       addto(acc, scale(st[j], ldm4(W + 16 * i)));
     }
     stm4(r.seeds + (long)mm * 16 * N + 16 * i, mul(scale(r.inv_dt2, acc), ldgm4(m.S + 16 * i)));
-    if (r.drag) {
-      // potential_terms' cotangents at instant mm (objective.cpp:45-68):
-      // cot = (0 + gravity) + (2 D / (t_m dt)^2) (T_m - T_hist1) S
+    if (r.cot_pi) {
+      // potential_terms' cotangents at instant mm (objective.cpp:45-101):
+      // cot = (0 + gravity) + (2 D / (t_m dt)^2) (T_m - T_hist1) S, then
+      // + dqdx ph^T of every active contact sample of the link, in order
       const M4 S = ldgm4(m.S + 16 * i);
-      const M4 base = r.grav ? add(m4_zero(), gravity_cot(*r.f, S)) : m4_zero();
-      const M4 diff_s = mul(sub(ldm4(r.wld(mm) + 16 * i), ldm4(r.hw1 + 16 * i)), S);
-      stm4(r.cot + (long)mm * 16 * N + 16 * i, add(base, scale(r.s2[mm], diff_s)));
+      M4 cot = r.grav ? add(m4_zero(), gravity_cot(*r.f, S)) : m4_zero();
+      if (r.drag) {
+        const M4 diff_s = mul(sub(ldm4(r.wld(mm) + 16 * i), ldm4(r.hw1 + 16 * i)), S);
+        cot = add(cot, scale(r.s2[mm], diff_s));
+      }
+      if (r.contact) {
+        const DForces& f = *r.f;
+        const double dtm = sc.times[2 + mm] * sc.dt;
+        for (int sidx = m.sample_off[i]; sidx < m.sample_off[i + 1]; ++sidx) {
+          double ph[4], pv[3], depth;
+          if (!contact_state(r, mm, i, sidx, ph, pv, &depth)) continue;
+          const double pv2 = dot3(pv, pv);
+          const double ca = -2.0 * f.d1 * depth - 2.0 * f.d2 * depth * pv2;
+          const double cb = 2.0 * f.d2 * depth * depth / dtm;
+          double dq[4];
+          for (int k = 0; k < 3; ++k) dq[k] = ca * f.normal[k] + cb * pv[k];
+          dq[3] = 0.0;
+          M4 oc;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) oc.a[rr + 4 * c] = dq[rr] * ph[c];
+          cot = add(cot, oc);
+        }
+      }
+      stm4(r.cot + (long)mm * 16 * N + 16 * i, cot);
     }
   }
   __syncthreads();
@@ -409,7 +467,7 @@ __device__ __noinline__ void adjoint_sweeps(const R& r) {
     // shared memory, not global loads ordered behind its own global stores
     for (int t = r.tid; t < nsw * N * 16; t += NT) {
       const int sw = t / (16 * N), k = t - sw * 16 * N;
-      const double* src = sw < u ? r.seeds + (long)sw * 16 * N : r.cot + (r.drag ? (long)(sw - u) * 16 * N : 0L);
+      const double* src = sw < u ? r.seeds + (long)sw * 16 * N : r.cot + (r.cot_pi ? (long)(sw - u) * 16 * N : 0L);
       Xs[sw * NS + SMS * (k >> 4) + (k & 15)] = src[k];
     }
     __syncthreads();
@@ -444,7 +502,7 @@ __device__ __noinline__ void adjoint_sweeps(const R& r) {
       const int sw = t / cnt;
       const int i = rd.lvl_links[l0 + t - sw * cnt];
       const int mm = sw < u ? sw : sw - u;
-      const double* src = sw < u ? r.seeds + (long)mm * 16 * N : r.cot + (r.drag ? (long)mm * 16 * N : 0L);
+      const double* src = sw < u ? r.seeds + (long)mm * 16 * N : r.cot + (r.cot_pi ? (long)mm * 16 * N : 0L);
       double* X = Xs + sw * NS;
       M4 adj = m4_zero();
       for (int c = rd.ch_start[i]; c < rd.ch_start[i + 1]; ++c) adj = add(adj, ldm4(X + SMS * rd.ch_list[c]));
@@ -670,6 +728,94 @@ __device__ __forceinline__ double ddot3(const L3& A, const M4& W) {
 }
 
 // Jacobian of the residuals (objective.cpp:310-320) into r.J
+// contact part of pot.hess (objective.cpp:104-123, flags.hess) at every
+// instant: per (instant, sample) the Hessian hxx and the sample Jacobian jx
+// (3 x n, zero off the sample's root path) into r.CJ; then every element of
+// the instant's n x n block adds (jx^T hxx) jx of the active samples, in
+// sample order, onto 0 (+ 2 scale ab with drag, PH's raw ab) -> PH.  The
+// cotangent functional_hess walk adds its term last (objective.cpp:132-135).
+__device__ __noinline__ void contact_hess(const R& r, const double* Vs, const double* Ls) {
+  const DModel& m = *r.m;
+  const DForces& f = *r.f;
+  const int N = r.N, n = r.n, u = r.u, ns = r.rd->ns;
+  const long NS = (long)SMS * N;
+  const long cs = 3L * n + 10;
+  const double* nrm = f.normal;
+  for (int t = r.tid; t < u * ns; t += NT) {
+    const int mm = t / ns, sidx = t - mm * ns;
+    int i = 0;
+    while (m.sample_off[i + 1] <= sidx) ++i;
+    double* cj = r.CJ + (long)t * cs;
+    double ph[4], pv[3], depth;
+    if (!contact_state(r, mm, i, sidx, ph, pv, &depth)) {
+      cj[9] = 0.0;
+      continue;
+    }
+    const double dtm = r.sc->times[2 + mm] * r.sc->dt;
+    const double pv2 = dot3(pv, pv);
+    double hxx[9];
+    for (int c = 0; c < 3; ++c)
+      for (int rr = 0; rr < 3; ++rr) hxx[rr + 3 * c] = ((2.0 * f.d1) * nrm[rr]) * nrm[c];
+    if (f.d2 > 0.0) {
+      double proj[9];
+      for (int c = 0; c < 3; ++c)
+        for (int rr = 0; rr < 3; ++rr) proj[rr + 3 * c] = ((rr == c) ? 1.0 : 0.0) - nrm[rr] * nrm[c];
+      const double k1 = (2.0 * f.d2) * pv2;
+      const double k2 = 4.0 * f.d2 * depth / dtm;
+      const double k3 = 2.0 * f.d2 * depth * depth / (dtm * dtm);
+      for (int c = 0; c < 3; ++c)
+        for (int rr = 0; rr < 3; ++rr) {
+          const double t1 = (k1 * nrm[rr]) * nrm[c];
+          const double t2 = k2 * (nrm[rr] * pv[c] + pv[rr] * nrm[c]);
+          const double t3 = k3 * proj[rr + 3 * c];
+          hxx[rr + 3 * c] = hxx[rr + 3 * c] + ((t1 - t2) + t3);
+        }
+    }
+    for (int k = 0; k < 9; ++k) cj[k] = hxx[k];
+    cj[9] = 1.0;
+    double* jx = cj + 10;
+    for (int k = 0; k < 3 * n; ++k) jx[k] = 0.0;
+    double y[4] = {ph[0], ph[1], ph[2], ph[3]};
+    for (int l = i; l >= 0; l = rss.parent[l]) {  // hinge: dof l = link l
+      double t4[4], y2[4];
+      mul_vec4(ldm4(Ls + mm * NS + SMS * l), y, t4);
+      jx[3 * l] = t4[0];
+      jx[3 * l + 1] = t4[1];
+      jx[3 * l + 2] = t4[2];
+      mul_vec4(ldm4(Vs + mm * NS + SMS * l), y, y2);
+      for (int k = 0; k < 4; ++k) y[k] = y2[k];
+    }
+  }
+  __syncthreads();
+  const long nn = (long)n * n;
+  for (long t = r.tid; t < u * nn; t += NT) {
+    const int mm = (int)(t / nn);
+    const long e = t - mm * nn;
+    const int b = (int)(e / n), a = (int)(e - (long)b * n);
+    double* P = r.PH + mm * nn + e;
+    double acc = r.drag ? 0.0 + r.s2[mm] * *P : 0.0;
+    for (int sidx = 0; sidx < ns; ++sidx) {
+      const double* cj = r.CJ + ((long)mm * ns + sidx) * cs;
+      if (cj[9] == 0.0) continue;
+      const double* jx = cj + 10;
+      double tmp[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double q = jx[3 * a] * cj[3 * c];
+        q = fma(jx[3 * a + 1], cj[1 + 3 * c], q);
+        q = fma(jx[3 * a + 2], cj[2 + 3 * c], q);
+        tmp[c] = q;
+      }
+      double v = tmp[0] * jx[3 * b];
+      v = fma(tmp[1], jx[3 * b + 1], v);
+      v = fma(tmp[2], jx[3 * b + 2], v);
+      acc = acc + v;
+    }
+    *P = acc;
+  }
+  __syncthreads();
+}
+
 __device__ __noinline__ void jacobian(const R& r) {
   const DModel& m = *r.m;
   const DSchedule& sc = *r.sc;
@@ -833,6 +979,7 @@ __device__ __noinline__ void jacobian(const R& r) {
     // hess_ab walks above
     PT_MARK(16);
   } else {
+  if (r.contact) contact_hess(r, Vs, Ls);
   // functional_hess (adjoint.cpp:66-101) of the inertial seeds and of the
   // gravity cotangents at every instant
   const int nsw = r.have_cot ? 2 * u : u;
@@ -847,17 +994,22 @@ __device__ __noinline__ void jacobian(const R& r) {
     const int p = rss.parent[i];
     const M4 pw = p >= 0 ? ldm4(r.wld(mm) + 16 * p) : m4_identity();
     // drag (cotangent sweeps): pot.hess = (0 + 2 scale ab) + functional_hess(cot),
-    // ab left in PH by the hess_ab walk above
-    const bool dr = r.drag && sw >= u;
+    // ab left in PH by the hess_ab walk above; with contact PH already holds
+    // everything before functional_hess (contact_hess)
+    const bool pc = r.contact && sw >= u;
+    const bool dr = r.drag && sw >= u && !pc;
     const double s2 = dr ? r.s2[mm] : 0.0;
     {
       const double h = 0.0 + ddot(mul(pw, ldm4(r.dd2(mm) + 16 * i)), a);
-      F[i + (long)n * i] = dr ? (0.0 + s2 * F[i + (long)n * i]) + h : h;
+      F[i + (long)n * i] = pc ? F[i + (long)n * i] + h : dr ? (0.0 + s2 * F[i + (long)n * i]) + h : h;
     }
     M4 walk = mul_bt(a, ldm4(r.dd1(mm) + 16 * i));
     for (int l = p; l >= 0; l = rss.parent[l]) {
       const double h = 0.0 + ddot3(ldl3(lm + SMS * l), walk);
-      if (dr) {
+      if (pc) {
+        F[l + (long)n * i] = F[l + (long)n * i] + h;
+        F[i + (long)n * l] = F[i + (long)n * l] + h;
+      } else if (dr) {
         F[l + (long)n * i] = (0.0 + s2 * F[l + (long)n * i]) + h;
         F[i + (long)n * l] = (0.0 + s2 * F[i + (long)n * l]) + h;
       } else {
@@ -2285,7 +2437,9 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
   r.K1 = sc.K1;
   r.grav = f.gravity_nonzero != 0;
   r.drag = f.drag_d > 0.0;
-  r.have_cot = r.grav || r.drag;
+  r.have_cot = r.grav || r.drag;  // contact runs only with one of them (resid_eligible)
+  r.contact = rd.ns > 0;
+  r.cot_pi = r.drag || r.contact;
   r.energy = sc.objective == 0;  // PBAD_ENERGY_FORM (include/pbad_gpu.h)
   for (int mm = 0; mm < 8; ++mm) {
     // potential_terms(..., dt = t_local dt): scale = D / (dt dt) (objective.cpp:62)
@@ -2316,6 +2470,7 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
     r.pg = g + rd.oPg;
     r.tau = g + rd.oTau;
     r.step = g + rd.oStep;
+    r.CJ = g + rd.oCJ;
   }
   const int n = r.n, u = r.u, U = r.U, N = r.N;
   for (int i = r.tid; i < N; i += NT) rss.parent[i] = m.parent[i];
@@ -2356,7 +2511,7 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
   fk_config(r, h1, r.hw1);
   if (r.energy) r.histc = energy_hist_const(r);
   // gravity cotangents (objective.cpp:48-58), the same at every instant
-  if (r.grav && !r.drag)
+  if (r.grav && !r.cot_pi)
     for (int i = r.tid; i < N; i += NT) stm4(r.cot + 16 * i, add(m4_zero(), gravity_cot(f, ldgm4(m.S + 16 * i))));
   __syncthreads();
   // solver construction (optim.cpp:82-93)

@@ -7,7 +7,7 @@ import pytest
 import oracle
 from paper_1709_04145_b200 import api
 from paper_1709_04145_b200.scenes import Scene, make_single_hinge_chain_scene, mt19937_uniform
-from paper_1709_04145_b200.types import (ActuationKind, ActuationSpec, JointKind, JointSpec, LinkSpec,
+from paper_1709_04145_b200.types import (ActuationKind, ActuationSpec, ContactModel, JointKind, JointSpec, LinkSpec,
                                          ObjectiveKind, SimConfig)
 
 from _parity_util import assert_traj_equal, random_tree
@@ -153,3 +153,57 @@ def test_resid_drag_tree(seed):
     sc.drag_d = 1.2
     sim = SimConfig(dt=0.02, duration=0.06, order=3, objective=ObjectiveKind.residual_form)
     _check(sc, sim, _sims(sim, 7, 2, lambda b: rng.uniform(-0.4, 0.4, 7)))
+
+
+# --- contact in the residual form: per-sample cotangents dqdx ph^T and the
+# pot.hess term jx^T hxx jx of every active sample, added after the drag term
+# and before functional_hess(cot) (objective.cpp:74-135); the contact scenes
+# run the tree walks (chains included)
+
+def _contact_links(rng, n, chain, per_link=2, spread=0.15):
+    base = random_tree(rng, n, chain=chain)
+    links = []
+    for l in base:
+        ax = rng.uniform(-1, 1, 3)
+        samples = [tuple(rng.uniform(-spread, spread, 3)) for _ in range(per_link)]
+        links.append(LinkSpec(l.parent, JointSpec(JointKind.hinge, tuple(ax / np.linalg.norm(ax)), l.joint.offset),
+                              l.geometry, contact_samples=samples))
+    return links
+
+
+@pytest.mark.parametrize("chain,order,d2", [(True, 3, 40.0), (False, 3, 40.0), (True, 4, 0.0), (False, 2, 25.0)])
+def test_resid_contact(chain, order, d2):
+    """Contact samples on every link against a tilted plane through the
+    structure: samples enter and leave contact along the trajectory."""
+    rng = np.random.default_rng(100 + order + (0 if chain else 7))
+    n = 7
+    sc = Scene(links=_contact_links(rng, n, chain), gravity=(0.2, -0.5, -9.81))
+    nrm = np.array([0.3, -0.2, 1.0])
+    sc.contact = ContactModel(tuple(nrm / np.linalg.norm(nrm)), 0.05, 3.0e3, d2)
+    sim = SimConfig(dt=0.01, duration=0.06, order=order, objective=ObjectiveKind.residual_form)
+    gpu, ref = _check(sc, sim, _sims(sim, n, 3, lambda b: rng.uniform(-0.6, 0.6, n)))
+
+
+def test_resid_contact_with_drag_no_gravity():
+    """Contact with drag and no gravity: the contact pot.hess terms land on
+    (0 + 2 scale ab) before functional_hess (objective.cpp:69-71, 118-123)."""
+    rng = np.random.default_rng(77)
+    n = 6
+    sc = Scene(links=_contact_links(rng, n, False, per_link=3), gravity=(0.0, 0.0, 0.0))
+    sc.drag_d = 1.1
+    sc.contact = ContactModel((0.0, 0.0, 1.0), 0.02, 5.0e3, 60.0)
+    sim = SimConfig(dt=0.02, duration=0.08, order=3, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, n, 2, lambda b: rng.uniform(-0.8, 0.8, n)))
+
+
+def test_resid_contact_larger_chain():
+    """A 40-link chain, samples on alternate links, K = 3."""
+    rng = np.random.default_rng(5)
+    n = 40
+    links = _contact_links(rng, n, True, per_link=1)
+    for i in range(1, n, 2):
+        links[i].contact_samples = []
+    sc = Scene(links=links, gravity=(0.0, 0.0, -9.81))
+    sc.contact = ContactModel((0.0, 0.0, 1.0), -0.05, 2.0e3, 10.0)
+    sim = SimConfig(dt=0.01, duration=0.03, order=3, objective=ObjectiveKind.residual_form)
+    _check(sc, sim, _sims(sim, n, 2, lambda b: rng.uniform(-0.4, 0.4, n)))
