@@ -58,7 +58,7 @@ constexpr int GP = GB + 1;   // padded smem row (odd: conflict-free staging stor
 // Cholesky tiling
 constexpr int CB = 32;       // block column width
 constexpr int LK = 16;       // k chunk of the block-column update
-constexpr int MAXU = 320;
+constexpr int MAXU = 400;       // U = u n; shared memory bounds it further (resid_eligible_sizes)
 constexpr int SMS = 18;      // shared-memory stride of a 4x4 (16 + 2 pad: conflict-free per-link double2 access)
 constexpr int LP = MAXU + 2; // padded smem row of the update panel
 constexpr int LSCAP = 16384; // shared-memory doubles for the Cholesky update panel
@@ -1576,6 +1576,14 @@ __device__ __forceinline__ void bcu_dmma(const R& r, double* A, const double* G,
       }
   }
 }
+// more than 6 row blocks per warp (U - c0 > 48 NW): its own function, so
+// the larger accumulator tile does not set the register budget of the rest
+template <int GS>
+__device__ __noinline__ void block_col_update_big(const R& r, double* A, const double* G, double lambda, bool fromG,
+                                                  int c0, int bw, int kb, int ke, double* panel, int cap, int bar) {
+  constexpr int NW = GS / 32;
+  bcu_dmma<GS, (MAXU / 8 + NW - 1) / NW>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+}
 template <int GS>
 __device__ __noinline__ void block_col_update(const R& r, double* A, const double* G, double lambda, bool fromG,
                                               int c0, int bw, int kb, int ke, double* panel, int cap, int bar) {
@@ -1586,7 +1594,7 @@ __device__ __noinline__ void block_col_update(const R& r, double* A, const doubl
   else if (q <= 3) bcu_dmma<GS, 3>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
   else if (q <= 4) bcu_dmma<GS, 4>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
   else if (q <= 6) bcu_dmma<GS, 6>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
-  else bcu_dmma<GS, (MAXU / 8 + NW - 1) / NW>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
+  else block_col_update_big<GS>(r, A, G, lambda, fromG, c0, bw, kb, ke, panel, cap, bar);
 }
 #else
 template <int GS>

@@ -114,3 +114,12 @@ def test_small_shapes_match_tree_kernel(name, monkeypatch):
     resid_gpu, _ = _check(sc, sim, sims, path=PATH_RESID)
     for a, b in zip(tree_gpu, resid_gpu):
         np.testing.assert_array_equal(np.array([s[1] for s in a.samples]), np.array([s[1] for s in b.samples]))
+
+
+def test_chain_beyond_320_dofs():
+    """A 360-link single-hinge chain (U = 360 > the round-1 bound of 320):
+    the larger accumulator tiles of the Cholesky block-column update."""
+    sc = make_single_hinge_chain_scene(360)
+    sim = _lm(0.01, 0.02)
+    sim.optimizer.max_iters = 40
+    _check(sc, sim, _sims(sim, 360, 2, lambda b: mt19937_uniform(b + 90, 360, -0.2, 0.2)))

@@ -207,3 +207,12 @@ def test_resid_contact_larger_chain():
     sc.contact = ContactModel((0.0, 0.0, 1.0), -0.05, 2.0e3, 10.0)
     sim = SimConfig(dt=0.01, duration=0.03, order=3, objective=ObjectiveKind.residual_form)
     _check(sc, sim, _sims(sim, n, 2, lambda b: rng.uniform(-0.4, 0.4, n)))
+
+
+def test_resid_u2_beyond_320():
+    """Residual form K = 3 (u = 2) on a 180-link chain: U = 360 unknowns."""
+    sc = make_single_hinge_chain_scene(180)
+    sim = SimConfig(dt=0.01, duration=0.02, order=3, objective=ObjectiveKind.residual_form,
+                    consecutive_fail_limit=10)
+    sim.optimizer.max_iters = 12
+    _check(sc, sim, _sims(sim, 180, 2, lambda b: mt19937_uniform(b + 60, 180, -0.3, 0.3)))
