@@ -444,7 +444,11 @@ __device__ __forceinline__ void issue_chunk(Ctx& C, int c, unsigned k) {
   const int lo = CL * c, hi = min(C.N, lo + CL);
   const int slot = (int)(k % kRing);
   const unsigned bytes = (unsigned)(C.roff[hi] - C.roff[lo]) * 8u;
+#if PBAD_C6_HINT & 2
+  bulk_load_ef(C.ws + slot * kSlot, C.rec + C.roff[lo], bytes, C.bar + slot);
+#else
   bulk_load(C.ws + slot * kSlot, C.rec + C.roff[lo], bytes, C.bar + slot);
+#endif
 }
 
 template <int PAT>
@@ -630,11 +634,24 @@ static_assert(kB % 4 == 0, "batch must keep the 32-partial dot order");
 // Vector passes run in batches of kB groups.  Batches of groups below nf
 // hold an element in every lane and run unpredicated from one base address
 // (F = true); the tail batch checks every group (F = false).
-template <bool F>
+// PBAD_C6_HINT (L2 eviction priority, bit mask): 1 (default): the two-loop
+// passes that are a history vector's last read of the iteration (loop 2 and
+// the scale pass) load it evict-first (ld.global.cs), leaving L2 to the link
+// records and the hot vectors (C3 93.7 -> 91.7 ms); 2 (A/B only, slower):
+// the reverse sweep's record bulk copies carry an L2 evict-first policy.
+// Measured and dropped: evict-last record stores, evict-last
+// loop-1 history loads, evict-first s / y stores.
+#ifndef PBAD_C6_HINT
+#define PBAD_C6_HINT 1
+#endif
+template <bool F, bool CS = false>
 __device__ __forceinline__ void ldb(const Ctx& C, const double* V, int g0, double* out) {
   const double* p = V + (long)g0 * kGS;
 #pragma unroll
-  for (int jj = 0; jj < kB; ++jj) out[jj] = (F || g0 + jj < C.n8) ? p[jj * kGS] : 0.0;
+  for (int jj = 0; jj < kB; ++jj) {
+    if (CS) out[jj] = (F || g0 + jj < C.n8) ? __ldcs(p + jj * kGS) : 0.0;
+    else out[jj] = (F || g0 + jj < C.n8) ? p[jj * kGS] : 0.0;
+  }
 }
 template <bool F>
 __device__ __forceinline__ bool gok(const Ctx& C, int g) { return F || elem_ok(C, g); }
@@ -651,10 +668,12 @@ template <bool F, int MODE, int DOT>
 __device__ __forceinline__ void tl_batch(const Ctx& C, const double* w, double a, const double* z, bool store_q, int g0,
                                          double* acc) {
   double qv_[kB], wv[kB], zv[kB];
+  // loop 2 and the scale pass are a history vector's last read of the iteration
+  constexpr bool LAST = (PBAD_C6_HINT & 1) && (MODE == M_ADD || MODE == M_SCALE);
   if (MODE != M_COPY) ldb<F>(C, C.q, g0, qv_);
-  if (MODE != M_SCALE) ldb<F>(C, w, g0, wv);
+  if (MODE != M_SCALE) ldb<F, LAST>(C, w, g0, wv);
   if (DOT == 2) ldb<F>(C, C.g, g0, zv);
-  else ldb<F>(C, z, g0, zv);
+  else ldb<F, LAST>(C, z, g0, zv);
   double* qo = C.q + (long)g0 * kGS;
   double* dout = C.dir + (long)g0 * kGS;
 #pragma unroll

@@ -32,6 +32,16 @@ __device__ __forceinline__ void bulk_load(double* dst, const double* src, unsign
                "l"(src), "r"(bytes), "r"(su32(bar))
                : "memory");
 }
+// the same with an L2 evict-first policy (the copy is the data's last read)
+__device__ __forceinline__ void bulk_load_ef(double* dst, const double* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   unsigned ok = 0;
   long spins = 0;
