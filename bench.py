@@ -469,9 +469,11 @@ def main():
     clocks.start()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.kernel_launches()
     e0.record(stream)
     ctx.advance(K, sh)
     e1.record(stream)
+    launches = ctx.kernel_launches() - l0
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
@@ -553,7 +555,7 @@ def main():
                      "dfma_latency_cycles": lat},
         "cpu_baseline": cb,
         "e2e": e2e,
-        "gpu_launches": K,
+        "gpu_launches": launches,
         "kernel": {0: "pbad_gpu::k_step (general, thread per env)", 1: "pbad_gpu::k_chain_step (quad per env)",
                    2: "pbad_gpu::c4::k_chain4_step (warp-synchronous quads, TMA-fed adjoint)",
                    3: "pbad_gpu::tree::k_tree_step (warp per env, Newton/LM, in-SMEM Cholesky)",

@@ -205,6 +205,10 @@ int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* ctx);
 #define PBAD_PATH_CHAIN6 6  /* 8 lanes per environment (two per row), axis-aligned hinge chains (pbad_chain6.cu) */
 #define PBAD_PATH_CHAIN7 7  /* 16 lanes per environment, link-parallel energy terms, axis-aligned hinge chains (pbad_chain7.cu) */
 int32_t pbad_gpu_path(const pbad_gpu_ctx* ctx);
+/* step kernels this context has launched so far (no reference counterpart;
+ * bench.py's gpu_launches): one per PBAD step, except the tree family's
+ * persistent multi-step launch for contact scenes (one per window) */
+int64_t pbad_gpu_kernel_launches(const pbad_gpu_ctx* ctx);
 
 /* batch_simulate on the GPU: q0/qdot0 host [B][n]; copies in, steps every
  * trajectory to completion, copies the requested outputs back.  The device

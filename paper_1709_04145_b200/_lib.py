@@ -23,7 +23,7 @@ HEADER_SYMBOLS = [
     "pbad_gpu_model_links", "pbad_gpu_model_info", "pbad_gpu_body_integral", "pbad_gpu_rotation_vector_matrix",
     "pbad_gpu_rotation_vector_from_matrix",
     "pbad_gpu_build_scheme", "pbad_gpu_validate_configuration", "pbad_gpu_create", "pbad_gpu_destroy",
-    "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
+    "pbad_gpu_total_steps", "pbad_gpu_path", "pbad_gpu_kernel_launches", "pbad_gpu_rollout", "pbad_gpu_begin", "pbad_gpu_advance", "pbad_gpu_sync_outputs",
     "pbad_gpu_state_device", "pbad_gpu_eval", "pbad_gpu_minimize", "pbad_gpu_correlation",
     "pbad_gpu_simulate_baseline", "pbad_gpu_rollout_sharded", "pbad_gpu_final_state",
     "pbad_gpu_device_count", "pbad_gpu_correlation_suite", "pbad_gpu_functional",
@@ -114,6 +114,7 @@ def load():
         "pbad_gpu_destroy": ([vp], None),
         "pbad_gpu_total_steps": ([vp], C.c_int32),
         "pbad_gpu_path": ([vp], C.c_int32),
+        "pbad_gpu_kernel_launches": ([vp], C.c_int64),
         "pbad_gpu_rollout": ([vp, C.c_int32, _dp, _dp, C.POINTER(RolloutOut)], C.c_int32),
         "pbad_gpu_begin": ([vp, C.c_int32, vp, vp, vp], C.c_int32),
         "pbad_gpu_advance": ([vp, C.c_int32, vp], C.c_int32),

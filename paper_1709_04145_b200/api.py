@@ -354,6 +354,10 @@ class GpuContext:
     def advance(self, n_steps: int, stream: int = 0):
         check(_lib.load().pbad_gpu_advance(self._h, int(n_steps), C.c_void_p(stream) if stream else None))
 
+    def kernel_launches(self) -> int:
+        """Step kernels this context has launched so far (pbad_gpu_kernel_launches)."""
+        return int(_lib.load().pbad_gpu_kernel_launches(self._h))
+
     def sync_outputs(self, want_q=True, want_energy=True) -> Dict[str, np.ndarray]:
         o, bufs = self._out_struct(self._B, want_q, want_energy)
         check(_lib.load().pbad_gpu_sync_outputs(self._h, C.byref(o)))

@@ -496,6 +496,8 @@ struct pbad_gpu_ctx {
   bool tree = false;       // rollouts use the warp-per-env Newton kernel (pbad_tree.cu)
   TreeDesc td{};
   double* tws = nullptr;   // tree-path per-env workspace (GN, history transforms)
+  int* tsync = nullptr;    // tree-path multi-step launch: task counter + per-env step flags
+  long launches = 0;       // step kernels launched by advance_steps (pbad_gpu_kernel_launches)
   bool resid = false;      // rollouts use the CTA-per-env residual-form kernel (pbad_resid.cu)
   ResidDesc rd{};
   double* rws = nullptr;
@@ -1186,6 +1188,13 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
       return fail(PBAD_E_CUDA, "cudaMalloc failed (tree workspace %.1f MB)", c->td.gstride * 8.0 * max_batch / 1e6);
     }
     c->owned.push_back(c->tws);
+    double* ts = dalloc<double>((size_t)(max_batch + 2) / 2 + 1);
+    if (!ts) {
+      delete c;
+      return fail(PBAD_E_CUDA, "cudaMalloc failed (tree step flags)");
+    }
+    c->owned.push_back(ts);
+    c->tsync = reinterpret_cast<int*>(ts);
   }
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
@@ -1199,6 +1208,7 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
 
 void pbad_gpu_destroy(pbad_gpu_ctx* c) { delete c; }
 int32_t pbad_gpu_total_steps(const pbad_gpu_ctx* c) { return c->total_steps; }
+int64_t pbad_gpu_kernel_launches(const pbad_gpu_ctx* c) { return c->launches; }
 int32_t pbad_gpu_path(const pbad_gpu_ctx* c) {
   return c->chain5 ? PBAD_PATH_CHAIN5
          : c->chain6 ? PBAD_PATH_CHAIN6
@@ -1317,7 +1327,14 @@ int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, cons
 
 int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
   c->work_stream = s;
-  for (long k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done)
+  if (c->tree && !c->td.lb) {
+    // the tree family runs a window's steps in one persistent launch (pbad_tree.cu)
+    const long k = std::min(n_steps, (long)c->total_steps - c->steps_done);
+    if (k > 0) CUDA_TRY(launch_tree_steps(c->ka, c->td, c->tws, c->dout, (int)k, c->tsync, s, &c->launches));
+    if (k > 0) c->steps_done += k;
+    return PBAD_OK;
+  }
+  for (long k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done, ++c->launches)
     CUDA_TRY(c->chain5  ? launch_chain5_step(c->ca, c->chain4_pat, c->chain4_recw / 8, c->dout, s)
              : c->chain6 ? launch_chain6_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain7 ? launch_chain7_step(c->ca, c->chain4_pat, c->dout, s)

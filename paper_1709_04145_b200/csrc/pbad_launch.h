@@ -57,6 +57,8 @@ bool tree_eligible_sizes(int N, int n);
 size_t tree_smem_bytes(const TreeDesc& td);
 cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
                              cudaStream_t s);
+cudaError_t launch_tree_steps(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out, int nsteps,
+                              int* sync, cudaStream_t s, long* launches);
 // L-BFGS on trees (pbad_tree_lbfgs.cu, same device code compiled as its own
 // translation unit so the LM kernel's register allocation is unaffected)
 cudaError_t launch_tree_lbfgs(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,

@@ -25,6 +25,9 @@
 // bit-identical to the reference build and the C oracle (tests/test_gpu_parity.py).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "pbad_joint.cuh"
 #include "pbad_kernels.cuh"
 #include "pbad_launch.h"
@@ -803,13 +806,9 @@ template <bool POT>
 #ifndef PBAD_TREE_MINB
 #define PBAD_TREE_MINB 11  // 168 registers: 12 single-warp blocks per SM by registers, ~10 by shared memory
 #endif
-__global__ void __launch_bounds__(32, PBAD_TREE_MINB) k_tree_step(const __grid_constant__ DModel m, const __grid_constant__ DForces f,
-                                                  const __grid_constant__ DSchedule sc, const __grid_constant__ Layout L,
-                                                  double* ws, int* iws, long B, const __grid_constant__ TreeDesc td,
-                                                  double* tws, const __grid_constant__ Outputs out) {
-  extern __shared__ __align__(16) double smem[];
-  const long e = blockIdx.x;
-  if (e >= B) return;
+__device__ __forceinline__ void tree_env_step(const DModel& m, const DForces& f, const DSchedule& sc, const Layout& L,
+                                              double* ws, int* iws, long B, const TreeDesc& td, double* tws,
+                                              const Outputs& out, long e, double* smem) {
   if (iws[(long)IS_RUN * B + e] != TR_RUNNING) return;
   W w;
   w.m = &m;
@@ -1093,6 +1092,74 @@ __global__ void __launch_bounds__(32, PBAD_TREE_MINB) k_tree_step(const __grid_c
   }
   if (out.q) {
     for (int k = w.lane; k < n; k += 32) out.q[out.qrow(e, step + 1) * n + k] = w.x[k];
+  }
+}
+
+// One PBAD step of environment blockIdx.x (one launch per step).
+template <bool POT>
+__global__ void __launch_bounds__(32, PBAD_TREE_MINB) k_tree_step(const __grid_constant__ DModel m, const __grid_constant__ DForces f,
+                                                  const __grid_constant__ DSchedule sc, const __grid_constant__ Layout L,
+                                                  double* ws, int* iws, long B, const __grid_constant__ TreeDesc td,
+                                                  double* tws, const __grid_constant__ Outputs out) {
+  extern __shared__ __align__(16) double smem[];
+  const long e = blockIdx.x;
+  if (e >= B) return;
+  tree_env_step<POT>(m, f, sc, L, ws, iws, B, td, tws, out, e, smem);
+}
+
+// nsteps PBAD steps of every environment in one persistent launch.  Warps
+// claim env-steps t = s B + e in order from a counter; an env-step waits (in
+// practice never: its predecessor was claimed B tasks earlier) until its
+// environment's previous step is done, so an environment starts its next
+// step as soon as its current one ends and the per-step tail -- the last
+// resident warps of a step running while the SMs drain -- is paid once per
+// launch instead of once per step.  The predecessor is always held by a
+// running warp, so the wait cannot deadlock.  Every env-step runs the same
+// code as k_tree_step, so results are bit-identical.
+#ifndef PBAD_TREE_STEP_CALL
+#define PBAD_TREE_STEP_CALL 0  // 1: the persistent kernel calls the env-step body out of line
+#endif
+template <bool POT>
+__device__ __noinline__ void tree_env_step_call(const DModel& m, const DForces& f, const DSchedule& sc, const Layout& L,
+                                                double* ws, int* iws, long B, const TreeDesc& td, double* tws,
+                                                const Outputs& out, long e, double* smem) {
+  tree_env_step<POT>(m, f, sc, L, ws, iws, B, td, tws, out, e, smem);
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <bool POT>
+__global__ void __launch_bounds__(32, PBAD_TREE_MINB) k_tree_steps(const __grid_constant__ DModel m, const __grid_constant__ DForces f,
+                                                   const __grid_constant__ DSchedule sc, const __grid_constant__ Layout L,
+                                                   double* ws, int* iws, long B, const __grid_constant__ TreeDesc td,
+                                                   double* tws, const __grid_constant__ Outputs out, int nsteps,
+                                                   unsigned long long* counter, int* done) {
+  extern __shared__ __align__(16) double smem[];
+  const unsigned long long total = (unsigned long long)nsteps * (unsigned long long)B;
+  for (;;) {
+    unsigned long long t = 0;
+    if (threadIdx.x == 0) t = atomicAdd(counter, 1ull);
+    t = __shfl_sync(FULL, t, 0);
+    if (t >= total) break;
+    const long s = (long)(t / (unsigned long long)B), e = (long)(t - (unsigned long long)s * B);
+    // lane 0's acquire (which also drops this SM's L1 lines) then the warp
+    // barrier order the other lanes' reads of the environment's state after
+    // the release below of the SM that ran its previous step
+    if (s > 0 && threadIdx.x == 0)
+      while (ld_acquire_gpu(done + e) < s) __nanosleep(100);
+    __syncwarp();
+#if PBAD_TREE_STEP_CALL
+    tree_env_step_call<POT>(m, f, sc, L, ws, iws, B, td, tws, out, e, smem);
+#else
+    tree_env_step<POT>(m, f, sc, L, ws, iws, B, td, tws, out, e, smem);
+#endif
+    __syncwarp();  // every lane's stores of this env-step before lane 0's release
+    if (threadIdx.x == 0) st_release_gpu(done + e, (int)s + 1);
   }
 }
 
@@ -1449,6 +1516,63 @@ cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tw
   }
   if (pot) tree::k_tree_step<true><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
   else tree::k_tree_step<false><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
+  return cudaGetLastError();
+}
+
+// Persistent launches pay where an env-step's LM iteration count varies a
+// lot across the batch (ground contact: 6 to 512 iterations, C4b 120 -> 113
+// ms/step); for smooth scenes the per-step launches are faster (C4 3.46 vs
+// 3.62 ms/step: the acquire's L1 invalidation per env-step costs more than
+// the short per-step tail).  PBAD_TREE_PERSIST: 0 never, 1 (default)
+// contact scenes, 2 always.
+bool tree_persistent(const TreeDesc& td, int nsteps) {
+  static const int mode = std::getenv("PBAD_TREE_PERSIST") ? std::atoi(std::getenv("PBAD_TREE_PERSIST")) : 1;
+  if (td.lb || nsteps <= 1 || mode == 0) return false;
+  return mode == 2 || (td.pot && td.ns > 0);
+}
+
+// nsteps steps: one persistent launch (k_tree_steps) where tree_persistent(),
+// else one k_tree_step launch per step.  sync: 2 + B ints of device memory.
+// *launches: kernels launched.
+cudaError_t launch_tree_steps(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out, int nsteps,
+                              int* sync, cudaStream_t s, long* launches) {
+  if (!tree_persistent(td, nsteps) || !sync) {
+    *launches += nsteps;
+    for (int k = 0; k < nsteps; ++k) {
+      const cudaError_t e = launch_tree_step(a, td, tws, out, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  const size_t smem = tree_smem_bytes(td);
+  const int pot = td.pot ? 1 : 0;
+  static size_t configured[2] = {0, 0};
+  static int slots[2] = {0, 0};
+  if (smem > configured[pot] || !slots[pot]) {
+    if (smem > 48 * 1024) {
+      cudaError_t e = pot ? cudaFuncSetAttribute(tree::k_tree_steps<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                          : cudaFuncSetAttribute(tree::k_tree_steps<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    configured[pot] = smem;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = pot ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tree::k_tree_steps<true>, 32, smem)
+                        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tree::k_tree_steps<false>, 32, smem);
+    if (e != cudaSuccess) return e;
+    slots[pot] = (per > 0 ? per : 1) * (sms > 0 ? sms : 148);
+  }
+  cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(int) * (size_t)(2 + a.B), s);
+  if (e != cudaSuccess) return e;
+  *launches += 1;
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(sync);
+  int* done = sync + 2;
+  const unsigned grid = (unsigned)std::min<long>(a.B, slots[pot]);
+  if (pot)
+    tree::k_tree_steps<true><<<grid, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out, nsteps, counter, done);
+  else
+    tree::k_tree_steps<false><<<grid, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out, nsteps, counter, done);
   return cudaGetLastError();
 }
 

@@ -254,3 +254,43 @@ def test_tree_path_lbfgs_equals_general_kernel(monkeypatch):
     for x, y in zip(a, b):
         np.testing.assert_array_equal(np.array([s[1] for s in x.samples]), np.array([s[1] for s in y.samples]))
         assert [r.iterations for r in x.solve_reports] == [r.iterations for r in y.solve_reports]
+
+
+def test_tree_persistent_multistep_contact(tmp_path):
+    """Contact scenes run a window of steps in one persistent launch
+    (k_tree_steps, pbad_tree.cu): warps claim env-steps in order and wait for
+    the environment's previous step, which ran on another SM.  With a batch
+    larger than the resident warps every environment changes SM between
+    steps.  The whole batch is bit-identical to one launch per step
+    (PBAD_TREE_PERSIST=0), and a sample matches the oracle."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    B, steps = 2500, 5
+    res = {}
+    for mode in ("1", "0"):
+        p = tmp_path / f"r{mode}.npz"
+        env = dict(os.environ, PBAD_TREE_PERSIST=mode, PYTHONPATH=os.path.dirname(here))
+        subprocess.run([sys.executable, os.path.join(here, "_tree_persist_run.py"), str(p), str(B), str(steps)],
+                       check=True, env=env, timeout=600)
+        res[mode] = np.load(p)
+    per, one = res["0"], res["1"]
+    assert int(one["path"]) == PATH_TREE
+    assert int(one["launches"]) == 1 and int(per["launches"]) == steps
+    for k in ("q", "energy", "iterations"):
+        np.testing.assert_array_equal(one[k], per[k])
+    assert one["iterations"].max() > one["iterations"].min()  # the iteration counts do vary
+    sys.path.insert(0, here)
+    import _tree_persist_run as tr
+    sc = tr.scene()
+    n = 41
+    q0 = tr.inputs(B, n, sc.q0)
+    sim = SimConfig(dt=0.01, duration=0.01 * steps)
+    envs = [0, 1777, B - 1]
+    ref = oracle.batch_simulate(oracle.Model(sc.links), sc.forces(), _sims(sim, n, len(envs), lambda i: q0[envs[i]]),
+                                workers=3)
+    for i, b in enumerate(envs):
+        k = ref[i].n_samples
+        np.testing.assert_array_equal(one["q"][b, :k], ref[i].q[:k])
+        np.testing.assert_array_equal(one["iterations"][b, :len(ref[i].iterations)], ref[i].iterations)
