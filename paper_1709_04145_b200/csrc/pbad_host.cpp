@@ -496,7 +496,7 @@ struct pbad_gpu_ctx {
   bool tree = false;       // rollouts use the warp-per-env Newton kernel (pbad_tree.cu)
   TreeDesc td{};
   double* tws = nullptr;   // tree-path per-env workspace (GN, history transforms)
-  int* tsync = nullptr;    // tree-path multi-step launch: task counter + per-env step flags
+  int* tsync = nullptr;    // tree / residual multi-step launches: task counter + per-env step flags
   long launches = 0;       // step kernels launched by advance_steps (pbad_gpu_kernel_launches)
   bool resid = false;      // rollouts use the CTA-per-env residual-form kernel (pbad_resid.cu)
   ResidDesc rd{};
@@ -1180,6 +1180,13 @@ int32_t pbad_gpu_create(const pbad_gpu_model* model, const pbad_forces* f, const
       return fail(PBAD_E_CUDA, "cudaMalloc failed (residual workspace %.1f MB)", rd.gstride * 8.0 * max_batch / 1e6);
     }
     c->owned.push_back(c->rws);
+    double* ts = dalloc<double>((size_t)(max_batch + 2) / 2 + 1);
+    if (!ts) {
+      delete c;
+      return fail(PBAD_E_CUDA, "cudaMalloc failed (residual step flags)");
+    }
+    c->owned.push_back(ts);
+    c->tsync = reinterpret_cast<int*>(ts);
   }
   if (c->tree) {
     c->tws = dalloc<double>((size_t)c->td.gstride * max_batch);
@@ -1327,6 +1334,13 @@ int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, cons
 
 int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
   c->work_stream = s;
+  if (c->resid) {
+    // one persistent launch per window (pbad_resid.cu k_resid_steps)
+    const long k = std::min(n_steps, (long)c->total_steps - c->steps_done);
+    if (k > 0) CUDA_TRY(launch_resid_steps(c->ka, c->rd, c->rws, c->dout, (int)k, c->tsync, s, &c->launches));
+    if (k > 0) c->steps_done += k;
+    return PBAD_OK;
+  }
   if (c->tree && !c->td.lb) {
     // the tree family runs a window's steps in one persistent launch (pbad_tree.cu)
     const long k = std::min(n_steps, (long)c->total_steps - c->steps_done);

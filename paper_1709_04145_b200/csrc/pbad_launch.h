@@ -69,6 +69,8 @@ bool resid_eligible_sizes(int N, int u);
 size_t resid_smem_bytes(int N, int u);
 cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out,
                               cudaStream_t s);
+cudaError_t launch_resid_steps(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out, int nsteps,
+                               int* sync, cudaStream_t s, long* launches);
 
 cudaError_t launch_init(const KernelArgs& a, const double* q0, const double* qdot0, const double* hist0,
                         const Outputs& out, cudaStream_t s);

@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "pbad_joint.cuh"
 #include "pbad_kernels.cuh"
@@ -2422,14 +2423,11 @@ __device__ __noinline__ void tau_at(const R& r, double t, double* dst) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DModel m,
-                                                      const __grid_constant__ DForces f,
-                                                      const __grid_constant__ DSchedule sc,
-                                                      const __grid_constant__ Layout L, double* ws, int* iws, long B,
-                                                      const __grid_constant__ ResidDesc rd, double* rws,
-                                                      const __grid_constant__ Outputs out) {
-  const long e = blockIdx.x;
-  if (e >= B) return;
+// One PBAD step of environment e by the whole CTA.  Every early return is
+// CTA-uniform.
+__device__ __forceinline__ void resid_env_step(const DModel& m, const DForces& f, const DSchedule& sc, const Layout& L,
+                                               double* ws, int* iws, long B, const ResidDesc& rd, double* rws,
+                                               const Outputs& out, const long e) {
   if (iws[(long)IS_RUN * B + e] != TR_RUNNING) return;
   R r;
   r.m = &m;
@@ -2615,6 +2613,52 @@ __global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DM
 #endif
 }
 
+__global__ void __launch_bounds__(NT, 1) k_resid_step(const __grid_constant__ DModel m,
+                                                      const __grid_constant__ DForces f,
+                                                      const __grid_constant__ DSchedule sc,
+                                                      const __grid_constant__ Layout L, double* ws, int* iws, long B,
+                                                      const __grid_constant__ ResidDesc rd, double* rws,
+                                                      const __grid_constant__ Outputs out) {
+  const long e = blockIdx.x;
+  if (e >= B) return;
+  resid_env_step(m, f, sc, L, ws, iws, B, rd, rws, out, e);
+}
+
+// nsteps PBAD steps of every environment in one persistent launch, one CTA
+// per SM claiming env-steps t = s B + e in order (the tree kernel's scheme,
+// pbad_tree.cu k_tree_steps): an env-step waits for its environment's
+// previous step (release / acquire on a per-environment flag), so the SMs
+// stay busy across step boundaries.  C5's 256 environments on 148 SMs need
+// two waves per step with per-step launches (1.73 waves of work).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void __launch_bounds__(NT, 1) k_resid_steps(const __grid_constant__ DModel m,
+                                                       const __grid_constant__ DForces f,
+                                                       const __grid_constant__ DSchedule sc,
+                                                       const __grid_constant__ Layout L, double* ws, int* iws, long B,
+                                                       const __grid_constant__ ResidDesc rd, double* rws,
+                                                       const __grid_constant__ Outputs out, int nsteps,
+                                                       unsigned long long* counter, int* done) {
+  __shared__ unsigned long long task;
+  const unsigned long long total = (unsigned long long)nsteps * (unsigned long long)B;
+  for (;;) {
+    if (threadIdx.x == 0) task = atomicAdd(counter, 1ull);
+    __syncthreads();
+    const unsigned long long t = task;
+    if (t >= total) break;
+    const long s = (long)(t / (unsigned long long)B), e = (long)(t - (unsigned long long)s * B);
+    if (s > 0 && threadIdx.x == 0)
+      while (ld_acquire_gpu(done + e) < s) __nanosleep(200);
+    __syncthreads();  // thread 0's acquire orders the CTA's reads of the environment's state
+    resid_env_step(m, f, sc, L, ws, iws, B, rd, rws, out, e);
+    __syncthreads();  // every thread's stores of this env-step before the release; task reusable
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(done + e), "r"((int)s + 1) : "memory");
+  }
+}
+
 }  // namespace resid
 
 bool resid_eligible_sizes(int N, int u) {
@@ -2644,6 +2688,43 @@ cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* 
     configured = smem;
   }
   resid::k_resid_step<<<(unsigned)a.B, resid::NT, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, rd, rws, out);
+  return cudaGetLastError();
+}
+
+// nsteps steps: one persistent launch (k_resid_steps) unless
+// PBAD_RESID_PERSIST=0, else one k_resid_step launch per step.  sync: 2 + B
+// ints of device memory; *launches: kernels launched.
+cudaError_t launch_resid_steps(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out, int nsteps,
+                               int* sync, cudaStream_t s, long* launches) {
+  static const int mode = std::getenv("PBAD_RESID_PERSIST") ? std::atoi(std::getenv("PBAD_RESID_PERSIST")) : 1;
+  if (mode == 0 || nsteps <= 1 || !sync) {
+    for (int k = 0; k < nsteps; ++k) {
+      const cudaError_t e = launch_resid_step(a, rd, rws, out, s);
+      if (e != cudaSuccess) return e;
+    }
+    *launches += nsteps;
+    return cudaSuccess;
+  }
+  const size_t smem = resid_smem_bytes(rd.N, rd.u);
+  static size_t configured = 0;
+  static int slots = 0;
+  if (smem > configured || !slots) {
+    cudaError_t e = cudaFuncSetAttribute(resid::k_resid_steps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, resid::k_resid_steps, resid::NT, smem);
+    if (e != cudaSuccess) return e;
+    slots = (per > 0 ? per : 1) * (sms > 0 ? sms : 148);
+  }
+  cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(int) * (size_t)(2 + a.B), s);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)std::min<long>(a.B, slots);
+  resid::k_resid_steps<<<grid, resid::NT, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, rd, rws, out, nsteps,
+                                                      reinterpret_cast<unsigned long long*>(sync), sync + 2);
+  *launches += 1;
   return cudaGetLastError();
 }
 

@@ -216,3 +216,30 @@ def test_resid_u2_beyond_320():
                     consecutive_fail_limit=10)
     sim.optimizer.max_iters = 12
     _check(sc, sim, _sims(sim, 180, 2, lambda b: mt19937_uniform(b + 60, 180, -0.3, 0.3)))
+
+
+def test_resid_persistent_multistep(tmp_path):
+    """The CTA kernel runs a window of steps in one persistent launch
+    (k_resid_steps, pbad_resid.cu), one CTA per SM claiming env-steps in
+    order.  300 environments on 148 SMs: environments change SM between
+    steps and wait on their previous step.  The whole batch is bit-identical
+    to one launch per step (PBAD_RESID_PERSIST=0), and a sample matches the
+    oracle."""
+    import _persist_run as pr
+    B, steps = 300, 4
+    one, per = pr.run_pair("resid", tmp_path, B, steps, "PBAD_RESID_PERSIST")
+    assert int(one["path"]) == PATH_RESID
+    assert int(one["launches"]) == 1 and int(per["launches"]) == steps
+    for k in ("q", "energy", "iterations"):
+        np.testing.assert_array_equal(one[k], per[k])
+    sc = pr.scene("resid")
+    n = 12
+    q0 = pr.inputs("resid", B, n, sc.q0)
+    sim = pr.sim("resid", steps)
+    envs = [0, 149, B - 1]
+    ref = oracle.batch_simulate(oracle.Model(sc.links), sc.forces(), _sims(sim, n, len(envs), lambda i: q0[envs[i]]),
+                                workers=3)
+    for i, b in enumerate(envs):
+        k = ref[i].n_samples
+        np.testing.assert_array_equal(one["q"][b, :k], ref[i].q[:k])
+        np.testing.assert_array_equal(one["iterations"][b, :len(ref[i].iterations)], ref[i].iterations)

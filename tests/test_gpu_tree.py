@@ -263,30 +263,18 @@ def test_tree_persistent_multistep_contact(tmp_path):
     larger than the resident warps every environment changes SM between
     steps.  The whole batch is bit-identical to one launch per step
     (PBAD_TREE_PERSIST=0), and a sample matches the oracle."""
-    import os
-    import subprocess
-    import sys
-    here = os.path.dirname(os.path.abspath(__file__))
+    import _persist_run as pr
     B, steps = 2500, 5
-    res = {}
-    for mode in ("1", "0"):
-        p = tmp_path / f"r{mode}.npz"
-        env = dict(os.environ, PBAD_TREE_PERSIST=mode, PYTHONPATH=os.path.dirname(here))
-        subprocess.run([sys.executable, os.path.join(here, "_tree_persist_run.py"), str(p), str(B), str(steps)],
-                       check=True, env=env, timeout=600)
-        res[mode] = np.load(p)
-    per, one = res["0"], res["1"]
+    one, per = pr.run_pair("tree_contact", tmp_path, B, steps, "PBAD_TREE_PERSIST")
     assert int(one["path"]) == PATH_TREE
     assert int(one["launches"]) == 1 and int(per["launches"]) == steps
     for k in ("q", "energy", "iterations"):
         np.testing.assert_array_equal(one[k], per[k])
     assert one["iterations"].max() > one["iterations"].min()  # the iteration counts do vary
-    sys.path.insert(0, here)
-    import _tree_persist_run as tr
-    sc = tr.scene()
+    sc = pr.scene("tree_contact")
     n = 41
-    q0 = tr.inputs(B, n, sc.q0)
-    sim = SimConfig(dt=0.01, duration=0.01 * steps)
+    q0 = pr.inputs("tree_contact", B, n, sc.q0)
+    sim = pr.sim("tree_contact", steps)
     envs = [0, 1777, B - 1]
     ref = oracle.batch_simulate(oracle.Model(sc.links), sc.forces(), _sims(sim, n, len(envs), lambda i: q0[envs[i]]),
                                 workers=3)
