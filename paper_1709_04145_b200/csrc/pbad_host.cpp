@@ -1334,6 +1334,12 @@ int32_t begin_batch(pbad_gpu_ctx* c, int32_t B, long W, const double* d_q0, cons
 
 int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
   c->work_stream = s;
+  if (c->chain6) {
+    const long k = std::min(n_steps, (long)c->total_steps - c->steps_done);
+    if (k > 0) CUDA_TRY(launch_chain6_steps(c->ca, c->chain4_pat, c->dout, (int)k, s, &c->launches));
+    if (k > 0) c->steps_done += k;
+    return PBAD_OK;
+  }
   if (c->resid) {
     // one persistent launch per window (pbad_resid.cu k_resid_steps)
     const long k = std::min(n_steps, (long)c->total_steps - c->steps_done);
@@ -1350,7 +1356,6 @@ int32_t advance_steps(pbad_gpu_ctx* c, long n_steps, cudaStream_t s) {
   }
   for (long k = 0; k < n_steps && c->steps_done < c->total_steps; ++k, ++c->steps_done, ++c->launches)
     CUDA_TRY(c->chain5  ? launch_chain5_step(c->ca, c->chain4_pat, c->chain4_recw / 8, c->dout, s)
-             : c->chain6 ? launch_chain6_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain7 ? launch_chain7_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain4 ? launch_chain4_step(c->ca, c->chain4_pat, c->dout, s)
              : c->chain ? launch_chain_step(c->ca, c->dout, s)

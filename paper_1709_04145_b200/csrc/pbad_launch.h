@@ -45,7 +45,8 @@ int chain5_waves(int N, int n, int mem, long B, int pattern, int device);
 // chain v6 (pbad_chain6.cu): v4 with two lanes per row, 4 environments per warp
 bool chain6_fits(int N, int mem);
 long chain6_vector_doubles(long B, int n);
-cudaError_t launch_chain6_step(const ChainArgs& a, int pattern, const Outputs& out, cudaStream_t s);
+cudaError_t launch_chain6_steps(const ChainArgs& a, int pattern, const Outputs& out, int nsteps, cudaStream_t s,
+                                long* launches);
 cudaError_t launch_chain5_step(const ChainArgs& a, int pattern, long recw, const Outputs& out, cudaStream_t s);
 // chain v7 (pbad_chain7.cu): 16 lanes per environment, link-parallel energy terms
 bool chain7_fits(int N, int mem, int pattern);
