@@ -624,6 +624,11 @@ struct Solver {
   double tdx;         // tau . cand of the pending candidate
   int status, iters, stag, acc, h0, hc, trial, phase;
   double* itv;        // per_iteration_values row of this step (lane j = 0 writes), or null
+  // s . g and y . y of the pair the last accepted step pushed (PBAD_C6_FUSE):
+  // the two-loop's first dot and its y_{hc-1} . y_{hc-1}, computed in the
+  // accepted-step pass with the same operands and partial order
+  double pre_sg, pre_yy;
+  bool pre;
 };
 
 #ifndef PBAD_C6_KB
@@ -664,17 +669,25 @@ __device__ __forceinline__ void l2_prefetch(const Ctx& C, const double* V) {
 }
 
 // two-loop passes: q' = op(q, w); then DOT 0: z . q'; 1: z . z; 2: dir = -q', dir . g
-enum { M_COPY = 0, M_SUB = 1, M_SCALE = 2, M_ADD = 3 };
+enum { M_COPY = 0, M_SUB = 1, M_SCALE = 2, M_ADD = 3, M_SUBSCALE = 4 };
+// PBAD_C6_FUSE (default 1): with the pushed pair's s . g and y . y from the
+// accepted-step pass, the two-loop skips its copy pass (q = g; the first
+// M_SUB pass reads g as q) and merges the scale pass into loop 1's last pass
+// (M_SUBSCALE: q = (q - a y_0) scl; y_0 . q): two of the iteration's vector
+// passes fewer, every value unchanged.
+#ifndef PBAD_C6_FUSE
+#define PBAD_C6_FUSE 1
+#endif
 template <bool F, int MODE, int DOT>
-__device__ __forceinline__ void tl_batch(const Ctx& C, const double* w, double a, const double* z, bool store_q, int g0,
-                                         double* acc) {
+__device__ __forceinline__ void tl_batch(const Ctx& C, const double* qs, const double* w, double a, double a2,
+                                         const double* z, bool store_q, int g0, double* acc) {
   double qv_[kB], wv[kB], zv[kB];
   // loop 2 and the scale pass are a history vector's last read of the iteration
-  constexpr bool LAST = (PBAD_C6_HINT & 1) && (MODE == M_ADD || MODE == M_SCALE);
-  if (MODE != M_COPY) ldb<F>(C, C.q, g0, qv_);
+  constexpr bool LAST = (PBAD_C6_HINT & 1) && (MODE == M_ADD || MODE == M_SCALE || MODE == M_SUBSCALE);
+  if (MODE != M_COPY) ldb<F>(C, qs, g0, qv_);
   if (MODE != M_SCALE) ldb<F, LAST>(C, w, g0, wv);
   if (DOT == 2) ldb<F>(C, C.g, g0, zv);
-  else ldb<F, LAST>(C, z, g0, zv);
+  else if (MODE != M_SUBSCALE) ldb<F, LAST>(C, z, g0, zv);  // M_SUBSCALE: z = w
   double* qo = C.q + (long)g0 * kGS;
   double* dout = C.dir + (long)g0 * kGS;
 #pragma unroll
@@ -684,6 +697,7 @@ __device__ __forceinline__ void tl_batch(const Ctx& C, const double* w, double a
     if (MODE == M_COPY) qn = wv[jj];
     else if (MODE == M_SUB) qn = qv_[jj] - a * wv[jj];
     else if (MODE == M_SCALE) qn = qv_[jj] * a;
+    else if (MODE == M_SUBSCALE) qn = (qv_[jj] - a * wv[jj]) * a2;
     else qn = qv_[jj] + a * wv[jj];
     if (DOT == 2) {
       const double d = -qn;
@@ -691,17 +705,20 @@ __device__ __forceinline__ void tl_batch(const Ctx& C, const double* w, double a
       acc[jj & 3] = fma(d, zv[jj], acc[jj & 3]);
     } else {
       if (store_q) qo[jj * kGS] = qn;
-      if (DOT == 0) acc[jj & 3] = fma(zv[jj], qn, acc[jj & 3]);
+      if (DOT == 0 && MODE == M_SUBSCALE) acc[jj & 3] = fma(wv[jj], qn, acc[jj & 3]);
+      else if (DOT == 0) acc[jj & 3] = fma(zv[jj], qn, acc[jj & 3]);
       else acc[jj & 3] = fma(zv[jj], zv[jj], acc[jj & 3]);
     }
   }
 }
 template <int MODE, int DOT>
-__device__ __forceinline__ double tl_pass(const Ctx& C, const double* w, double a, const double* z, bool store_q) {
+__device__ __forceinline__ double tl_pass(const Ctx& C, const double* w, double a, const double* z, bool store_q,
+                                         const double* qs = nullptr, double a2 = 0.0) {
+  if (!qs) qs = C.q;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   int g0 = 0;
-  for (; g0 + kB <= C.nf; g0 += kB) tl_batch<true, MODE, DOT>(C, w, a, z, store_q, g0, acc);
-  for (; g0 < C.n8; g0 += kB) tl_batch<false, MODE, DOT>(C, w, a, z, store_q, g0, acc);
+  for (; g0 + kB <= C.nf; g0 += kB) tl_batch<true, MODE, DOT>(C, qs, w, a, a2, z, store_q, g0, acc);
+  for (; g0 < C.n8; g0 += kB) tl_batch<false, MODE, DOT>(C, qs, w, a, a2, z, store_q, g0, acc);
   return dot_finish(C, acc);
 }
 
@@ -718,6 +735,50 @@ __device__ __forceinline__ const double* hist_y(const Ctx& C, const Solver& s, i
 }
 __device__ __forceinline__ double hist_sy(const Ctx& C, const Solver& s, int i) { return C.hsy[hslot(C, s, i)]; }
 
+// loop 2 of the two-loop from q and y_0 . q (shared by both variants)
+__device__ __forceinline__ double two_loop_2(const Ctx& C, const Solver& s, const double* alpha, double d) {
+  const int hc = s.hc;
+  double slope = 0.0;
+  for (int i = 0; i < hc; ++i) {
+    const double beta = d / hist_sy(C, s, i);
+    const double c = alpha[i] - beta;
+    if (i + 2 < hc) {
+      l2_prefetch(C, hist_s(C, s, i + 1));
+      l2_prefetch(C, hist_y(C, s, i + 2));
+    } else if (i + 1 < hc) {
+      l2_prefetch(C, hist_s(C, s, i + 1));
+    }
+    if (i + 1 < hc) d = tl_pass<M_ADD, 0>(C, hist_s(C, s, i), c, hist_y(C, s, i + 1), true);
+    else slope = tl_pass<M_ADD, 2>(C, hist_s(C, s, i), c, nullptr, false);  // dir = -q; dir . g
+  }
+  return slope;
+}
+
+// the two-loop with the pushed pair's s . g and y . y known (PBAD_C6_FUSE):
+// no copy pass (loop 1's first pass reads g as q) and loop 1's last pass
+// applies the scale (M_SUBSCALE)
+__device__ __forceinline__ double direction_fused(const Ctx& C, const Solver& s, double* alpha) {
+  const int hc = s.hc;
+  double d = s.pre_sg;  // s_{hc-1} . g
+  const double scl = hist_sy(C, s, hc - 1) / s.pre_yy;
+  for (int i = hc - 1; i >= 0; --i) {
+    const double a = d / hist_sy(C, s, i);
+    alpha[i] = a;
+    if (i >= 2) {
+      l2_prefetch(C, hist_y(C, s, i - 1));
+      l2_prefetch(C, hist_s(C, s, i - 2));
+    } else if (i == 1) {
+      l2_prefetch(C, hist_y(C, s, 0));
+    }
+    const double* qs = (i == hc - 1) ? C.g : C.q;  // q = g before the first pass
+    if (i > 0) d = tl_pass<M_SUB, 0>(C, hist_y(C, s, i), a, hist_s(C, s, i - 1), true, qs);
+    else d = tl_pass<M_SUBSCALE, 0>(C, hist_y(C, s, 0), a, nullptr, true, qs, scl);  // q = (q - a y_0) scl; y_0 . q
+  }
+  l2_prefetch(C, hist_s(C, s, 0));
+  if (hc > 1) l2_prefetch(C, hist_y(C, s, 1));
+  return two_loop_2(C, s, alpha, d);
+}
+
 // two_loop (optim.cpp:213-229) fused with dir = -q and slope = dir . g
 // (optim.cpp:162-170); returns the slope
 __device__ __forceinline__ double direction(const Ctx& C, const Solver& s) {
@@ -727,6 +788,7 @@ __device__ __forceinline__ double direction(const Ctx& C, const Solver& s) {
   l2_prefetch(C, hist_y(C, s, hc - 1));
   if (hc > 1) l2_prefetch(C, hist_s(C, s, hc - 2));
   double* alpha = C.hsy + kMaxMem + 1;
+  if (PBAD_C6_FUSE && s.pre) return direction_fused(C, s, alpha);
   double d = tl_pass<M_COPY, 0>(C, C.g, 0.0, hist_s(C, s, hc - 1), true);  // q = g; s . q
   double yy = 0.0;
   for (int i = hc - 1; i >= 0; --i) {
@@ -745,20 +807,7 @@ __device__ __forceinline__ double direction(const Ctx& C, const Solver& s) {
   if (hc > 1) l2_prefetch(C, hist_y(C, s, 1));
   const double scl = hist_sy(C, s, hc - 1) / yy;
   d = tl_pass<M_SCALE, 0>(C, nullptr, scl, hist_y(C, s, 0), true);  // q *= scl; y_0 . q
-  double slope = 0.0;
-  for (int i = 0; i < hc; ++i) {
-    const double beta = d / hist_sy(C, s, i);
-    const double c = alpha[i] - beta;
-    if (i + 2 < hc) {
-      l2_prefetch(C, hist_s(C, s, i + 1));
-      l2_prefetch(C, hist_y(C, s, i + 2));
-    } else if (i + 1 < hc) {
-      l2_prefetch(C, hist_s(C, s, i + 1));
-    }
-    if (i + 1 < hc) d = tl_pass<M_ADD, 0>(C, hist_s(C, s, i), c, hist_y(C, s, i + 1), true);
-    else slope = tl_pass<M_ADD, 2>(C, hist_s(C, s, i), c, nullptr, false);  // dir = -q; dir . g
-  }
-  return slope;
+  return two_loop_2(C, s, alpha, d);
 }
 
 // start of LbfgsSolver::iterate: termination tests, direction, slope
@@ -775,6 +824,7 @@ __device__ __forceinline__ void begin_iteration(const Ctx& C, Solver& s) {
     return;
   }
   double slope = direction(C, s);
+  s.pre = false;
   if (!(slope < 0.0)) {
     s.hc = 0;
     s.h0 = 0;
@@ -830,8 +880,8 @@ __device__ __forceinline__ void next_candidate(const Ctx& C, Solver& s) {
 }
 
 template <bool F>
-__device__ __forceinline__ void acc_batch(const Ctx& C, double t, double* sv, double* yv, int g0, double* acc, double& gm,
-                                          double& xm) {
+__device__ __forceinline__ void acc_batch(const Ctx& C, double t, double* sv, double* yv, int g0, double* acc, double* asg,
+                                          double* ayy, double& gm, double& xm) {
   double dv[kB], ev[kB], gv[kB], cv[kB];
   ldb<F>(C, C.dir, g0, dv);
   ldb<F>(C, C.evg, g0, ev);
@@ -849,6 +899,10 @@ __device__ __forceinline__ void acc_batch(const Ctx& C, double t, double* sv, do
     C.x[o] = cv[jj];
     C.g[o] = ev[jj];
     acc[jj & 3] = fma(sj, yj, acc[jj & 3]);
+    if (PBAD_C6_FUSE) {
+      asg[jj & 3] = fma(sj, ev[jj], asg[jj & 3]);  // s . g(new): the copy pass's z . q
+      ayy[jj & 3] = fma(yj, yj, ayy[jj & 3]);      // y . y: loop 1's DOT 1
+    }
     gm = fmax(gm, fabs(ev[jj]));
     xm = fmax(xm, fabs(cv[jj]));
   }
@@ -862,15 +916,21 @@ __device__ __forceinline__ void accept_step(const Ctx& C, Solver& s, double v) {
   double* sv = C.hs + slot * C.VS;
   double* yv = C.hy + slot * C.VS;
   const double t = s.t;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double acc[4] = {0.0, 0.0, 0.0, 0.0}, asg[4] = {0.0, 0.0, 0.0, 0.0}, ayy[4] = {0.0, 0.0, 0.0, 0.0};
   double gm = 0.0, xm = 0.0;
   int g0 = 0;
-  for (; g0 + kB <= C.nf; g0 += kB) acc_batch<true>(C, t, sv, yv, g0, acc, gm, xm);
-  for (; g0 < C.n8; g0 += kB) acc_batch<false>(C, t, sv, yv, g0, acc, gm, xm);
+  for (; g0 + kB <= C.nf; g0 += kB) acc_batch<true>(C, t, sv, yv, g0, acc, asg, ayy, gm, xm);
+  for (; g0 < C.n8; g0 += kB) acc_batch<false>(C, t, sv, yv, g0, acc, asg, ayy, gm, xm);
   const double sy = dot_finish(C, acc);
+  s.pre = false;
   s.ginf = emax(C, gm);
   s.xinf = emax(C, xm);
   if (sy > 1e-12) {
+    if (PBAD_C6_FUSE) {
+      s.pre = true;
+      s.pre_sg = dot_finish(C, asg);
+      s.pre_yy = dot_finish(C, ayy);
+    }
     if (C.j == 0) C.hsy[slot] = sy;
     ++s.hc;
     if (s.hc > C.o.mem) {
