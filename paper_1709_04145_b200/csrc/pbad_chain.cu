@@ -1103,7 +1103,8 @@ unsigned chain_grid(long B) { return (unsigned)((B + kEnvsPerBlock - 1) / kEnvsP
 
 static cudaError_t chain_smem_attr(int N, size_t* bytes) {
   *bytes = chain_smem_bytes(N);
-  static size_t configured = 0;  // per process; raised monotonically
+  static SmemAttr attr_;  // per device; raised monotonically
+  size_t& configured = attr_.here();
   if (*bytes > configured) {
     cudaError_t e = cudaFuncSetAttribute(k_chain_init, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*bytes);
     if (e == cudaSuccess)

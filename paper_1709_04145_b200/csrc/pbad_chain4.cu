@@ -1103,7 +1103,8 @@ __global__ void __launch_bounds__(kT) k_chain4_step(DModel m, DForces f, DSchedu
 template <int PAT>
 cudaError_t launch(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
   const size_t sm = smem_bytes(a.m.N);
-  static size_t configured = 0;
+  static SmemAttr attr_;
+  size_t& configured = attr_.here();
   if (sm > configured) {
     const cudaError_t e = cudaFuncSetAttribute(k_chain4_step<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -888,7 +888,8 @@ template <int PAT>
 cudaError_t launch(const ChainArgs& a, long recw, const Outputs& out, cudaStream_t s) {
   const int wpb = launch_wpb(a.m.N, a.m.n, a.sc.opt.mem, a.B, sm_count());
   const size_t sm = block_smem_bytes(a.m.N, a.m.n, a.sc.opt.mem, wpb) + 64;
-  static size_t configured = 0;
+  static SmemAttr attr_;
+  size_t& configured = attr_.here();
   if (sm > configured) {
     const cudaError_t e = cudaFuncSetAttribute(k_chain5_step<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

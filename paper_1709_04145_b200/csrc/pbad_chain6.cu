@@ -1184,7 +1184,8 @@ __global__ void __launch_bounds__(32 * KW) k_chain6_step(DModel m, DForces f, DS
 template <int PAT, int KW>
 cudaError_t launch_kw(const ChainArgs& a, const Outputs& out, int nsteps, cudaStream_t s) {
   const size_t sm = smem_bytes(a.m.N, KW);
-  static size_t configured = 0;
+  static SmemAttr attr_;
+  size_t& configured = attr_.here();
   if (sm > configured) {
     const cudaError_t e =
         cudaFuncSetAttribute(k_chain6_step<PAT, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

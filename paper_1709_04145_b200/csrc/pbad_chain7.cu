@@ -1111,7 +1111,8 @@ __global__ void __launch_bounds__(kT, 2) k_chain7_step(DModel m, DForces f, DSch
 template <int PAT>
 cudaError_t launch(const ChainArgs& a, const Outputs& out, cudaStream_t s) {
   const size_t sm = smem_bytes(a.m.N, PAT);
-  static size_t configured = 0;
+  static SmemAttr attr_;
+  size_t& configured = attr_.here();
   if (sm > configured) {
     const cudaError_t e = cudaFuncSetAttribute(k_chain7_step<PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

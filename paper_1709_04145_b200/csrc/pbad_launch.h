@@ -7,6 +7,18 @@
 
 namespace pbad_gpu {
 
+// Dynamic shared memory a kernel has been enabled for, per device:
+// cudaFuncSetAttribute acts on the current device only, so one process
+// driving several GPUs (pbad_gpu_rollout_sharded) sets it on each.
+struct SmemAttr {
+  size_t bytes[64] = {};
+  size_t& here() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return bytes[d & 63];
+  }
+};
+
 struct KernelArgs {
   DModel m;
   DForces f;

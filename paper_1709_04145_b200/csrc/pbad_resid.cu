@@ -2681,7 +2681,8 @@ size_t resid_smem_bytes(int N, int u) {
 cudaError_t launch_resid_step(const KernelArgs& a, const ResidDesc& rd, double* rws, const Outputs& out,
                               cudaStream_t s) {
   const size_t smem = resid_smem_bytes(rd.N, rd.u);
-  static size_t configured = 0;
+  static SmemAttr attr_;
+  size_t& configured = attr_.here();
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(resid::k_resid_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -2706,7 +2707,8 @@ cudaError_t launch_resid_steps(const KernelArgs& a, const ResidDesc& rd, double*
     return cudaSuccess;
   }
   const size_t smem = resid_smem_bytes(rd.N, rd.u);
-  static size_t configured = 0;
+  static SmemAttr attr_;
+  size_t& configured = attr_.here();
   static int slots = 0;
   if (smem > configured || !slots) {
     cudaError_t e = cudaFuncSetAttribute(resid::k_resid_steps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1506,13 +1506,13 @@ cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tw
                              cudaStream_t s) {
   const size_t smem = tree_smem_bytes(td);
   if (td.lb) return launch_tree_lbfgs(a, td, tws, out, s);
-  static size_t configured[2] = {0, 0};
+  static SmemAttr attr_[2];
   const int pot = td.pot ? 1 : 0;
-  if (smem > 48 * 1024 && smem > configured[pot]) {
+  if (smem > 48 * 1024 && smem > attr_[pot].here()) {
     cudaError_t e = pot ? cudaFuncSetAttribute(tree::k_tree_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                         : cudaFuncSetAttribute(tree::k_tree_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured[pot] = smem;
+    attr_[pot].here() = smem;
   }
   if (pot) tree::k_tree_step<true><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
   else tree::k_tree_step<false><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
@@ -1525,7 +1525,7 @@ cudaError_t launch_tree_step(const KernelArgs& a, const TreeDesc& td, double* tw
 // 3.62 ms/step: the acquire's L1 invalidation per env-step costs more than
 // the short per-step tail).  PBAD_TREE_PERSIST: 0 never, 1 (default)
 // contact scenes, 2 always.
-bool tree_persistent(const TreeDesc& td, int nsteps) {
+static bool tree_persistent(const TreeDesc& td, int nsteps) {
   static const int mode = std::getenv("PBAD_TREE_PERSIST") ? std::atoi(std::getenv("PBAD_TREE_PERSIST")) : 1;
   if (td.lb || nsteps <= 1 || mode == 0) return false;
   return mode == 2 || (td.pot && td.ns > 0);
@@ -1546,15 +1546,15 @@ cudaError_t launch_tree_steps(const KernelArgs& a, const TreeDesc& td, double* t
   }
   const size_t smem = tree_smem_bytes(td);
   const int pot = td.pot ? 1 : 0;
-  static size_t configured[2] = {0, 0};
+  static SmemAttr attr_[2];
   static int slots[2] = {0, 0};
-  if (smem > configured[pot] || !slots[pot]) {
+  if (smem > attr_[pot].here() || !slots[pot]) {
     if (smem > 48 * 1024) {
       cudaError_t e = pot ? cudaFuncSetAttribute(tree::k_tree_steps<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                           : cudaFuncSetAttribute(tree::k_tree_steps<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
-    configured[pot] = smem;
+    attr_[pot].here() = smem;
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1583,13 +1583,13 @@ cudaError_t launch_tree_steps(const KernelArgs& a, const TreeDesc& td, double* t
 cudaError_t launch_tree_lbfgs(const KernelArgs& a, const TreeDesc& td, double* tws, const Outputs& out,
                               cudaStream_t s) {
   const size_t smem = tree_smem_bytes(td);
-  static size_t configured[2] = {0, 0};
+  static SmemAttr attr_[2];
   const int pot = td.pot ? 1 : 0;
-  if (smem > 48 * 1024 && smem > configured[pot]) {
+  if (smem > 48 * 1024 && smem > attr_[pot].here()) {
     cudaError_t e = pot ? cudaFuncSetAttribute(PBAD_TREE_NS::k_tree_lbfgs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                         : cudaFuncSetAttribute(PBAD_TREE_NS::k_tree_lbfgs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured[pot] = smem;
+    attr_[pot].here() = smem;
   }
   if (pot) PBAD_TREE_NS::k_tree_lbfgs<true><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
   else PBAD_TREE_NS::k_tree_lbfgs<false><<<(unsigned)a.B, 32, smem, s>>>(a.m, a.f, a.sc, a.L, a.ws, a.iws, a.B, td, tws, out);
