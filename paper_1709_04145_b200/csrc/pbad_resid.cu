@@ -2719,7 +2719,15 @@ cudaError_t launch_resid_steps(const KernelArgs& a, const ResidDesc& rd, double*
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, resid::k_resid_steps, resid::NT, smem);
     if (e != cudaSuccess) return e;
-    slots = (per > 0 ? per : 1) * (sms > 0 ? sms : 148);
+    slots = per > 0 ? per * (sms > 0 ? sms : 148) : -1;  // -1: does not fit (its 8 extra bytes of shared memory)
+  }
+  if (slots < 0) {
+    for (int k = 0; k < nsteps; ++k) {
+      const cudaError_t e = launch_resid_step(a, rd, rws, out, s);
+      if (e != cudaSuccess) return e;
+    }
+    *launches += nsteps;
+    return cudaSuccess;
   }
   cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(int) * (size_t)(2 + a.B), s);
   if (e != cudaSuccess) return e;

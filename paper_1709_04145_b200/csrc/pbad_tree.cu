@@ -1561,7 +1561,15 @@ cudaError_t launch_tree_steps(const KernelArgs& a, const TreeDesc& td, double* t
     cudaError_t e = pot ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tree::k_tree_steps<true>, 32, smem)
                         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tree::k_tree_steps<false>, 32, smem);
     if (e != cudaSuccess) return e;
-    slots[pot] = (per > 0 ? per : 1) * (sms > 0 ? sms : 148);
+    slots[pot] = per > 0 ? per * (sms > 0 ? sms : 148) : -1;  // -1: does not fit
+  }
+  if (slots[pot] < 0) {
+    for (int k = 0; k < nsteps; ++k) {
+      const cudaError_t e = launch_tree_step(a, td, tws, out, s);
+      if (e != cudaSuccess) return e;
+    }
+    *launches += nsteps;
+    return cudaSuccess;
   }
   cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(int) * (size_t)(2 + a.B), s);
   if (e != cudaSuccess) return e;
