@@ -1580,8 +1580,9 @@ cudaError_t launch_tree_steps(const KernelArgs& a, const TreeDesc& td, double* t
   cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(int) * (size_t)(2 + a.B), s);
   if (e != cudaSuccess) return e;
   *launches += 1;
-  // steps per task (one acquire per task): C4b 112.5 (1) -> 103.5 (4) ms/step
-  static const int chunk = std::getenv("PBAD_TREE_CHUNK") ? std::max(1, std::atoi(std::getenv("PBAD_TREE_CHUNK"))) : 4;
+  // steps per task (one acquire per task): C4b 112.5 (1) -> 103.5 (4) ms/step in one
+  // run; 97.7 (4), 96.3 (8), 95.0 (16) in another
+  static const int chunk = std::getenv("PBAD_TREE_CHUNK") ? std::max(1, std::atoi(std::getenv("PBAD_TREE_CHUNK"))) : 16;
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(sync);
   int* done = sync + 2;
   const unsigned grid = (unsigned)std::min<long>(a.B, slots[pot]);
