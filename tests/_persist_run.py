@@ -48,21 +48,24 @@ def main(kind, out_path, B, steps):
              launches=ctx.kernel_launches())
 
 
-def run_pair(kind, tmp_path, B, steps, switch):
-    """The rollout with the persistent launch (switch=1) and with one launch
-    per step (switch=0), each in its own process."""
+def run_env(kind, tmp_path, B, steps, tag, **env_vars):
+    """The rollout in its own process with the given environment variables."""
     import os
     import subprocess
     here = os.path.dirname(os.path.abspath(__file__))
-    res = {}
-    for mode in ("1", "0"):
-        p = tmp_path / f"{kind}{mode}.npz"
-        env = dict(os.environ, PYTHONPATH=os.path.dirname(here))
-        env[switch] = mode
-        subprocess.run([sys.executable, os.path.abspath(__file__), kind, str(p), str(B), str(steps)], check=True,
-                       env=env, timeout=900)
-        res[mode] = np.load(p)
-    return res["1"], res["0"]
+    p = tmp_path / f"{kind}_{tag}.npz"
+    env = dict(os.environ, PYTHONPATH=os.path.dirname(here))
+    env.update({k: str(v) for k, v in env_vars.items()})
+    subprocess.run([sys.executable, os.path.abspath(__file__), kind, str(p), str(B), str(steps)], check=True, env=env,
+                   timeout=900)
+    return np.load(p)
+
+
+def run_pair(kind, tmp_path, B, steps, switch):
+    """The rollout with the persistent launch (switch=1) and with one launch
+    per step (switch=0), each in its own process."""
+    return (run_env(kind, tmp_path, B, steps, "p1", **{switch: 1}),
+            run_env(kind, tmp_path, B, steps, "p0", **{switch: 0}))
 
 
 if __name__ == "__main__":

@@ -258,18 +258,26 @@ def test_tree_path_lbfgs_equals_general_kernel(monkeypatch):
 
 def test_tree_persistent_multistep_contact(tmp_path):
     """Contact scenes run a window of steps in one persistent launch
-    (k_tree_steps, pbad_tree.cu): warps claim env-steps in order and wait for
-    the environment's previous step, which ran on another SM.  With a batch
-    larger than the resident warps every environment changes SM between
-    steps.  The whole batch is bit-identical to one launch per step
-    (PBAD_TREE_PERSIST=0), and a sample matches the oracle."""
+    (k_tree_steps, pbad_tree.cu): warps claim tasks (PBAD_TREE_CHUNK
+    consecutive steps of one environment) in order and wait for the
+    environment's previous task, which ran on another SM.  With a batch
+    larger than the resident warps and 1- or 2-step tasks, environments change
+    SM between steps.  The whole batch is bit-identical to one launch per
+    step (PBAD_TREE_PERSIST=0) for task lengths 1, 2 and the default, and a
+    sample matches the oracle."""
     import _persist_run as pr
     B, steps = 2500, 5
-    one, per = pr.run_pair("tree_contact", tmp_path, B, steps, "PBAD_TREE_PERSIST")
-    assert int(one["path"]) == PATH_TREE
-    assert int(one["launches"]) == 1 and int(per["launches"]) == steps
-    for k in ("q", "energy", "iterations"):
-        np.testing.assert_array_equal(one[k], per[k])
+    per = pr.run_env("tree_contact", tmp_path, B, steps, "per_step", PBAD_TREE_PERSIST=0)
+    assert int(per["launches"]) == steps
+    for chunk in (1, 2, None):
+        env = {"PBAD_TREE_PERSIST": 1}
+        if chunk:
+            env["PBAD_TREE_CHUNK"] = chunk
+        one = pr.run_env("tree_contact", tmp_path, B, steps, f"chunk{chunk}", **env)
+        assert int(one["path"]) == PATH_TREE
+        assert int(one["launches"]) == 1
+        for k in ("q", "energy", "iterations"):
+            np.testing.assert_array_equal(one[k], per[k])
     assert one["iterations"].max() > one["iterations"].min()  # the iteration counts do vary
     sc = pr.scene("tree_contact")
     n = 41
